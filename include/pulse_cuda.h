@@ -1,0 +1,207 @@
+/*
+ * pulse_cuda.h -- C ABI of libpulse_cuda.so, the B200-native PULSE hot path.
+ *
+ * The reference (arxiv 2602.03839, /root/reference/proj/include/pulse) is a
+ * header-only C++20 library with no FFI; its drop-in surface for this path is
+ * the set of functions in patch.hpp, index_coding.hpp, patch_file.hpp,
+ * compression.hpp and sha256.hpp.  This header is the C boundary those
+ * functions are re-expressed over: plain pointers, sizes and status codes, no
+ * C++ or torch types.  The headers in include/pulse/ re-create the reference's C++ API
+ * on top of it, and paper_2602_03839_b200/_native.py binds it with ctypes.
+ *
+ * Two families of entry points:
+ *   pulse_encode / pulse_decode / pulse_*_payloads / pulse_*_patch_bytes ...
+ *       host-buffer calls that mirror the reference functions one for one
+ *       (the reference interface each replaces is cited on the declaration);
+ *       inputs are staged to the GPU, every per-element step runs in CUDA.
+ *   pulse_plan_* / pulse_encode_scan / pulse_encode_emit / pulse_apply ...
+ *       device-resident calls over snapshots already in HBM, asynchronous on
+ *       a caller-supplied cudaStream_t (passed as void*).  These are what the
+ *       throughput numbers measure and what the multi-GPU driver shards.
+ *
+ * Errors: every function returns a pulse_status; the numbering maps one to one
+ * onto the reference exception classes (error.hpp:10-115).  No exception
+ * crosses the ABI.  pulse_last_error() returns the thread-local message of the
+ * last failing call on the calling thread.
+ */
+#ifndef PULSE_CUDA_H
+#define PULSE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum pulse_status {
+    PULSE_OK = 0,
+    PULSE_E_ERROR = 1,           /* pulse::Error                 error.hpp:10  */
+    PULSE_E_ARGUMENT = 2,        /* pulse::ArgumentError         error.hpp:16  */
+    PULSE_E_FORMAT = 3,          /* pulse::FormatError           error.hpp:22  */
+    PULSE_E_BAD_MAGIC = 4,       /* pulse::BadMagicError         error.hpp:27  */
+    PULSE_E_VERSION = 5,         /* pulse::VersionError          error.hpp:32  */
+    PULSE_E_TRUNCATION = 6,      /* pulse::TruncationError       error.hpp:37  */
+    PULSE_E_CORRUPT_STREAM = 7,  /* pulse::CorruptStreamError    error.hpp:42  */
+    PULSE_E_MODEL_MISMATCH = 8,  /* pulse::ModelMismatchError    error.hpp:49  */
+    PULSE_E_SHAPE_MISMATCH = 9,  /* pulse::ShapeMismatchError    error.hpp:54  */
+    PULSE_E_TENSOR_SET = 10,     /* pulse::TensorSetError        error.hpp:59  */
+    PULSE_E_INDEX_RANGE = 11,    /* pulse::IndexRangeError       error.hpp:64  */
+    PULSE_E_DIMENSION = 12,      /* pulse::DimensionError        error.hpp:71  */
+    PULSE_E_HASH_MISMATCH = 13,  /* pulse::HashMismatchError     error.hpp:77  */
+    PULSE_E_CUDA = 14,           /* device/runtime failure (no reference analogue) */
+    PULSE_E_CAPACITY = 15        /* caller arena too small; see `required` */
+} pulse_status;
+
+/* SparseRepresentation (patch.hpp:20-24) and CodecId (compression.hpp:31-37). */
+enum { PULSE_COO_DOWNSCALED = 0, PULSE_COO_INT32 = 1, PULSE_FLAT_INT32 = 2 };
+enum { PULSE_IDENTITY = 0, PULSE_LZ4 = 1, PULSE_ZSTD1 = 2, PULSE_ZSTD3 = 3, PULSE_GZIP6 = 4 };
+
+const char* pulse_last_error(void);
+const char* pulse_version(void);
+
+/* ======================================================================= */
+/* Device-resident API                                                      */
+/* ======================================================================= */
+
+typedef struct pulse_context pulse_context;
+typedef struct pulse_plan pulse_plan;
+
+/* One context per device; callable from one host thread per GPU. */
+pulse_status pulse_context_create(int device, pulse_context** out);
+void pulse_context_destroy(pulse_context* ctx);
+
+/* Geometry of one tensor of a name-sorted state dict (checkpoint.hpp:18-28). */
+typedef struct pulse_tensor_geom {
+    uint64_t numel; /* elements, > 0 */
+    uint64_t cols;  /* shape.back(): COO_DOWNSCALED column extent (patch.hpp:105-109) */
+} pulse_tensor_geom;
+
+/* A plan fixes the tensor table (in ascending name order, the PULP order,
+ * patch_file.hpp:34-35) and owns the device scratch for up to `max_changes`
+ * changed elements per encode/apply.  Tensors may exceed 2^32 elements. */
+pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tensors,
+                               uint32_t n_tensors, uint64_t max_changes, pulse_plan** out);
+void pulse_plan_destroy(pulse_plan* plan);
+
+/* Binds one device pointer per tensor (bf16 data, 16-byte aligned) to slot
+ * 0..3.  Encode reads two slots; apply writes one. */
+enum { PULSE_MAX_SLOTS = 4 };
+pulse_status pulse_plan_bind(pulse_plan* plan, uint32_t slot, const void* const* dev_ptrs);
+
+/* FLAT_INT32 threads one gap stream across tensors (patch.hpp:131-156); when a
+ * state dict is sharded across ranks, each rank's stream continues from the
+ * previous rank's last emitted index.  gap_base = numel(last changed tensor)
+ * - last index in it; the first entry of the next shard is idx + gap_base. */
+typedef struct pulse_flat_carry {
+    uint64_t has_prev;
+    uint64_t gap_base;
+} pulse_flat_carry;
+
+/* Per-shard summary after the diff scan; all-gathered across ranks so each
+ * rank can place its section and continue the FLAT stream. */
+typedef struct pulse_scan_summary {
+    uint64_t n_changes;
+    uint64_t has_change;
+    uint64_t last_gap_base; /* numel - last index of this shard's last changed tensor */
+    uint64_t status;        /* 0 or PULSE_E_CAPACITY */
+} pulse_scan_summary;
+
+/* One entry per changed tensor, in name order -- the device image of the PULP
+ * per-tensor header record (patch_file.hpp:63-71) and its two blobs. */
+typedef struct pulse_patch_entry {
+    uint32_t tensor; /* plan tensor index */
+    uint32_t reserved;
+    uint64_t count;      /* changed elements = values */
+    uint64_t idx_off;    /* byte offset of the raw index payload in the body */
+    uint64_t idx_nbytes; /* patch.hpp:116-174 payload length */
+    uint64_t val_off;    /* byte offset of the u16 LE value payload (2*count B) */
+} pulse_patch_entry;
+
+/* The reference check behind a failure (ordered as the reference evaluates
+ * them); lets the host rebuild the reference's exception message. */
+enum {
+    PULSE_CHECK_TRUNCATED = 1,     /* wire.hpp:58-60 */
+    PULSE_CHECK_ZERO_GAP = 2,      /* patch.hpp:201-203, 225-227 */
+    PULSE_CHECK_ZERO_COL_GAP = 3,  /* index_coding.hpp:147-149 */
+    PULSE_CHECK_COL_RANGE = 4,     /* patch.hpp:247-250 */
+    PULSE_CHECK_INDEX_RANGE = 5,   /* patch.hpp:206-208, 231-233, 252-254 */
+    PULSE_CHECK_TRAILING = 6,      /* patch.hpp:211-213, index_coding.hpp:154-156 */
+    PULSE_CHECK_NEGATIVE = 7,      /* index_coding.hpp:19-21, 118 */
+    PULSE_CHECK_ORDER = 8,         /* index_coding.hpp:22-24, 119-121; patch.hpp:142-144 */
+    PULSE_CHECK_FLAT_GAP = 9,      /* patch.hpp:145-147 */
+    PULSE_CHECK_ROW_GAP = 10,      /* index_coding.hpp:69-71 */
+    PULSE_CHECK_COL_ENTRY = 11,    /* index_coding.hpp:80-82 */
+    PULSE_CHECK_INT32 = 12,        /* patch.hpp:99-103 */
+    PULSE_CHECK_APPLY_ORDER = 13,  /* patch.hpp:329-332 */
+    PULSE_CHECK_APPLY_RANGE = 14,  /* patch.hpp:333-336 */
+    PULSE_CHECK_CAPACITY = 15
+};
+
+typedef struct pulse_result {
+    uint64_t n_changes;
+    uint64_t body_bytes; /* encode: bytes written to the body */
+    uint32_t n_entries;  /* encode: changed tensors */
+    int32_t status;      /* pulse_status of the device pipeline */
+    uint32_t err_check;  /* which reference check failed first (PULSE_CHECK_*) */
+    uint32_t err_stage;
+    uint64_t err_tensor; /* plan tensor (encode) / patch entry (apply) of the first failure */
+    uint64_t err_elem;   /* element / entry ordinal of the first failure */
+    uint64_t required;   /* bytes or changes needed when status == PULSE_E_CAPACITY */
+    pulse_flat_carry carry_out;
+} pulse_result;
+
+/* K1: bitwise diff of slot `curr_slot` against `prev_slot` and ordered
+ * compaction (decoupled look-back) of every changed element -- the loop at
+ * patch.hpp:296-301.  Writes the plan's scan summary (device). */
+pulse_status pulse_encode_scan(pulse_plan* plan, uint32_t curr_slot, uint32_t prev_slot,
+                               void* stream);
+/* Device pointer to the plan's pulse_scan_summary (for NCCL all-gather). */
+pulse_scan_summary* pulse_plan_scan_summary(pulse_plan* plan);
+
+/* K2: index coding (patch.hpp:116-174, index_coding.hpp:14-128) and the PULP
+ * body layout: for each changed tensor, [index payload][value payload]
+ * concatenated in name order (the identity-codec blob area of
+ * patch_file.hpp:76-82).  `gathered`/`n_ranks`/`rank` (device array of all
+ * ranks' scan summaries) continue a sharded FLAT_INT32 stream and offset the
+ * section; pass NULL/1/0 on one GPU.  Writes `dev_entries[n_tensors]`,
+ * `dev_result`. */
+pulse_status pulse_encode_emit(pulse_plan* plan, uint32_t representation,
+                               const pulse_scan_summary* gathered, uint32_t n_ranks,
+                               uint32_t rank, uint8_t* dev_body, uint64_t body_capacity,
+                               pulse_patch_entry* dev_entries, pulse_result* dev_result,
+                               void* stream);
+
+/* Apply a device-resident patch body in place to slot `weights_slot`:
+ * parse + validate every entry first (patch.hpp:178-262, 325-336), then
+ * scatter (patch.hpp:337) only if nothing failed, so a bad patch never
+ * half-applies.  `carry` continues a sharded FLAT_INT32 stream (NULL on one
+ * GPU).  Writes `dev_result`. */
+pulse_status pulse_apply(pulse_plan* plan, uint32_t weights_slot, uint32_t representation,
+                         const uint8_t* dev_body, const pulse_patch_entry* dev_entries,
+                         uint32_t n_entries, const pulse_flat_carry* dev_carry,
+                         pulse_result* dev_result, void* stream);
+
+/* Decode only: parse the payloads to flat int64 indices (dev_indices, in
+ * entry order) without touching weights. */
+pulse_status pulse_decode_indices(pulse_plan* plan, uint32_t representation,
+                                  const uint8_t* dev_body, const pulse_patch_entry* dev_entries,
+                                  uint32_t n_entries, const pulse_flat_carry* dev_carry,
+                                  int64_t* dev_indices, pulse_result* dev_result, void* stream);
+
+/* Synthetic snapshots on device (fixture; the reference generator's knobs,
+ * synthetic.hpp:21-28,62-107): log-normal |w| (median, sigma), random sign,
+ * then exactly llround((1-sparsity)*n) changed positions in half-density
+ * windows of `cluster_width`, each an LSB flip.  Counter-based RNG, so the
+ * bytes are a function of (seed, n) only. */
+pulse_status pulse_synth_base(uint16_t* dev_out, uint64_t n, uint64_t seed, double median,
+                              double sigma, void* stream);
+pulse_status pulse_synth_mutate(pulse_context* ctx, const uint16_t* dev_base, uint16_t* dev_out,
+                                uint64_t n, double sparsity, uint64_t cluster_width,
+                                uint64_t seed, uint64_t* changed_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PULSE_CUDA_H */

@@ -1,0 +1,214 @@
+// Device-side building blocks shared by the PULSE kernels (sm_100a).
+//
+//  * single-pass decoupled look-back over tile status words (K1, K3 scans)
+//  * 256-thread block scans
+//  * streaming 128-bit loads that do not pollute L1 (each snapshot byte is
+//    read exactly once per encode)
+//  * first-error keys that reproduce the reference's sequential error order
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/pulse_cuda.h"
+
+namespace pulse {
+namespace dev {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+// ------------------------------------------------------------------------------------------
+// First-error keys.  The reference throws at the first failing check of a
+// sequential walk (tensor order, then stage, then element).  Kernels detect
+// failures in parallel and atomicMin a key whose ordering is that walk's:
+//   key = tensor:20 | stage:4 | element:36 | check:4
+// `check` ranks the checks one element can fail, in the order the reference
+// evaluates them (e.g. a truncated read precedes the zero-gap test on the value
+// it would have read).  The host maps `check` to the exception type/message.
+// ------------------------------------------------------------------------------------------
+enum Check : uint32_t {
+    kTrunc = 1,        // TruncationError            wire.hpp:58-60
+    kZeroGap = 2,      // CorruptStreamError         patch.hpp:201-203, 225-227
+    kZeroColGap = 3,   // CorruptStreamError         index_coding.hpp:147-149
+    kColRange = 4,     // CorruptStreamError         patch.hpp:247-250
+    kIdxRange = 5,     // CorruptStreamError         patch.hpp:206-208, 231-233, 252-254
+    kTrailing = 6,     // CorruptStreamError         patch.hpp:211-213, index_coding.hpp:154-156
+    kArgNegative = 7,  // ArgumentError              index_coding.hpp:19-21, 118
+    kArgOrder = 8,     // ArgumentError              index_coding.hpp:22-24, 119-121; patch.hpp:142-144
+    kDimFlatGap = 9,   // DimensionError             patch.hpp:145-147
+    kDimRow = 10,      // DimensionError             index_coding.hpp:69-71
+    kDimCol = 11,      // DimensionError             index_coding.hpp:80-82
+    kDimInt32 = 12,    // DimensionError             patch.hpp:99-103
+    kApplyOrder = 13,  // IndexRangeError            patch.hpp:329-332
+    kApplyRange = 14,  // IndexRangeError            patch.hpp:333-336
+    kCapacity = 15,    // arena too small (no reference analogue)
+};
+
+// Stages within one tensor, in the reference's evaluation order.
+enum Stage : uint32_t { kStageTensor = 0, kStageRows = 1, kStageCols = 2, kStageTrailing = 3, kStageRange = 4 };
+
+constexpr uint64_t kNoError = ~0ull;
+
+__host__ __device__ inline uint64_t error_key(uint64_t tensor, uint32_t stage, uint64_t elem, uint32_t check) {
+    return (tensor << 44) | (uint64_t(stage & 15) << 40) | ((elem & ((1ull << 36) - 1)) << 4) | (check & 15);
+}
+__host__ __device__ inline uint32_t key_tensor(uint64_t k) { return uint32_t(k >> 44); }
+__host__ __device__ inline uint32_t key_stage(uint64_t k) { return uint32_t((k >> 40) & 15); }
+__host__ __device__ inline uint64_t key_elem(uint64_t k) { return (k >> 4) & ((1ull << 36) - 1); }
+__host__ __device__ inline uint32_t key_check(uint64_t k) { return uint32_t(k & 15); }
+
+// pulse_status for a failed check (error.hpp class of the reference throw).
+__host__ __device__ inline int32_t check_status(uint32_t check) {
+    switch (check) {
+        case kTrunc: return PULSE_E_TRUNCATION;
+        case kZeroGap: case kZeroColGap: case kColRange: case kIdxRange: case kTrailing:
+            return PULSE_E_CORRUPT_STREAM;
+        case kArgNegative: case kArgOrder: return PULSE_E_ARGUMENT;
+        case kDimFlatGap: case kDimRow: case kDimCol: case kDimInt32: return PULSE_E_DIMENSION;
+        case kApplyOrder: case kApplyRange: return PULSE_E_INDEX_RANGE;
+        default: return PULSE_E_CAPACITY;
+    }
+}
+
+__device__ __forceinline__ void report(uint64_t* err, uint64_t key) {
+    atomicMin(reinterpret_cast<unsigned long long*>(err), static_cast<unsigned long long>(key));
+}
+
+// ------------------------------------------------------------------------------------------
+// Memory helpers
+// ------------------------------------------------------------------------------------------
+// 128-bit streaming load: read-only path, no L1 allocation, 256-B L2 prefetch.
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Unaligned little-endian reads from a byte stream.
+__device__ __forceinline__ uint32_t rd_u16(const uint8_t* p) { return uint32_t(p[0]) | uint32_t(p[1]) << 8; }
+__device__ __forceinline__ uint32_t rd_u32(const uint8_t* p) {
+    return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
+}
+__device__ __forceinline__ void wr_u16(uint8_t* p, uint32_t v) {
+    p[0] = uint8_t(v);
+    p[1] = uint8_t(v >> 8);
+}
+__device__ __forceinline__ void wr_u32(uint8_t* p, uint32_t v) {
+    p[0] = uint8_t(v);
+    p[1] = uint8_t(v >> 8);
+    p[2] = uint8_t(v >> 16);
+    p[3] = uint8_t(v >> 24);
+}
+
+// Largest i in [lo, hi) with a[i] <= x (a non-decreasing, a[lo] <= x).
+template <class T>
+__device__ __forceinline__ uint32_t upper_index(const T* a, uint32_t lo, uint32_t hi, T x) {
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// ------------------------------------------------------------------------------------------
+// Scan operators over 62-bit payloads (status words keep 2 flag bits).
+// ------------------------------------------------------------------------------------------
+struct SumOp {
+    static __device__ __forceinline__ uint64_t op(uint64_t earlier, uint64_t later) { return earlier + later; }
+};
+// Segmented sum: bit 61 marks "a segment head lies in this span"; a later
+// span with a head discards everything before it.
+struct SegSumOp {
+    static constexpr uint64_t kHead = 1ull << 61;
+    static __device__ __forceinline__ uint64_t op(uint64_t earlier, uint64_t later) {
+        return (later & kHead) ? later : earlier + later;
+    }
+};
+
+enum : uint64_t { kStatInvalid = 0, kStatAggregate = 1, kStatPrefix = 2 };
+
+// Decoupled look-back (single-pass scan).  Called by all 32 lanes of ONE warp
+// of the tile's block; `tile` ids must be handed out in launch order (dynamic
+// ticket) so every predecessor is already resident.  Publishes this tile's
+// aggregate, walks back over predecessors 32 at a time until it meets an
+// inclusive prefix, publishes the inclusive prefix and returns the exclusive
+// prefix (identity 0 for tile 0).
+template <class Op>
+__device__ __forceinline__ uint64_t lookback(uint64_t* status, uint64_t tile, uint64_t agg) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) st_relaxed(status, (agg << 2) | kStatPrefix);
+        return 0;
+    }
+    if (lane == 0) st_relaxed(status + tile, (agg << 2) | kStatAggregate);
+    uint64_t excl = 0;
+    int64_t base = int64_t(tile) - 1;
+    while (true) {
+        const int64_t idx = base - lane;
+        uint64_t s = kStatPrefix;  // before tile 0: an identity prefix
+        if (idx >= 0) {
+            do {
+                s = ld_relaxed(status + idx);
+            } while ((s & 3) == kStatInvalid);
+        }
+        const uint32_t pmask = __ballot_sync(0xffffffffu, (s & 3) == kStatPrefix);
+        const int stop = pmask ? __ffs(pmask) - 1 : 31;
+        uint64_t v = lane <= stop ? (s >> 2) : 0;
+        // Ordered reduction: higher lanes are earlier tiles.
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint64_t o = __shfl_down_sync(0xffffffffu, v, off);
+            if (lane + off < 32) v = Op::op(o, v);
+        }
+        v = __shfl_sync(0xffffffffu, v, 0);
+        excl = Op::op(v, excl);
+        if (pmask) break;
+        base -= 32;
+    }
+    if (lane == 0) st_relaxed(status + tile, (Op::op(excl, agg) << 2) | kStatPrefix);
+    return excl;
+}
+
+// Block-wide exclusive scan of one value per thread (kThreads threads).
+// `s_warp` holds kWarps entries.  Returns the exclusive prefix; `total` gets
+// the block aggregate.  Contains two __syncthreads().
+template <class Op>
+__device__ __forceinline__ uint64_t block_exclusive(uint64_t v, uint64_t* s_warp, uint64_t& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc = Op::op(o, inc);
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    uint64_t before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint64_t x = s_warp[w];
+        if (w < warp) before = Op::op(before, x);
+        all = Op::op(all, x);
+    }
+    total = all;
+    // exclusive within warp
+    uint64_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = 0;
+    __syncthreads();
+    return Op::op(before, ex);
+}
+
+}  // namespace dev
+}  // namespace pulse

@@ -1,0 +1,128 @@
+// Internal interface between the plan/ABI layer (plan.cu) and the kernel
+// translation units (encode.cu, decode.cu, synth.cu).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/pulse_cuda.h"
+
+namespace pulse {
+namespace dev {
+
+// K1 tile: 8192 bf16 of each snapshot (16 KiB + 16 KiB); 256 threads x 4 x 128-bit loads.
+constexpr uint32_t kTileElems = 8192;
+// Segments split tensors so that a compacted u32 index (relative to the
+// segment) always fits; tiles never straddle segments (nor tensors).
+constexpr uint64_t kSegElems = 1ull << 31;
+// K2 / decode chunk: 2048 entries = 256 threads x 8.
+constexpr uint32_t kChunkEntries = 2048;
+constexpr uint32_t kEntriesPerThread = 8;
+// COO_DOWNSCALED parse tiles: 256 threads x 16 bytes.
+constexpr uint32_t kParseBytes = 16;
+constexpr uint32_t kParseTile = 256 * kParseBytes;
+
+struct SegDesc {
+    uint64_t elem_off;    // element offset of the segment inside its tensor
+    uint64_t tile_start;  // first global K1 tile id
+    uint32_t tensor;      // tensor index in the plan
+    uint32_t numel;       // elements in the segment (<= 2^31)
+};
+
+// Per-tensor encode layout (written by the layout kernel).
+struct TensorLayout {
+    uint64_t idx_off;     // byte offset of the index payload in the body
+    uint64_t val_off;     // byte offset of the value payload in the body
+    uint64_t row_bytes;   // COO_DOWNSCALED: bytes of the row stream
+    uint64_t rts;         // row escapes before this tensor (global)
+    uint64_t cts;         // col escapes before this tensor (global)
+    uint64_t gap_base;    // FLAT: numel - last of the previous changed tensor
+    uint32_t has_prev;    // FLAT: an earlier index exists in the stream
+    uint32_t count_nz;    // tensor has changes
+};
+
+// Per-entry decode layout (one per patch entry).
+struct EntryLayout {
+    uint64_t tensor;      // plan tensor index
+    uint64_t count;
+    uint64_t idx_off, idx_nbytes, val_off;
+    uint64_t es;          // first entry ordinal (exclusive scan of counts)
+    uint64_t ck;          // first parse chunk (row grammar)
+    uint64_t numel, cols;
+    uint64_t flat_base;   // FLAT: sum of numel of earlier patch entries
+    uint64_t col_start;   // COO_DS: byte offset (within idx blob) where the col stream starts
+    uint64_t cu;          // COO_DS: first col-grammar chunk
+};
+
+// Everything the kernels need, as device pointers.
+struct PlanDev {
+    uint32_t n_tensors, n_segs;
+    uint64_t n_tiles, cap;
+    const SegDesc* segs;
+    const uint32_t* seg_first;  // [T+1] first segment of each tensor
+    const uint64_t* numel;      // [T]
+    const uint64_t* cols;       // [T]
+    uint16_t* const* slot[PULSE_MAX_SLOTS];  // device arrays of T data pointers
+
+    // encode scratch
+    uint32_t* idx32;            // [cap]
+    uint16_t* val16;            // [cap]
+    uint64_t* seg_start;        // [S+1] entry offset of each segment
+    uint64_t* k1_status;        // [n_tiles]
+    uint64_t* counters;         // [8] tickets
+    pulse_scan_summary* scan;   // device
+    uint2* chunk_esc;           // [cap/2048+1]
+    ulonglong2* chunk_pre;      // [cap/2048+1]
+    uint32_t* t_resc;           // [T]
+    uint32_t* t_cesc;           // [T]
+    TensorLayout* tlay;         // [T]
+    uint64_t* err;              // first-error key
+    pulse_result* result;       // device (internal copy)
+
+    // mode-B (host int64 indices) entry map: one segment per tensor
+    const SegDesc* id_segs;     // [T]
+    const uint32_t* id_first;   // [T+1] = 0..T
+    uint64_t* id_start;         // [T+1] entry offsets, uploaded per call
+
+    // decode scratch
+    EntryLayout* elay;          // [T]
+    uint64_t* d_es;             // [T+1] first entry ordinal of each patch entry
+    uint64_t* d_ck;             // [T+1] first row-grammar chunk
+    uint64_t* d_cu;             // [T+1] first col-grammar chunk
+    uint32_t* rowgap;           // [cap]
+    uint32_t* colent;           // [cap]
+    uint64_t* flat;             // [cap]
+    uint64_t* d_status;         // look-back status words, 4 regions of d_status_len
+    uint64_t d_status_len;      // words per region
+    uint64_t dec_bytes_cap;     // max index-payload bytes a decode may parse
+    uint64_t* d_totals;         // [16] totals + tickets
+};
+
+// ---- launchers (stream-ordered, no host sync) -------------------------------------------
+void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot, cudaStream_t s);
+void launch_encode_emit(const PlanDev& p, uint32_t repr, const pulse_scan_summary* gathered,
+                        uint32_t n_ranks, uint32_t rank, uint8_t* body, uint64_t body_cap,
+                        pulse_patch_entry* entries, pulse_result* result, cudaStream_t s);
+void launch_decode(const PlanDev& p, uint32_t repr, const uint8_t* body,
+                   const pulse_patch_entry* entries, uint32_t n_entries,
+                   const pulse_flat_carry* carry, int weights_slot, int64_t* out_indices,
+                   pulse_result* result, cudaStream_t s);
+// Validate caller-provided int64 indices (decode over an in-memory SparsePatch,
+// patch.hpp:325-336) and scatter values into `weights_slot`.
+void launch_apply_idx64(const PlanDev& p, const int64_t* idx64, const uint16_t* vals,
+                        const pulse_patch_entry* entries, uint32_t n_entries, int weights_slot,
+                        pulse_result* result, cudaStream_t s);
+
+// Host-index encode (index coding of caller-provided int64 indices, the
+// reference's encode_index_payloads over a host SparsePatch).
+void launch_encode_emit_idx64(const PlanDev& p, uint32_t repr, const int64_t* idx64,
+                              uint8_t* body, uint64_t body_cap, pulse_patch_entry* entries,
+                              pulse_result* result, cudaStream_t s);
+
+int sm_count();
+
+}  // namespace dev
+}  // namespace pulse

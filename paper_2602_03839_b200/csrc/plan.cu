@@ -1,0 +1,234 @@
+// Contexts, plans and the device-resident C ABI (include/pulse_cuda.h).
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "internal.hpp"
+#include "plan.hpp"
+
+using namespace pulse::dev;
+
+namespace pulse {
+
+thread_local std::string g_last_error;
+
+pulse_status fail(pulse_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+pulse_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(PULSE_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace pulse
+
+using pulse::cuda_fail;
+using pulse::fail;
+
+// ---------------------------------------------------------------------------------------------
+// Device arena helpers
+// ---------------------------------------------------------------------------------------------
+template <class T>
+static cudaError_t dalloc(std::vector<void*>& owned, T** p, size_t n) {
+    void* raw = nullptr;
+    const cudaError_t e = cudaMalloc(&raw, std::max<size_t>(n, 1) * sizeof(T));
+    if (e == cudaSuccess) owned.push_back(raw);
+    *p = static_cast<T*>(raw);
+    return e;
+}
+
+pulse_context::~pulse_context() {
+    for (auto* p : owned) cudaFree(p);
+    if (pinned) cudaFreeHost(pinned);
+}
+
+pulse_plan::~pulse_plan() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    for (auto* p : owned) cudaFree(p);
+    if (host_pinned) cudaFreeHost(host_pinned);
+    cudaSetDevice(prev);
+}
+
+extern "C" {
+
+const char* pulse_last_error(void) { return pulse::g_last_error.c_str(); }
+const char* pulse_version(void) { return "pulse-b200 0.1 (sm_100a)"; }
+
+pulse_status pulse_context_create(int device, pulse_context** out) {
+    if (!out) return fail(PULSE_E_ARGUMENT, "null output pointer");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    auto* c = new pulse_context();
+    c->device = device;
+    *out = c;
+    return PULSE_OK;
+}
+
+void pulse_context_destroy(pulse_context* ctx) { delete ctx; }
+
+pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tensors, uint32_t n_tensors,
+                               uint64_t max_changes, pulse_plan** out) {
+    if (!ctx || !out || (n_tensors && !tensors)) return fail(PULSE_E_ARGUMENT, "null argument");
+    if (n_tensors >= (1u << 20)) return fail(PULSE_E_ARGUMENT, "too many tensors (max 2^20)");
+    cudaSetDevice(ctx->device);
+    auto plan = new pulse_plan();
+    plan->ctx = ctx;
+    plan->device = ctx->device;
+    plan->geom.assign(tensors, tensors + n_tensors);
+
+    // segments (<= 2^31 elements) and K1 tiles
+    std::vector<SegDesc> segs;
+    std::vector<uint32_t> seg_first(n_tensors + 1);
+    uint64_t tiles = 0;
+    for (uint32_t t = 0; t < n_tensors; ++t) {
+        const uint64_t n = tensors[t].numel;
+        if (n == 0 || tensors[t].cols == 0 || n % tensors[t].cols != 0) {
+            delete plan;
+            return fail(PULSE_E_ARGUMENT, "tensor " + std::to_string(t) + " has invalid geometry");
+        }
+        seg_first[t] = uint32_t(segs.size());
+        for (uint64_t off = 0; off < n; off += kSegElems) {
+            SegDesc d;
+            d.elem_off = off;
+            d.tile_start = tiles;
+            d.tensor = t;
+            d.numel = uint32_t(std::min<uint64_t>(kSegElems, n - off));
+            tiles += (d.numel + kTileElems - 1) / kTileElems;
+            segs.push_back(d);
+        }
+    }
+    seg_first[n_tensors] = uint32_t(segs.size());
+    PlanDev& p = plan->dev;
+    std::memset(&p, 0, sizeof(p));
+    p.n_tensors = n_tensors;
+    p.n_segs = uint32_t(segs.size());
+    p.n_tiles = tiles;
+    p.cap = std::max<uint64_t>(max_changes, 1);
+    const uint64_t T = n_tensors, S = segs.size(), cap = p.cap;
+    const uint64_t n_chunks = cap / kChunkEntries + 2;
+    p.dec_bytes_cap = 10 * cap + kParseBytes * (T + 1);
+    p.d_status_len = std::max<uint64_t>(n_chunks, p.dec_bytes_cap / kParseTile + T + 2);
+
+    auto& o = plan->owned;
+    cudaError_t e = cudaSuccess;
+    SegDesc* segs_d; uint32_t* first_d; uint64_t *numel_d, *cols_d;
+    SegDesc* id_segs_d; uint32_t* id_first_d;
+#define A(ptr, n) if (e == cudaSuccess) e = dalloc(o, &(ptr), (n))
+    A(segs_d, S); A(first_d, T + 1); A(numel_d, T); A(cols_d, T);
+    for (int s = 0; s < PULSE_MAX_SLOTS; ++s) { uint16_t** sp = nullptr; A(sp, T); p.slot[s] = sp; }
+    A(p.idx32, cap); A(p.val16, cap); A(p.seg_start, S + 1); A(p.k1_status, tiles + 1);
+    A(p.counters, 8); A(p.scan, 1); A(p.chunk_esc, n_chunks); A(p.chunk_pre, n_chunks);
+    A(p.t_resc, T); A(p.t_cesc, T); A(p.tlay, T); A(p.err, 1); A(p.result, 1);
+    A(id_segs_d, T); A(id_first_d, T + 1); A(p.id_start, T + 1);
+    A(p.elay, T); A(p.d_es, T + 1); A(p.d_ck, T + 1); A(p.d_cu, T + 1);
+    A(p.rowgap, cap); A(p.colent, cap); A(p.flat, cap);
+    A(p.d_status, 4 * p.d_status_len); A(p.d_totals, 16);
+#undef A
+    if (e != cudaSuccess) {
+        delete plan;
+        return cuda_fail(e, "plan allocation");
+    }
+    p.segs = segs_d;
+    p.seg_first = first_d;
+    p.numel = numel_d;
+    p.cols = cols_d;
+    p.id_segs = id_segs_d;
+    p.id_first = id_first_d;
+
+    std::vector<uint64_t> numel(T), cols(T);
+    std::vector<SegDesc> id_segs(T);
+    std::vector<uint32_t> id_first(T + 1);
+    for (uint32_t t = 0; t < n_tensors; ++t) {
+        numel[t] = tensors[t].numel;
+        cols[t] = tensors[t].cols;
+        id_segs[t] = SegDesc{0, 0, t, 0};
+        id_first[t] = t;
+    }
+    id_first[T] = uint32_t(T);
+    cudaMemcpy(segs_d, segs.data(), S * sizeof(SegDesc), cudaMemcpyHostToDevice);
+    cudaMemcpy(first_d, seg_first.data(), (T + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    cudaMemcpy(numel_d, numel.data(), T * sizeof(uint64_t), cudaMemcpyHostToDevice);
+    cudaMemcpy(cols_d, cols.data(), T * sizeof(uint64_t), cudaMemcpyHostToDevice);
+    cudaMemcpy(id_segs_d, id_segs.data(), T * sizeof(SegDesc), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(id_first_d, id_first.data(), (T + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        delete plan;
+        return cuda_fail(e, "plan upload");
+    }
+    *out = plan;
+    return PULSE_OK;
+}
+
+void pulse_plan_destroy(pulse_plan* plan) { delete plan; }
+
+pulse_status pulse_plan_bind(pulse_plan* plan, uint32_t slot, const void* const* dev_ptrs) {
+    if (!plan || slot >= PULSE_MAX_SLOTS || (plan->dev.n_tensors && !dev_ptrs))
+        return fail(PULSE_E_ARGUMENT, "bad plan/slot/pointers");
+    for (uint32_t t = 0; t < plan->dev.n_tensors; ++t)
+        if (reinterpret_cast<uintptr_t>(dev_ptrs[t]) % 16 != 0)
+            return fail(PULSE_E_ARGUMENT, "tensor " + std::to_string(t) + " is not 16-byte aligned");
+    cudaSetDevice(plan->device);
+    cudaError_t e = cudaMemcpy(const_cast<uint16_t**>(plan->dev.slot[slot]), dev_ptrs,
+                               plan->dev.n_tensors * sizeof(void*), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "bind");
+    plan->bound[slot] = true;
+    return PULSE_OK;
+}
+
+pulse_status pulse_encode_scan(pulse_plan* plan, uint32_t curr_slot, uint32_t prev_slot, void* stream) {
+    if (!plan || curr_slot >= PULSE_MAX_SLOTS || prev_slot >= PULSE_MAX_SLOTS ||
+        !plan->bound[curr_slot] || !plan->bound[prev_slot])
+        return fail(PULSE_E_ARGUMENT, "encode_scan: unbound slot");
+    cudaSetDevice(plan->device);
+    launch_encode_scan(plan->dev, curr_slot, prev_slot, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "encode_scan launch");
+}
+
+pulse_scan_summary* pulse_plan_scan_summary(pulse_plan* plan) { return plan ? plan->dev.scan : nullptr; }
+
+pulse_status pulse_encode_emit(pulse_plan* plan, uint32_t repr, const pulse_scan_summary* gathered,
+                               uint32_t n_ranks, uint32_t rank, uint8_t* dev_body, uint64_t body_capacity,
+                               pulse_patch_entry* dev_entries, pulse_result* dev_result, void* stream) {
+    if (!plan || repr > 2 || !dev_entries || !dev_result || (gathered && rank >= n_ranks))
+        return fail(PULSE_E_ARGUMENT, "encode_emit: bad argument");
+    cudaSetDevice(plan->device);
+    launch_encode_emit(plan->dev, repr, gathered, n_ranks, rank, dev_body, dev_body ? body_capacity : 0,
+                       dev_entries, dev_result, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "encode_emit launch");
+}
+
+pulse_status pulse_apply(pulse_plan* plan, uint32_t weights_slot, uint32_t repr, const uint8_t* dev_body,
+                         const pulse_patch_entry* dev_entries, uint32_t n_entries,
+                         const pulse_flat_carry* dev_carry, pulse_result* dev_result, void* stream) {
+    if (!plan || repr > 2 || weights_slot >= PULSE_MAX_SLOTS || !plan->bound[weights_slot] || !dev_result ||
+        n_entries > plan->dev.n_tensors)
+        return fail(PULSE_E_ARGUMENT, "apply: bad argument");
+    cudaSetDevice(plan->device);
+    launch_decode(plan->dev, repr, dev_body, dev_entries, n_entries, dev_carry, int(weights_slot), nullptr,
+                  dev_result, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "apply launch");
+}
+
+pulse_status pulse_decode_indices(pulse_plan* plan, uint32_t repr, const uint8_t* dev_body,
+                                  const pulse_patch_entry* dev_entries, uint32_t n_entries,
+                                  const pulse_flat_carry* dev_carry, int64_t* dev_indices,
+                                  pulse_result* dev_result, void* stream) {
+    if (!plan || repr > 2 || !dev_result || n_entries > plan->dev.n_tensors)
+        return fail(PULSE_E_ARGUMENT, "decode_indices: bad argument");
+    cudaSetDevice(plan->device);
+    launch_decode(plan->dev, repr, dev_body, dev_entries, n_entries, dev_carry, -1, dev_indices, dev_result,
+                  static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "decode launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,150 @@
+"""GPU parity of the device-resident path (K1/K2 encode, D* apply) against
+the reference's own bytes (golden fixtures + oracle/_ref) on the same inputs."""
+import struct
+
+import numpy as np
+import pytest
+
+from oracle.oracle import COO_DOWNSCALED, COO_INT32, FLAT_INT32, IDENTITY, have_reference, reference, restatement
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _dev():
+    from paper_2602_03839_b200 import device as D
+    return D
+
+
+def split_pulp(wire: bytes):
+    """PULP -> (header dict, body bytes)  (patch_file.hpp:30-83)."""
+    import json
+    assert wire[:4] == b"PULP"
+    ver, hlen = struct.unpack_from("<IQ", wire, 4)
+    return json.loads(wire[16:16 + hlen]), wire[16 + hlen:]
+
+
+def upload(ck):
+    ts = ck.sorted()
+    return ts, [torch.from_numpy(t.data.view(np.int16).copy()).cuda() for t in ts]
+
+
+def make_plan(ts, max_changes=None):
+    D = _dev()
+    geoms = [(t.data.size, t.shape[-1]) for t in ts]
+    cap = max_changes or max(16, sum(t.data.size for t in ts))
+    return D.DevicePlan(geoms, cap)
+
+
+@pytest.mark.parametrize("repr_", [COO_DOWNSCALED, COO_INT32, FLAT_INT32])
+def test_encode_body_matches_reference_pulp(golden, repr_):
+    for name in golden.names:
+        prev, curr, m = golden.case(name)
+        want = golden.pulp(name, repr_, IDENTITY)
+        if want is None:
+            continue
+        header, body = split_pulp(want)
+        ts, prev_d = upload(prev)
+        _, curr_d = upload(curr)
+        plan = make_plan(ts)
+        plan.bind(0, prev_d)
+        plan.bind(1, curr_d)
+        p = plan.encode(1, 0, repr_)
+        p.raise_for_status([t.name for t in ts])
+        assert p.n_entries == len(header["tensors"]), name
+        got = p.body[: p.body_bytes].cpu().numpy().tobytes()
+        assert got == body, (name, repr_)
+        for e, h in zip(p.host_entries, header["tensors"]):
+            assert ts[int(e["tensor"])].name == h["name"]
+            assert int(e["count"]) == h["count"]
+            assert int(e["idx_nbytes"]) == h["index_nbytes"]
+
+
+@pytest.mark.parametrize("repr_", [COO_DOWNSCALED, COO_INT32, FLAT_INT32])
+def test_apply_rebuilds_current_bitwise(golden, repr_):
+    for name in golden.names:
+        prev, curr, _ = golden.case(name)
+        ts, prev_d = upload(prev)
+        _, curr_d = upload(curr)
+        _, w_d = upload(prev)
+        plan = make_plan(ts)
+        plan.bind(0, prev_d)
+        plan.bind(1, curr_d)
+        plan.bind(2, w_d)
+        p = plan.encode(1, 0, repr_)
+        res = _dev().parse_result(plan.apply(2, p))
+        assert int(res["status"]) == 0, (name, res)
+        for a, b in zip(w_d, curr_d):
+            assert torch.equal(a, b), name
+        # decode-only path returns the reference's indices
+        idx, res = plan.decode_indices(p)
+        ref_idx = np.concatenate([restatement().diff(q.data, c.data)[0] for q, c in zip(prev.sorted(), curr.sorted())])
+        assert np.array_equal(idx.cpu().numpy(), ref_idx), name
+
+
+def test_empty_patch_and_identical_snapshots():
+    D = _dev()
+    x = torch.arange(4096, dtype=torch.int16, device="cuda")
+    plan = D.DevicePlan([(4096, 64)], 100)
+    plan.bind(0, [x])
+    plan.bind(1, [x.clone()])
+    for r in (0, 1, 2):
+        p = plan.encode(1, 0, r)
+        assert p.status == 0 and p.n_entries == 0 and p.body_bytes == 0 and p.n_changes == 0
+
+
+def test_capacity_overflow_is_reported():
+    D = _dev()
+    a = torch.zeros(10000, dtype=torch.int16, device="cuda")
+    b = torch.ones(10000, dtype=torch.int16, device="cuda")
+    plan = D.DevicePlan([(10000, 100)], 100)
+    plan.bind(0, [a])
+    plan.bind(1, [b])
+    p = plan.encode(1, 0, COO_INT32)
+    assert p.status == 15 and int(p.host_result["required"]) == 10000
+
+
+def test_large_tensor_tiles_and_partial_tail():
+    """Several tensors, sizes not multiples of the 8192-element tile, dense and sparse regions."""
+    D = _dev()
+    R = restatement()
+    rng = np.random.default_rng(3)
+    sizes = [(8192 * 3 + 40, 8), (17, 17), (8192, 4096), (1000008, 24)]
+    prevs, currs = [], []
+    for n, _ in sizes:
+        a = rng.integers(0, 65536, n, dtype=np.uint16)
+        b = a.copy()
+        k = rng.random(n) < rng.choice([0.001, 0.01, 0.5])
+        b[k] ^= 1
+        prevs.append(a)
+        currs.append(b)
+    plan = D.DevicePlan(sizes, sum(n for n, _ in sizes))
+    plan.bind(0, [torch.from_numpy(a.view(np.int16)).cuda() for a in prevs])
+    plan.bind(1, [torch.from_numpy(b.view(np.int16)).cuda() for b in currs])
+    for repr_ in (0, 1, 2):
+        p = plan.encode(1, 0, repr_)
+        assert p.status == 0
+        idx, _ = plan.decode_indices(p)
+        want = np.concatenate([R.diff(a, b)[0] for a, b in zip(prevs, currs)])
+        assert np.array_equal(idx.cpu().numpy(), want)
+
+
+@pytest.mark.skipif(not have_reference(), reason="oracle/_ref not built")
+def test_config1_16m_matches_reference_bytes(golden):
+    """BASELINE configs[0]: 4096^2, 99%, cluster 64, seed 7 from the reference
+    generator itself; the device body must equal the reference PULP body."""
+    R = reference()
+    prev, curr = R.generate_synthetic([(4096, 4096)], 0.99, 64, 7)
+    ts, prev_d = upload(prev)
+    _, curr_d = upload(curr)
+    plan = make_plan(ts, 400000)
+    plan.bind(0, prev_d)
+    plan.bind(1, curr_d)
+    for r in (0, 1, 2):
+        p = plan.encode(1, 0, r)
+        assert p.n_changes == golden.manifest["config1"]["changes"] == 167772
+        want = R.write_patch_bytes(R.encode(curr, prev, r, IDENTITY))
+        header, body = split_pulp(want)
+        assert p.body[: p.body_bytes].cpu().numpy().tobytes() == body
+        assert len(want) == golden.manifest["config1"]["pulp_nbytes"][f"{r}/0"]
