@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""PULSE encode+apply benchmark (BASELINE.json metric: "encode+apply weight GB/s
+(frac. of HBM peak) at 1/2/4/8 B200; patch MB").
+
+One step = one pass of the hot path over the configured state dict:
+  encode  K1 diff+compaction -> [NCCL size exchange] -> K2 index coding / PULP body
+          -> D2H of the entry table (the PULP header fields)
+  apply   parse + validate + scatter the body into resident weights, in place.
+Steps alternate direction (prev->curr, then curr->prev) so every step does the
+same work on the same resident weights.  value = 2*d bytes of weights per step
+/ step time, whole job (all ranks), max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload qwen2.5-7b]
+  python bench.py --impl reference ...   # the reference CPU path on host cores
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2602_03839_b200.shapes import numel, shard, workload  # noqa: E402
+
+REPR_NAMES = {0: "COO_DOWNSCALED", 1: "COO_INT32", 2: "FLAT_INT32"}
+METRIC = "encode+apply weight GB/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="pulse", choices=["pulse", "reference"])
+    ap.add_argument("--workload", default="qwen2.5-7b")
+    ap.add_argument("--sparsity", type=float, default=0.99)
+    ap.add_argument("--cluster-width", type=int, default=64)
+    ap.add_argument("--repr", type=int, default=0, choices=[0, 1, 2])
+    ap.add_argument("--seed", type=int, default=1002)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-elems", type=int, default=96_000_000)
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------------------------------
+# clocks during the timed region
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# reference CPU path (oracle/_ref: the unmodified reference headers), host cores
+# ------------------------------------------------------------------------------------------
+def numpy_pair(shapes, sparsity, cluster, seed):
+    """Sample input for the CPU legs: log-normal bf16 weights and clustered
+    half-density LSB flips (the reference generator's knobs, numpy RNG)."""
+    rng = np.random.default_rng(seed)
+    prev, curr = [], []
+    for shp in shapes:
+        n = numel(shp)
+        x = np.exp(np.log(0.0117) + rng.standard_normal(n, dtype=np.float32)).astype(np.float32)
+        x[rng.random(n, dtype=np.float32) < 0.5] *= -1
+        u = x.view(np.uint32)
+        b = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)  # RNE to bf16
+        c = b.copy()
+        n_change = int(round((1 - sparsity) * n))
+        starts = rng.integers(0, n, max(1, 2 * n_change // max(1, cluster)))
+        pos = (starts[:, None] + np.arange(cluster)[None, :]).ravel()
+        pos = pos[(pos < n) & (rng.random(pos.size) < 0.5)]
+        pos = np.unique(pos)[:n_change]
+        c[pos] ^= 1
+        prev.append(b)
+        curr.append(c)
+    return prev, curr
+
+
+def time_reference(names, shapes, prev, curr, repr_, steps, warmup):
+    """Times the reference's own hot path on one core: encode (patch.hpp:264,
+    incl. its SHA-256 target hash) + write_patch_bytes + read_patch_bytes +
+    decode(verify=false) (patch.hpp:309).  Returns per-step seconds + parts."""
+    from oracle.oracle import Checkpoint, Tensor, reference, IDENTITY
+    R = reference()
+    hp = R.ckpt_handle(Checkpoint(0, [Tensor(n, s, a) for n, s, a in zip(names, shapes, prev)]))
+    hc = R.ckpt_handle(Checkpoint(1, [Tensor(n, s, a) for n, s, a in zip(names, shapes, curr)]))
+    try:
+        per, parts = [], []
+        for k in range(warmup + steps):
+            a, b = (hp, hc) if k % 2 == 0 else (hc, hp)
+            t, nbytes, changes = R.time_step(a, b, repr_, IDENTITY, verify=False)
+            if k >= warmup:
+                per.append(sum(t[x] for x in ("encode", "write", "read", "decode")))
+                parts.append(t)
+        return per, parts, nbytes, changes
+    finally:
+        R.L.ref_ckpt_free(hp)
+        R.L.ref_ckpt_free(hc)
+
+
+def cpu_sample(tensors, target_elems):
+    """A bounded, representative slice of the workload: whole tensors in name
+    order starting after the embeddings, up to ~target_elems elements."""
+    picked, total = [], 0
+    start = 2 if len(tensors) > 3 else 0
+    for name, shp in tensors[start:]:
+        n = numel(shp)
+        if total and total + n > target_elems:
+            continue
+        picked.append((name, shp))
+        total += n
+        if total >= target_elems * 0.9:
+            break
+    return picked, total
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    tensors = workload(args.workload)
+    picked, total = cpu_sample(tensors, args.cpu_sample_elems)
+    names, shapes = [n for n, _ in picked], [s for _, s in picked]
+    prev, curr = numpy_pair(shapes, args.sparsity, args.cluster_width, args.seed)
+    per, parts, nbytes, changes = time_reference(names, shapes, prev, curr, args.repr, args.steps, args.warmup)
+    sec = statistics.mean(per)
+    value = 2 * total / sec / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16 (bf16 bit patterns)",
+        "data": "synthetic (numpy log-normal bf16, clustered LSB flips)",
+        "config": {"workload": args.workload, "sample_tensors": len(picked), "sample_elements": total,
+                   "sparsity": args.sparsity, "cluster_width": args.cluster_width,
+                   "representation": REPR_NAMES[args.repr], "codec": "identity"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "reference",
+                         "sample": f"{len(picked)} tensors / {total} elements of {args.workload}",
+                         "parts_s": {k: round(statistics.mean(p[k] for p in parts), 4) for k in parts[0]}},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "patch_mb": round(nbytes / 1e6, 3), "changes": changes,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+# the PULSE arm
+# ------------------------------------------------------------------------------------------
+def run_pulse(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_03839_b200 import device as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    tensors = workload(args.workload)
+    d_total = sum(numel(s) for _, s in tensors)
+    bounds = shard(tensors, world)
+    mine = tensors[bounds[rank]:bounds[rank + 1]]
+    sizes = [numel(s) for _, s in mine]
+    D_el = sum(sizes)
+    assert all(n % 8 == 0 for n in sizes), "tensors must keep 16-byte alignment in the arena"
+
+    # ---- resident snapshots (synthetic, generated on device) ----------------------------
+    prev = torch.empty(max(8, D_el), dtype=torch.int16, device=dev)
+    curr = torch.empty_like(prev)
+    w = torch.empty_like(prev)
+    D.synth_base(prev, seed=args.seed + 7919 * rank)
+    n_mut = D.synth_mutate(prev, curr, args.sparsity, args.cluster_width, seed=args.seed + 104729 * rank) if D_el else 0
+    w.copy_(prev)
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    views = lambda buf: [buf[int(offs[i]):int(offs[i + 1])] for i in range(len(sizes))]
+    cap = int(D_el * (1 - args.sparsity) * 1.02) + 65536
+    plan = D.DevicePlan([(n, s[-1]) for n, (_, s) in zip(sizes, mine)], cap)
+    plan.bind(0, views(prev))
+    plan.bind(1, views(curr))
+    plan.bind(2, views(w))
+    patch = plan.new_patch(args.repr)
+    send = torch.zeros(32, dtype=torch.uint8, device=dev)
+    gathered = torch.zeros(32 * world, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    carry_h = torch.zeros(16, dtype=torch.uint8).pin_memory()
+    carry_d = torch.zeros(16, dtype=torch.uint8, device=dev)
+
+    ev = {k: [] for k in ("s0", "s1", "a0", "a1")}
+    state = {"body": 0, "changes": 0}
+
+    def step(k, record=False):
+        cs, ps = (1, 0) if k % 2 == 0 else (0, 1)
+        if record:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        plan.scan(cs, ps, summary_out=send)
+        if record:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(stream)
+        if world > 1:  # size exchange: all ranks' scan summaries (NCCL over NVLink)
+            dist.all_gather_into_tensor(gathered, send)
+            plan.emit(patch, gathered=gathered, n_ranks=world, rank=rank)
+        else:
+            plan.emit(patch)
+        patch.fetch()  # entry table -> host (PULP header fields); syncs
+        carry = None
+        if world > 1 and args.repr == 2:
+            g = gathered.cpu().numpy().view(D.N.SUMMARY_DTYPE)
+            hp, gb = 0, 0
+            for q in range(rank - 1, -1, -1):
+                if g[q]["has_change"]:
+                    hp, gb = 1, int(g[q]["last_gap_base"])
+                    break
+            carry_h.numpy().view(np.uint64)[:] = [hp, gb]
+            carry_d.copy_(carry_h, non_blocking=True)
+            carry = carry_d
+        if record:
+            a0 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+        plan.apply(2, patch, carry=carry)
+        if record:
+            a1 = torch.cuda.Event(enable_timing=True)
+            a1.record(stream)
+            ev["s0"].append(e0); ev["s1"].append(e1); ev["a0"].append(a0); ev["a1"].append(a1)
+        state["body"] = patch.body_bytes
+        state["changes"] = patch.n_changes
+        if patch.status != 0:
+            patch.raise_for_status([n for n, _ in mine])
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for k in range(args.warmup):
+        step(k)
+    # W must equal prev again before the timed loop starts on an even step
+    if args.warmup % 2 == 1:
+        step(args.warmup)
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        t0.record(stream)
+        for k in range(args.steps):
+            step(k, record=True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    scan_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["s0"], ev["s1"]))
+    apply_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["a0"], ev["a1"]))
+
+    # correctness of the final state: W == prev after an even number of steps
+    if args.steps % 2 == 0:
+        ok = bool(torch.equal(w, prev))
+    else:
+        ok = bool(torch.equal(w, curr))
+
+    t_ms = torch.tensor([ms, scan_ms, apply_ms, float(not ok)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        tot = torch.tensor([float(state["body"]), float(state["changes"])], dtype=torch.float64, device=dev)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        body_total, changes_total = tot.tolist()
+    else:
+        body_total, changes_total = float(state["body"]), float(state["changes"])
+    ms_max, scan_max, apply_max, bad = t_ms.tolist()
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, mine, prev, curr, views, world, rank)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        picked, total = cpu_sample(tensors, args.cpu_sample_elems)
+        pn, ps = [n for n, _ in picked], [s for _, s in picked]
+        cp, cc = numpy_pair(ps, args.sparsity, args.cluster_width, args.seed)
+        per, parts, nb, _ = time_reference(pn, ps, cp, cc, args.repr, 2, 1)
+        cpu = {"value": round(2 * total / statistics.mean(per) / 1e9, 4), "unit": "GB/s", "cores": 1,
+               "kind": "reference", "sample": f"{len(picked)} tensors / {total} elements of {args.workload}, "
+                                               "reference encode+write+read+decode(verify=false), 1 thread",
+               "parts_s": {k: round(statistics.mean(p[k] for p in parts), 4) for k in parts[0]}}
+
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        value = 2 * d_total / (ms_max / 1e3) / 1e9
+        # dominant kernel K1: reads both snapshots (4 B/elem) + writes 6 B per change (u32 idx + u16 value)
+        k1_bytes = 4 * D_el + 6 * state["changes"]
+        k1_gbs = k1_bytes / (scan_ms / 1e3) / 1e9
+        n_apply = 7 if args.repr == 0 else 4
+        n_emit = 3 if args.repr == 0 else 2
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u16 (bf16 bit patterns; integer/bitwise path)",
+            "data": "synthetic (device log-normal bf16, clustered half-density LSB flips)",
+            "config": {"workload": args.workload, "tensors": len(tensors), "elements": d_total,
+                       "sparsity": args.sparsity, "cluster_width": args.cluster_width,
+                       "representation": REPR_NAMES[args.repr], "codec": "identity (device body)",
+                       "parallelism": f"tensor-shard x{world}" if world > 1 else "single GPU",
+                       "l2": f"inputs {4 * d_total / 1e9:.1f} GB per step >> 126 MB L2 (no flush needed)"},
+            "frac_of_hbm": round(value / peak, 4),
+            "encode_ms": round(scan_max, 4), "apply_ms": round(apply_max, 4),
+            "patch_mb": round(body_total / 1e6, 3), "changes": int(changes_total),
+            "roofline": {"kernel": "k1_diff_compact", "bound": "hbm", "achieved": round(k1_gbs, 2),
+                         "peak": peak, "unit": "GB/s", "frac": round(k1_gbs / peak, 4), "traffic": None,
+                         "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": k1_bytes},
+            "gpu_launches": (2 + n_emit + n_apply) * args.steps,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "verified": not bool(bad),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, mine, prev, curr, views, world, rank):
+    """End to end through the reference-facing host API (filled in by
+    paper_2602_03839_b200.host once available)."""
+    try:
+        from paper_2602_03839_b200 import host  # noqa: F401
+    except Exception:
+        return None
+    return host.bench_e2e(args, mine, prev, curr, world, rank)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_pulse(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -153,9 +153,11 @@ typedef struct pulse_result {
 
 /* K1: bitwise diff of slot `curr_slot` against `prev_slot` and ordered
  * compaction (decoupled look-back) of every changed element -- the loop at
- * patch.hpp:296-301.  Writes the plan's scan summary (device). */
+ * patch.hpp:296-301.  Writes the plan's scan summary and, when
+ * `dev_summary_out` is non-NULL, a copy of it there (e.g. straight into an
+ * NCCL all-gather send buffer). */
 pulse_status pulse_encode_scan(pulse_plan* plan, uint32_t curr_slot, uint32_t prev_slot,
-                               void* stream);
+                               pulse_scan_summary* dev_summary_out, void* stream);
 /* Device pointer to the plan's pulse_scan_summary (for NCCL all-gather). */
 pulse_scan_summary* pulse_plan_scan_summary(pulse_plan* plan);
 

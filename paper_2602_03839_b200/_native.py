@@ -101,7 +101,7 @@ _SIGS = {
     "pulse_plan_create": (i32, [vp, C.POINTER(TensorGeom), u32, u64, C.POINTER(vp)]),
     "pulse_plan_destroy": (None, [vp]),
     "pulse_plan_bind": (i32, [vp, u32, C.POINTER(vp)]),
-    "pulse_encode_scan": (i32, [vp, u32, u32, vp]),
+    "pulse_encode_scan": (i32, [vp, u32, u32, vp, vp]),
     "pulse_plan_scan_summary": (vp, [vp]),
     "pulse_encode_emit": (i32, [vp, u32, vp, u32, u32, vp, u64, vp, vp, vp]),
     "pulse_apply": (i32, [vp, u32, u32, vp, vp, u32, vp, vp, vp]),

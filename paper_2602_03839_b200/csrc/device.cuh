@@ -96,6 +96,48 @@ __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// ---- mbarrier / TMA bulk-copy helpers (sm_90+ PTX, used on sm_100a) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+// Bulk async copy global -> shared (TMA engine), completion counted in bytes on `bar`.
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// Named barriers for warp-specialised groups (id 0 is __syncthreads).
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 // Unaligned little-endian reads from a byte stream.
 __device__ __forceinline__ uint32_t rd_u16(const uint8_t* p) { return uint32_t(p[0]) | uint32_t(p[1]) << 8; }
 __device__ __forceinline__ uint32_t rd_u32(const uint8_t* p) {
@@ -167,6 +209,38 @@ __device__ __forceinline__ uint64_t lookback(uint64_t* status, uint64_t tile, ui
         const int stop = pmask ? __ffs(pmask) - 1 : 31;
         uint64_t v = lane <= stop ? (s >> 2) : 0;
         // Ordered reduction: higher lanes are earlier tiles.
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint64_t o = __shfl_down_sync(0xffffffffu, v, off);
+            if (lane + off < 32) v = Op::op(o, v);
+        }
+        v = __shfl_sync(0xffffffffu, v, 0);
+        excl = Op::op(v, excl);
+        if (pmask) break;
+        base -= 32;
+    }
+    if (lane == 0) st_relaxed(status + tile, (Op::op(excl, agg) << 2) | kStatPrefix);
+    return excl;
+}
+
+// Look-back for a tile whose aggregate the caller already published (so the
+// tile could be counted on by successors before this warp started waiting).
+template <class Op>
+__device__ __forceinline__ uint64_t lookback_published(uint64_t* status, uint64_t tile, uint64_t agg) {
+    const int lane = threadIdx.x & 31;
+    uint64_t excl = 0;
+    int64_t base = int64_t(tile) - 1;
+    while (true) {
+        const int64_t idx = base - lane;
+        uint64_t s = kStatPrefix;
+        if (idx >= 0) {
+            do {
+                s = ld_relaxed(status + idx);
+            } while ((s & 3) == kStatInvalid);
+        }
+        const uint32_t pmask = __ballot_sync(0xffffffffu, (s & 3) == kStatPrefix);
+        const int stop = pmask ? __ffs(pmask) - 1 : 31;
+        uint64_t v = lane <= stop ? (s >> 2) : 0;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const uint64_t o = __shfl_down_sync(0xffffffffu, v, off);

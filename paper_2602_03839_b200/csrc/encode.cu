@@ -16,6 +16,8 @@
 //                         (patch_file.hpp:76-82), for all three representations
 //                         (patch.hpp:116-174).
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 
 #include "device.cuh"
 #include "internal.hpp"
@@ -26,123 +28,555 @@ namespace dev {
 // =============================================================================================
 // K1
 // =============================================================================================
-__global__ void __launch_bounds__(kThreads, 4)
-k1_diff_compact(const SegDesc* __restrict__ segs, uint32_t n_segs, uint64_t n_tiles,
-                const uint16_t* const* __restrict__ prev_ptrs,
-                const uint16_t* const* __restrict__ curr_ptrs, uint32_t* __restrict__ out_idx,
-                uint16_t* __restrict__ out_val, uint64_t capacity, uint64_t* __restrict__ seg_start,
-                uint64_t* __restrict__ status, unsigned long long* __restrict__ ticket) {
+// Tile = 8192 elements of one segment (16 KiB of each snapshot): 256 threads x
+// 4 x 128-bit vectors per snapshot.  Two schedules share the tile body:
+//   static  persistent grid launched cooperatively (co-residency guaranteed);
+//           CTA b owns tiles b, b+G, b+2G ... and issues the loads of its next
+//           tile before the current tile's look-back, so the look-back latency
+//           hides behind memory traffic.  All CTAs sit at the same iteration,
+//           so the predecessors a look-back needs are being counted concurrently.
+//   ticket  one tile per dynamic ticket (atomic counter), no prefetch; kept as a
+//           fallback when a cooperative launch is unavailable.
+struct TileCtx {
+    const uint16_t* pp;  // prev tile base
+    const uint16_t* cp;  // curr tile base
+    uint32_t si;         // segment
+    uint32_t toff;       // element offset of the tile inside its segment
+    uint32_t nin;        // elements in the tile (<= kTileElems)
+};
+
+__device__ __forceinline__ TileCtx locate_tile(uint64_t tile, const uint32_t* __restrict__ tile_seg,
+                                               const SegDesc* __restrict__ segs,
+                                               const uint16_t* const* __restrict__ prev_ptrs,
+                                               const uint16_t* const* __restrict__ curr_ptrs) {
+    TileCtx c;
+    c.si = tile_seg[tile];
+    const SegDesc sd = segs[c.si];
+    c.toff = uint32_t((tile - sd.tile_start) * kTileElems);
+    c.nin = min(kTileElems, sd.numel - c.toff);
+    c.pp = prev_ptrs[sd.tensor] + sd.elem_off + c.toff;
+    c.cp = curr_ptrs[sd.tensor] + sd.elem_off + c.toff;
+    return c;
+}
+
+__device__ __forceinline__ void load_tile(const TileCtx& c, int tid, uint4 (&a)[4], uint4 (&b)[4]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t e = (uint32_t(j) * kThreads + tid) * 8;
+        if (e + 8 <= c.nin) {
+            a[j] = ld_stream(c.pp + e);
+            b[j] = ld_stream(c.cp + e);
+        } else {
+            uint32_t ta[4] = {0, 0, 0, 0}, tb[4] = {0, 0, 0, 0};
+            for (uint32_t k = 0; k < 8 && e + k < c.nin; ++k) {
+                ta[k >> 1] |= uint32_t(c.pp[e + k]) << ((k & 1) * 16);
+                tb[k >> 1] |= uint32_t(c.cp[e + k]) << ((k & 1) * 16);
+            }
+            a[j] = make_uint4(ta[0], ta[1], ta[2], ta[3]);
+            b[j] = make_uint4(tb[0], tb[1], tb[2], tb[3]);
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t change_mask(const uint4& a, const uint4& b) {
+    const uint32_t w0 = __vcmpne2(a.x, b.x), w1 = __vcmpne2(a.y, b.y);
+    const uint32_t w2 = __vcmpne2(a.z, b.z), w3 = __vcmpne2(a.w, b.w);
+    return (w0 & 1) | ((w0 >> 15) & 2) | ((w1 & 1) << 2) | ((w1 >> 13) & 8) | ((w2 & 1) << 4) |
+           ((w2 >> 11) & 32) | ((w3 & 1) << 6) | ((w3 >> 9) & 128);
+}
+
+__device__ __forceinline__ uint16_t lane_value(const uint4& v, int k) {
+    const uint32_t w = k < 4 ? (k < 2 ? v.x : v.y) : (k < 6 ? v.z : v.w);
+    return uint16_t(w >> ((k & 1) * 16));
+}
+
+struct K1Args {
+    const SegDesc* segs;
+    const uint32_t* tile_seg;
+    uint32_t n_segs;
+    uint64_t n_tiles;
+    const uint16_t* const* prev_ptrs;
+    const uint16_t* const* curr_ptrs;
+    uint32_t* out_idx;
+    uint16_t* out_val;
+    uint64_t capacity;
+    uint64_t* seg_start;
+    uint64_t* status;
+    unsigned long long* ticket;
+};
+
+// Count / order / look-back / write for one loaded tile.  `prefetch` is called
+// after the count is known and before the look-back (issues the next loads).
+template <class Prefetch>
+__device__ __forceinline__ void k1_tile(const K1Args& k, uint64_t tile, const TileCtx& cur, const uint4 (&a)[4],
+                                        const uint4 (&b)[4], uint64_t* s_warp, uint64_t* s_excl,
+                                        Prefetch&& prefetch) {
+    const int tid = threadIdx.x;
+    uint32_t m[4];
+    uint64_t packed = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        m[j] = change_mask(a[j], b[j]);
+        packed |= uint64_t(__popc(m[j])) << (16 * j);
+    }
+    uint64_t tot;
+    const uint64_t ex = block_exclusive<SumOp>(packed, s_warp, tot);
+    const uint64_t count = (tot & 0xFFFF) + ((tot >> 16) & 0xFFFF) + ((tot >> 32) & 0xFFFF) + (tot >> 48);
+    prefetch();
+    const bool seg_first = cur.toff == 0;
+    const bool last = tile == k.n_tiles - 1;
+    if (tid < 32) {
+        uint64_t excl = 0;
+        if (count > 0 || seg_first || last) {
+            excl = lookback<SumOp>(k.status, tile, count);
+        } else if (tid == 0) {
+            st_relaxed(k.status + tile, kStatAggregate);  // aggregate 0; never needs its prefix
+        }
+        if (tid == 0) {
+            *s_excl = excl;
+            if (seg_first) k.seg_start[cur.si] = excl;
+            if (last) k.seg_start[k.n_segs] = excl + count;
+        }
+    }
+    __syncthreads();
+    if (count > 0) {
+        uint64_t base = *s_excl;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t mj = m[j];
+            uint64_t pos = base + ((ex >> (16 * j)) & 0xFFFF);
+            const uint32_t e = cur.toff + (uint32_t(j) * kThreads + tid) * 8;
+            while (mj) {
+                const int q = __ffs(mj) - 1;
+                mj &= mj - 1;
+                if (pos < k.capacity) {
+                    k.out_idx[pos] = e + q;
+                    k.out_val[pos] = lane_value(b[j], q);
+                }
+                ++pos;
+            }
+            base += (tot >> (16 * j)) & 0xFFFF;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 3) k1_static(K1Args k) {
     __shared__ uint64_t s_warp[kWarps];
     __shared__ uint64_t s_excl;
-    __shared__ uint64_t s_tile;
-    __shared__ uint32_t s_seg;
+    const int tid = threadIdx.x;
+    uint64_t tile = blockIdx.x;
+    if (tile >= k.n_tiles) return;
+    TileCtx cur = locate_tile(tile, k.tile_seg, k.segs, k.prev_ptrs, k.curr_ptrs);
+    uint4 a[4], b[4];
+    load_tile(cur, tid, a, b);
+    while (true) {
+        const uint64_t next = tile + gridDim.x;
+        const bool more = next < k.n_tiles;
+        TileCtx nx = cur;
+        if (more) nx = locate_tile(next, k.tile_seg, k.segs, k.prev_ptrs, k.curr_ptrs);
+        uint4 an[4], bn[4];
+        k1_tile(k, tile, cur, a, b, s_warp, &s_excl, [&] {
+            if (more) load_tile(nx, tid, an, bn);
+        });
+        if (!more) break;
+        __syncthreads();  // s_excl / s_warp reuse
+        cur = nx;
+        tile = next;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            a[j] = an[j];
+            b[j] = bn[j];
+        }
+    }
+}
 
+__global__ void __launch_bounds__(kThreads, 4) k1_ticket(K1Args k) {
+    __shared__ uint64_t s_warp[kWarps];
+    __shared__ uint64_t s_excl, s_tile;
     const int tid = threadIdx.x;
     while (true) {
-        if (tid == 0) {
-            const uint64_t t = atomicAdd(ticket, 1ull);
-            s_tile = t;
-            if (t < n_tiles) {
-                // segment containing tile t: last seg with tile_start <= t
-                uint32_t lo = 0, hi = n_segs;
-                while (hi - lo > 1) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (segs[mid].tile_start <= t) lo = mid; else hi = mid;
-                }
-                s_seg = lo;
-            }
-        }
+        if (tid == 0) s_tile = atomicAdd(k.ticket, 1ull);
         __syncthreads();
         const uint64_t tile = s_tile;
-        if (tile >= n_tiles) break;
-        const uint32_t si = s_seg;
-        const SegDesc sd = segs[si];
-        const uint64_t tin = tile - sd.tile_start;           // tile within segment
-        const uint32_t toff = uint32_t(tin * kTileElems);    // element offset in segment
-        const uint32_t nin = min(kTileElems, sd.numel - toff);
-        const uint16_t* pp = prev_ptrs[sd.tensor] + sd.elem_off + toff;
-        const uint16_t* cp = curr_ptrs[sd.tensor] + sd.elem_off + toff;
-
-        // ---- stream both snapshots: 4 x 128-bit loads each, all in flight ----
+        if (tile >= k.n_tiles) break;
+        const TileCtx cur = locate_tile(tile, k.tile_seg, k.segs, k.prev_ptrs, k.curr_ptrs);
         uint4 a[4], b[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t e = (uint32_t(j) * kThreads + tid) * 8;
-            if (e + 8 <= nin) {
-                a[j] = ld_stream(pp + e);
-                b[j] = ld_stream(cp + e);
-            } else {
-                uint16_t ta[8], tb[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const bool in = e + k < nin;
-                    ta[k] = in ? pp[e + k] : 0;
-                    tb[k] = in ? cp[e + k] : 0;
-                }
-                a[j] = make_uint4(ta[0] | uint32_t(ta[1]) << 16, ta[2] | uint32_t(ta[3]) << 16,
-                                  ta[4] | uint32_t(ta[5]) << 16, ta[6] | uint32_t(ta[7]) << 16);
-                b[j] = make_uint4(tb[0] | uint32_t(tb[1]) << 16, tb[2] | uint32_t(tb[3]) << 16,
-                                  tb[4] | uint32_t(tb[5]) << 16, tb[6] | uint32_t(tb[7]) << 16);
-            }
-        }
-
-        // ---- bitwise compare: 8-bit change mask per vector ----
-        uint32_t m[4];
-        uint64_t packed = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t w0 = __vcmpne2(a[j].x, b[j].x), w1 = __vcmpne2(a[j].y, b[j].y);
-            const uint32_t w2 = __vcmpne2(a[j].z, b[j].z), w3 = __vcmpne2(a[j].w, b[j].w);
-            m[j] = (w0 & 1) | ((w0 >> 15) & 2) | ((w1 & 1) << 2) | ((w1 >> 13) & 8) |
-                   ((w2 & 1) << 4) | ((w2 >> 11) & 32) | ((w3 & 1) << 6) | ((w3 >> 9) & 128);
-            packed |= uint64_t(__popc(m[j])) << (16 * j);
-        }
-
-        // ---- block scan of the four per-vector counts (packed 4 x 16 bit) ----
-        uint64_t tot;
-        const uint64_t ex = block_exclusive<SumOp>(packed, s_warp, tot);
-        const uint64_t count = (tot & 0xFFFF) + ((tot >> 16) & 0xFFFF) + ((tot >> 32) & 0xFFFF) + (tot >> 48);
-
-        // ---- decoupled look-back for the tile's global offset ----
-        const bool seg_first = tin == 0;
-        const bool last = tile == n_tiles - 1;
-        if (tid < 32) {
-            uint64_t excl = 0;
-            if (count > 0 || seg_first || last) {
-                excl = lookback<SumOp>(status, tile, count);
-            } else if (tid == 0) {
-                st_relaxed(status + tile, kStatAggregate);  // aggregate 0, never needs its prefix
-            }
-            if (tid == 0) {
-                s_excl = excl;
-                if (seg_first) seg_start[si] = excl;
-                if (last) seg_start[n_segs] = excl + count;
-            }
-        }
+        load_tile(cur, tid, a, b);
+        k1_tile(k, tile, cur, a, b, s_warp, &s_excl, [] {});
         __syncthreads();
+    }
+}
 
-        // ---- write the compacted (index, value) pairs in element order ----
-        if (count > 0) {
-            uint64_t base = s_excl;
+// ---------------------------------------------------------------------------------------------
+// K1 (default): warp-specialised, TMA-fed.  One CTA per SM.
+//   warp 8      producer: takes 64 Ki-element tickets, streams each as 8
+//               sub-tiles of 8192 elements (16 KiB prev + 16 KiB curr) into a
+//               4-stage shared-memory ring with cp.async.bulk + mbarriers.
+//   warps 0-7   consumers: bitwise compare from shared memory, ordered
+//               compaction into a per-ticket staging buffer, publish the
+//               ticket aggregate as soon as the ticket is counted.
+//   warps 9-12  look-back group: decoupled look-back for a counted ticket
+//               (warp 9, 4 status words per lane per round), then a coalesced
+//               flush of the staged (index, value) pairs -- overlapped with the
+//               consumers streaming the next ticket (double-buffered staging).
+// A ticket is taken only after the previous one is fully issued and its
+// aggregate depends on nothing but its own data, so look-backs never wait on
+// a ticket held by a stalled CTA.
+// ---------------------------------------------------------------------------------------------
+namespace tma {
+constexpr int kStages = 4;
+constexpr uint32_t kSubElems = 8192;                 // elements per stage
+constexpr uint32_t kTicketElemsT = ::pulse::dev::kTicketElems;  // elements per ticket
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;      // 256
+constexpr int kProducerWarp = kConsumerWarps;        // warp 8
+constexpr int kLbWarps = 4;                          // warps 9..12
+constexpr int kLbFirst = kConsumerWarps + 1;
+constexpr int kThreadsTotal = (kConsumerWarps + 1 + kLbWarps) * 32;  // 416
+constexpr uint32_t kStageCap = 8192;                 // staged entries per ticket buffer
+constexpr uint32_t kBarConsumers = 1, kBarLb = 2;    // named barrier ids
+
+struct StageDesc {
+    uint64_t tile;          // ticket id, ~0 = end of stream
+    const uint16_t* pp;     // sub-tile bases (for the < 8-element tail)
+    const uint16_t* cp;
+    uint32_t si, toff;      // segment, element offset of the ticket in the segment
+    uint32_t sub, n_sub;    // sub-tile index within the ticket
+    uint32_t elems;         // elements in this sub-tile
+    uint32_t vec_bytes;     // bytes delivered by TMA (multiple of 16)
+};
+
+struct TicketInfo {
+    uint64_t tile;
+    uint32_t si, toff, count, n_sub;
+};
+
+struct Smem {
+    uint4 prev[kStages][kSubElems / 8];
+    uint4 curr[kStages][kSubElems / 8];
+    uint16_t st_idx[2][kStageCap];
+    uint16_t st_val[2][kStageCap];
+    StageDesc desc[kStages];
+    TicketInfo info[2];
+    uint64_t full[kStages], empty[kStages];
+    uint64_t tk_full[2], tk_empty[2];
+    uint32_t warp_tot[2][kConsumerWarps];
+    uint32_t warp_tot_hi[2][kConsumerWarps];
+    uint32_t lb_warp_tot[kLbWarps];
+    uint32_t lb_run;
+    uint64_t lb_G;
+};
+}  // namespace tma
+
+// Look-back with 4 status words per lane per round (128 predecessors).
+__device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t tile, uint64_t agg) {
+    const int lane = threadIdx.x & 31;
+    uint64_t excl = 0;
+    int64_t base = int64_t(tile) - 1;  // newest predecessor not yet consumed
+    while (true) {
+        uint64_t w[4];
+        bool stop_here = false;
+        int stop_k = 4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t idx = base - (lane * 4 + k);
+            uint64_t v = kStatPrefix;  // before tile 0: identity prefix
+            if (idx >= 0) {
+                do {
+                    v = ld_relaxed(status + idx);
+                } while ((v & 3) == kStatInvalid);
+            }
+            w[k] = v;
+            if (!stop_here && (v & 3) == kStatPrefix) {
+                stop_here = true;
+                stop_k = k;
+            }
+        }
+        const uint32_t pmask = __ballot_sync(0xffffffffu, stop_here);
+        const int stop_lane = pmask ? __ffs(pmask) - 1 : 32;
+        uint64_t v = 0;
+        if (lane < stop_lane) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v += w[k] >> 2;
+        } else if (lane == stop_lane) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v += k <= stop_k ? (w[k] >> 2) : 0;
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        excl += v;
+        if (pmask) break;
+        base -= 128;
+    }
+    if (lane == 0) st_relaxed(status + tile, ((excl + agg) << 2) | kStatPrefix);
+    return excl;
+}
+
+__global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
+    using namespace tma;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&S.full[i], 1);
+            mbar_init(&S.empty[i], kConsumerWarps);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&S.tk_full[i], 1);
+            mbar_init(&S.tk_empty[i], 1);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == kProducerWarp) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            while (true) {
+                const uint64_t tile = atomicAdd(k.ticket, 1ull);
+                if (tile >= k.n_tiles) {
+                    mbar_wait(&S.empty[stage], phase ^ 1);
+                    S.desc[stage].tile = ~0ull;
+                    mbar_arrive(&S.full[stage]);
+                    break;
+                }
+                const uint32_t si = k.tile_seg[tile];
+                const SegDesc sd = k.segs[si];
+                const uint32_t toff = uint32_t((tile - sd.ticket_start) * kTicketElemsT);
+                const uint32_t nin = min(kTicketElemsT, sd.numel - toff);
+                const uint16_t* pp = k.prev_ptrs[sd.tensor] + sd.elem_off + toff;
+                const uint16_t* cp = k.curr_ptrs[sd.tensor] + sd.elem_off + toff;
+                const uint32_t n_sub = (nin + kSubElems - 1) / kSubElems;
+                for (uint32_t sub = 0; sub < n_sub; ++sub) {
+                    mbar_wait(&S.empty[stage], phase ^ 1);
+                    StageDesc& d = S.desc[stage];
+                    d.tile = tile;
+                    d.si = si;
+                    d.toff = toff;
+                    d.sub = sub;
+                    d.n_sub = n_sub;
+                    d.elems = min(kSubElems, nin - sub * kSubElems);
+                    d.pp = pp + sub * kSubElems;
+                    d.cp = cp + sub * kSubElems;
+                    d.vec_bytes = (d.elems * 2) & ~15u;
+                    if (d.vec_bytes) {
+                        mbar_arrive_tx(&S.full[stage], 2 * d.vec_bytes);
+                        tma_load_1d(S.prev[stage], d.pp, d.vec_bytes, &S.full[stage]);
+                        tma_load_1d(S.curr[stage], d.cp, d.vec_bytes, &S.full[stage]);
+                    } else {
+                        mbar_arrive(&S.full[stage]);
+                    }
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    if (warp < kConsumerWarps) {
+        // ------------------------------------------------------------ consumers
+        int stage = 0, buf = 0;
+        uint32_t phase = 0, bphase = 0;
+        uint32_t count = 0;
+        while (true) {
+            mbar_wait(&S.full[stage], phase);
+            const StageDesc d = S.desc[stage];
+            if (d.tile == ~0ull) {
+                if (tid == 0) {
+                    mbar_wait(&S.tk_empty[buf], bphase ^ 1);
+                    S.info[buf].tile = ~0ull;
+                    mbar_arrive(&S.tk_full[buf]);
+                }
+                break;
+            }
+            if (d.sub == 0) {
+                mbar_wait(&S.tk_empty[buf], bphase ^ 1);  // staging buffer flushed by the look-back group
+                count = 0;
+            }
+            // 4 vectors of 8 elements per thread: v = tid + 256*j
+            uint32_t m[4];
+            uint4 cv[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                uint32_t mj = m[j];
-                uint64_t pos = base + ((ex >> (16 * j)) & 0xFFFF);
-                const uint32_t e = (uint32_t(j) * kThreads + tid) * 8;
-                while (mj) {
-                    const int k = __ffs(mj) - 1;
-                    mj &= mj - 1;
-                    if (pos < capacity) {
-                        const uint32_t w = k < 4 ? (k < 2 ? b[j].x : b[j].y) : (k < 6 ? b[j].z : b[j].w);
-                        out_idx[pos] = toff + e + k;
-                        out_val[pos] = uint16_t(w >> ((k & 1) * 16));
+                const uint32_t v = tid + kConsumers * j;
+                const uint32_t e = v * 8;
+                uint4 a = make_uint4(0, 0, 0, 0), b = a;
+                if ((v + 1) * 16 <= d.vec_bytes) {
+                    a = S.prev[stage][v];
+                    b = S.curr[stage][v];
+                } else if (e < d.elems) {  // < 8-element tail, straight from global
+                    uint32_t ta[4] = {0, 0, 0, 0}, tb[4] = {0, 0, 0, 0};
+                    for (uint32_t q = 0; q < 8 && e + q < d.elems; ++q) {
+                        ta[q >> 1] |= uint32_t(d.pp[e + q]) << ((q & 1) * 16);
+                        tb[q >> 1] |= uint32_t(d.cp[e + q]) << ((q & 1) * 16);
+                    }
+                    a = make_uint4(ta[0], ta[1], ta[2], ta[3]);
+                    b = make_uint4(tb[0], tb[1], tb[2], tb[3]);
+                }
+                m[j] = change_mask(a, b);
+                cv[j] = b;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[stage]);  // stage may be refilled
+            // order: element e = 8*(tid + 256 j) + q  ->  (j, tid, q) lexicographic;
+            // one scan per j across the 256 consumers, as two 16-bit packed pairs
+            uint32_t lo = __popc(m[0]) | (__popc(m[1]) << 16), hi = __popc(m[2]) | (__popc(m[3]) << 16);
+            uint32_t ilo = lo, ihi = hi;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t a1 = __shfl_up_sync(0xffffffffu, ilo, off);
+                const uint32_t a2 = __shfl_up_sync(0xffffffffu, ihi, off);
+                if (lane >= off) { ilo += a1; ihi += a2; }
+            }
+            const int wb = d.sub & 1;
+            if (lane == 31) {
+                S.warp_tot[wb][warp] = ilo;  // fields j0 | j1
+                S.warp_tot_hi[wb][warp] = ihi;  // fields j2 | j3
+            }
+            named_sync(kBarConsumers, kConsumers);
+            uint32_t blo = 0, bhi = 0, tlo = 0, thi = 0;
+#pragma unroll
+            for (int w = 0; w < kConsumerWarps; ++w) {
+                const uint32_t xl = S.warp_tot[wb][w], xh = S.warp_tot_hi[wb][w];
+                if (w < warp) { blo += xl; bhi += xh; }
+                tlo += xl;
+                thi += xh;
+            }
+            const uint32_t exlo = blo + ilo - lo, exhi = bhi + ihi - hi;
+            const uint32_t t0 = tlo & 0xFFFF, t1 = tlo >> 16, t2 = thi & 0xFFFF, t3 = thi >> 16;
+            const uint32_t base_j[4] = {0, t0, t0 + t1, t0 + t1 + t2};
+            const uint32_t ex_j[4] = {exlo & 0xFFFF, exlo >> 16, exhi & 0xFFFF, exhi >> 16};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t pos = count + base_j[j] + ex_j[j];
+                uint32_t mm = m[j];
+                const uint32_t e = d.sub * kSubElems + (tid + kConsumers * j) * 8;
+                while (mm) {
+                    const int q = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    if (pos < kStageCap) {
+                        S.st_idx[buf][pos] = uint16_t(e + q);
+                        S.st_val[buf][pos] = lane_value(cv[j], q);
                     }
                     ++pos;
                 }
-                base += (tot >> (16 * j)) & 0xFFFF;
+            }
+            count += t0 + t1 + t2 + t3;
+            if (d.sub + 1 == d.n_sub) {
+                // ticket fully counted: publish its aggregate now, hand it to the look-back group
+                named_sync(kBarConsumers, kConsumers);  // staging writes complete
+                if (tid == 0) {
+                    if (d.tile == 0) st_relaxed(k.status, (uint64_t(count) << 2) | kStatPrefix);
+                    else st_relaxed(k.status + d.tile, (uint64_t(count) << 2) | kStatAggregate);
+                    TicketInfo& ti = S.info[buf];
+                    ti.tile = d.tile;
+                    ti.si = d.si;
+                    ti.toff = d.toff;
+                    ti.count = count;
+                    ti.n_sub = d.n_sub;
+                    mbar_arrive(&S.tk_full[buf]);
+                }
+                if (++buf == 2) {
+                    buf = 0;
+                    bphase ^= 1;
+                }
+            }
+            if (++stage == kStages) {
+                stage = 0;
+                phase ^= 1;
             }
         }
-        __syncthreads();
+        return;
+    }
+
+    // ---------------------------------------------------------------- look-back group
+    {
+        const int lt = tid - kLbFirst * 32;  // 0..127
+        int buf = 0;
+        uint32_t bphase = 0;
+        while (true) {
+            mbar_wait(&S.tk_full[buf], bphase);
+            const TicketInfo ti = S.info[buf];
+            if (ti.tile == ~0ull) break;
+            const SegDesc sd = k.segs[ti.si];
+            const bool seg_first = ti.toff == 0;
+            const bool last = ti.tile == k.n_tiles - 1;
+            if (warp == kLbFirst) {
+                uint64_t G = 0;
+                if ((ti.count > 0 || seg_first || last) && ti.tile > 0)
+                    G = lookback_wide(k.status, ti.tile, ti.count);
+                if (lane == 0) {
+                    S.lb_G = G;
+                    if (seg_first) k.seg_start[ti.si] = G;
+                    if (last) k.seg_start[k.n_segs] = G + ti.count;
+                }
+            }
+            named_sync(kBarLb, kLbWarps * 32);
+            const uint64_t G = S.lb_G;
+            if (ti.count <= kStageCap) {
+                for (uint32_t q = lt; q < ti.count; q += kLbWarps * 32) {
+                    if (G + q < k.capacity) {
+                        k.out_idx[G + q] = ti.toff + S.st_idx[buf][q];
+                        k.out_val[G + q] = S.st_val[buf][q];
+                    }
+                }
+            } else {
+                // dense ticket (> kStageCap changes): re-stream it from global memory
+                const uint16_t* pp = k.prev_ptrs[sd.tensor] + sd.elem_off + ti.toff;
+                const uint16_t* cp = k.curr_ptrs[sd.tensor] + sd.elem_off + ti.toff;
+                const uint32_t nin = min(kTicketElems, sd.numel - ti.toff);
+                if (lt == 0) S.lb_run = 0;
+                named_sync(kBarLb, kLbWarps * 32);
+                for (uint32_t e0 = 0; e0 < nin; e0 += kLbWarps * 32 * 8) {
+                    const uint32_t e = e0 + lt * 8;
+                    uint32_t mm = 0;
+                    uint16_t vals[8];
+                    for (uint32_t q = 0; q < 8 && e + q < nin; ++q) {
+                        vals[q] = cp[e + q];
+                        if (vals[q] != pp[e + q]) mm |= 1u << q;
+                    }
+                    uint32_t inc = __popc(mm);
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
+                        if (lane >= off) inc += o;
+                    }
+                    if (lane == 31) S.lb_warp_tot[warp - kLbFirst] = inc;
+                    named_sync(kBarLb, kLbWarps * 32);
+                    uint32_t before = 0, all = 0;
+                    for (int w = 0; w < kLbWarps; ++w) {
+                        if (w < warp - kLbFirst) before += S.lb_warp_tot[w];
+                        all += S.lb_warp_tot[w];
+                    }
+                    uint64_t pos = G + S.lb_run + before + inc - __popc(mm);
+                    while (mm) {
+                        const int q = __ffs(mm) - 1;
+                        mm &= mm - 1;
+                        if (pos < k.capacity) {
+                            k.out_idx[pos] = ti.toff + e + q;
+                            k.out_val[pos] = vals[q];
+                        }
+                        ++pos;
+                    }
+                    named_sync(kBarLb, kLbWarps * 32);
+                    if (lt == 0) S.lb_run += all;
+                    named_sync(kBarLb, kLbWarps * 32);
+                }
+            }
+            named_sync(kBarLb, kLbWarps * 32);  // flush done before the buffer is reused
+            if (lt == 0) mbar_arrive(&S.tk_empty[buf]);
+            if (++buf == 2) {
+                buf = 0;
+                bphase ^= 1;
+            }
+        }
     }
 }
 
@@ -151,7 +585,7 @@ k1_diff_compact(const SegDesc* __restrict__ segs, uint32_t n_segs, uint64_t n_ti
 __global__ void k1_finalize(const SegDesc* __restrict__ segs, uint32_t n_segs,
                             const uint64_t* __restrict__ numel, const uint64_t* __restrict__ seg_start,
                             const uint32_t* __restrict__ idx32, uint64_t capacity,
-                            pulse_scan_summary* out) {
+                            pulse_scan_summary* out, pulse_scan_summary* copy_out) {
     if (threadIdx.x != 0) return;
     const uint64_t n = seg_start[n_segs];
     pulse_scan_summary s;
@@ -166,6 +600,7 @@ __global__ void k1_finalize(const SegDesc* __restrict__ segs, uint32_t n_segs,
         s.last_gap_base = numel[sd.tensor] - (sd.elem_off + idx32[i]);
     }
     *out = s;
+    if (copy_out) *copy_out = s;
 }
 
 // =============================================================================================
@@ -608,26 +1043,57 @@ int sm_count() {
     return g_sms;
 }
 
-static int k1_grid() {
-    static int blocks = 0;
-    if (!blocks) {
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_diff_compact, kThreads, 0);
-        if (per_sm <= 0) per_sm = 1;
-        blocks = per_sm * sm_count();
+// PULSE_K1 = tma (default) | static | ticket
+static int k1_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PULSE_K1");
+        const std::string s = e ? e : "tma";
+        v = s == "ticket" ? 1 : s == "static" ? 2 : 0;
     }
-    return blocks;
+    return v;
 }
 
-void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot, cudaStream_t s) {
+void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot, pulse_scan_summary* copy_out,
+                        cudaStream_t s) {
     // status words + ticket must start at zero each launch
     cudaMemsetAsync(p.k1_status, 0, p.n_tiles * sizeof(uint64_t), s);
     cudaMemsetAsync(p.counters, 0, 8 * sizeof(uint64_t), s);
-    const uint64_t grid = std::min<uint64_t>(uint64_t(k1_grid()), std::max<uint64_t>(1, p.n_tiles));
-    k1_diff_compact<<<unsigned(grid), kThreads, 0, s>>>(
-        p.segs, p.n_segs, p.n_tiles, p.slot[prev_slot], p.slot[curr_slot], p.idx32, p.val16, p.cap,
-        p.seg_start, p.k1_status, reinterpret_cast<unsigned long long*>(p.counters));
-    k1_finalize<<<1, 32, 0, s>>>(p.segs, p.n_segs, p.numel, p.seg_start, p.idx32, p.cap, p.scan);
+    K1Args k{p.segs, p.tile_seg, p.n_segs, p.n_tiles, p.slot[prev_slot], p.slot[curr_slot], p.idx32, p.val16,
+             p.cap, p.seg_start, p.k1_status, reinterpret_cast<unsigned long long*>(p.counters)};
+    if (p.n_tiles > 0) {
+        static int per_sm_static = 0, per_sm_ticket = 0;
+        if (!per_sm_static) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_static, k1_static, kThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ticket, k1_ticket, kThreads, 0);
+        }
+        bool launched = false;
+        if (k1_variant() == 0 && p.tma_tiles > 0) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(tma::Smem)));
+                attr = true;
+            }
+            K1Args kt = k;
+            kt.n_tiles = p.tma_tiles;
+            kt.tile_seg = p.tma_tile_seg;
+            const uint64_t grid = std::min<uint64_t>(uint64_t(sm_count()), p.tma_tiles);
+            k1_tma<<<unsigned(grid), tma::kThreadsTotal, sizeof(tma::Smem), s>>>(kt);
+            launched = true;
+        }
+        if (!launched && k1_variant() == 2 && per_sm_static > 0) {
+            const uint64_t grid = std::min<uint64_t>(uint64_t(per_sm_static) * sm_count(), p.n_tiles);
+            void* args[] = {&k};
+            launched = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k1_static), dim3(unsigned(grid)),
+                                                   dim3(kThreads), args, 0, s) == cudaSuccess;
+            if (!launched) cudaGetLastError();  // clear, fall back to tickets
+        }
+        if (!launched) {
+            const uint64_t grid = std::min<uint64_t>(uint64_t(std::max(1, per_sm_ticket)) * sm_count(), p.n_tiles);
+            k1_ticket<<<unsigned(grid), kThreads, 0, s>>>(k);
+        }
+    }
+    k1_finalize<<<1, 32, 0, s>>>(p.segs, p.n_segs, p.numel, p.seg_start, p.idx32, p.cap, p.scan, copy_out);
 }
 
 static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, bool validate_args,

@@ -13,7 +13,7 @@
 namespace pulse {
 namespace dev {
 
-// K1 tile: 8192 bf16 of each snapshot (16 KiB + 16 KiB); 256 threads x 4 x 128-bit loads.
+// K1 tile: 8192 bf16 of each snapshot (16 KiB + 16 KiB) inside one segment.
 constexpr uint32_t kTileElems = 8192;
 // Segments split tensors so that a compacted u32 index (relative to the
 // segment) always fits; tiles never straddle segments (nor tensors).
@@ -26,11 +26,13 @@ constexpr uint32_t kParseBytes = 16;
 constexpr uint32_t kParseTile = 256 * kParseBytes;
 
 struct SegDesc {
-    uint64_t elem_off;    // element offset of the segment inside its tensor
-    uint64_t tile_start;  // first global K1 tile id
-    uint32_t tensor;      // tensor index in the plan
-    uint32_t numel;       // elements in the segment (<= 2^31)
+    uint64_t elem_off;     // element offset of the segment inside its tensor
+    uint64_t tile_start;   // first global K1 tile id (8192-element tiles)
+    uint64_t ticket_start; // first global K1 ticket id (65536-element TMA tickets)
+    uint32_t tensor;       // tensor index in the plan
+    uint32_t numel;        // elements in the segment (<= 2^31)
 };
+constexpr uint32_t kTicketElems = 65536;
 
 // Per-tensor encode layout (written by the layout kernel).
 struct TensorLayout {
@@ -62,6 +64,9 @@ struct PlanDev {
     uint32_t n_tensors, n_segs;
     uint64_t n_tiles, cap;
     const SegDesc* segs;
+    const uint32_t* tile_seg;   // [n_tiles] segment of each K1 tile
+    uint64_t tma_tiles;         // number of 65536-element tickets
+    const uint32_t* tma_tile_seg;  // [tma_tiles] segment of each ticket
     const uint32_t* seg_first;  // [T+1] first segment of each tensor
     const uint64_t* numel;      // [T]
     const uint64_t* cols;       // [T]
@@ -102,7 +107,8 @@ struct PlanDev {
 };
 
 // ---- launchers (stream-ordered, no host sync) -------------------------------------------
-void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot, cudaStream_t s);
+void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot, pulse_scan_summary* copy_out,
+                        cudaStream_t s);
 void launch_encode_emit(const PlanDev& p, uint32_t repr, const pulse_scan_summary* gathered,
                         uint32_t n_ranks, uint32_t rank, uint8_t* body, uint64_t body_cap,
                         pulse_patch_entry* entries, pulse_result* result, cudaStream_t s);

@@ -85,7 +85,7 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
     // segments (<= 2^31 elements) and K1 tiles
     std::vector<SegDesc> segs;
     std::vector<uint32_t> seg_first(n_tensors + 1);
-    uint64_t tiles = 0;
+    uint64_t tiles = 0, tickets = 0;
     for (uint32_t t = 0; t < n_tensors; ++t) {
         const uint64_t n = tensors[t].numel;
         if (n == 0 || tensors[t].cols == 0 || n % tensors[t].cols != 0) {
@@ -97,9 +97,11 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
             SegDesc d;
             d.elem_off = off;
             d.tile_start = tiles;
+            d.ticket_start = tickets;
             d.tensor = t;
             d.numel = uint32_t(std::min<uint64_t>(kSegElems, n - off));
             tiles += (d.numel + kTileElems - 1) / kTileElems;
+            tickets += (d.numel + kTicketElems - 1) / kTicketElems;
             segs.push_back(d);
         }
     }
@@ -109,6 +111,7 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
     p.n_tensors = n_tensors;
     p.n_segs = uint32_t(segs.size());
     p.n_tiles = tiles;
+    p.tma_tiles = tickets;
     p.cap = std::max<uint64_t>(max_changes, 1);
     const uint64_t T = n_tensors, S = segs.size(), cap = p.cap;
     const uint64_t n_chunks = cap / kChunkEntries + 2;
@@ -117,10 +120,10 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
 
     auto& o = plan->owned;
     cudaError_t e = cudaSuccess;
-    SegDesc* segs_d; uint32_t* first_d; uint64_t *numel_d, *cols_d;
+    SegDesc* segs_d; uint32_t* first_d; uint64_t *numel_d, *cols_d; uint32_t* tile_seg_d; uint32_t* ticket_seg_d;
     SegDesc* id_segs_d; uint32_t* id_first_d;
 #define A(ptr, n) if (e == cudaSuccess) e = dalloc(o, &(ptr), (n))
-    A(segs_d, S); A(first_d, T + 1); A(numel_d, T); A(cols_d, T);
+    A(segs_d, S); A(first_d, T + 1); A(numel_d, T); A(cols_d, T); A(tile_seg_d, tiles); A(ticket_seg_d, tickets);
     for (int s = 0; s < PULSE_MAX_SLOTS; ++s) { uint16_t** sp = nullptr; A(sp, T); p.slot[s] = sp; }
     A(p.idx32, cap); A(p.val16, cap); A(p.seg_start, S + 1); A(p.k1_status, tiles + 1);
     A(p.counters, 8); A(p.scan, 1); A(p.chunk_esc, n_chunks); A(p.chunk_pre, n_chunks);
@@ -135,6 +138,8 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
         return cuda_fail(e, "plan allocation");
     }
     p.segs = segs_d;
+    p.tile_seg = tile_seg_d;
+    p.tma_tile_seg = ticket_seg_d;
     p.seg_first = first_d;
     p.numel = numel_d;
     p.cols = cols_d;
@@ -147,10 +152,24 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
     for (uint32_t t = 0; t < n_tensors; ++t) {
         numel[t] = tensors[t].numel;
         cols[t] = tensors[t].cols;
-        id_segs[t] = SegDesc{0, 0, t, 0};
+        id_segs[t] = SegDesc{0, 0, 0, t, 0};
         id_first[t] = t;
     }
     id_first[T] = uint32_t(T);
+    std::vector<uint32_t> tile_seg(tiles);
+    for (uint32_t si = 0; si < S; ++si) {
+        const uint64_t t0 = segs[si].tile_start;
+        const uint64_t t1 = si + 1 < S ? segs[si + 1].tile_start : tiles;
+        for (uint64_t t = t0; t < t1; ++t) tile_seg[t] = si;
+    }
+    cudaMemcpy(tile_seg_d, tile_seg.data(), tiles * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    std::vector<uint32_t> ticket_seg(tickets);
+    for (uint32_t si = 0; si < S; ++si) {
+        const uint64_t t0 = segs[si].ticket_start;
+        const uint64_t t1 = si + 1 < S ? segs[si + 1].ticket_start : tickets;
+        for (uint64_t t = t0; t < t1; ++t) ticket_seg[t] = si;
+    }
+    cudaMemcpy(ticket_seg_d, ticket_seg.data(), tickets * sizeof(uint32_t), cudaMemcpyHostToDevice);
     cudaMemcpy(segs_d, segs.data(), S * sizeof(SegDesc), cudaMemcpyHostToDevice);
     cudaMemcpy(first_d, seg_first.data(), (T + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice);
     cudaMemcpy(numel_d, numel.data(), T * sizeof(uint64_t), cudaMemcpyHostToDevice);
@@ -181,12 +200,13 @@ pulse_status pulse_plan_bind(pulse_plan* plan, uint32_t slot, const void* const*
     return PULSE_OK;
 }
 
-pulse_status pulse_encode_scan(pulse_plan* plan, uint32_t curr_slot, uint32_t prev_slot, void* stream) {
+pulse_status pulse_encode_scan(pulse_plan* plan, uint32_t curr_slot, uint32_t prev_slot,
+                               pulse_scan_summary* dev_summary_out, void* stream) {
     if (!plan || curr_slot >= PULSE_MAX_SLOTS || prev_slot >= PULSE_MAX_SLOTS ||
         !plan->bound[curr_slot] || !plan->bound[prev_slot])
         return fail(PULSE_E_ARGUMENT, "encode_scan: unbound slot");
     cudaSetDevice(plan->device);
-    launch_encode_scan(plan->dev, curr_slot, prev_slot, static_cast<cudaStream_t>(stream));
+    launch_encode_scan(plan->dev, curr_slot, prev_slot, dev_summary_out, static_cast<cudaStream_t>(stream));
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "encode_scan launch");
 }

@@ -132,8 +132,10 @@ class DevicePlan:
                            torch.zeros(72, dtype=torch.uint8, device=dev))
 
     # ---- encode -------------------------------------------------------------------------
-    def scan(self, curr_slot: int, prev_slot: int, stream=None):
-        N.check(N.lib.pulse_encode_scan(self._plan, curr_slot, prev_slot, _stream_ptr(stream)))
+    def scan(self, curr_slot: int, prev_slot: int, summary_out: torch.Tensor | None = None, stream=None):
+        """K1.  `summary_out` (32-byte uint8 device tensor) receives a copy of the
+        pulse_scan_summary, e.g. an NCCL all-gather send buffer."""
+        N.check(N.lib.pulse_encode_scan(self._plan, curr_slot, prev_slot, _ptr(summary_out), _stream_ptr(stream)))
 
     def scan_summary_ptr(self) -> int:
         return N.lib.pulse_plan_scan_summary(self._plan)
@@ -148,7 +150,7 @@ class DevicePlan:
                patch: DevicePatch | None = None, stream=None, fetch=True) -> DevicePatch:
         patch = patch or self.new_patch(representation)
         patch.representation = representation
-        self.scan(curr_slot, prev_slot, stream)
+        self.scan(curr_slot, prev_slot, stream=stream)
         self.emit(patch, stream=stream)
         if fetch:
             patch.fetch(stream)

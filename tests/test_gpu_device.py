@@ -148,3 +148,22 @@ def test_config1_16m_matches_reference_bytes(golden):
         header, body = split_pulp(want)
         assert p.body[: p.body_bytes].cpu().numpy().tobytes() == body
         assert len(want) == golden.manifest["config1"]["pulp_nbytes"][f"{r}/0"]
+
+
+def test_dense_ticket_slow_path():
+    """A fully changed ticket overflows the shared-memory staging of K1 and is
+    re-streamed from global memory; results must not change."""
+    D = _dev()
+    R = restatement()
+    n = 65536 * 3 + 1000
+    a = np.arange(n, dtype=np.uint16)
+    b = a ^ 1
+    b[70000:80000] = a[70000:80000]  # one sparse region in the middle
+    plan = D.DevicePlan([(n, 8)], n)
+    plan.bind(0, [torch.from_numpy(a.view(np.int16)).cuda()])
+    plan.bind(1, [torch.from_numpy(b.view(np.int16)).cuda()])
+    for repr_ in (0, 1, 2):
+        p = plan.encode(1, 0, repr_)
+        assert p.status == 0 and p.n_changes == n - 10000
+        idx, _ = plan.decode_indices(p)
+        assert np.array_equal(idx.cpu().numpy(), R.diff(a, b)[0])
