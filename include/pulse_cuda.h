@@ -60,6 +60,11 @@ enum { PULSE_IDENTITY = 0, PULSE_LZ4 = 1, PULSE_ZSTD1 = 2, PULSE_ZSTD3 = 3, PULS
 const char* pulse_last_error(void);
 const char* pulse_version(void);
 
+/* Device spin-wait watchdog: returns 1 (and clears it) if some kernel gave up
+ * a wait after the spin limit; out7 = {fired, kind, block, thread, a, b, c}.
+ * A fired watchdog means the results of that launch are invalid. */
+int pulse_watchdog(uint64_t* out7);
+
 /* ======================================================================= */
 /* Device-resident API                                                      */
 /* ======================================================================= */
@@ -160,6 +165,8 @@ pulse_status pulse_encode_scan(pulse_plan* plan, uint32_t curr_slot, uint32_t pr
                                pulse_scan_summary* dev_summary_out, void* stream);
 /* Device pointer to the plan's pulse_scan_summary (for NCCL all-gather). */
 pulse_scan_summary* pulse_plan_scan_summary(pulse_plan* plan);
+/* Debug: K1 per-ticket progress trace (device, NULL unless PULSE_TRACE is set). */
+uint32_t* pulse_plan_trace(pulse_plan* plan, uint64_t* n);
 
 /* K2: index coding (patch.hpp:116-174, index_coding.hpp:14-128) and the PULP
  * body layout: for each changed tensor, [index payload][value payload]

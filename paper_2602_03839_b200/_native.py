@@ -96,6 +96,7 @@ vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32
 _SIGS = {
     "pulse_last_error": (C.c_char_p, []),
     "pulse_version": (C.c_char_p, []),
+    "pulse_watchdog": (C.c_int, [C.POINTER(C.c_uint64)]),
     "pulse_context_create": (i32, [C.c_int, C.POINTER(vp)]),
     "pulse_context_destroy": (None, [vp]),
     "pulse_plan_create": (i32, [vp, C.POINTER(TensorGeom), u32, u64, C.POINTER(vp)]),
@@ -103,6 +104,7 @@ _SIGS = {
     "pulse_plan_bind": (i32, [vp, u32, C.POINTER(vp)]),
     "pulse_encode_scan": (i32, [vp, u32, u32, vp, vp]),
     "pulse_plan_scan_summary": (vp, [vp]),
+    "pulse_plan_trace": (vp, [vp, C.POINTER(u64)]),
     "pulse_encode_emit": (i32, [vp, u32, vp, u32, u32, vp, u64, vp, vp, vp]),
     "pulse_apply": (i32, [vp, u32, u32, vp, vp, u32, vp, vp, vp]),
     "pulse_decode_indices": (i32, [vp, u32, vp, vp, u32, vp, vp, vp, vp]),
@@ -113,6 +115,14 @@ for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)
     _f.restype = _res
     _f.argtypes = _args
+
+
+def watchdog():
+    """None, or the 7 words of a fired device watchdog (kind, block, thread, a, b, c)."""
+    out = (C.c_uint64 * 7)()
+    if lib.pulse_watchdog(out):
+        return list(out)
+    return None
 
 
 def exported_symbols():

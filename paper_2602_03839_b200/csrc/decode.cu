@@ -577,5 +577,7 @@ void launch_apply_idx64(const PlanDev& p, const int64_t* idx64, const uint16_t* 
     d_finalize<<<1, 32, 0, s>>>(p.d_totals, n_entries, p.err, result);
 }
 
+PULSE_DEFINE_WATCHDOG_SETTER(set_watchdog_decode)
+
 }  // namespace dev
 }  // namespace pulse

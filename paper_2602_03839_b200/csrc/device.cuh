@@ -71,6 +71,32 @@ __host__ __device__ inline int32_t check_status(uint32_t check) {
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Watchdog for device spin-waits (look-back polling, mbarrier waits).  A wait
+// that exceeds kSpinLimit polls records where it was stuck into a host-mapped
+// slot and gives up, so a protocol bug surfaces as PULSE_E_CUDA on the host
+// instead of a hung GPU.  One slot pointer per translation unit.
+// ------------------------------------------------------------------------------------------
+constexpr uint64_t kSpinLimit = 1ull << 25;
+static __device__ unsigned long long* g_wd_slot = nullptr;
+
+static __device__ __noinline__ void watchdog_fire(uint32_t kind, uint64_t a, uint64_t b, uint64_t c) {
+    unsigned long long* w = g_wd_slot;
+    if (!w) return;
+    if (atomicCAS(w, 0ull, 1ull) == 0ull) {
+        w[1] = kind;
+        w[2] = blockIdx.x;
+        w[3] = threadIdx.x;
+        w[4] = a;
+        w[5] = b;
+        w[6] = c;
+        __threadfence_system();
+    }
+}
+// Host side: point this translation unit's watchdog at `slot` (device address).
+#define PULSE_DEFINE_WATCHDOG_SETTER(name)                                                         \
+    void name(unsigned long long* slot) { cudaMemcpyToSymbol(g_wd_slot, &slot, sizeof(slot)); }
+
 __device__ __forceinline__ void report(uint64_t* err, uint64_t key) {
     atomicMin(reinterpret_cast<unsigned long long*>(err), static_cast<unsigned long long>(key));
 }
@@ -115,7 +141,12 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0;
+    uint64_t spins = 0;
     while (!done) {
+        if (++spins > kSpinLimit) {
+            watchdog_fire(2, smem_u32(bar), parity, 0);
+            return;
+        }
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -201,8 +232,14 @@ __device__ __forceinline__ uint64_t lookback(uint64_t* status, uint64_t tile, ui
         const int64_t idx = base - lane;
         uint64_t s = kStatPrefix;  // before tile 0: an identity prefix
         if (idx >= 0) {
+            uint64_t spins = 0;
             do {
                 s = ld_relaxed(status + idx);
+                if (++spins > kSpinLimit) {
+                    watchdog_fire(1, tile, uint64_t(idx), s);
+                    s = kStatPrefix;
+                    break;
+                }
             } while ((s & 3) == kStatInvalid);
         }
         const uint32_t pmask = __ballot_sync(0xffffffffu, (s & 3) == kStatPrefix);
@@ -234,8 +271,14 @@ __device__ __forceinline__ uint64_t lookback_published(uint64_t* status, uint64_
         const int64_t idx = base - lane;
         uint64_t s = kStatPrefix;
         if (idx >= 0) {
+            uint64_t spins = 0;
             do {
                 s = ld_relaxed(status + idx);
+                if (++spins > kSpinLimit) {
+                    watchdog_fire(1, tile, uint64_t(idx), s);
+                    s = kStatPrefix;
+                    break;
+                }
             } while ((s & 3) == kStatInvalid);
         }
         const uint32_t pmask = __ballot_sync(0xffffffffu, (s & 3) == kStatPrefix);

@@ -91,6 +91,7 @@ __device__ __forceinline__ uint16_t lane_value(const uint4& v, int k) {
 }
 
 struct K1Args {
+    uint32_t* trace;  // optional per-ticket progress trace (debug)
     const SegDesc* segs;
     const uint32_t* tile_seg;
     uint32_t n_segs;
@@ -225,16 +226,19 @@ __global__ void __launch_bounds__(kThreads, 4) k1_ticket(K1Args k) {
 // ---------------------------------------------------------------------------------------------
 namespace tma {
 constexpr int kStages = 4;
-constexpr uint32_t kSubElems = 8192;                 // elements per stage
-constexpr uint32_t kTicketElemsT = ::pulse::dev::kTicketElems;  // elements per ticket
+constexpr uint32_t kSubElems = 8192;                 // elements per stage (16 KiB + 16 KiB)
+constexpr uint32_t kSubs = kTicketElems / kSubElems; // 8 sub-tiles per ticket
 constexpr int kConsumerWarps = 8;
-constexpr int kConsumers = kConsumerWarps * 32;      // 256
+constexpr uint32_t kVecPerWarp = kSubElems / 8 / kConsumerWarps;  // 128 vectors = 4 per lane
 constexpr int kProducerWarp = kConsumerWarps;        // warp 8
 constexpr int kLbWarps = 4;                          // warps 9..12
 constexpr int kLbFirst = kConsumerWarps + 1;
+constexpr int kLbThreads = kLbWarps * 32;
 constexpr int kThreadsTotal = (kConsumerWarps + 1 + kLbWarps) * 32;  // 416
 constexpr uint32_t kStageCap = 8192;                 // staged entries per ticket buffer
-constexpr uint32_t kBarConsumers = 1, kBarLb = 2;    // named barrier ids
+constexpr uint32_t kChunks = kSubs * kConsumerWarps; // (sub-tile, warp) chunks per ticket
+constexpr uint32_t kBarLb = 2;                       // named barrier id of the look-back group
+static_assert(kVecPerWarp % 32 == 0, "whole vectors per lane");
 
 struct StageDesc {
     uint64_t tile;          // ticket id, ~0 = end of stream
@@ -248,22 +252,25 @@ struct StageDesc {
 
 struct TicketInfo {
     uint64_t tile;
-    uint32_t si, toff, count, n_sub;
+    uint32_t si, toff, n_sub;
 };
 
 struct Smem {
     uint4 prev[kStages][kSubElems / 8];
     uint4 curr[kStages][kSubElems / 8];
-    uint16_t st_idx[2][kStageCap];
+    uint16_t st_idx[2][kStageCap];   // element offset within the ticket
     uint16_t st_val[2][kStageCap];
+    uint32_t chunk_off[2][kChunks];  // where each (sub, warp) chunk was staged
+    uint32_t chunk_cnt[2][kChunks];
+    uint32_t chunk_pre[kChunks + 1]; // ordered prefix (look-back group)
+    uint32_t fill[2];                // staging bump allocator
+    uint32_t overflow[2];
     StageDesc desc[kStages];
     TicketInfo info[2];
     uint64_t full[kStages], empty[kStages];
     uint64_t tk_full[2], tk_empty[2];
-    uint32_t warp_tot[2][kConsumerWarps];
-    uint32_t warp_tot_hi[2][kConsumerWarps];
     uint32_t lb_warp_tot[kLbWarps];
-    uint32_t lb_run;
+    uint32_t lb_run, lb_count;
     uint64_t lb_G;
 };
 }  // namespace tma
@@ -282,8 +289,14 @@ __device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t til
             const int64_t idx = base - (lane * 4 + k);
             uint64_t v = kStatPrefix;  // before tile 0: identity prefix
             if (idx >= 0) {
+                uint64_t spins = 0;
                 do {
                     v = ld_relaxed(status + idx);
+                    if (++spins > kSpinLimit) {
+                        watchdog_fire(3, tile, uint64_t(idx), v);
+                        v = kStatPrefix;
+                        break;
+                    }
                 } while ((v & 3) == kStatInvalid);
             }
             w[k] = v;
@@ -324,8 +337,10 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
             mbar_init(&S.empty[i], kConsumerWarps);
         }
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&S.tk_full[i], 1);
+            mbar_init(&S.tk_full[i], kConsumerWarps);
             mbar_init(&S.tk_empty[i], 1);
+            S.fill[i] = 0;
+            S.overflow[i] = 0;
         }
         mbar_fence_init();
     }
@@ -344,10 +359,11 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                     mbar_arrive(&S.full[stage]);
                     break;
                 }
+                if (k.trace) k.trace[tile] = (blockIdx.x << 8) | 1u;
                 const uint32_t si = k.tile_seg[tile];
                 const SegDesc sd = k.segs[si];
-                const uint32_t toff = uint32_t((tile - sd.ticket_start) * kTicketElemsT);
-                const uint32_t nin = min(kTicketElemsT, sd.numel - toff);
+                const uint32_t toff = uint32_t((tile - sd.ticket_start) * kTicketElems);
+                const uint32_t nin = min(kTicketElems, sd.numel - toff);
                 const uint16_t* pp = k.prev_ptrs[sd.tensor] + sd.elem_off + toff;
                 const uint16_t* cp = k.curr_ptrs[sd.tensor] + sd.elem_off + toff;
                 const uint32_t n_sub = (nin + kSubElems - 1) / kSubElems;
@@ -382,106 +398,118 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
 
     if (warp < kConsumerWarps) {
         // ------------------------------------------------------------ consumers
+        // Warp w owns vectors [w*128, (w+1)*128) of every sub-tile, lane l the
+        // vectors w*128 + 32 j + l: each warp's slice is contiguous, so it is
+        // compacted with warp-level scans only -- no CTA barrier per sub-tile.
         int stage = 0, buf = 0;
         uint32_t phase = 0, bphase = 0;
-        uint32_t count = 0;
         while (true) {
             mbar_wait(&S.full[stage], phase);
             const StageDesc d = S.desc[stage];
             if (d.tile == ~0ull) {
-                if (tid == 0) {
+                // End of stream.  Every warp first waits until `buf` is free, like at a
+                // ticket start: warps can be skewed by several 1-sub-tile tickets, and an
+                // early arrival would otherwise complete the previous ticket's phase.
+                if (lane == 0) {
                     mbar_wait(&S.tk_empty[buf], bphase ^ 1);
-                    S.info[buf].tile = ~0ull;
+                    if (warp == 0) S.info[buf].tile = ~0ull;
                     mbar_arrive(&S.tk_full[buf]);
                 }
                 break;
             }
-            if (d.sub == 0) {
-                mbar_wait(&S.tk_empty[buf], bphase ^ 1);  // staging buffer flushed by the look-back group
-                count = 0;
-            }
-            // 4 vectors of 8 elements per thread: v = tid + 256*j
-            uint32_t m[4];
-            uint4 cv[4];
+            if (d.sub == 0) mbar_wait(&S.tk_empty[buf], bphase ^ 1);  // staging buffer flushed
+            uint32_t m[kVecPerWarp / 32];
+            uint4 cv[kVecPerWarp / 32];
+            const uint32_t v0 = warp * kVecPerWarp + lane;
+            if (d.vec_bytes == kSubElems * 2) {  // full sub-tile (block-uniform)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t v = tid + kConsumers * j;
-                const uint32_t e = v * 8;
-                uint4 a = make_uint4(0, 0, 0, 0), b = a;
-                if ((v + 1) * 16 <= d.vec_bytes) {
-                    a = S.prev[stage][v];
-                    b = S.curr[stage][v];
-                } else if (e < d.elems) {  // < 8-element tail, straight from global
-                    uint32_t ta[4] = {0, 0, 0, 0}, tb[4] = {0, 0, 0, 0};
-                    for (uint32_t q = 0; q < 8 && e + q < d.elems; ++q) {
-                        ta[q >> 1] |= uint32_t(d.pp[e + q]) << ((q & 1) * 16);
-                        tb[q >> 1] |= uint32_t(d.cp[e + q]) << ((q & 1) * 16);
-                    }
-                    a = make_uint4(ta[0], ta[1], ta[2], ta[3]);
-                    b = make_uint4(tb[0], tb[1], tb[2], tb[3]);
+                for (int j = 0; j < int(kVecPerWarp / 32); ++j) {
+                    const uint4 a = S.prev[stage][v0 + 32 * j];
+                    cv[j] = S.curr[stage][v0 + 32 * j];
+                    m[j] = change_mask(a, cv[j]);
                 }
-                m[j] = change_mask(a, b);
-                cv[j] = b;
+            } else {
+#pragma unroll
+                for (int j = 0; j < int(kVecPerWarp / 32); ++j) {
+                    const uint32_t v = v0 + 32 * j, e = v * 8;
+                    uint4 a = make_uint4(0, 0, 0, 0), b = a;
+                    if ((v + 1) * 16 <= d.vec_bytes) {
+                        a = S.prev[stage][v];
+                        b = S.curr[stage][v];
+                    } else if (e < d.elems) {  // < 8-element tail, straight from global
+                        uint32_t ta[4] = {0, 0, 0, 0}, tb[4] = {0, 0, 0, 0};
+                        for (uint32_t q = 0; q < 8 && e + q < d.elems; ++q) {
+                            ta[q >> 1] |= uint32_t(d.pp[e + q]) << ((q & 1) * 16);
+                            tb[q >> 1] |= uint32_t(d.cp[e + q]) << ((q & 1) * 16);
+                        }
+                        a = make_uint4(ta[0], ta[1], ta[2], ta[3]);
+                        b = make_uint4(tb[0], tb[1], tb[2], tb[3]);
+                    }
+                    m[j] = change_mask(a, b);
+                    cv[j] = b;
+                }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&S.empty[stage]);  // stage may be refilled
-            // order: element e = 8*(tid + 256 j) + q  ->  (j, tid, q) lexicographic;
-            // one scan per j across the 256 consumers, as two 16-bit packed pairs
-            uint32_t lo = __popc(m[0]) | (__popc(m[1]) << 16), hi = __popc(m[2]) | (__popc(m[3]) << 16);
+            if (lane == 0) mbar_arrive(&S.empty[stage]);  // the stage may be refilled now
+
+            // order inside the warp slice: (j, lane, q); packed 16-bit scans for j pairs
+            const uint32_t lo = __popc(m[0]) | (__popc(m[1]) << 16);
+            const uint32_t hi = __popc(m[2]) | (__popc(m[3]) << 16);
             uint32_t ilo = lo, ihi = hi;
+            if (__any_sync(0xffffffffu, (lo | hi) != 0)) {
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t a1 = __shfl_up_sync(0xffffffffu, ilo, off);
-                const uint32_t a2 = __shfl_up_sync(0xffffffffu, ihi, off);
-                if (lane >= off) { ilo += a1; ihi += a2; }
-            }
-            const int wb = d.sub & 1;
-            if (lane == 31) {
-                S.warp_tot[wb][warp] = ilo;  // fields j0 | j1
-                S.warp_tot_hi[wb][warp] = ihi;  // fields j2 | j3
-            }
-            named_sync(kBarConsumers, kConsumers);
-            uint32_t blo = 0, bhi = 0, tlo = 0, thi = 0;
-#pragma unroll
-            for (int w = 0; w < kConsumerWarps; ++w) {
-                const uint32_t xl = S.warp_tot[wb][w], xh = S.warp_tot_hi[wb][w];
-                if (w < warp) { blo += xl; bhi += xh; }
-                tlo += xl;
-                thi += xh;
-            }
-            const uint32_t exlo = blo + ilo - lo, exhi = bhi + ihi - hi;
-            const uint32_t t0 = tlo & 0xFFFF, t1 = tlo >> 16, t2 = thi & 0xFFFF, t3 = thi >> 16;
-            const uint32_t base_j[4] = {0, t0, t0 + t1, t0 + t1 + t2};
-            const uint32_t ex_j[4] = {exlo & 0xFFFF, exlo >> 16, exhi & 0xFFFF, exhi >> 16};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t pos = count + base_j[j] + ex_j[j];
-                uint32_t mm = m[j];
-                const uint32_t e = d.sub * kSubElems + (tid + kConsumers * j) * 8;
-                while (mm) {
-                    const int q = __ffs(mm) - 1;
-                    mm &= mm - 1;
-                    if (pos < kStageCap) {
-                        S.st_idx[buf][pos] = uint16_t(e + q);
-                        S.st_val[buf][pos] = lane_value(cv[j], q);
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t a1 = __shfl_up_sync(0xffffffffu, ilo, off);
+                    const uint32_t a2 = __shfl_up_sync(0xffffffffu, ihi, off);
+                    if (lane >= off) {
+                        ilo += a1;
+                        ihi += a2;
                     }
-                    ++pos;
                 }
             }
-            count += t0 + t1 + t2 + t3;
+            const uint32_t tlo = __shfl_sync(0xffffffffu, ilo, 31), thi = __shfl_sync(0xffffffffu, ihi, 31);
+            const uint32_t t0 = tlo & 0xFFFF, t1 = tlo >> 16, t2 = thi & 0xFFFF, t3 = thi >> 16;
+            const uint32_t total = t0 + t1 + t2 + t3;
+            uint32_t off = 0;
+            if (lane == 0 && total) off = atomicAdd(&S.fill[buf], total);
+            off = __shfl_sync(0xffffffffu, off, 0);
+            if (lane == 0) {
+                S.chunk_off[buf][d.sub * kConsumerWarps + warp] = off;
+                S.chunk_cnt[buf][d.sub * kConsumerWarps + warp] = total;
+                if (off + total > kStageCap) S.overflow[buf] = 1;
+            }
+            if (total) {
+                const uint32_t exlo = ilo - lo, exhi = ihi - hi;
+                const uint32_t pj[4] = {exlo & 0xFFFF, t0 + (exlo >> 16), t0 + t1 + (exhi & 0xFFFF),
+                                        t0 + t1 + t2 + (exhi >> 16)};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t mm = m[j];
+                    uint32_t pos = off + pj[j];
+                    const uint32_t e = d.sub * kSubElems + (v0 + 32 * j) * 8;
+                    while (mm) {
+                        const int q = __ffs(mm) - 1;
+                        mm &= mm - 1;
+                        if (pos < kStageCap) {
+                            S.st_idx[buf][pos] = uint16_t(e + q);
+                            S.st_val[buf][pos] = lane_value(cv[j], q);
+                        }
+                        ++pos;
+                    }
+                }
+            }
             if (d.sub + 1 == d.n_sub) {
-                // ticket fully counted: publish its aggregate now, hand it to the look-back group
-                named_sync(kBarConsumers, kConsumers);  // staging writes complete
-                if (tid == 0) {
-                    if (d.tile == 0) st_relaxed(k.status, (uint64_t(count) << 2) | kStatPrefix);
-                    else st_relaxed(k.status + d.tile, (uint64_t(count) << 2) | kStatAggregate);
-                    TicketInfo& ti = S.info[buf];
-                    ti.tile = d.tile;
-                    ti.si = d.si;
-                    ti.toff = d.toff;
-                    ti.count = count;
-                    ti.n_sub = d.n_sub;
-                    mbar_arrive(&S.tk_full[buf]);
+                __syncwarp();
+                if (lane == 0) {
+                    if (warp == 0) {
+                        if (k.trace) atomicOr(k.trace + d.tile, 2u);
+                        TicketInfo& ti = S.info[buf];
+                        ti.tile = d.tile;
+                        ti.si = d.si;
+                        ti.toff = d.toff;
+                        ti.n_sub = d.n_sub;
+                    }
+                    mbar_arrive(&S.tk_full[buf]);  // release: staging + chunk table visible
                 }
                 if (++buf == 2) {
                     buf = 0;
@@ -497,85 +525,122 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
     }
 
     // ---------------------------------------------------------------- look-back group
-    {
-        const int lt = tid - kLbFirst * 32;  // 0..127
-        int buf = 0;
-        uint32_t bphase = 0;
-        while (true) {
-            mbar_wait(&S.tk_full[buf], bphase);
-            const TicketInfo ti = S.info[buf];
-            if (ti.tile == ~0ull) break;
-            const SegDesc sd = k.segs[ti.si];
+    const int lt = tid - kLbFirst * 32;  // 0..127
+    int buf = 0;
+    uint32_t bphase = 0;
+    while (true) {
+        mbar_wait(&S.tk_full[buf], bphase);
+        const TicketInfo ti = S.info[buf];
+        if (ti.tile == ~0ull) break;
+        const uint32_t nch = ti.n_sub * kConsumerWarps;
+        if (warp == kLbFirst) {
+            // ordered chunk prefix (kChunks = 64: two per lane) and the ticket count
+            const uint32_t c0 = 2 * lane < nch ? S.chunk_cnt[buf][2 * lane] : 0;
+            const uint32_t c1 = 2 * lane + 1 < nch ? S.chunk_cnt[buf][2 * lane + 1] : 0;
+            uint32_t inc = c0 + c1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += x;
+            }
+            const uint32_t ex = inc - c0 - c1;
+            S.chunk_pre[2 * lane] = ex;
+            S.chunk_pre[2 * lane + 1] = ex + c0;
+            const uint32_t count = __shfl_sync(0xffffffffu, inc, 31);
+            if (lane == 31) S.chunk_pre[kChunks] = count;
+            // publish the aggregate first, then look back
+            if (lane == 0) {
+                if (ti.tile == 0) st_relaxed(k.status, (uint64_t(count) << 2) | kStatPrefix);
+                else st_relaxed(k.status + ti.tile, (uint64_t(count) << 2) | kStatAggregate);
+                if (k.trace) atomicOr(k.trace + ti.tile, 4u);
+            }
             const bool seg_first = ti.toff == 0;
             const bool last = ti.tile == k.n_tiles - 1;
-            if (warp == kLbFirst) {
-                uint64_t G = 0;
-                if ((ti.count > 0 || seg_first || last) && ti.tile > 0)
-                    G = lookback_wide(k.status, ti.tile, ti.count);
-                if (lane == 0) {
-                    S.lb_G = G;
-                    if (seg_first) k.seg_start[ti.si] = G;
-                    if (last) k.seg_start[k.n_segs] = G + ti.count;
+            uint64_t G = 0;
+            if ((count > 0 || seg_first || last) && ti.tile > 0) G = lookback_wide(k.status, ti.tile, count);
+            if (lane == 0) {
+                if (k.trace) atomicOr(k.trace + ti.tile, 8u);
+                S.lb_G = G;
+                S.lb_count = count;
+                if (seg_first) k.seg_start[ti.si] = G;
+                if (last) k.seg_start[k.n_segs] = G + count;
+            }
+        }
+        named_sync(kBarLb, kLbThreads);
+        const uint64_t G = S.lb_G;
+        const uint32_t count = S.lb_count;
+        if (!S.overflow[buf]) {
+            for (uint32_t q = lt; q < count; q += kLbThreads) {
+                // chunk holding output ordinal q: last c with chunk_pre[c] <= q
+                uint32_t lo = 0, hi = nch;
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (S.chunk_pre[mid] <= q) lo = mid; else hi = mid;
+                }
+                const uint32_t src = S.chunk_off[buf][lo] + (q - S.chunk_pre[lo]);
+                if (G + q < k.capacity) {
+                    k.out_idx[G + q] = ti.toff + S.st_idx[buf][src];
+                    k.out_val[G + q] = S.st_val[buf][src];
                 }
             }
-            named_sync(kBarLb, kLbWarps * 32);
-            const uint64_t G = S.lb_G;
-            if (ti.count <= kStageCap) {
-                for (uint32_t q = lt; q < ti.count; q += kLbWarps * 32) {
-                    if (G + q < k.capacity) {
-                        k.out_idx[G + q] = ti.toff + S.st_idx[buf][q];
-                        k.out_val[G + q] = S.st_val[buf][q];
-                    }
-                }
-            } else {
-                // dense ticket (> kStageCap changes): re-stream it from global memory
-                const uint16_t* pp = k.prev_ptrs[sd.tensor] + sd.elem_off + ti.toff;
-                const uint16_t* cp = k.curr_ptrs[sd.tensor] + sd.elem_off + ti.toff;
-                const uint32_t nin = min(kTicketElems, sd.numel - ti.toff);
-                if (lt == 0) S.lb_run = 0;
-                named_sync(kBarLb, kLbWarps * 32);
-                for (uint32_t e0 = 0; e0 < nin; e0 += kLbWarps * 32 * 8) {
-                    const uint32_t e = e0 + lt * 8;
-                    uint32_t mm = 0;
-                    uint16_t vals[8];
-                    for (uint32_t q = 0; q < 8 && e + q < nin; ++q) {
+        } else {
+            // dense ticket (staging overflowed): re-stream it from global memory
+            const SegDesc sd = k.segs[ti.si];
+            const uint16_t* pp = k.prev_ptrs[sd.tensor] + sd.elem_off + ti.toff;
+            const uint16_t* cp = k.curr_ptrs[sd.tensor] + sd.elem_off + ti.toff;
+            const uint32_t nin = min(kTicketElems, sd.numel - ti.toff);
+            if (lt == 0) S.lb_run = 0;
+            named_sync(kBarLb, kLbThreads);
+            for (uint32_t e0 = 0; e0 < nin; e0 += kLbThreads * 8) {
+                const uint32_t e = e0 + lt * 8;
+                uint32_t mm = 0;
+                uint16_t vals[8];
+#pragma unroll
+                for (uint32_t q = 0; q < 8; ++q) {
+                    vals[q] = 0;
+                    if (e + q < nin) {
                         vals[q] = cp[e + q];
                         if (vals[q] != pp[e + q]) mm |= 1u << q;
                     }
-                    uint32_t inc = __popc(mm);
-#pragma unroll
-                    for (int off = 1; off < 32; off <<= 1) {
-                        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
-                        if (lane >= off) inc += o;
-                    }
-                    if (lane == 31) S.lb_warp_tot[warp - kLbFirst] = inc;
-                    named_sync(kBarLb, kLbWarps * 32);
-                    uint32_t before = 0, all = 0;
-                    for (int w = 0; w < kLbWarps; ++w) {
-                        if (w < warp - kLbFirst) before += S.lb_warp_tot[w];
-                        all += S.lb_warp_tot[w];
-                    }
-                    uint64_t pos = G + S.lb_run + before + inc - __popc(mm);
-                    while (mm) {
-                        const int q = __ffs(mm) - 1;
-                        mm &= mm - 1;
-                        if (pos < k.capacity) {
-                            k.out_idx[pos] = ti.toff + e + q;
-                            k.out_val[pos] = vals[q];
-                        }
-                        ++pos;
-                    }
-                    named_sync(kBarLb, kLbWarps * 32);
-                    if (lt == 0) S.lb_run += all;
-                    named_sync(kBarLb, kLbWarps * 32);
                 }
+                uint32_t inc = __popc(mm);
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += x;
+                }
+                if (lane == 31) S.lb_warp_tot[warp - kLbFirst] = inc;
+                named_sync(kBarLb, kLbThreads);
+                uint32_t before = 0, all = 0;
+                for (int w = 0; w < kLbWarps; ++w) {
+                    if (w < warp - kLbFirst) before += S.lb_warp_tot[w];
+                    all += S.lb_warp_tot[w];
+                }
+                uint64_t pos = G + S.lb_run + before + inc - __popc(mm);
+                while (mm) {
+                    const int q = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    if (pos < k.capacity) {
+                        k.out_idx[pos] = ti.toff + e + q;
+                        k.out_val[pos] = vals[q];
+                    }
+                    ++pos;
+                }
+                named_sync(kBarLb, kLbThreads);
+                if (lt == 0) S.lb_run += all;
+                named_sync(kBarLb, kLbThreads);
             }
-            named_sync(kBarLb, kLbWarps * 32);  // flush done before the buffer is reused
-            if (lt == 0) mbar_arrive(&S.tk_empty[buf]);
-            if (++buf == 2) {
-                buf = 0;
-                bphase ^= 1;
-            }
+        }
+        named_sync(kBarLb, kLbThreads);  // flush done before the buffer is reused
+        if (lt == 0) {
+            if (k.trace) atomicOr(k.trace + ti.tile, 16u);
+            S.fill[buf] = 0;
+            S.overflow[buf] = 0;
+            mbar_arrive(&S.tk_empty[buf]);
+        }
+        if (++buf == 2) {
+            buf = 0;
+            bphase ^= 1;
         }
     }
 }
@@ -1059,7 +1124,7 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
     // status words + ticket must start at zero each launch
     cudaMemsetAsync(p.k1_status, 0, p.n_tiles * sizeof(uint64_t), s);
     cudaMemsetAsync(p.counters, 0, 8 * sizeof(uint64_t), s);
-    K1Args k{p.segs, p.tile_seg, p.n_segs, p.n_tiles, p.slot[prev_slot], p.slot[curr_slot], p.idx32, p.val16,
+    K1Args k{p.trace, p.segs, p.tile_seg, p.n_segs, p.n_tiles, p.slot[prev_slot], p.slot[curr_slot], p.idx32, p.val16,
              p.cap, p.seg_start, p.k1_status, reinterpret_cast<unsigned long long*>(p.counters)};
     if (p.n_tiles > 0) {
         static int per_sm_static = 0, per_sm_ticket = 0;
@@ -1135,6 +1200,8 @@ void launch_encode_emit(const PlanDev& p, uint32_t repr, const pulse_scan_summar
     emit_common(p, em, repr, false, gathered, n_ranks, rank, p.val16, body, body_cap, entries, result,
                 p.cap, s);
 }
+
+PULSE_DEFINE_WATCHDOG_SETTER(set_watchdog_encode)
 
 }  // namespace dev
 }  // namespace pulse

@@ -67,6 +67,7 @@ struct PlanDev {
     const uint32_t* tile_seg;   // [n_tiles] segment of each K1 tile
     uint64_t tma_tiles;         // number of 65536-element tickets
     const uint32_t* tma_tile_seg;  // [tma_tiles] segment of each ticket
+    uint32_t* trace;            // [tma_tiles] optional K1 progress trace (PULSE_TRACE=1)
     const uint32_t* seg_first;  // [T+1] first segment of each tensor
     const uint64_t* numel;      // [T]
     const uint64_t* cols;       // [T]
@@ -129,6 +130,9 @@ void launch_encode_emit_idx64(const PlanDev& p, uint32_t repr, const int64_t* id
                               pulse_result* result, cudaStream_t s);
 
 int sm_count();
+void set_watchdog_encode(unsigned long long* slot);
+void set_watchdog_decode(unsigned long long* slot);
+void set_watchdog_synth(unsigned long long* slot);
 
 }  // namespace dev
 }  // namespace pulse

@@ -1,5 +1,6 @@
 // Contexts, plans and the device-resident C ABI (include/pulse_cuda.h).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -55,7 +56,43 @@ pulse_plan::~pulse_plan() {
     cudaSetDevice(prev);
 }
 
+// Host-mapped watchdog slot shared by all devices of the process (see device.cuh).
+static unsigned long long* g_wd_host = nullptr;
+static unsigned long long* g_wd_dev = nullptr;
+static std::mutex g_wd_mu;
+
+static void install_watchdog(int device) {
+    std::lock_guard<std::mutex> lk(g_wd_mu);
+    if (!g_wd_host) {
+        void* h = nullptr;
+        if (cudaHostAlloc(&h, 8 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable) !=
+            cudaSuccess)
+            return;
+        std::memset(h, 0, 8 * sizeof(unsigned long long));
+        g_wd_host = static_cast<unsigned long long*>(h);
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&g_wd_dev), h, 0);
+    }
+    static bool done[64] = {};
+    if (device >= 0 && device < 64 && !done[device]) {
+        set_watchdog_encode(g_wd_dev);
+        set_watchdog_decode(g_wd_dev);
+        set_watchdog_synth(g_wd_dev);
+        done[device] = true;
+    }
+}
+
 extern "C" {
+
+int pulse_watchdog(uint64_t* out7) {
+    if (!g_wd_host) return 0;
+    volatile unsigned long long* w = g_wd_host;
+    const int fired = w[0] != 0;
+    if (out7)
+        for (int i = 0; i < 7; ++i) out7[i] = w[i];
+    if (fired)
+        for (int i = 0; i < 8; ++i) w[i] = 0;
+    return fired;
+}
 
 const char* pulse_last_error(void) { return pulse::g_last_error.c_str(); }
 const char* pulse_version(void) { return "pulse-b200 0.1 (sm_100a)"; }
@@ -66,6 +103,7 @@ pulse_status pulse_context_create(int device, pulse_context** out) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
     auto* c = new pulse_context();
     c->device = device;
+    install_watchdog(device);
     *out = c;
     return PULSE_OK;
 }
@@ -132,6 +170,7 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
     A(p.elay, T); A(p.d_es, T + 1); A(p.d_ck, T + 1); A(p.d_cu, T + 1);
     A(p.rowgap, cap); A(p.colent, cap); A(p.flat, cap);
     A(p.d_status, 4 * p.d_status_len); A(p.d_totals, 16);
+    if (getenv("PULSE_TRACE")) A(p.trace, tickets);
 #undef A
     if (e != cudaSuccess) {
         delete plan;
@@ -212,6 +251,12 @@ pulse_status pulse_encode_scan(pulse_plan* plan, uint32_t curr_slot, uint32_t pr
 }
 
 pulse_scan_summary* pulse_plan_scan_summary(pulse_plan* plan) { return plan ? plan->dev.scan : nullptr; }
+
+// Debug: device pointer + length of the K1 ticket trace (NULL unless PULSE_TRACE is set).
+uint32_t* pulse_plan_trace(pulse_plan* plan, uint64_t* n) {
+    if (n) *n = plan ? plan->dev.tma_tiles : 0;
+    return plan ? plan->dev.trace : nullptr;
+}
 
 pulse_status pulse_encode_emit(pulse_plan* plan, uint32_t repr, const pulse_scan_summary* gathered,
                                uint32_t n_ranks, uint32_t rank, uint8_t* dev_body, uint64_t body_capacity,

@@ -122,6 +122,8 @@ __global__ void k_synth_flip(const uint16_t* __restrict__ base, uint16_t* __rest
     }
 }
 
+PULSE_DEFINE_WATCHDOG_SETTER(set_watchdog_synth)
+
 }  // namespace dev
 }  // namespace pulse
 

@@ -45,6 +45,10 @@ class DevicePatch:
     def fetch(self, stream=None) -> "DevicePatch":
         """D2H of the result and entry table (small); synchronizes the stream."""
         r = self.result.to("cpu", non_blocking=False).numpy().view(N.RESULT_DTYPE)[0]
+        wd = N.watchdog()
+        if wd is not None:
+            raise PulseError(14, f"device watchdog fired: kind={wd[1]} block={wd[2]} thread={wd[3]} "
+                                 f"a={wd[4]} b={wd[5]} c={wd[6]:#x}")
         self.host_result = r
         n = int(r["n_entries"])
         self.host_entries = self.entries[: n * 40].to("cpu").numpy().view(N.ENTRY_DTYPE).copy()
