@@ -92,6 +92,7 @@ __device__ __forceinline__ uint16_t lane_value(const uint4& v, int k) {
 
 struct K1Args {
     uint32_t* trace;  // optional per-ticket progress trace (debug)
+    int experiment;   // 1: consumers only release stages (TMA streaming rate)
     const SegDesc* segs;
     const uint32_t* tile_seg;
     uint32_t n_segs;
@@ -236,6 +237,7 @@ constexpr int kLbFirst = kConsumerWarps + 1;
 constexpr int kLbThreads = kLbWarps * 32;
 constexpr int kThreadsTotal = (kConsumerWarps + 1 + kLbWarps) * 32;  // 416
 constexpr uint32_t kStageCap = 8192;                 // staged entries per ticket buffer
+constexpr int kBufs = 3;                             // ticket staging buffers (consumers may run ahead)
 constexpr uint32_t kChunks = kSubs * kConsumerWarps; // (sub-tile, warp) chunks per ticket
 constexpr uint32_t kBarLb = 2;                       // named barrier id of the look-back group
 static_assert(kVecPerWarp % 32 == 0, "whole vectors per lane");
@@ -258,17 +260,19 @@ struct TicketInfo {
 struct Smem {
     uint4 prev[kStages][kSubElems / 8];
     uint4 curr[kStages][kSubElems / 8];
-    uint16_t st_idx[2][kStageCap];   // element offset within the ticket
-    uint16_t st_val[2][kStageCap];
-    uint32_t chunk_off[2][kChunks];  // where each (sub, warp) chunk was staged
-    uint32_t chunk_cnt[2][kChunks];
+    uint16_t st_idx[kBufs][kStageCap];   // element offset within the ticket
+    uint16_t st_val[kBufs][kStageCap];
+    uint32_t chunk_off[kBufs][kChunks];  // where each (sub, warp) chunk was staged
+    uint32_t chunk_cnt[kBufs][kChunks];
     uint32_t chunk_pre[kChunks + 1]; // ordered prefix (look-back group)
-    uint32_t fill[2];                // staging bump allocator
-    uint32_t overflow[2];
+    uint32_t fill[kBufs];            // staging bump allocator
+    uint32_t overflow[kBufs];
+    uint32_t tk_cnt[kBufs];          // ticket count, summed by the consumer warps
+    uint32_t tk_arrived[kBufs];      // consumer warps done with the ticket
     StageDesc desc[kStages];
-    TicketInfo info[2];
+    TicketInfo info[kBufs];
     uint64_t full[kStages], empty[kStages];
-    uint64_t tk_full[2], tk_empty[2];
+    uint64_t tk_full[kBufs], tk_empty[kBufs];
     uint32_t lb_warp_tot[kLbWarps];
     uint32_t lb_run, lb_count;
     uint64_t lb_G;
@@ -336,11 +340,13 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
             mbar_init(&S.full[i], 1);
             mbar_init(&S.empty[i], kConsumerWarps);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kBufs; ++i) {
             mbar_init(&S.tk_full[i], kConsumerWarps);
             mbar_init(&S.tk_empty[i], 1);
             S.fill[i] = 0;
             S.overflow[i] = 0;
+            S.tk_cnt[i] = 0;
+            S.tk_arrived[i] = 0;
         }
         mbar_fence_init();
     }
@@ -403,6 +409,36 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
         // compacted with warp-level scans only -- no CTA barrier per sub-tile.
         int stage = 0, buf = 0;
         uint32_t phase = 0, bphase = 0;
+        uint32_t wcount = 0;  // this warp's changes in the current ticket
+        // Last warp of a ticket publishes its aggregate right away, so other CTAs'
+        // look-backs never wait on this CTA's look-back group.
+        auto finish_ticket = [&](const StageDesc& d) {
+            __syncwarp();
+            if (lane == 0) {
+                if (warp == 0) {
+                    if (k.trace) atomicOr(k.trace + d.tile, 2u);
+                    TicketInfo& ti = S.info[buf];
+                    ti.tile = d.tile;
+                    ti.si = d.si;
+                    ti.toff = d.toff;
+                    ti.n_sub = d.n_sub;
+                }
+                atomicAdd(&S.tk_cnt[buf], wcount);
+                __threadfence_block();
+                if (atomicAdd(&S.tk_arrived[buf], 1u) == kConsumerWarps - 1) {
+                    const uint32_t count = atomicAdd(&S.tk_cnt[buf], 0u);
+                    if (d.tile == 0) st_relaxed(k.status, (uint64_t(count) << 2) | kStatPrefix);
+                    else st_relaxed(k.status + d.tile, (uint64_t(count) << 2) | kStatAggregate);
+                    if (k.trace) atomicOr(k.trace + d.tile, 4u);
+                }
+                mbar_arrive(&S.tk_full[buf]);  // release: staging + chunk table + info visible
+            }
+            wcount = 0;
+            if (++buf == kBufs) {
+                buf = 0;
+                bphase ^= 1;
+            }
+        };
         while (true) {
             mbar_wait(&S.full[stage], phase);
             const StageDesc d = S.desc[stage];
@@ -417,16 +453,29 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                 }
                 break;
             }
+            if (k.experiment == 1) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.empty[stage]);
+                if (d.sub + 1 == d.n_sub) {
+                    if (lane == 0) {
+                        if (warp == 0) {
+                            S.chunk_cnt[buf][0] = 0;
+                            TicketInfo& ti = S.info[buf];
+                            ti.tile = d.tile; ti.si = d.si; ti.toff = d.toff; ti.n_sub = 1;
+                        }
+                    }
+                }
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
+                continue;
+            }
             if (d.sub == 0) mbar_wait(&S.tk_empty[buf], bphase ^ 1);  // staging buffer flushed
-            uint32_t m[kVecPerWarp / 32];
-            uint4 cv[kVecPerWarp / 32];
+            uint4 av[kVecPerWarp / 32], cv[kVecPerWarp / 32];
             const uint32_t v0 = warp * kVecPerWarp + lane;
             if (d.vec_bytes == kSubElems * 2) {  // full sub-tile (block-uniform)
 #pragma unroll
                 for (int j = 0; j < int(kVecPerWarp / 32); ++j) {
-                    const uint4 a = S.prev[stage][v0 + 32 * j];
+                    av[j] = S.prev[stage][v0 + 32 * j];
                     cv[j] = S.curr[stage][v0 + 32 * j];
-                    m[j] = change_mask(a, cv[j]);
                 }
             } else {
 #pragma unroll
@@ -445,26 +494,44 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                         a = make_uint4(ta[0], ta[1], ta[2], ta[3]);
                         b = make_uint4(tb[0], tb[1], tb[2], tb[3]);
                     }
-                    m[j] = change_mask(a, b);
+                    av[j] = a;
                     cv[j] = b;
                 }
             }
+            // any difference in this lane's 32 elements? (XOR-OR, LOP3-fusable)
+            uint32_t diff = 0;
+#pragma unroll
+            for (int j = 0; j < int(kVecPerWarp / 32); ++j)
+                diff |= (av[j].x ^ cv[j].x) | (av[j].y ^ cv[j].y) | (av[j].z ^ cv[j].z) | (av[j].w ^ cv[j].w);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&S.empty[stage]);  // the stage may be refilled now
+            if (lane == 0) mbar_arrive(&S.empty[stage]);  // operands are in registers: stage may be refilled
+            const bool warp_changed = __any_sync(0xffffffffu, diff != 0);
+            uint32_t m[kVecPerWarp / 32] = {0, 0, 0, 0};
+            if (warp_changed && diff) {
+#pragma unroll
+                for (int j = 0; j < int(kVecPerWarp / 32); ++j) m[j] = change_mask(av[j], cv[j]);
+            }
+            if (!warp_changed) {  // common case at high sparsity: nothing to stage
+                if (lane == 0) S.chunk_cnt[buf][d.sub * kConsumerWarps + warp] = 0;
+                if (d.sub + 1 == d.n_sub) finish_ticket(d);
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+                continue;
+            }
 
             // order inside the warp slice: (j, lane, q); packed 16-bit scans for j pairs
             const uint32_t lo = __popc(m[0]) | (__popc(m[1]) << 16);
             const uint32_t hi = __popc(m[2]) | (__popc(m[3]) << 16);
             uint32_t ilo = lo, ihi = hi;
-            if (__any_sync(0xffffffffu, (lo | hi) != 0)) {
 #pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const uint32_t a1 = __shfl_up_sync(0xffffffffu, ilo, off);
-                    const uint32_t a2 = __shfl_up_sync(0xffffffffu, ihi, off);
-                    if (lane >= off) {
-                        ilo += a1;
-                        ihi += a2;
-                    }
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t a1 = __shfl_up_sync(0xffffffffu, ilo, off);
+                const uint32_t a2 = __shfl_up_sync(0xffffffffu, ihi, off);
+                if (lane >= off) {
+                    ilo += a1;
+                    ihi += a2;
                 }
             }
             const uint32_t tlo = __shfl_sync(0xffffffffu, ilo, 31), thi = __shfl_sync(0xffffffffu, ihi, 31);
@@ -498,24 +565,8 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                     }
                 }
             }
-            if (d.sub + 1 == d.n_sub) {
-                __syncwarp();
-                if (lane == 0) {
-                    if (warp == 0) {
-                        if (k.trace) atomicOr(k.trace + d.tile, 2u);
-                        TicketInfo& ti = S.info[buf];
-                        ti.tile = d.tile;
-                        ti.si = d.si;
-                        ti.toff = d.toff;
-                        ti.n_sub = d.n_sub;
-                    }
-                    mbar_arrive(&S.tk_full[buf]);  // release: staging + chunk table visible
-                }
-                if (++buf == 2) {
-                    buf = 0;
-                    bphase ^= 1;
-                }
-            }
+            wcount += total;
+            if (d.sub + 1 == d.n_sub) finish_ticket(d);
             if (++stage == kStages) {
                 stage = 0;
                 phase ^= 1;
@@ -548,12 +599,7 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
             S.chunk_pre[2 * lane + 1] = ex + c0;
             const uint32_t count = __shfl_sync(0xffffffffu, inc, 31);
             if (lane == 31) S.chunk_pre[kChunks] = count;
-            // publish the aggregate first, then look back
-            if (lane == 0) {
-                if (ti.tile == 0) st_relaxed(k.status, (uint64_t(count) << 2) | kStatPrefix);
-                else st_relaxed(k.status + ti.tile, (uint64_t(count) << 2) | kStatAggregate);
-                if (k.trace) atomicOr(k.trace + ti.tile, 4u);
-            }
+            // (the aggregate was published by the last consumer warp)
             const bool seg_first = ti.toff == 0;
             const bool last = ti.tile == k.n_tiles - 1;
             uint64_t G = 0;
@@ -636,9 +682,11 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
             if (k.trace) atomicOr(k.trace + ti.tile, 16u);
             S.fill[buf] = 0;
             S.overflow[buf] = 0;
+            S.tk_cnt[buf] = 0;
+            S.tk_arrived[buf] = 0;
             mbar_arrive(&S.tk_empty[buf]);
         }
-        if (++buf == 2) {
+        if (++buf == kBufs) {
             buf = 0;
             bphase ^= 1;
         }
@@ -1124,7 +1172,8 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
     // status words + ticket must start at zero each launch
     cudaMemsetAsync(p.k1_status, 0, p.n_tiles * sizeof(uint64_t), s);
     cudaMemsetAsync(p.counters, 0, 8 * sizeof(uint64_t), s);
-    K1Args k{p.trace, p.segs, p.tile_seg, p.n_segs, p.n_tiles, p.slot[prev_slot], p.slot[curr_slot], p.idx32, p.val16,
+    static const int experiment = getenv("PULSE_K1_EXPERIMENT") ? atoi(getenv("PULSE_K1_EXPERIMENT")) : 0;
+    K1Args k{p.trace, experiment, p.segs, p.tile_seg, p.n_segs, p.n_tiles, p.slot[prev_slot], p.slot[curr_slot], p.idx32, p.val16,
              p.cap, p.seg_start, p.k1_status, reinterpret_cast<unsigned long long*>(p.counters)};
     if (p.n_tiles > 0) {
         static int per_sm_static = 0, per_sm_ticket = 0;
