@@ -323,11 +323,13 @@ def run_pulse(args):
     scan_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["s0"], ev["s1"]))
     apply_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["a0"], ev["a1"]))
 
-    # correctness of the final state: W == prev after an even number of steps
-    if args.steps % 2 == 0:
-        ok = bool(torch.equal(w, prev))
-    else:
-        ok = bool(torch.equal(w, curr))
+    # correctness: after the timed loop W must equal the last step's target, and
+    # two more (untimed) steps must each land exactly on theirs
+    ok = bool(torch.equal(w, prev if args.steps % 2 == 0 else curr))
+    for k in (args.steps, args.steps + 1):
+        step(k)
+        torch.cuda.synchronize()
+        ok = ok and bool(torch.equal(w, curr if k % 2 == 0 else prev))
 
     t_ms = torch.tensor([ms, scan_ms, apply_ms, float(not ok)], dtype=torch.float64, device=dev)
     if world > 1:

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kLT, 1)
 d_layout(const pulse_patch_entry* __restrict__ entries, uint32_t n_e, const uint64_t* __restrict__ numel,
          const uint64_t* __restrict__ cols, uint32_t repr, EntryLayout* __restrict__ el,
          uint64_t* __restrict__ es, uint64_t* __restrict__ ck, uint64_t* __restrict__ totals,
-         uint64_t* __restrict__ err) {
+         uint64_t* __restrict__ err, uint32_t* __restrict__ flags) {
     __shared__ uint64_t s_tmp[32];
     uint64_t base_e = 0, base_c = 0, base_f = 0;
     for (uint32_t e0 = 0; e0 < n_e; e0 += kLT) {
@@ -124,6 +124,8 @@ d_layout(const pulse_patch_entry* __restrict__ entries, uint32_t n_e, const uint
             el[e] = L;
             es[e] = L.es;
             ck[e] = L.ck;
+            // fixed-layout fast path (apply_fast.cu) only if no entry needs escapes
+            if (pe.idx_nbytes != (repr == PULSE_COO_DOWNSCALED ? 3 : 4) * pe.count) atomicExch(flags, 1u);
             if (repr != PULSE_COO_DOWNSCALED) {
                 // patch.hpp:193,217: require_int32_indexable; then u32 reads of `count`
                 // entries (truncation) and the trailing-bytes check.
@@ -156,7 +158,8 @@ __global__ void __launch_bounds__(kThreads)
 d_fixed(const EntryLayout* __restrict__ el, const uint64_t* __restrict__ es, uint32_t n_e,
         const uint8_t* __restrict__ body, const pulse_flat_carry* __restrict__ carry,
         uint64_t* __restrict__ status, uint64_t* __restrict__ totals, uint64_t* __restrict__ out,
-        uint64_t* __restrict__ err) {
+        uint64_t* __restrict__ err, const uint32_t* __restrict__ flags) {
+    if (*(volatile const uint32_t*)flags == 0) return;  // fixed-layout fast path handled it
     using Op = typename std::conditional<kFlat, SumOp, SegSumOp>::type;
     constexpr uint64_t H = SegSumOp::kHead;
     __shared__ uint64_t s_warp[kWarps];
@@ -234,7 +237,8 @@ __device__ __forceinline__ uint64_t row_sync_start(const uint8_t* blob, uint64_t
 __global__ void __launch_bounds__(kThreads)
 d_rows(EntryLayout* __restrict__ el, const uint64_t* __restrict__ ck, uint32_t n_e,
        const uint8_t* __restrict__ body, uint64_t* __restrict__ status, uint64_t* __restrict__ totals,
-       uint32_t* __restrict__ rowgap, uint64_t* __restrict__ err) {
+       uint32_t* __restrict__ rowgap, uint64_t* __restrict__ err, const uint32_t* __restrict__ flags) {
+    if (*(volatile const uint32_t*)flags == 0) return;  // fixed-layout fast path handled it
     constexpr uint64_t H = SegSumOp::kHead;
     __shared__ uint64_t s_warp[kWarps];
     __shared__ uint64_t s_tile, s_excl;
@@ -298,7 +302,9 @@ d_rows(EntryLayout* __restrict__ el, const uint64_t* __restrict__ ck, uint32_t n
 // =============================================================================================
 __global__ void __launch_bounds__(kLT, 1)
 d_col_layout(EntryLayout* __restrict__ el, uint32_t n_e, uint64_t* __restrict__ cu,
-             uint64_t* __restrict__ totals, uint64_t* __restrict__ err) {
+             uint64_t* __restrict__ totals, uint64_t* __restrict__ err,
+             const uint32_t* __restrict__ flags) {
+    if (*(volatile const uint32_t*)flags == 0) return;
     __shared__ uint64_t s_tmp[32];
     uint64_t base = 0;
     for (uint32_t e0 = 0; e0 < n_e; e0 += kLT) {
@@ -345,7 +351,8 @@ __device__ __forceinline__ uint64_t col_sync_start(const uint8_t* s, uint64_t a,
 __global__ void __launch_bounds__(kThreads)
 d_cols(const EntryLayout* __restrict__ el, const uint64_t* __restrict__ cu, uint32_t n_e,
        const uint8_t* __restrict__ body, uint64_t* __restrict__ status, uint64_t* __restrict__ totals,
-       uint32_t* __restrict__ colent, uint64_t* __restrict__ err) {
+       uint32_t* __restrict__ colent, uint64_t* __restrict__ err, const uint32_t* __restrict__ flags) {
+    if (*(volatile const uint32_t*)flags == 0) return;  // fixed-layout fast path handled it
     constexpr uint64_t H = SegSumOp::kHead;
     __shared__ uint64_t s_warp[kWarps];
     __shared__ uint64_t s_tile, s_excl;
@@ -412,7 +419,8 @@ __global__ void __launch_bounds__(kThreads)
 d_assemble(const EntryLayout* __restrict__ el, const uint64_t* __restrict__ es, uint32_t n_e,
            const uint32_t* __restrict__ rowgap, const uint32_t* __restrict__ colent,
            uint64_t* __restrict__ st_rows, uint64_t* __restrict__ st_cols, uint64_t* __restrict__ totals,
-           uint64_t* __restrict__ out, uint64_t* __restrict__ err) {
+           uint64_t* __restrict__ out, uint64_t* __restrict__ err, const uint32_t* __restrict__ flags) {
+    if (*(volatile const uint32_t*)flags == 0) return;  // fixed-layout fast path handled it
     constexpr uint64_t H = SegSumOp::kHead;
     __shared__ uint64_t s_warp[kWarps];
     __shared__ uint64_t s_tile, s_xr, s_xc;
@@ -473,8 +481,9 @@ d_scatter(const EntryLayout* __restrict__ el, const uint64_t* __restrict__ es, u
           const uint8_t* __restrict__ body, const uint16_t* __restrict__ vals,
           const uint64_t* __restrict__ flat, const int64_t* __restrict__ flat64,
           uint16_t* const* __restrict__ weights, const uint64_t* __restrict__ totals,
-          const uint64_t* __restrict__ err) {
+          const uint64_t* __restrict__ err, const uint32_t* __restrict__ flags) {
     if (*err != kNoError) return;
+    if (flags && *(volatile const uint32_t*)flags == 0) return;  // fixed-layout fast path scattered
     const uint64_t n = totals[kTotEntries];
     const uint64_t stride = uint64_t(gridDim.x) * kThreads * kEntriesPerThread;
     for (uint64_t i0 = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) * kEntriesPerThread; i0 < n; i0 += stride) {
@@ -527,11 +536,18 @@ static unsigned persistent_grid() { return unsigned(sm_count() * 8); }
 
 static void decode_prologue(const PlanDev& p, const pulse_patch_entry* entries, uint32_t n_entries,
                             uint32_t repr, cudaStream_t s) {
-    cudaMemsetAsync(p.d_status, 0, 4 * p.d_status_len * sizeof(uint64_t), s);
     cudaMemsetAsync(p.d_totals, 0, 16 * sizeof(uint64_t), s);
+    cudaMemsetAsync(p.d_flags, 0, 4 * sizeof(uint32_t), s);
     cudaMemsetAsync(p.err, 0xFF, sizeof(uint64_t), s);
     d_layout<<<1, kLT, 0, s>>>(entries, n_entries, p.numel, p.cols, repr, p.elay, p.d_es, p.d_ck,
-                              p.d_totals, p.err);
+                              p.d_totals, p.err, p.d_flags);
+}
+
+// Look-back status words only matter on the general path; clear them there.
+__global__ void d_clear_status(uint64_t* __restrict__ st, uint64_t n, const uint32_t* __restrict__ flags) {
+    if (*(volatile const uint32_t*)flags == 0) return;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        st[i] = 0;
 }
 
 void launch_decode(const PlanDev& p, uint32_t repr, const uint8_t* body,
@@ -546,19 +562,23 @@ void launch_decode(const PlanDev& p, uint32_t repr, const uint8_t* body,
     uint64_t* st2 = p.d_status + 2 * p.d_status_len;
     uint64_t* st3 = p.d_status + 3 * p.d_status_len;
     if (n_entries > 0) {
+        // common case: fixed-layout payloads (no escapes) -- apply_fast.cu
+        launch_apply_fast(p, repr, body, n_entries, carry, weights_slot, out_indices, p.d_flags, s);
+        // general path (escapes, malformed sizes): runs only if d_layout / F1 raised flags[0]
+        d_clear_status<<<g, kThreads, 0, s>>>(p.d_status, 4 * p.d_status_len, p.d_flags);
         if (repr == PULSE_COO_INT32) {
-            d_fixed<false><<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, body, nullptr, st0, p.d_totals, out, p.err);
+            d_fixed<false><<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, body, nullptr, st0, p.d_totals, out, p.err, p.d_flags);
         } else if (repr == PULSE_FLAT_INT32) {
-            d_fixed<true><<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, body, carry, st0, p.d_totals, out, p.err);
+            d_fixed<true><<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, body, carry, st0, p.d_totals, out, p.err, p.d_flags);
         } else {
-            d_rows<<<g, kThreads, 0, s>>>(p.elay, p.d_ck, n_entries, body, st2, p.d_totals, p.rowgap, p.err);
-            d_col_layout<<<1, kLT, 0, s>>>(p.elay, n_entries, p.d_cu, p.d_totals, p.err);
-            d_cols<<<g, kThreads, 0, s>>>(p.elay, p.d_cu, n_entries, body, st3, p.d_totals, p.colent, p.err);
-            d_assemble<<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, p.rowgap, p.colent, st0, st1, p.d_totals, out, p.err);
+            d_rows<<<g, kThreads, 0, s>>>(p.elay, p.d_ck, n_entries, body, st2, p.d_totals, p.rowgap, p.err, p.d_flags);
+            d_col_layout<<<1, kLT, 0, s>>>(p.elay, n_entries, p.d_cu, p.d_totals, p.err, p.d_flags);
+            d_cols<<<g, kThreads, 0, s>>>(p.elay, p.d_cu, n_entries, body, st3, p.d_totals, p.colent, p.err, p.d_flags);
+            d_assemble<<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, p.rowgap, p.colent, st0, st1, p.d_totals, out, p.err, p.d_flags);
         }
         if (weights_slot >= 0)
             d_scatter<<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, body, nullptr, out, nullptr,
-                                             p.slot[weights_slot], p.d_totals, p.err);
+                                             p.slot[weights_slot], p.d_totals, p.err, p.d_flags);
     }
     d_finalize<<<1, 32, 0, s>>>(p.d_totals, n_entries, p.err, result);
 }
@@ -572,7 +592,7 @@ void launch_apply_idx64(const PlanDev& p, const int64_t* idx64, const uint16_t* 
         d_validate_idx64<<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, idx64, p.d_totals, p.err);
         if (weights_slot >= 0)
             d_scatter<<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, nullptr, vals, nullptr, idx64,
-                                             p.slot[weights_slot], p.d_totals, p.err);
+                                             p.slot[weights_slot], p.d_totals, p.err, nullptr);
     }
     d_finalize<<<1, 32, 0, s>>>(p.d_totals, n_entries, p.err, result);
 }

@@ -7,14 +7,7 @@
 //                         ballot/popc counts, a block scan, and a decoupled
 //                         look-back across tiles give each change its global
 //                         slot.  Output: u32 segment-relative index + u16 value.
-//   K2a k2_escapes        COO_DOWNSCALED: per-chunk row/col escape counts
-//                         (index_coding.hpp:68-90) and argument checks.
-//   K2L k2_layout         one CTA: per-tensor payload sizes, body offsets,
-//                         FLAT_INT32 cross-tensor gap bases (patch.hpp:131-156).
-//   K2b k2_emit           writes every index payload byte and value byte of the
-//                         body, i.e. the identity-codec PULP blob area
-//                         (patch_file.hpp:76-82), for all three representations
-//                         (patch.hpp:116-174).
+// The index coders (K2) are in index_code.cu.
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -717,432 +710,6 @@ __global__ void k1_finalize(const SegDesc* __restrict__ segs, uint32_t n_segs,
 }
 
 // =============================================================================================
-// Entry sources for K2: compacted K1 output (segment-relative u32) or host
-// int64 indices (encode_index_payloads over an in-memory SparsePatch).
-// =============================================================================================
-struct EntryMap {
-    const SegDesc* segs;
-    const uint32_t* seg_first;
-    const uint64_t* seg_start;  // [n_segs + 1]
-    uint32_t n_segs;
-    const uint32_t* idx32;      // mode A
-    const int64_t* idx64;       // mode B (segments == tensors, elem_off 0)
-
-    __device__ __forceinline__ uint32_t seg_of(uint64_t i) const {
-        return upper_index<uint64_t>(seg_start, 0, n_segs, i);
-    }
-    __device__ __forceinline__ int64_t local(uint64_t i, uint32_t sg) const {
-        return idx64 ? idx64[i] : int64_t(segs[sg].elem_off + idx32[i]);
-    }
-};
-
-// One entry's COO_DOWNSCALED view (patch.hpp:164-167, index_coding.hpp:117-126).
-struct CooEntry {
-    int64_t row_gap;   // first entry: absolute row
-    int64_t col_val;   // new row: absolute col, else within-row gap
-    int64_t row, col;
-};
-
-__device__ __forceinline__ void coo_view(int64_t L, int64_t cols, int64_t& row, int64_t& col) {
-    if (L >= 0 && L < (int64_t(1) << 32) && cols < (int64_t(1) << 32)) {
-        const uint32_t q = uint32_t(L) / uint32_t(cols);
-        row = q;
-        col = int64_t(uint32_t(L) - q * uint32_t(cols));
-    } else {
-        row = L / cols;
-        col = L % cols;
-    }
-}
-
-// Walks entries [i0, i1) of one thread, calling f(i, t, j, L, Lprev) where t is
-// the tensor, j the ordinal inside the tensor, Lprev the previous entry's
-// local index in the same tensor (-1 when j == 0).
-template <class F>
-__device__ __forceinline__ void for_entries(const EntryMap& em, uint64_t i0, uint64_t i1, F&& f) {
-    if (i0 >= i1) return;
-    uint32_t sg = em.seg_of(i0);
-    uint32_t t = em.segs[sg].tensor;
-    uint64_t ts = em.seg_start[em.seg_first[t]];
-    int64_t Lprev = -1;
-    if (i0 > ts) {
-        const uint32_t sp = em.seg_of(i0 - 1);
-        Lprev = em.local(i0 - 1, sp);
-    }
-    for (uint64_t i = i0; i < i1; ++i) {
-        while (em.seg_start[sg + 1] <= i) {
-            ++sg;
-            const uint32_t nt = em.segs[sg].tensor;
-            if (nt != t) {
-                t = nt;
-                ts = em.seg_start[em.seg_first[t]];
-                Lprev = -1;
-            }
-        }
-        const int64_t L = em.local(i, sg);
-        f(i, t, i - ts, L, Lprev);
-        Lprev = L;
-    }
-}
-
-// =============================================================================================
-// K2a: escape counts (COO_DOWNSCALED) + argument validation (host indices)
-// =============================================================================================
-__global__ void __launch_bounds__(kThreads)
-k2_escapes(EntryMap em, const uint64_t* __restrict__ cols_ext, uint32_t repr,
-           uint2* __restrict__ chunk_esc, uint32_t* __restrict__ t_resc, uint32_t* __restrict__ t_cesc,
-           uint64_t* __restrict__ err) {
-    __shared__ uint64_t s_warp[kWarps];
-    const uint64_t n = em.seg_start[em.n_segs];
-    const uint64_t n_chunks = (n + kChunkEntries - 1) / kChunkEntries;
-    const bool coo = repr == PULSE_COO_DOWNSCALED;
-    for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
-        const uint64_t i0 = c * kChunkEntries + uint64_t(threadIdx.x) * kEntriesPerThread;
-        const uint64_t i1 = min(i0 + kEntriesPerThread, n);
-        uint32_t r_esc = 0, c_esc = 0;
-        for_entries(em, i0, i1, [&](uint64_t, uint32_t t, uint64_t j, int64_t L, int64_t Lp) {
-            const int64_t cols = int64_t(cols_ext[t]);
-            int64_t row = 0, col = 0, prow = 0, pcol = 0;
-            if (coo) {
-                coo_view(L, cols, row, col);
-                if (j > 0) coo_view(Lp, cols, prow, pcol);
-            }
-            // argument checks: only host indices can violate them (K1 output is
-            // sorted by construction).  Same check order as the reference.
-            if (em.idx64) {
-                if (repr == PULSE_COO_INT32) {  // delta_encode_indices, index_coding.hpp:18-25
-                    if (L < 0) { report(err, error_key(t, kStageRows, j, kArgNegative)); return; }
-                    if (j > 0 && L <= Lp) { report(err, error_key(t, kStageRows, j, kArgOrder)); return; }
-                } else if (repr == PULSE_FLAT_INT32) {  // patch.hpp:139-147 (first entry: k2_layout)
-                    if (j > 0 && L <= Lp) { report(err, error_key(t, kStageRows, j, kArgOrder)); return; }
-                    if (j > 0 && L - Lp > 0xFFFFFFFFll) { report(err, error_key(t, kStageRows, j, kDimFlatGap)); return; }
-                } else {  // downscale_coo, index_coding.hpp:117-121
-                    if (row < 0 || col < 0) { report(err, error_key(t, kStageRows, j, kArgNegative)); return; }
-                    if (j > 0 && (row < prow || (row == prow && col <= pcol))) {
-                        report(err, error_key(t, kStageRows, j, kArgOrder));
-                        return;
-                    }
-                }
-            }
-            if (!coo) return;
-            const int64_t rg = j == 0 ? row : row - prow;
-            const bool new_row = j == 0 || row != prow;
-            const int64_t cv = new_row ? col : col - pcol;
-            if (rg > 0xFFFFFFFFll) report(err, error_key(t, kStageRows, j, kDimRow));
-            if (cv > 0xFFFFFFFFll) report(err, error_key(t, kStageCols, j, kDimCol));
-            if (rg >= 0xFF) { ++r_esc; atomicAdd(t_resc + t, 1u); }
-            if (cv >= 0xFFFF) { ++c_esc; atomicAdd(t_cesc + t, 1u); }
-        });
-        if (coo) {
-            uint64_t tot;
-            block_exclusive<SumOp>(uint64_t(r_esc) | uint64_t(c_esc) << 32, s_warp, tot);
-            if (threadIdx.x == 0) chunk_esc[c] = make_uint2(uint32_t(tot), uint32_t(tot >> 32));
-        }
-    }
-}
-
-// =============================================================================================
-// K2L: layout (one CTA of 1024 threads)
-// =============================================================================================
-constexpr int kLayoutThreads = 1024;
-
-template <int NT>
-__device__ __forceinline__ uint64_t cta_exclusive(uint64_t v, uint64_t* s_tmp, uint64_t& total) {
-    // generic block exclusive sum for NT threads (NT/32 <= 32)
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t inc = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint64_t o = __shfl_up_sync(0xffffffffu, inc, off);
-        if (lane >= off) inc += o;
-    }
-    if (lane == 31) s_tmp[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        uint64_t w = lane < NT / 32 ? s_tmp[lane] : 0, wi = w;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint64_t o = __shfl_up_sync(0xffffffffu, wi, off);
-            if (lane >= off) wi += o;
-        }
-        if (lane < NT / 32) s_tmp[32 + lane] = wi - w;
-        if (lane == 31) s_tmp[64] = wi;
-    }
-    __syncthreads();
-    const uint64_t r = s_tmp[32 + warp] + inc - v;
-    total = s_tmp[64];
-    __syncthreads();
-    return r;
-}
-
-template <int NT>
-__device__ __forceinline__ int64_t cta_inclusive_max(int64_t v, int64_t* s_tmp, int64_t& total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int64_t inc = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const int64_t o = __shfl_up_sync(0xffffffffu, inc, off);
-        if (lane >= off) inc = max(inc, o);
-    }
-    if (lane == 31) s_tmp[warp] = inc;
-    __syncthreads();
-    int64_t before = -1, all = -1;
-    for (int w = 0; w < NT / 32; ++w) {
-        if (w < warp) before = max(before, s_tmp[w]);
-        all = max(all, s_tmp[w]);
-    }
-    total = all;
-    __syncthreads();
-    return max(before, inc);
-}
-
-struct LayoutArgs {
-    EntryMap em;
-    uint32_t n_tensors;
-    const uint64_t* numel;
-    uint32_t repr;
-    const uint2* chunk_esc;
-    ulonglong2* chunk_pre;
-    const uint32_t* t_resc;
-    const uint32_t* t_cesc;
-    TensorLayout* tlay;
-    const pulse_scan_summary* gathered;  // may be null
-    uint32_t n_ranks, rank;
-    uint64_t body_cap;
-    pulse_patch_entry* entries;
-    pulse_result* result;
-    uint64_t* err;
-    uint64_t cap;  // K1 capacity (mode A); ~0 for mode B
-};
-
-__global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
-    __shared__ uint64_t s_tmp[72];
-    __shared__ int64_t s_max[32];
-    const int tid = threadIdx.x;
-    const EntryMap& em = a.em;
-    const uint64_t n = em.seg_start[em.n_segs];
-    const bool coo = a.repr == PULSE_COO_DOWNSCALED;
-    const bool overflow = n > a.cap;
-
-    // (1) COO_DOWNSCALED: exclusive scan of chunk escape counts.
-    if (coo && !overflow) {
-        const uint64_t n_chunks = (n + kChunkEntries - 1) / kChunkEntries;
-        const uint64_t per = (n_chunks + kLayoutThreads - 1) / kLayoutThreads;
-        const uint64_t c0 = min(n_chunks, per * tid), c1 = min(n_chunks, c0 + per);
-        uint64_t r = 0, c = 0;
-        for (uint64_t k = c0; k < c1; ++k) { r += a.chunk_esc[k].x; c += a.chunk_esc[k].y; }
-        uint64_t tr, tc;
-        uint64_t er = cta_exclusive<kLayoutThreads>(r, s_tmp, tr);
-        uint64_t ec = cta_exclusive<kLayoutThreads>(c, s_tmp, tc);
-        for (uint64_t k = c0; k < c1; ++k) {
-            a.chunk_pre[k] = make_ulonglong2(er, ec);
-            er += a.chunk_esc[k].x;
-            ec += a.chunk_esc[k].y;
-        }
-    }
-
-    // FLAT carry from earlier shards.
-    uint64_t carry_has = 0, carry_gap = 0;
-    if (a.gathered) {
-        for (int q = int(a.rank) - 1; q >= 0; --q) {
-            if (a.gathered[q].has_change) { carry_has = 1; carry_gap = a.gathered[q].last_gap_base; break; }
-        }
-    }
-
-    // (2) per-tensor sizes and offsets, 1024 tensors per round.
-    uint64_t body_base = 0, rts_base = 0, cts_base = 0, entry_base = 0;
-    int64_t prev_changed = -1;  // last changed tensor of earlier rounds
-    for (uint32_t t0 = 0; t0 < a.n_tensors; t0 += kLayoutThreads) {
-        const uint32_t t = t0 + tid;
-        const bool valid = t < a.n_tensors;
-        uint64_t count = 0, resc = 0, cesc = 0, idx_nb = 0;
-        if (valid) {
-            count = em.seg_start[em.seg_first[t + 1]] - em.seg_start[em.seg_first[t]];
-            if (coo) {
-                resc = a.t_resc[t];
-                cesc = a.t_cesc[t];
-                idx_nb = 3 * count + 4 * (resc + cesc);
-            } else {
-                idx_nb = 4 * count;
-            }
-        }
-        const bool changed = count > 0 && !overflow;
-        uint64_t tb, tr, tc, te;
-        const uint64_t eb = cta_exclusive<kLayoutThreads>(changed ? idx_nb + 2 * count : 0, s_tmp, tb);
-        const uint64_t er = cta_exclusive<kLayoutThreads>(resc, s_tmp, tr);
-        const uint64_t ec = cta_exclusive<kLayoutThreads>(cesc, s_tmp, tc);
-        const uint64_t ee = cta_exclusive<kLayoutThreads>(changed ? 1 : 0, s_tmp, te);
-        int64_t mx;
-        const int64_t pc_incl = cta_inclusive_max<kLayoutThreads>(changed ? int64_t(t) : -1, s_max, mx);
-        // previous changed tensor strictly before t
-        int64_t pc = prev_changed;
-        {
-            // exclusive max: recompute from the inclusive value of the left neighbour
-            const int64_t left = __shfl_up_sync(0xffffffffu, pc_incl, 1);
-            int64_t cand;
-            if ((tid & 31) != 0) cand = left;
-            else {
-                // first lane of a warp: max over earlier warps (recomputed from s_max)
-                cand = -1;
-                for (int w = 0; w < (tid >> 5); ++w) cand = max(cand, s_max[w]);
-            }
-            pc = max(pc, cand);
-        }
-        if (valid) {
-            TensorLayout L;
-            L.idx_off = body_base + eb;
-            L.val_off = L.idx_off + idx_nb;
-            L.row_bytes = count + 4 * resc;
-            L.rts = rts_base + er;
-            L.cts = cts_base + ec;
-            L.count_nz = changed;
-            L.has_prev = 0;
-            L.gap_base = 0;
-            if (a.repr == PULSE_FLAT_INT32) {
-                if (pc >= 0) {
-                    // last local index of tensor pc
-                    const uint64_t last_i = em.seg_start[em.seg_first[pc + 1]] - 1;
-                    const uint32_t sg = em.seg_of(last_i);
-                    L.has_prev = 1;
-                    L.gap_base = a.numel[pc] - uint64_t(em.local(last_i, sg));
-                } else if (carry_has) {
-                    L.has_prev = 1;
-                    L.gap_base = carry_gap;
-                }
-            }
-            a.tlay[t] = L;
-            if (changed) {
-                if (a.repr != PULSE_COO_DOWNSCALED && a.numel[t] >= (1ull << 31))
-                    report(a.err, error_key(t, kStageTensor, 0, kDimInt32));
-                if (a.repr == PULSE_FLAT_INT32) {
-                    const uint32_t sg = em.seg_of(em.seg_start[em.seg_first[t]]);
-                    const int64_t first = em.local(em.seg_start[em.seg_first[t]], sg);
-                    // patch.hpp:141-147 for the tensor's first entry
-                    const int64_t entry = first + int64_t(L.has_prev ? L.gap_base : 0);
-                    if (entry < 0 || (L.has_prev && entry == 0))
-                        report(a.err, error_key(t, kStageRows, 0, kArgOrder));
-                    else if (entry > 0xFFFFFFFFll)
-                        report(a.err, error_key(t, kStageRows, 0, kDimFlatGap));
-                }
-                pulse_patch_entry e;
-                e.tensor = t;
-                e.reserved = 0;
-                e.count = count;
-                e.idx_off = L.idx_off;
-                e.idx_nbytes = idx_nb;
-                e.val_off = L.idx_off + idx_nb;
-                a.entries[entry_base + ee] = e;
-            }
-        }
-        body_base += tb;
-        rts_base += tr;
-        cts_base += tc;
-        entry_base += te;
-        prev_changed = max(prev_changed, mx);
-        __syncthreads();
-    }
-
-    if (tid == 0) {
-        pulse_result r;
-        r.n_changes = n;
-        r.body_bytes = body_base;
-        r.n_entries = uint32_t(entry_base);
-        r.err_tensor = 0;
-        r.err_elem = 0;
-        r.err_check = 0;
-        r.err_stage = 0;
-        r.required = 0;
-        r.status = 0;
-        // FLAT continuation for the next shard
-        if (prev_changed >= 0) {
-            const uint64_t last_i = n - 1;
-            const uint32_t sg = em.seg_of(last_i);
-            r.carry_out.has_prev = 1;
-            r.carry_out.gap_base = a.numel[prev_changed] - uint64_t(em.local(last_i, sg));
-        } else {
-            r.carry_out.has_prev = carry_has;
-            r.carry_out.gap_base = carry_gap;
-        }
-        const uint64_t k = *a.err;
-        if (overflow) {
-            r.status = PULSE_E_CAPACITY;
-            r.required = n;
-        } else if (k != kNoError) {
-            r.status = check_status(key_check(k));
-            r.err_check = key_check(k);
-            r.err_stage = key_stage(k);
-            r.err_tensor = key_tensor(k);
-            r.err_elem = key_elem(k);
-        } else if (body_base > a.body_cap) {
-            r.status = PULSE_E_CAPACITY;
-            r.required = body_base;
-        }
-        *a.result = r;
-    }
-}
-
-// =============================================================================================
-// K2b: emit body bytes
-// =============================================================================================
-__global__ void __launch_bounds__(kThreads)
-k2_emit(EntryMap em, const uint64_t* __restrict__ cols_ext, uint32_t repr,
-        const TensorLayout* __restrict__ tlay, const ulonglong2* __restrict__ chunk_pre,
-        const uint16_t* __restrict__ vals, const pulse_result* __restrict__ result,
-        uint8_t* __restrict__ body) {
-    __shared__ uint64_t s_warp[kWarps];
-    if (result->status != 0) return;
-    const uint64_t n = em.seg_start[em.n_segs];
-    const uint64_t n_chunks = (n + kChunkEntries - 1) / kChunkEntries;
-    for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
-        const uint64_t i0 = c * kChunkEntries + uint64_t(threadIdx.x) * kEntriesPerThread;
-        const uint64_t i1 = min(i0 + kEntriesPerThread, n);
-        if (repr == PULSE_COO_DOWNSCALED) {
-            // pass 1: this thread's escape counts -> block exclusive -> global prefix
-            uint32_t r_esc = 0, c_esc = 0;
-            for_entries(em, i0, i1, [&](uint64_t, uint32_t t, uint64_t j, int64_t L, int64_t Lp) {
-                const int64_t cols = int64_t(cols_ext[t]);
-                int64_t row, col, prow = 0, pcol = 0;
-                coo_view(L, cols, row, col);
-                if (j > 0) coo_view(Lp, cols, prow, pcol);
-                const bool new_row = j == 0 || row != prow;
-                r_esc += (j == 0 ? row : row - prow) >= 0xFF;
-                c_esc += (new_row ? col : col - pcol) >= 0xFFFF;
-            });
-            uint64_t tot;
-            const uint64_t ex = block_exclusive<SumOp>(uint64_t(r_esc) | uint64_t(c_esc) << 32, s_warp, tot);
-            uint64_t R = chunk_pre[c].x + (ex & 0xFFFFFFFFull);
-            uint64_t Cc = chunk_pre[c].y + (ex >> 32);
-            // pass 2: row entry, col entry and value of every change
-            for_entries(em, i0, i1, [&](uint64_t i, uint32_t t, uint64_t j, int64_t L, int64_t Lp) {
-                const TensorLayout& tl = tlay[t];
-                const int64_t cols = int64_t(cols_ext[t]);
-                int64_t row, col, prow = 0, pcol = 0;
-                coo_view(L, cols, row, col);
-                if (j > 0) coo_view(Lp, cols, prow, pcol);
-                const uint64_t rg = uint64_t(j == 0 ? row : row - prow);
-                const bool new_row = j == 0 || row != prow;
-                const uint64_t cv = uint64_t(new_row ? col : col - pcol);
-                uint8_t* rp = body + tl.idx_off + j + 4 * (R - tl.rts);
-                if (rg >= 0xFF) { rp[0] = 0xFF; wr_u32(rp + 1, uint32_t(rg)); ++R; }
-                else rp[0] = uint8_t(rg);
-                uint8_t* cq = body + tl.idx_off + tl.row_bytes + 2 * j + 4 * (Cc - tl.cts);
-                if (cv >= 0xFFFF) { wr_u16(cq, 0xFFFF); wr_u32(cq + 2, uint32_t(cv)); ++Cc; }
-                else wr_u16(cq, uint32_t(cv));
-                wr_u16(body + tl.val_off + 2 * j, vals[i]);
-            });
-        } else {
-            for_entries(em, i0, i1, [&](uint64_t i, uint32_t t, uint64_t j, int64_t L, int64_t Lp) {
-                const TensorLayout& tl = tlay[t];
-                uint64_t g;
-                if (j > 0) g = uint64_t(L - Lp);
-                else g = uint64_t(L) + (repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0);
-                wr_u32(body + tl.idx_off + 4 * j, uint32_t(g));
-                wr_u16(body + tl.val_off + 2 * j, vals[i]);
-            });
-        }
-    }
-}
-
-// =============================================================================================
 // launchers
 // =============================================================================================
 static int g_sms = 0;
@@ -1208,46 +775,6 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
         }
     }
     k1_finalize<<<1, 32, 0, s>>>(p.segs, p.n_segs, p.numel, p.seg_start, p.idx32, p.cap, p.scan, copy_out);
-}
-
-static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, bool validate_args,
-                        const pulse_scan_summary* gathered, uint32_t n_ranks, uint32_t rank,
-                        const uint16_t* vals, uint8_t* body, uint64_t body_cap,
-                        pulse_patch_entry* entries, pulse_result* result, uint64_t cap, cudaStream_t s) {
-    const unsigned grid = unsigned(sm_count() * 8);
-    cudaMemsetAsync(p.t_resc, 0, p.n_tensors * sizeof(uint32_t), s);
-    cudaMemsetAsync(p.t_cesc, 0, p.n_tensors * sizeof(uint32_t), s);
-    cudaMemsetAsync(p.err, 0xFF, sizeof(uint64_t), s);
-    if (repr == PULSE_COO_DOWNSCALED || validate_args)
-        k2_escapes<<<grid, kThreads, 0, s>>>(em, p.cols, repr, p.chunk_esc, p.t_resc, p.t_cesc, p.err);
-    LayoutArgs a;
-    a.em = em;
-    a.n_tensors = p.n_tensors;
-    a.numel = p.numel;
-    a.repr = repr;
-    a.chunk_esc = p.chunk_esc;
-    a.chunk_pre = p.chunk_pre;
-    a.t_resc = p.t_resc;
-    a.t_cesc = p.t_cesc;
-    a.tlay = p.tlay;
-    a.gathered = gathered;
-    a.n_ranks = n_ranks;
-    a.rank = rank;
-    a.body_cap = body_cap;
-    a.entries = entries;
-    a.result = result;
-    a.err = p.err;
-    a.cap = cap;
-    k2_layout<<<1, kLayoutThreads, 0, s>>>(a);
-    k2_emit<<<grid, kThreads, 0, s>>>(em, p.cols, repr, p.tlay, p.chunk_pre, vals, result, body);
-}
-
-void launch_encode_emit(const PlanDev& p, uint32_t repr, const pulse_scan_summary* gathered,
-                        uint32_t n_ranks, uint32_t rank, uint8_t* body, uint64_t body_cap,
-                        pulse_patch_entry* entries, pulse_result* result, cudaStream_t s) {
-    EntryMap em{p.segs, p.seg_first, p.seg_start, p.n_segs, p.idx32, nullptr};
-    emit_common(p, em, repr, false, gathered, n_ranks, rank, p.val16, body, body_cap, entries, result,
-                p.cap, s);
 }
 
 PULSE_DEFINE_WATCHDOG_SETTER(set_watchdog_encode)

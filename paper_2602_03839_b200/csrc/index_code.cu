@@ -1,0 +1,740 @@
+// PULSE index coding on sm_100a (K2): the raw index payloads of
+// encode_index_payloads (patch.hpp:116-174) and the value payloads, written
+// straight into the identity-codec PULP body (patch_file.hpp:76-82).
+//
+//   K2a k2_scan_escapes  COO_DOWNSCALED: per warp of 256 entries and per chunk
+//                        of 2048, the number of row / column entries that need
+//                        the 0xFF / 0xFFFF escape (index_coding.hpp:68-90), plus
+//                        the argument checks the reference applies to
+//                        caller-provided indices.
+//   K2L k2_layout        one CTA: exclusive scan of the chunk escape counts,
+//                        per-tensor payload sizes and body offsets, FLAT_INT32
+//                        cross-tensor gap bases (patch.hpp:131-156).
+//   K2b k2_emit          single pass: every row/column entry (or u32 gap) and
+//                        every value, at its final byte offset.
+//
+// Entries are walked warp-contiguously: warp w of a 2048-entry chunk owns 256
+// consecutive entries, 8 rounds of 32 (lane l -> entry round*32 + l).  Loads are
+// coalesced, the previous entry (delta coding) comes from a shuffle, and the
+// segment/tensor context is warp-uniform and reloaded only at boundaries.
+#include <algorithm>
+
+#include "device.cuh"
+#include "internal.hpp"
+
+namespace pulse {
+namespace dev {
+
+// ---- entry sources -------------------------------------------------------------------------
+// Compacted K1 output (segment-relative u32) or caller int64 indices
+// (encode_index_payloads over an in-memory SparsePatch; segments == tensors).
+struct EntryMap {
+    const SegDesc* segs;
+    const uint32_t* seg_first;
+    const uint64_t* seg_start;  // [n_segs + 1] entry offsets
+    uint32_t n_segs;
+    const uint32_t* idx32;
+    const int64_t* idx64;
+    const ColDiv* coldiv;       // per tensor
+    const uint64_t* numel;      // per tensor
+    const TensorLayout* tlay;   // per tensor (emit only; may be null)
+};
+
+// Division of a local index by the tensor's column extent (patch.hpp:165-166):
+// 32-bit magic multiply when both fit, 64-bit division otherwise.
+__device__ __forceinline__ void coo_split(int64_t L, const ColDiv& cd, int64_t& row, int64_t& col) {
+    if (!cd.wide && L >= 0 && L < (int64_t(1) << 32)) {
+        const uint32_t n = uint32_t(L);
+        const uint32_t q = uint32_t((uint64_t(__umulhi(n, cd.magic)) + n) >> cd.shift);
+        row = q;
+        col = int64_t(n - q * cd.cols32);
+    } else {
+        const int64_t c = int64_t(cd.cols);
+        row = L / c;
+        col = L % c;
+    }
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Warp-uniform context of the segment a round starts in.
+struct SegCtx {
+    uint32_t sg, t;
+    uint64_t hi;        // first entry after the segment
+    uint64_t ts;        // first entry of the tensor
+    uint64_t elem_off;  // segment offset inside the tensor
+    bool fast;          // 32-bit fast path allowed: tensor < 2^32 elements, compacted input
+    uint32_t cols32, magic, shift;
+    TensorLayout tl;    // emit only
+};
+
+__device__ __forceinline__ SegCtx load_ctx(const EntryMap& em, uint32_t sg) {
+    SegCtx c;
+    c.sg = sg;
+    c.hi = em.seg_start[sg + 1];
+    const SegDesc d = em.segs[sg];
+    c.t = d.tensor;
+    c.elem_off = d.elem_off;
+    c.ts = em.seg_start[em.seg_first[d.tensor]];
+    const ColDiv cd = em.coldiv[d.tensor];
+    c.cols32 = cd.cols32;
+    c.magic = cd.magic;
+    c.shift = cd.shift;
+    c.fast = !em.idx64 && !cd.wide && em.numel[d.tensor] < (1ull << 32);
+    if (em.tlay) c.tl = em.tlay[d.tensor];
+    return c;
+}
+
+__device__ __forceinline__ uint32_t div_magic(uint32_t n, uint32_t magic, uint32_t shift) {
+    return uint32_t((uint64_t(__umulhi(n, magic)) + n) >> shift);
+}
+
+// One entry of a round, with its predecessor in the same tensor.
+struct Ent {
+    bool valid;
+    uint32_t t;
+    uint64_t i, j;      // global entry, ordinal inside the tensor
+    int64_t L, Lp;      // local index; previous local index (-1 when j == 0)
+};
+
+constexpr uint32_t kRangeEntries = 4096;  // entries per warp range (K2)
+
+struct Walker {
+    const EntryMap& em;
+    uint64_t n, base, end;
+    SegCtx ctx;
+    int64_t carry_L;   // previous round's lane-31 L (same tensor when j > 0)
+    uint32_t cur[8];   // this lane's compacted indices for the current batch of 8 rounds
+    uint32_t nxt[8];   // ... and the next batch (prefetched)
+
+    __device__ __forceinline__ void fetch(uint32_t (&dst)[8], uint64_t b) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const uint64_t i = b + uint64_t(r) * 32 + lane;
+            dst[r] = i < end ? em.idx32[i] : 0;
+        }
+    }
+
+    __device__ Walker(const EntryMap& e, uint64_t n_, uint64_t first, uint64_t last)
+        : em(e), n(n_), base(first), end(min(last, n_)) {
+        if (!em.idx64) {
+            fetch(cur, first);
+            fetch(nxt, first + 256);
+        }
+        const uint64_t f = first < n ? first : (n ? n - 1 : 0);
+        ctx = load_ctx(em, em.n_segs ? upper_index<uint64_t>(em.seg_start, 0, em.n_segs, f) : 0);
+        carry_L = -1;
+        if (first > 0 && first < n) {
+            const uint32_t sp = upper_index<uint64_t>(em.seg_start, 0, em.n_segs, first - 1);
+            carry_L = em.idx64 ? em.idx64[first - 1] : int64_t(em.segs[sp].elem_off + em.idx32[first - 1]);
+        }
+    }
+
+    __device__ __forceinline__ bool done() const { return base >= end; }
+
+    // Warp-uniform: the whole round lies in the current segment and the 32-bit
+    // fast path applies.
+    __device__ __forceinline__ bool fast_round() const { return ctx.fast && base + 32 <= ctx.hi; }
+
+    // Fast-path round: this lane's ordinal j, local index L, predecessor Lp
+    // (shuffled; lane 0 from the previous round).  Advances the walker.
+    __device__ __forceinline__ void fast_step(int rr, uint32_t& j, uint32_t& L, uint32_t& Lp, bool& valid) {
+        const int lane = threadIdx.x & 31;
+        valid = base + lane < end;
+        j = uint32_t(base - ctx.ts) + lane;
+        L = uint32_t(ctx.elem_off) + cur[rr];
+        uint32_t up = __shfl_up_sync(0xffffffffu, L, 1);
+        if (lane == 0) up = uint32_t(carry_L);
+        Lp = up;
+        carry_L = int64_t(__shfl_sync(0xffffffffu, L, 31));
+        base += 32;
+    }
+
+    // Round `rr` (0..7) of the current batch; call with a compile-time rr
+    // (unrolled loop) so the batch arrays stay in registers, then rotate().
+    __device__ __forceinline__ Ent next(int rr) {
+        const int lane = threadIdx.x & 31;
+        Ent r;
+        r.i = base + lane;
+        r.valid = r.i < end;
+        uint32_t t = ctx.t;
+        uint64_t ts = ctx.ts, eoff = ctx.elem_off;
+        uint32_t sg = ctx.sg;
+        const bool crosses = base + 32 > ctx.hi && ctx.hi < end;  // warp-uniform
+        if (crosses && r.valid && r.i >= ctx.hi) {  // rare: walk to this lane's segment
+            while (em.seg_start[sg + 1] <= r.i) ++sg;
+            const SegDesc d = em.segs[sg];
+            t = d.tensor;
+            eoff = d.elem_off;
+            ts = em.seg_start[em.seg_first[t]];
+        }
+        r.t = t;
+        r.j = r.i - ts;
+        r.L = !r.valid ? 0 : em.idx64 ? em.idx64[r.i] : int64_t(eoff + cur[rr]);
+        int64_t up = __shfl_up_sync(0xffffffffu, r.L, 1);
+        if (lane == 0) up = carry_L;
+        r.Lp = (r.valid && r.j > 0) ? up : -1;
+        carry_L = __shfl_sync(0xffffffffu, r.L, 31);
+        if (crosses) {
+            const uint32_t last_sg = __shfl_sync(0xffffffffu, sg, 31);
+            if (last_sg != ctx.sg) ctx = load_ctx(em, last_sg);
+        }
+        base += 32;
+        return r;
+    }
+
+    __device__ __forceinline__ void rotate() {  // next batch becomes current; prefetch the one after
+        if (!em.idx64) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+            fetch(nxt, base + 256);
+        }
+    }
+};
+
+// COO_DOWNSCALED fields of an entry: row gap (first: absolute row) and column
+// entry (absolute on a new row, else within-row gap), index_coding.hpp:117-126.
+// The predecessor's (row, col) comes from the neighbouring lane.
+struct Coo {
+    int64_t rg, cv;
+};
+
+struct CooWalker {
+    int64_t carry_row = 0, carry_col = 0;
+    __device__ __forceinline__ Coo fields(const Ent& r, const ColDiv& cd) {
+        const int lane = threadIdx.x & 31;
+        int64_t row = 0, col = 0;
+        if (r.valid) coo_split(r.L, cd, row, col);
+        int64_t prow = __shfl_up_sync(0xffffffffu, row, 1), pcol = __shfl_up_sync(0xffffffffu, col, 1);
+        if (lane == 0) {
+            prow = carry_row;
+            pcol = carry_col;
+        }
+        carry_row = __shfl_sync(0xffffffffu, row, 31);
+        carry_col = __shfl_sync(0xffffffffu, col, 31);
+        Coo f;
+        const bool new_row = r.j == 0 || row != prow;
+        f.rg = r.j == 0 ? row : row - prow;
+        f.cv = new_row ? col : col - pcol;
+        return f;
+    }
+};
+
+// =============================================================================================
+// K2a
+// =============================================================================================
+__global__ void __launch_bounds__(kThreads)
+k2_scan_escapes(EntryMap em, uint32_t repr, uint64_t* __restrict__ range_cnt, uint32_t* __restrict__ t_resc,
+                uint32_t* __restrict__ t_cesc, uint64_t* __restrict__ err) {
+    const uint64_t n = em.seg_start[em.n_segs];
+    const uint64_t n_ranges = (n + kRangeEntries - 1) / kRangeEntries;
+    const bool coo = repr == PULSE_COO_DOWNSCALED;
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = uint64_t(gridDim.x) * kWarps;
+    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5); rg < n_ranges; rg += stride) {
+        const uint64_t first = rg * kRangeEntries;
+        Walker w(em, n, first, first + kRangeEntries);
+        CooWalker cw;
+        uint32_t re = 0, ce = 0;
+        bool seeded = false;
+        while (!w.done()) {
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) {
+            if (seeded && w.fast_round()) {
+                if (coo) {
+                    uint32_t j, L, Lp;
+                    bool valid;
+                    w.fast_step(rr, j, L, Lp, valid);
+                    const uint32_t row = div_magic(L, w.ctx.magic, w.ctx.shift);
+                    const uint32_t col = L - row * w.ctx.cols32;
+                    uint32_t prow = __shfl_up_sync(0xffffffffu, row, 1), pcol = __shfl_up_sync(0xffffffffu, col, 1);
+                    if (lane == 0) {
+                        prow = uint32_t(cw.carry_row);
+                        pcol = uint32_t(cw.carry_col);
+                    }
+                    cw.carry_row = __shfl_sync(0xffffffffu, row, 31);
+                    cw.carry_col = __shfl_sync(0xffffffffu, col, 31);
+                    const bool nr = j == 0 || row != prow;
+                    const uint32_t rgap = j == 0 ? row : row - prow;
+                    const uint32_t cval = nr ? col : col - pcol;
+                    const bool rf = valid && rgap >= 0xFF, cf = valid && cval >= 0xFFFF;
+                    if (rf) atomicAdd(t_resc + w.ctx.t, 1u);
+                    if (cf) atomicAdd(t_cesc + w.ctx.t, 1u);
+                    re += __popc(__ballot_sync(0xffffffffu, rf));
+                    ce += __popc(__ballot_sync(0xffffffffu, cf));
+                } else {
+                    uint32_t j, L, Lp;
+                    bool valid;
+                    w.fast_step(rr, j, L, Lp, valid);
+                }
+                continue;
+            }
+            const Ent r = w.next(rr);
+            const ColDiv cd = em.coldiv[r.t];
+            if (!seeded) {  // predecessor (row, col) of the range's first entry
+                seeded = true;
+                const int64_t Lp0 = __shfl_sync(0xffffffffu, r.Lp, 0);
+                const uint32_t t0 = __shfl_sync(0xffffffffu, r.t, 0);
+                if (coo && Lp0 >= 0) coo_split(Lp0, em.coldiv[t0], cw.carry_row, cw.carry_col);
+            }
+            bool rf = false, cf = false;
+            if (em.idx64 && r.valid) {  // argument checks, in the reference's order
+                if (repr == PULSE_COO_INT32) {  // delta_encode_indices, index_coding.hpp:18-25
+                    if (r.L < 0) report(err, error_key(r.t, kStageRows, r.j, kArgNegative));
+                    else if (r.j > 0 && r.L <= r.Lp) report(err, error_key(r.t, kStageRows, r.j, kArgOrder));
+                } else if (repr == PULSE_FLAT_INT32) {  // patch.hpp:139-147 (first entry: k2_layout)
+                    if (r.j > 0 && r.L <= r.Lp) report(err, error_key(r.t, kStageRows, r.j, kArgOrder));
+                    else if (r.j > 0 && r.L - r.Lp > 0xFFFFFFFFll)
+                        report(err, error_key(r.t, kStageRows, r.j, kDimFlatGap));
+                }
+            }
+            if (coo) {
+                const Coo f = cw.fields(r, cd);
+                if (r.valid) {
+                    if (em.idx64) {  // downscale_coo, index_coding.hpp:117-121
+                        int64_t row, col;
+                        coo_split(r.L, cd, row, col);
+                        if (row < 0 || col < 0) report(err, error_key(r.t, kStageRows, r.j, kArgNegative));
+                        else if (r.j > 0 && r.L <= r.Lp) report(err, error_key(r.t, kStageRows, r.j, kArgOrder));
+                    }
+                    if (f.rg > 0xFFFFFFFFll) report(err, error_key(r.t, kStageRows, r.j, kDimRow));
+                    if (f.cv > 0xFFFFFFFFll) report(err, error_key(r.t, kStageCols, r.j, kDimCol));
+                    rf = f.rg >= 0xFF;
+                    cf = f.cv >= 0xFFFF;
+                    if (rf) atomicAdd(t_resc + r.t, 1u);
+                    if (cf) atomicAdd(t_cesc + r.t, 1u);
+                }
+            }
+            re += __popc(__ballot_sync(0xffffffffu, rf));
+            ce += __popc(__ballot_sync(0xffffffffu, cf));
+          }
+          w.rotate();
+        }
+        if (coo && lane == 0) range_cnt[rg] = uint64_t(re) | (uint64_t(ce) << 32);
+    }
+}
+
+// =============================================================================================
+// K2L: layout (one CTA of 1024 threads)
+// =============================================================================================
+constexpr int kLayoutThreads = 1024;
+
+__device__ __forceinline__ uint64_t cta_exclusive(uint64_t v, uint64_t* s_tmp, uint64_t& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += o;
+    }
+    if (lane == 31) s_tmp[warp] = inc;
+    __syncthreads();
+    uint64_t before = 0, all = 0;
+    for (int w = 0; w < kLayoutThreads / 32; ++w) {
+        const uint64_t x = s_tmp[w];
+        if (w < warp) before += x;
+        all += x;
+    }
+    total = all;
+    __syncthreads();
+    return before + inc - v;
+}
+
+__device__ __forceinline__ int64_t cta_exclusive_max(int64_t v, int64_t* s_tmp, int64_t& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int64_t o = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc = max(inc, o);
+    }
+    if (lane == 31) s_tmp[warp] = inc;
+    __syncthreads();
+    int64_t before = -1, all = -1;
+    for (int w = 0; w < kLayoutThreads / 32; ++w) {
+        const int64_t x = s_tmp[w];
+        if (w < warp) before = max(before, x);
+        all = max(all, x);
+    }
+    total = all;
+    int64_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = -1;
+    __syncthreads();
+    return max(before, ex);
+}
+
+struct LayoutArgs {
+    const uint64_t* range_cnt;   // COO: packed (row | col << 32) escapes per 4096-entry warp range
+    ulonglong2* range_pre;       // COO: global escapes before each range
+    EntryMap em;
+    uint32_t n_tensors;
+    const uint64_t* numel;
+    uint32_t repr;
+    const uint32_t* t_resc;
+    const uint32_t* t_cesc;
+    TensorLayout* tlay;
+    const pulse_scan_summary* gathered;  // may be null
+    uint32_t n_ranks, rank;
+    uint64_t body_cap;
+    pulse_patch_entry* entries;
+    pulse_result* result;
+    uint64_t* err;
+    uint64_t cap;  // K1 capacity (mode A); ~0 for mode B
+};
+
+__device__ __forceinline__ int64_t entry_local(const EntryMap& em, uint64_t i) {
+    const uint32_t sg = upper_index<uint64_t>(em.seg_start, 0, em.n_segs, i);
+    return em.idx64 ? em.idx64[i] : int64_t(em.segs[sg].elem_off + em.idx32[i]);
+}
+
+__global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
+    __shared__ uint64_t s_tmp[32];
+    __shared__ int64_t s_max[32];
+    const int tid = threadIdx.x;
+    const EntryMap& em = a.em;
+    const uint64_t n = em.seg_start[em.n_segs];
+    const bool coo = a.repr == PULSE_COO_DOWNSCALED;
+    const bool overflow = n > a.cap;
+
+    // (1) COO_DOWNSCALED: exclusive scan of the per-range escape counts (each
+    // thread sums a contiguous block, one CTA scan, then writes its block)
+    if (coo && !overflow) {
+        const uint64_t n_ranges = (n + kRangeEntries - 1) / kRangeEntries;
+        const uint64_t per = (n_ranges + kLayoutThreads - 1) / kLayoutThreads;
+        const uint64_t q0 = min(n_ranges, per * tid), q1 = min(n_ranges, q0 + per);
+        uint64_t sr = 0, sc = 0;
+        for (uint64_t q = q0; q < q1; ++q) {
+            const uint64_t v = a.range_cnt[q];
+            sr += v & 0xFFFFFFFFull;
+            sc += v >> 32;
+        }
+        uint64_t tr, tc;
+        uint64_t er = cta_exclusive(sr, s_tmp, tr);
+        uint64_t ec = cta_exclusive(sc, s_tmp, tc);
+        for (uint64_t q = q0; q < q1; ++q) {
+            const uint64_t v = a.range_cnt[q];
+            a.range_pre[q] = make_ulonglong2(er, ec);
+            er += v & 0xFFFFFFFFull;
+            ec += v >> 32;
+        }
+    }
+
+    // FLAT carry from earlier shards
+    uint64_t carry_has = 0, carry_gap = 0;
+    if (a.gathered) {
+        for (int q = int(a.rank) - 1; q >= 0; --q) {
+            if (a.gathered[q].has_change) {
+                carry_has = 1;
+                carry_gap = a.gathered[q].last_gap_base;
+                break;
+            }
+        }
+    }
+
+    uint64_t body_base = 0, rts_base = 0, cts_base = 0, entry_base = 0;
+    int64_t prev_changed = -1;  // last changed tensor of earlier rounds
+    for (uint32_t t0 = 0; t0 < a.n_tensors; t0 += kLayoutThreads) {
+        const uint32_t t = t0 + tid;
+        const bool valid = t < a.n_tensors;
+        uint64_t count = 0, resc = 0, cesc = 0, idx_nb = 0;
+        if (valid) {
+            count = em.seg_start[em.seg_first[t + 1]] - em.seg_start[em.seg_first[t]];
+            if (coo) {
+                resc = a.t_resc[t];
+                cesc = a.t_cesc[t];
+                idx_nb = 3 * count + 4 * (resc + cesc);
+            } else {
+                idx_nb = 4 * count;
+            }
+        }
+        const bool changed = count > 0 && !overflow;
+        uint64_t tb, tr, tc, te;
+        const uint64_t eb = cta_exclusive(changed ? idx_nb + 2 * count : 0, s_tmp, tb);
+        const uint64_t er = cta_exclusive(resc, s_tmp, tr);
+        const uint64_t ec = cta_exclusive(cesc, s_tmp, tc);
+        const uint64_t ee = cta_exclusive(changed ? 1 : 0, s_tmp, te);
+        int64_t mx;
+        const int64_t pc_round = cta_exclusive_max(changed ? int64_t(t) : -1, s_max, mx);
+        const int64_t pc = max(prev_changed, pc_round);  // previous changed tensor before t
+        if (valid) {
+            TensorLayout L;
+            L.idx_off = body_base + eb;
+            L.val_off = L.idx_off + idx_nb;
+            L.row_bytes = count + 4 * resc;
+            L.rts = rts_base + er;
+            L.cts = cts_base + ec;
+            L.count_nz = changed;
+            L.has_prev = 0;
+            L.gap_base = 0;
+            if (a.repr == PULSE_FLAT_INT32) {
+                if (pc >= 0) {
+                    const uint64_t last_i = em.seg_start[em.seg_first[pc + 1]] - 1;
+                    L.has_prev = 1;
+                    L.gap_base = a.numel[pc] - uint64_t(entry_local(em, last_i));
+                } else if (carry_has) {
+                    L.has_prev = 1;
+                    L.gap_base = carry_gap;
+                }
+            }
+            a.tlay[t] = L;
+            if (changed) {
+                if (a.repr != PULSE_COO_DOWNSCALED && a.numel[t] >= (1ull << 31))
+                    report(a.err, error_key(t, kStageTensor, 0, kDimInt32));
+                if (a.repr == PULSE_FLAT_INT32) {
+                    // patch.hpp:141-147 for the tensor's first entry
+                    const int64_t first = entry_local(em, em.seg_start[em.seg_first[t]]);
+                    const int64_t entry = first + int64_t(L.has_prev ? L.gap_base : 0);
+                    if (entry < 0 || (L.has_prev && entry == 0))
+                        report(a.err, error_key(t, kStageRows, 0, kArgOrder));
+                    else if (entry > 0xFFFFFFFFll)
+                        report(a.err, error_key(t, kStageRows, 0, kDimFlatGap));
+                }
+                pulse_patch_entry e;
+                e.tensor = t;
+                e.reserved = 0;
+                e.count = count;
+                e.idx_off = L.idx_off;
+                e.idx_nbytes = idx_nb;
+                e.val_off = L.idx_off + idx_nb;
+                a.entries[entry_base + ee] = e;
+            }
+        }
+        body_base += tb;
+        rts_base += tr;
+        cts_base += tc;
+        entry_base += te;
+        prev_changed = max(prev_changed, mx);
+        __syncthreads();
+    }
+
+    if (tid == 0) {
+        pulse_result r{};
+        r.n_changes = n;
+        r.body_bytes = body_base;
+        r.n_entries = uint32_t(entry_base);
+        if (prev_changed >= 0) {  // FLAT continuation for the next shard
+            r.carry_out.has_prev = 1;
+            r.carry_out.gap_base = a.numel[prev_changed] - uint64_t(entry_local(em, n - 1));
+        } else {
+            r.carry_out.has_prev = carry_has;
+            r.carry_out.gap_base = carry_gap;
+        }
+        const uint64_t k = *a.err;
+        if (overflow) {
+            r.status = PULSE_E_CAPACITY;
+            r.err_check = kCapacity;
+            r.required = n;
+        } else if (k != kNoError) {
+            r.status = check_status(key_check(k));
+            r.err_check = key_check(k);
+            r.err_stage = key_stage(k);
+            r.err_tensor = key_tensor(k);
+            r.err_elem = key_elem(k);
+        } else if (body_base > a.body_cap) {
+            r.status = PULSE_E_CAPACITY;
+            r.err_check = kCapacity;
+            r.required = body_base;
+        }
+        *a.result = r;
+    }
+}
+
+// =============================================================================================
+// K2b: emit
+// =============================================================================================
+__device__ __forceinline__ void st_u16_any(uint8_t* p, uint32_t v) {
+    if ((reinterpret_cast<uintptr_t>(p) & 1) == 0) *reinterpret_cast<uint16_t*>(p) = uint16_t(v);
+    else wr_u16(p, v);
+}
+__device__ __forceinline__ void st_u32_any(uint8_t* p, uint32_t v) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    if ((a & 3) == 0) {
+        *reinterpret_cast<uint32_t*>(p) = v;
+    } else if ((a & 1) == 0) {
+        reinterpret_cast<uint16_t*>(p)[0] = uint16_t(v);
+        reinterpret_cast<uint16_t*>(p)[1] = uint16_t(v >> 16);
+    } else {
+        wr_u32(p, v);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
+        const ulonglong2* __restrict__ range_pre, const uint16_t* __restrict__ vals,
+        const pulse_result* __restrict__ result, uint8_t* __restrict__ body) {
+    if (result->status != 0) return;
+    const uint64_t n = em.seg_start[em.n_segs];
+    const uint64_t n_ranges = (n + kRangeEntries - 1) / kRangeEntries;
+    const int lane = threadIdx.x & 31;
+    const bool coo = repr == PULSE_COO_DOWNSCALED;
+    const uint64_t stride = uint64_t(gridDim.x) * kWarps;
+    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5); rg < n_ranges; rg += stride) {
+        const uint64_t first = rg * kRangeEntries;
+        Walker w(em, n, first, first + kRangeEntries);
+        CooWalker cw;
+        uint64_t R = 0, Cc = 0;
+        if (coo) {
+            const ulonglong2 p = range_pre[rg];
+            R = p.x;
+            Cc = p.y;
+        }
+        bool seeded = false;
+        while (!w.done()) {
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) {
+            if (seeded && w.fast_round()) {
+                const TensorLayout& tl = w.ctx.tl;
+                const uint64_t i = w.base + lane;
+                uint32_t j, L, Lp;
+                bool valid;
+                w.fast_step(rr, j, L, Lp, valid);
+                if (coo) {
+                    const uint32_t row = div_magic(L, w.ctx.magic, w.ctx.shift);
+                    const uint32_t col = L - row * w.ctx.cols32;
+                    uint32_t prow = __shfl_up_sync(0xffffffffu, row, 1), pcol = __shfl_up_sync(0xffffffffu, col, 1);
+                    if (lane == 0) {
+                        prow = uint32_t(cw.carry_row);
+                        pcol = uint32_t(cw.carry_col);
+                    }
+                    cw.carry_row = __shfl_sync(0xffffffffu, row, 31);
+                    cw.carry_col = __shfl_sync(0xffffffffu, col, 31);
+                    const bool nr = j == 0 || row != prow;
+                    const uint32_t rgap = j == 0 ? row : row - prow;
+                    const uint32_t cval = nr ? col : col - pcol;
+                    const bool rf = valid && rgap >= 0xFF, cf = valid && cval >= 0xFFFF;
+                    const uint32_t br = __ballot_sync(0xffffffffu, rf), bc = __ballot_sync(0xffffffffu, cf);
+                    if (valid) {
+                        const uint64_t Ri = R + __popc(br & lanemask_lt());
+                        const uint64_t Ci = Cc + __popc(bc & lanemask_lt());
+                        uint8_t* rp = body + tl.idx_off + j + 4 * (Ri - tl.rts);
+                        if (rf) {
+                            rp[0] = 0xFF;
+                            wr_u32(rp + 1, rgap);
+                        } else {
+                            rp[0] = uint8_t(rgap);
+                        }
+                        uint8_t* cq = body + tl.idx_off + tl.row_bytes + 2ull * j + 4 * (Ci - tl.cts);
+                        if (cf) {
+                            wr_u16(cq, 0xFFFF);
+                            wr_u32(cq + 2, cval);
+                        } else {
+                            st_u16_any(cq, cval);
+                        }
+                        st_u16_any(body + tl.val_off + 2ull * j, vals[i]);
+                    }
+                    R += __popc(br);
+                    Cc += __popc(bc);
+                } else if (valid) {
+                    uint64_t g;
+                    if (j > 0) g = L - Lp;
+                    else g = uint64_t(L) + (repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0);
+                    st_u32_any(body + tl.idx_off + 4ull * j, uint32_t(g));
+                    st_u16_any(body + tl.val_off + 2ull * j, vals[i]);
+                }
+                continue;
+            }
+            const Ent r = w.next(rr);
+            const TensorLayout& tl = tlay[r.t];
+            if (coo) {
+                const ColDiv cd = em.coldiv[r.t];
+                if (!seeded) {
+                    const int64_t Lp0 = __shfl_sync(0xffffffffu, r.Lp, 0);
+                    const uint32_t t0 = __shfl_sync(0xffffffffu, r.t, 0);
+                    if (Lp0 >= 0) coo_split(Lp0, em.coldiv[t0], cw.carry_row, cw.carry_col);
+                }
+                const Coo f = cw.fields(r, cd);
+                const bool rf = r.valid && f.rg >= 0xFF, cf = r.valid && f.cv >= 0xFFFF;
+                const uint32_t br = __ballot_sync(0xffffffffu, rf), bc = __ballot_sync(0xffffffffu, cf);
+                if (r.valid) {
+                    const uint64_t Ri = R + __popc(br & lanemask_lt());
+                    const uint64_t Ci = Cc + __popc(bc & lanemask_lt());
+                    uint8_t* rp = body + tl.idx_off + r.j + 4 * (Ri - tl.rts);
+                    if (rf) {
+                        rp[0] = 0xFF;
+                        wr_u32(rp + 1, uint32_t(f.rg));
+                    } else {
+                        rp[0] = uint8_t(f.rg);
+                    }
+                    uint8_t* cq = body + tl.idx_off + tl.row_bytes + 2 * r.j + 4 * (Ci - tl.cts);
+                    if (cf) {
+                        wr_u16(cq, 0xFFFF);
+                        wr_u32(cq + 2, uint32_t(f.cv));
+                    } else {
+                        st_u16_any(cq, uint32_t(f.cv));
+                    }
+                    st_u16_any(body + tl.val_off + 2 * r.j, vals[r.i]);
+                }
+                R += __popc(br);
+                Cc += __popc(bc);
+            } else if (r.valid) {
+                uint64_t g;
+                if (r.j > 0) g = uint64_t(r.L - r.Lp);
+                else g = uint64_t(r.L) + (repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0);
+                st_u32_any(body + tl.idx_off + 4 * r.j, uint32_t(g));
+                st_u16_any(body + tl.val_off + 2 * r.j, vals[r.i]);
+            }
+            seeded = true;
+          }
+          w.rotate();
+        }
+    }
+}
+
+// =============================================================================================
+// launchers
+// =============================================================================================
+static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, bool validate_args,
+                        const pulse_scan_summary* gathered, uint32_t n_ranks, uint32_t rank,
+                        const uint16_t* vals, uint8_t* body, uint64_t body_cap, pulse_patch_entry* entries,
+                        pulse_result* result, uint64_t cap, cudaStream_t s) {
+    const unsigned grid = unsigned(sm_count() * 4);
+    cudaMemsetAsync(p.t_resc, 0, p.n_tensors * sizeof(uint32_t), s);
+    cudaMemsetAsync(p.t_cesc, 0, p.n_tensors * sizeof(uint32_t), s);
+    cudaMemsetAsync(p.err, 0xFF, sizeof(uint64_t), s);
+    if (repr == PULSE_COO_DOWNSCALED || validate_args)
+        k2_scan_escapes<<<grid, kThreads, 0, s>>>(em, repr, p.range_cnt, p.t_resc, p.t_cesc, p.err);
+    LayoutArgs a;
+    a.range_cnt = p.range_cnt;
+    a.range_pre = p.range_pre;
+    a.em = em;
+    a.n_tensors = p.n_tensors;
+    a.numel = p.numel;
+    a.repr = repr;
+    a.t_resc = p.t_resc;
+    a.t_cesc = p.t_cesc;
+    a.tlay = p.tlay;
+    a.gathered = gathered;
+    a.n_ranks = n_ranks;
+    a.rank = rank;
+    a.body_cap = body_cap;
+    a.entries = entries;
+    a.result = result;
+    a.err = p.err;
+    a.cap = cap;
+    k2_layout<<<1, kLayoutThreads, 0, s>>>(a);
+    k2_emit<<<grid, kThreads, 0, s>>>(em, repr, p.tlay, p.range_pre, vals, result, body);
+}
+
+void launch_encode_emit(const PlanDev& p, uint32_t repr, const pulse_scan_summary* gathered, uint32_t n_ranks,
+                        uint32_t rank, uint8_t* body, uint64_t body_cap, pulse_patch_entry* entries,
+                        pulse_result* result, cudaStream_t s) {
+    EntryMap em{p.segs, p.seg_first, p.seg_start, p.n_segs, p.idx32, nullptr, p.coldiv, p.numel, p.tlay};
+    emit_common(p, em, repr, false, gathered, n_ranks, rank, p.val16, body, body_cap, entries, result, p.cap, s);
+}
+
+void launch_encode_emit_idx64(const PlanDev& p, uint32_t repr, const int64_t* idx64, const uint16_t* vals,
+                              uint8_t* body, uint64_t body_cap, pulse_patch_entry* entries, pulse_result* result,
+                              cudaStream_t s) {
+    EntryMap em{p.id_segs, p.id_first, p.id_start, p.n_tensors, nullptr, idx64, p.coldiv, p.numel, p.tlay};
+    emit_common(p, em, repr, true, nullptr, 1, 0, vals, body, body_cap, entries, result, ~0ull, s);
+}
+
+PULSE_DEFINE_WATCHDOG_SETTER(set_watchdog_index)
+
+}  // namespace dev
+}  // namespace pulse

@@ -34,6 +34,27 @@ struct SegDesc {
 };
 constexpr uint32_t kTicketElems = 65536;
 
+// Division by a tensor's column extent (COO_DOWNSCALED view, patch.hpp:105-109):
+// q = (umulhi(n, magic) + n) >> shift for 32-bit n when cols < 2^32.
+struct ColDiv {
+    uint64_t cols;
+    uint32_t cols32, magic, shift, wide;
+};
+
+inline ColDiv make_coldiv(uint64_t cols) {
+    ColDiv d{};
+    d.cols = cols;
+    d.wide = cols >= (1ull << 32);
+    if (!d.wide) {
+        d.cols32 = uint32_t(cols);
+        uint32_t l = 0;
+        while ((1ull << l) < cols) ++l;  // ceil(log2(cols))
+        d.shift = l;
+        d.magic = uint32_t(((unsigned __int128)1 << 32) * ((1ull << l) - cols) / cols + 1);
+    }
+    return d;
+}
+
 // Per-tensor encode layout (written by the layout kernel).
 struct TensorLayout {
     uint64_t idx_off;     // byte offset of the index payload in the body
@@ -80,8 +101,9 @@ struct PlanDev {
     uint64_t* k1_status;        // [n_tiles]
     uint64_t* counters;         // [8] tickets
     pulse_scan_summary* scan;   // device
-    uint2* chunk_esc;           // [cap/2048+1]
-    ulonglong2* chunk_pre;      // [cap/2048+1]
+    const ColDiv* coldiv;       // [T]
+    uint64_t* range_cnt;        // [cap/4096 + 2] packed (row | col << 32) escapes per 4096-entry warp range
+    ulonglong2* range_pre;      // [cap/4096 + 2] global (row, col) escapes before each range
     uint32_t* t_resc;           // [T]
     uint32_t* t_cesc;           // [T]
     TensorLayout* tlay;         // [T]
@@ -105,6 +127,7 @@ struct PlanDev {
     uint64_t d_status_len;      // words per region
     uint64_t dec_bytes_cap;     // max index-payload bytes a decode may parse
     uint64_t* d_totals;         // [16] totals + tickets
+    uint32_t* d_flags;          // [4] flags[0]: patch needs the general (escape-aware) decoder
 };
 
 // ---- launchers (stream-ordered, no host sync) -------------------------------------------
@@ -119,13 +142,16 @@ void launch_decode(const PlanDev& p, uint32_t repr, const uint8_t* body,
                    pulse_result* result, cudaStream_t s);
 // Validate caller-provided int64 indices (decode over an in-memory SparsePatch,
 // patch.hpp:325-336) and scatter values into `weights_slot`.
+void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uint32_t n_entries,
+                       const pulse_flat_carry* carry, int weights_slot, int64_t* out_indices, uint32_t* flags,
+                       cudaStream_t s);
 void launch_apply_idx64(const PlanDev& p, const int64_t* idx64, const uint16_t* vals,
                         const pulse_patch_entry* entries, uint32_t n_entries, int weights_slot,
                         pulse_result* result, cudaStream_t s);
 
 // Host-index encode (index coding of caller-provided int64 indices, the
 // reference's encode_index_payloads over a host SparsePatch).
-void launch_encode_emit_idx64(const PlanDev& p, uint32_t repr, const int64_t* idx64,
+void launch_encode_emit_idx64(const PlanDev& p, uint32_t repr, const int64_t* idx64, const uint16_t* vals,
                               uint8_t* body, uint64_t body_cap, pulse_patch_entry* entries,
                               pulse_result* result, cudaStream_t s);
 
@@ -133,6 +159,8 @@ int sm_count();
 void set_watchdog_encode(unsigned long long* slot);
 void set_watchdog_decode(unsigned long long* slot);
 void set_watchdog_synth(unsigned long long* slot);
+void set_watchdog_index(unsigned long long* slot);
+void set_watchdog_apply(unsigned long long* slot);
 
 }  // namespace dev
 }  // namespace pulse

@@ -77,6 +77,8 @@ static void install_watchdog(int device) {
         set_watchdog_encode(g_wd_dev);
         set_watchdog_decode(g_wd_dev);
         set_watchdog_synth(g_wd_dev);
+        set_watchdog_index(g_wd_dev);
+        set_watchdog_apply(g_wd_dev);
         done[device] = true;
     }
 }
@@ -164,12 +166,14 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
     A(segs_d, S); A(first_d, T + 1); A(numel_d, T); A(cols_d, T); A(tile_seg_d, tiles); A(ticket_seg_d, tickets);
     for (int s = 0; s < PULSE_MAX_SLOTS; ++s) { uint16_t** sp = nullptr; A(sp, T); p.slot[s] = sp; }
     A(p.idx32, cap); A(p.val16, cap); A(p.seg_start, S + 1); A(p.k1_status, tiles + 1);
-    A(p.counters, 8); A(p.scan, 1); A(p.chunk_esc, n_chunks); A(p.chunk_pre, n_chunks);
+    A(p.counters, 8); A(p.scan, 1);
+    ColDiv* coldiv_d = nullptr; A(coldiv_d, T);
+    A(p.range_cnt, cap / 4096 + 2); A(p.range_pre, cap / 4096 + 2);
     A(p.t_resc, T); A(p.t_cesc, T); A(p.tlay, T); A(p.err, 1); A(p.result, 1);
     A(id_segs_d, T); A(id_first_d, T + 1); A(p.id_start, T + 1);
     A(p.elay, T); A(p.d_es, T + 1); A(p.d_ck, T + 1); A(p.d_cu, T + 1);
     A(p.rowgap, cap); A(p.colent, cap); A(p.flat, cap);
-    A(p.d_status, 4 * p.d_status_len); A(p.d_totals, 16);
+    A(p.d_status, 4 * p.d_status_len); A(p.d_totals, 16); A(p.d_flags, 4);
     if (getenv("PULSE_TRACE")) A(p.trace, tickets);
 #undef A
     if (e != cudaSuccess) {
@@ -177,6 +181,7 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
         return cuda_fail(e, "plan allocation");
     }
     p.segs = segs_d;
+    p.coldiv = coldiv_d;
     p.tile_seg = tile_seg_d;
     p.tma_tile_seg = ticket_seg_d;
     p.seg_first = first_d;
@@ -186,6 +191,9 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
     p.id_first = id_first_d;
 
     std::vector<uint64_t> numel(T), cols(T);
+    std::vector<ColDiv> coldiv(T);
+    for (uint32_t t = 0; t < n_tensors; ++t) coldiv[t] = make_coldiv(tensors[t].cols);
+    cudaMemcpy(coldiv_d, coldiv.data(), T * sizeof(ColDiv), cudaMemcpyHostToDevice);
     std::vector<SegDesc> id_segs(T);
     std::vector<uint32_t> id_first(T + 1);
     for (uint32_t t = 0; t < n_tensors; ++t) {

@@ -20,8 +20,14 @@ for it in range(int(sys.argv[1])):
         wd = N.watchdog()
         if wd: print('WATCHDOG', it, wd, flush=True); break
 print('scans done', time.time() - t, flush=True)
+bad = 0
 for it in range(int(sys.argv[2])):
     cs, ps = (1, 0) if it % 2 == 0 else (0, 1)
-    plan.scan(cs, ps); plan.emit(patch); patch.fetch(); plan.apply(2, patch)
+    plan.scan(cs, ps); plan.emit(patch); patch.fetch(); res = plan.apply(2, patch)
+    if it < 4:
+        r = D.parse_result(res)
+        ok = torch.equal(w, curr if it % 2 == 0 else prev)
+        print('step', it, 'status', int(r['status']), 'ok', ok, flush=True)
+        bad += not ok
 torch.cuda.synchronize()
 print('steps done', time.time() - t, N.watchdog(), bool(torch.equal(w, prev if int(sys.argv[2]) % 2 == 0 else curr)), flush=True)
