@@ -227,11 +227,13 @@ def run_pulse(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
+    from paper_2602_03839_b200.shard import ShardedPulse
+
     tensors = workload(args.workload)
     d_total = sum(numel(s) for _, s in tensors)
-    bounds = shard(tensors, world)
-    mine = tensors[bounds[rank]:bounds[rank + 1]]
-    sizes = [numel(s) for _, s in mine]
+    sp = ShardedPulse(tensors, max_change_frac=(1 - args.sparsity) * 1.02)
+    mine = sp.mine
+    sizes = sp.sizes
     D_el = sum(sizes)
     assert all(n % 8 == 0 for n in sizes), "tensors must keep 16-byte alignment in the arena"
 
@@ -240,21 +242,15 @@ def run_pulse(args):
     curr = torch.empty_like(prev)
     w = torch.empty_like(prev)
     D.synth_base(prev, seed=args.seed + 7919 * rank)
-    n_mut = D.synth_mutate(prev, curr, args.sparsity, args.cluster_width, seed=args.seed + 104729 * rank) if D_el else 0
+    D.synth_mutate(prev, curr, args.sparsity, args.cluster_width, seed=args.seed + 104729 * rank) if D_el else 0
     w.copy_(prev)
     offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
     views = lambda buf: [buf[int(offs[i]):int(offs[i + 1])] for i in range(len(sizes))]
-    cap = int(D_el * (1 - args.sparsity) * 1.02) + 65536
-    plan = D.DevicePlan([(n, s[-1]) for n, (_, s) in zip(sizes, mine)], cap)
-    plan.bind(0, views(prev))
-    plan.bind(1, views(curr))
-    plan.bind(2, views(w))
-    patch = plan.new_patch(args.repr)
-    send = torch.zeros(32, dtype=torch.uint8, device=dev)
-    gathered = torch.zeros(32 * world, dtype=torch.uint8, device=dev)
+    sp.bind(0, views(prev))
+    sp.bind(1, views(curr))
+    sp.bind(2, views(w))
+    patch = sp.new_patch(args.repr)
     stream = torch.cuda.current_stream()
-    carry_h = torch.zeros(16, dtype=torch.uint8).pin_memory()
-    carry_d = torch.zeros(16, dtype=torch.uint8, device=dev)
 
     ev = {k: [] for k in ("s0", "s1", "a0", "a1")}
     state = {"body": 0, "changes": 0}
@@ -264,31 +260,16 @@ def run_pulse(args):
         if record:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-        plan.scan(cs, ps, summary_out=send)
+        sp.plan.scan(cs, ps, summary_out=sp.send)
         if record:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record(stream)
-        if world > 1:  # size exchange: all ranks' scan summaries (NCCL over NVLink)
-            dist.all_gather_into_tensor(gathered, send)
-            plan.emit(patch, gathered=gathered, n_ranks=world, rank=rank)
-        else:
-            plan.emit(patch)
-        patch.fetch()  # entry table -> host (PULP header fields); syncs
-        carry = None
-        if world > 1 and args.repr == 2:
-            g = gathered.cpu().numpy().view(D.N.SUMMARY_DTYPE)
-            hp, gb = 0, 0
-            for q in range(rank - 1, -1, -1):
-                if g[q]["has_change"]:
-                    hp, gb = 1, int(g[q]["last_gap_base"])
-                    break
-            carry_h.numpy().view(np.uint64)[:] = [hp, gb]
-            carry_d.copy_(carry_h, non_blocking=True)
-            carry = carry_d
+        # K1 summaries all-gathered (NCCL), K2, entry table to host, size exchange (NCCL)
+        sec = sp.encode_after_scan(patch)
         if record:
             a0 = torch.cuda.Event(enable_timing=True)
             a0.record(stream)
-        plan.apply(2, patch, carry=carry)
+        sp.apply(2, sec)
         if record:
             a1 = torch.cuda.Event(enable_timing=True)
             a1.record(stream)
@@ -362,7 +343,7 @@ def run_pulse(args):
         # dominant kernel K1: reads both snapshots (4 B/elem) + writes 6 B per change (u32 idx + u16 value)
         k1_bytes = 4 * D_el + 6 * state["changes"]
         k1_gbs = k1_bytes / (scan_ms / 1e3) / 1e9
-        n_apply = 7 if args.repr == 0 else 4
+        n_apply = 6  # d_layout, f_range_agg, f_range_scan, f_apply x2, d_finalize (general-path kernels exit early)
         n_emit = 3 if args.repr == 0 else 2
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,

@@ -1,0 +1,188 @@
+"""Multi-GPU PULSE: the state dict sharded by tensor, one process per GPU.
+
+The name-sorted tensor list is cut into contiguous, byte-balanced ranges
+(`shapes.shard`), so the rank-major concatenation of the per-rank patch
+sections *is* the PULP blob area in name order (patch_file.hpp:34-35, 76-82).
+Every rank encodes and applies its own shard independently; NCCL over NVLink
+carries only:
+
+  1. an all-gather of the 32-byte per-rank scan summaries after K1 -- the
+     FLAT_INT32 stream continues across ranks (patch.hpp:131-156: each rank's
+     first gap is relative to the previous rank's last changed index);
+  2. an all-gather of (body bytes, entries) after K2 -- the size exchange that
+     places every section in the final patch;
+  3. optionally, a gather of the sections to one rank (point-to-point
+     send/recv; NCCL has no gatherv) to assemble the full PULP body there.
+
+The exchange helpers take/return torch tensors and work with any
+torch.distributed backend (NCCL on GPUs, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .shapes import numel, shard
+
+SUMMARY_BYTES = 32  # pulse_scan_summary
+SIZES_FIELDS = 2    # (body_bytes, n_entries)
+
+
+# ---- exchange logic (device-agnostic) ---------------------------------------------------------
+def flat_carry(summaries: np.ndarray, rank: int):
+    """(has_prev, gap_base) for `rank` from all ranks' scan summaries
+    (structured array with has_change / last_gap_base): the nearest earlier
+    rank that emitted an index continues the FLAT_INT32 gap stream."""
+    for q in range(rank - 1, -1, -1):
+        if int(summaries[q]["has_change"]):
+            return 1, int(summaries[q]["last_gap_base"])
+    return 0, 0
+
+
+def section_offsets(body_bytes, n_entries):
+    """Byte offset and first entry index of every rank's section in the full
+    patch (rank-major)."""
+    b = np.asarray(body_bytes, dtype=np.int64)
+    e = np.asarray(n_entries, dtype=np.int64)
+    return np.concatenate([[0], np.cumsum(b)])[:-1], np.concatenate([[0], np.cumsum(e)])[:-1]
+
+
+def all_gather_bytes(local: torch.Tensor, world: int) -> torch.Tensor:
+    out = torch.empty(world * local.numel(), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, local)
+    return out
+
+
+def exchange_sizes(body_bytes: int, n_entries: int, device) -> tuple[np.ndarray, np.ndarray]:
+    """Size exchange: every rank learns every section's (body bytes, entries)."""
+    world = dist.get_world_size()
+    t = torch.tensor([body_bytes, n_entries], dtype=torch.int64, device=device)
+    g = all_gather_bytes(t, world).view(world, SIZES_FIELDS).cpu().numpy()
+    return g[:, 0], g[:, 1]
+
+
+def gather_sections(section: torch.Tensor, sizes, root: int = 0):
+    """Gather every rank's section (uint8, `sizes[r]` bytes) to `root`; returns
+    the concatenation on root, None elsewhere."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if rank == root:
+        total = int(np.sum(sizes))
+        out = torch.empty(max(1, total), dtype=torch.uint8, device=section.device)
+        offs, _ = section_offsets(sizes, np.zeros(len(sizes)))
+        ops = []
+        for q in range(world):
+            n = int(sizes[q])
+            if n == 0:
+                continue
+            dst = out[int(offs[q]):int(offs[q]) + n]
+            if q == rank:
+                dst.copy_(section[:n])
+            else:
+                ops.append(dist.P2POp(dist.irecv, dst, q))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        return out[:total]
+    n = int(sizes[rank])
+    if n:
+        for r in dist.batch_isend_irecv([dist.P2POp(dist.isend, section[:n].contiguous(), root)]):
+            r.wait()
+    return None
+
+
+# ---- the sharded driver ------------------------------------------------------------------------
+@dataclass
+class Section:
+    patch: object                 # device.DevicePatch of this rank
+    summaries: np.ndarray         # all ranks' scan summaries
+    body_bytes: np.ndarray        # all ranks' section sizes
+    n_entries: np.ndarray
+    carry: tuple                  # this rank's FLAT carry (has_prev, gap_base)
+
+
+class ShardedPulse:
+    """One rank's view of a sharded state dict: its tensors, its plan, and the
+    collectives that tie the sections together."""
+
+    def __init__(self, tensors, max_change_frac: float = 0.0102, device=None):
+        from . import device as D
+
+        self.D = D
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.tensors = list(tensors)
+        self.bounds = shard(self.tensors, self.world)
+        self.mine = self.tensors[self.bounds[self.rank]:self.bounds[self.rank + 1]]
+        self.sizes = [numel(s) for _, s in self.mine]
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        cap = int(sum(self.sizes) * max_change_frac) + 65536
+        self.plan = D.DevicePlan([(n, s[-1]) for n, (_, s) in zip(self.sizes, self.mine)], cap)
+        self.send = torch.zeros(SUMMARY_BYTES, dtype=torch.uint8, device=self.device)
+        self.gathered = torch.zeros(SUMMARY_BYTES * self.world, dtype=torch.uint8, device=self.device)
+        self.carry_dev = torch.zeros(16, dtype=torch.uint8, device=self.device)
+        self._carry_host = torch.zeros(16, dtype=torch.uint8).pin_memory()
+
+    def bind(self, slot: int, local_tensors):
+        self.plan.bind(slot, local_tensors)
+
+    def new_patch(self, representation: int):
+        return self.plan.new_patch(representation)
+
+    def encode(self, curr_slot: int, prev_slot: int, patch, sizes: bool = True) -> Section:
+        """K1 -> all-gather summaries -> K2 (FLAT continued across ranks) ->
+        D2H of this section's entry table -> size exchange."""
+        self.plan.scan(curr_slot, prev_slot, summary_out=self.send)
+        return self.encode_after_scan(patch, sizes)
+
+    def encode_after_scan(self, patch, sizes: bool = True) -> Section:
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.gathered, self.send)
+            self.plan.emit(patch, gathered=self.gathered, n_ranks=self.world, rank=self.rank)
+        else:
+            self.plan.emit(patch)
+        patch.fetch()
+        if self.world > 1:
+            summ = self.gathered.cpu().numpy().view(self.D.N.SUMMARY_DTYPE)
+        else:
+            summ = self.send.cpu().numpy().view(self.D.N.SUMMARY_DTYPE)
+        carry = flat_carry(summ, self.rank)
+        if sizes and self.world > 1:
+            bb, ne = exchange_sizes(patch.body_bytes, patch.n_entries, self.device)
+        else:
+            bb, ne = np.array([patch.body_bytes]), np.array([patch.n_entries])
+        return Section(patch, summ, bb, ne, carry)
+
+    def apply(self, weights_slot: int, sec: Section):
+        """Validate-then-scatter this rank's section into its resident shard."""
+        carry = None
+        if sec.patch.representation == 2 and sec.carry[0]:
+            self._carry_host.numpy().view(np.uint64)[:] = sec.carry
+            self.carry_dev.copy_(self._carry_host, non_blocking=True)
+            carry = self.carry_dev
+        return self.plan.apply(weights_slot, sec.patch, carry=carry)
+
+    def gather(self, sec: Section, root: int = 0):
+        """Full PULP body and entry table (global tensor ids) on `root`."""
+        body = gather_sections(sec.patch.body, sec.body_bytes, root)
+        n = int(sec.patch.n_entries)
+        ent = torch.from_numpy(sec.patch.host_entries[:n].view(np.uint8).copy()).to(self.device)
+        # entries are variable-count per rank: pad to the max and all-gather
+        mx = int(np.max(sec.n_entries)) if len(sec.n_entries) else 0
+        pad = torch.zeros(max(1, mx) * 40, dtype=torch.uint8, device=self.device)
+        pad[: ent.numel()] = ent
+        allent = all_gather_bytes(pad, self.world).cpu().numpy() if self.world > 1 else pad.cpu().numpy()
+        if self.rank != root:
+            return None, None
+        boffs, _ = section_offsets(sec.body_bytes, sec.n_entries)
+        rows = []
+        per = max(1, mx) * 40
+        for q in range(self.world):
+            e = allent[q * per:q * per + int(sec.n_entries[q]) * 40].view(self.D.N.ENTRY_DTYPE).copy()
+            e["tensor"] += np.uint32(self.bounds[q])
+            e["idx_off"] += np.uint64(boffs[q])
+            e["val_off"] += np.uint64(boffs[q])
+            rows.append(e)
+        return body, (np.concatenate(rows) if rows else np.zeros(0, self.D.N.ENTRY_DTYPE))

@@ -1,0 +1,53 @@
+"""torchrun check: the sharded multi-GPU encode gathered to rank 0 is byte-identical
+to a single-GPU encode of the whole state dict (all three representations), and
+sharded apply reproduces `curr` on every rank.
+
+  python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/check_shard.py
+"""
+import os, sys
+import numpy as np
+import torch
+import torch.distributed as dist
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_03839_b200 import device as D
+from paper_2602_03839_b200.shapes import workload, numel
+from paper_2602_03839_b200.shard import ShardedPulse
+
+local = int(os.environ.get('LOCAL_RANK', 0))
+torch.cuda.set_device(local)
+dist.init_process_group('nccl', device_id=torch.device('cuda', local))
+rank, world = dist.get_rank(), dist.get_world_size()
+tensors = workload(sys.argv[1] if len(sys.argv) > 1 else 'qwen2.5-1.5b')
+sizes = [numel(s) for _, s in tensors]
+offs = np.concatenate([[0], np.cumsum(sizes)])
+prev = torch.empty(int(offs[-1]), dtype=torch.int16, device='cuda'); curr = torch.empty_like(prev)
+D.synth_base(prev, seed=77); D.synth_mutate(prev, curr, 0.99, 64, seed=78)
+sp = ShardedPulse(tensors)
+lo, hi = sp.bounds[rank], sp.bounds[rank + 1]
+view = lambda b: [b[int(offs[i]):int(offs[i + 1])] for i in range(lo, hi)]
+w = prev.clone()
+sp.bind(0, view(prev)); sp.bind(1, view(curr)); sp.bind(2, view(w))
+ok = True
+full = None
+if rank == 0:
+    full = D.DevicePlan([(n, s[-1]) for n, (_, s) in zip(sizes, tensors)], int(offs[-1] * 0.0102) + 65536)
+    full.bind(0, [prev[int(offs[i]):int(offs[i + 1])] for i in range(len(sizes))])
+    full.bind(1, [curr[int(offs[i]):int(offs[i + 1])] for i in range(len(sizes))])
+for repr_ in (0, 1, 2):
+    patch = sp.new_patch(repr_)
+    sec = sp.encode(1, 0, patch)
+    body, ents = sp.gather(sec)
+    w.copy_(prev)
+    res = D.parse_result(sp.apply(2, sec))
+    good = int(res['status']) == 0 and all(torch.equal(a, b) for a, b in zip(view(w), view(curr)))
+    if rank == 0:
+        ref = full.encode(1, 0, repr_)
+        same_body = torch.equal(body, ref.body[:ref.body_bytes])
+        same_ent = np.array_equal(ents, ref.host_entries[:ref.n_entries])
+        print(f'repr {repr_}: sections {list(sec.body_bytes)} gathered == single-GPU body: {same_body}, entries: {same_ent}', flush=True)
+        ok = ok and same_body and same_ent
+    t = torch.tensor([int(good)], device='cuda'); dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if rank == 0: print(f'repr {repr_}: sharded apply exact on all ranks: {bool(t.item())}', flush=True)
+    ok = ok and bool(t.item())
+if rank == 0: print('CHECK_SHARD', 'PASS' if ok else 'FAIL', flush=True)
+dist.destroy_process_group()
