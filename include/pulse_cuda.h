@@ -209,6 +209,103 @@ pulse_status pulse_synth_mutate(pulse_context* ctx, const uint16_t* dev_base, ui
                                 uint64_t n, double sparsity, uint64_t cluster_width,
                                 uint64_t seed, uint64_t* changed_out, void* stream);
 
+/* ======================================================================= */
+/* Host-buffer API: the reference's functions over host memory              */
+/* ======================================================================= */
+
+/* One named bf16 tensor, row-major (checkpoint.hpp:18-28 TensorRecord). */
+typedef struct pulse_tensor {
+    const char* name;     /* NUL-terminated */
+    const int64_t* shape;
+    uint32_t rank;
+    const uint16_t* data; /* numel bf16 bit patterns */
+    uint64_t numel;       /* data length; validated against shape */
+} pulse_tensor;
+
+/* A snapshot at one optimizer step (checkpoint.hpp:32-71 Checkpoint). */
+typedef struct pulse_checkpoint {
+    uint64_t step;
+    const pulse_tensor* tensors;
+    uint32_t n_tensors;
+} pulse_checkpoint;
+
+/* SparsePatch (patch.hpp:54-70), library-owned. */
+typedef struct pulse_patch pulse_patch;
+typedef struct pulse_patch_header {
+    int64_t base_step, target_step, anchor_step;
+    uint32_t representation, codec;
+    uint8_t target_hash[32];
+} pulse_patch_header;
+/* TensorPatch view (patch.hpp:45-52); pointers stay valid until the patch is freed. */
+typedef struct pulse_tensor_patch {
+    const char* name;
+    const int64_t* shape;
+    uint32_t rank;
+    const int64_t* indices;
+    uint64_t n_indices;
+    const uint16_t* values;
+    uint64_t n_values;
+} pulse_tensor_patch;
+
+pulse_status pulse_patch_new(pulse_patch** out);
+void pulse_patch_free(pulse_patch* patch);
+pulse_status pulse_patch_get_header(const pulse_patch* patch, pulse_patch_header* out);
+pulse_status pulse_patch_set_header(pulse_patch* patch, const pulse_patch_header* header);
+uint32_t pulse_patch_num_tensors(const pulse_patch* patch);
+pulse_status pulse_patch_get_tensor(const pulse_patch* patch, uint32_t i, pulse_tensor_patch* out);
+pulse_status pulse_patch_add_tensor(pulse_patch* patch, const pulse_tensor_patch* tensor); /* copies */
+
+/* Library-owned byte buffer (the reference's Bytes, wire.hpp:15). */
+typedef struct pulse_bytes pulse_bytes;
+const uint8_t* pulse_bytes_data(const pulse_bytes* b);
+uint64_t pulse_bytes_size(const pulse_bytes* b);
+void pulse_bytes_free(pulse_bytes* b);
+
+/* encode(current, previous, repr, codec) -- patch.hpp:264-307.  Bitwise diff
+ * and compaction on the GPU (K1); target_hash = SHA-256 of `current`
+ * (sha256.hpp:93-116) on a host thread in parallel. */
+pulse_status pulse_encode(const pulse_checkpoint* current, const pulse_checkpoint* previous,
+                          uint32_t representation, uint32_t codec, pulse_patch** out);
+
+/* decode(previous, patch, verify_hash) -- patch.hpp:309-348.  The result has
+ * previous's tensors (same order, same shapes); out_data[i] receives tensor i's
+ * numel values.  Validation precedes any scatter (IndexRangeError etc.). */
+pulse_status pulse_decode(const pulse_checkpoint* previous, const pulse_patch* patch, int verify_hash,
+                          uint16_t* const* out_data, uint64_t* out_step);
+
+/* encode_index_payloads -- patch.hpp:116-174.  All payloads concatenated in
+ * patch order; sizes[i] = payload i's length (array of num_tensors). */
+pulse_status pulse_encode_index_payloads(const pulse_patch* patch, pulse_bytes** concat, uint64_t* sizes);
+
+/* decode_index_payloads -- patch.hpp:178-262.  Fills each tensor's indices;
+ * each tensor's count is its number of values. */
+pulse_status pulse_decode_index_payloads(pulse_patch* patch, const uint8_t* const* payloads,
+                                         const uint64_t* sizes, uint32_t n_payloads);
+
+/* write_patch_bytes / read_patch_bytes -- patch_file.hpp:30-83 / 85-147. */
+pulse_status pulse_write_patch_bytes(const pulse_patch* patch, pulse_bytes** out);
+pulse_status pulse_read_patch_bytes(const uint8_t* data, uint64_t n, pulse_patch** out);
+
+/* hash_weights -- sha256.hpp:93-116; Sha256 -- sha256.hpp:51-87. */
+pulse_status pulse_hash_weights(const pulse_checkpoint* checkpoint, uint8_t* out32);
+typedef struct pulse_sha256_ctx pulse_sha256_ctx;
+pulse_status pulse_sha256_new(pulse_sha256_ctx** out);
+pulse_status pulse_sha256_update(pulse_sha256_ctx* ctx, const uint8_t* data, uint64_t n);
+pulse_status pulse_sha256_final(pulse_sha256_ctx* ctx, uint8_t* out32);
+void pulse_sha256_free(pulse_sha256_ctx* ctx);
+
+/* Index helpers -- index_coding.hpp:14-50 (delta) and 108-158 (COO downscale). */
+pulse_status pulse_delta_encode_indices(const int64_t* indices, uint64_t n, int64_t* gaps_out);
+pulse_status pulse_delta_decode_indices(const int64_t* gaps, uint64_t n, int64_t* indices_out);
+pulse_status pulse_downscale_coo(const int64_t* rows, uint64_t n_rows, const int64_t* cols, uint64_t n_cols,
+                                 pulse_bytes** out);
+pulse_status pulse_upscale_coo(const uint8_t* payload, uint64_t n, uint64_t count, int64_t* rows_out,
+                               int64_t* cols_out);
+
+/* Codec envelope -- compression.hpp:119-204 (host libzstd / liblz4 / zlib). */
+pulse_status pulse_compress(const uint8_t* raw, uint64_t n, uint32_t codec, pulse_bytes** out);
+pulse_status pulse_decompress(const uint8_t* enveloped, uint64_t n, uint32_t codec, pulse_bytes** out);
+
 #ifdef __cplusplus
 }
 #endif

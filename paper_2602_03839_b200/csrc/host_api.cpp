@@ -1,0 +1,1271 @@
+// Host-buffer C ABI (include/pulse_cuda.h, "host-buffer API"): the reference's
+// functions over host memory, one entry point each.  Every per-element step
+// of the path (diff/compaction, index coding, payload parsing, validation,
+// scatter, and the index helpers) runs in the CUDA kernels; the host keeps what
+// the reference keeps on the host and the GPU cannot reproduce bit-exactly:
+// validation of names/shapes, the PULP JSON header (nlohmann, as the
+// reference), the codec stage (the same libzstd / liblz4 / zlib calls as
+// compression.hpp:79-147) and SHA-256 (OpenSSL EVP, as sha256.hpp:51-87;
+// a serial Merkle-Damgard chain).
+//
+// Inputs are staged to the device through a pinned double buffer; the memcpy
+// into pinned memory is split across a small thread pool.
+#include <openssl/evp.h>
+#include <zlib.h>
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <future>
+#include <memory>
+#include <mutex>
+#include <nlohmann/json.hpp>
+#include <queue>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "errors.hpp"
+#include "internal.hpp"
+#include "plan.hpp"
+
+extern "C" {
+size_t ZSTD_compress(void* dst, size_t dst_capacity, const void* src, size_t src_size, int level);
+size_t ZSTD_decompress(void* dst, size_t dst_capacity, const void* src, size_t src_size);
+size_t ZSTD_compressBound(size_t src_size);
+unsigned ZSTD_isError(size_t code);
+int LZ4_compress_default(const char* src, char* dst, int src_size, int dst_capacity);
+int LZ4_decompress_safe(const char* src, char* dst, int compressed_size, int dst_capacity);
+int LZ4_compressBound(int input_size);
+}
+
+using pulse::fail;
+using namespace pulse::dev;
+
+// ---------------------------------------------------------------------------------------------
+// library-owned objects
+// ---------------------------------------------------------------------------------------------
+struct pulse_bytes {
+    std::vector<uint8_t> v;
+};
+
+struct PatchTensor {
+    std::string name;
+    std::vector<int64_t> shape;
+    std::vector<int64_t> indices;
+    std::vector<uint16_t> values;
+};
+
+struct pulse_patch {
+    int64_t base_step = 0, target_step = 0, anchor_step = 0;
+    uint32_t representation = PULSE_COO_DOWNSCALED, codec = PULSE_ZSTD1;
+    uint8_t target_hash[32] = {};
+    std::vector<PatchTensor> tensors;
+};
+
+struct pulse_sha256_ctx {
+    EVP_MD_CTX* ctx;
+};
+
+namespace {
+
+// A failure with the reference's exception class and message.
+struct Failure {
+    pulse_status st;
+    std::string msg;
+};
+
+[[noreturn]] void raise(pulse_status st, std::string msg) { throw Failure{st, std::move(msg)}; }
+
+template <class F>
+pulse_status guarded(F&& f) {
+    try {
+        f();
+        return PULSE_OK;
+    } catch (const Failure& e) {
+        return fail(e.st, e.msg);
+    } catch (const std::bad_alloc&) {
+        return fail(PULSE_E_ERROR, "out of memory");
+    } catch (const std::exception& e) {
+        return fail(PULSE_E_ERROR, e.what());
+    }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) raise(PULSE_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- thread pool -----------------------------------------------------------------------------
+class Pool {
+public:
+    explicit Pool(unsigned n) {
+        for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    // f(i) for i in [0, n), parallel; returns when all are done.
+    void parallel_for(size_t n, const std::function<void(size_t)>& f) {
+        if (n <= 1 || workers_.empty()) {
+            for (size_t i = 0; i < n; ++i) f(i);
+            return;
+        }
+        std::atomic<size_t> next{0}, done{0};
+        std::mutex m;
+        std::condition_variable c;
+        auto body = [&] {
+            size_t i;
+            while ((i = next.fetch_add(1)) < n) {
+                f(i);
+                if (done.fetch_add(1) + 1 == n) {
+                    std::lock_guard<std::mutex> lk(m);
+                    c.notify_all();
+                }
+            }
+        };
+        const size_t helpers = std::min<size_t>(workers_.size(), n - 1);
+        for (size_t h = 0; h < helpers; ++h) submit(body);
+        body();
+        std::unique_lock<std::mutex> lk(m);
+        c.wait(lk, [&] { return done.load() == n; });
+    }
+
+private:
+    void submit(std::function<void()> f) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            q_.push(std::move(f));
+        }
+        cv_.notify_one();
+    }
+    void loop() {
+        while (true) {
+            std::function<void()> f;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+                if (stop_ && q_.empty()) return;
+                f = std::move(q_.front());
+                q_.pop();
+            }
+            f();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::queue<std::function<void()>> q_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    bool stop_ = false;
+};
+
+Pool& pool() {
+    static Pool p(std::max(2u, std::min(16u, std::thread::hardware_concurrency())) - 1);
+    return p;
+}
+
+void par_memcpy(void* dst, const void* src, size_t n) {
+    constexpr size_t kPiece = 4 << 20;
+    const size_t pieces = (n + kPiece - 1) / kPiece;
+    if (pieces <= 1) {
+        if (n) std::memcpy(dst, src, n);
+        return;
+    }
+    pool().parallel_for(pieces, [&](size_t i) {
+        const size_t off = i * kPiece, len = std::min(kPiece, n - off);
+        std::memcpy(static_cast<uint8_t*>(dst) + off, static_cast<const uint8_t*>(src) + off, len);
+    });
+}
+
+// ---- device buffers + staging ----------------------------------------------------------------
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            const size_t want = std::max<size_t>(bytes + bytes / 8, 1 << 20);
+            cuda_check(cudaMalloc(&p, want), "device arena");
+            cap = want;
+        }
+        return p;
+    }
+    template <class T>
+    T* as(size_t count) { return static_cast<T*>(get(std::max<size_t>(count, 1) * sizeof(T))); }
+};
+
+// Pinned double buffer between pageable host memory and the device.
+class Stager {
+public:
+    static constexpr size_t kChunk = 64u << 20;
+    Stager() {
+        for (int i = 0; i < 2; ++i) {
+            cuda_check(cudaHostAlloc(&buf_[i], kChunk, cudaHostAllocDefault), "pinned staging");
+            cuda_check(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming), "event");
+        }
+    }
+    void h2d(void* dst, const void* src, size_t n, cudaStream_t s) {
+        if (n < (1 << 20)) {
+            cuda_check(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s), "H2D");
+            return;
+        }
+        for (size_t off = 0, k = 0; off < n; off += kChunk, ++k) {
+            const int b = int(k & 1);
+            const size_t len = std::min(kChunk, n - off);
+            cuda_check(cudaEventSynchronize(ev_[b]), "staging wait");
+            par_memcpy(buf_[b], static_cast<const uint8_t*>(src) + off, len);
+            cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, buf_[b], len, cudaMemcpyHostToDevice, s), "H2D");
+            cuda_check(cudaEventRecord(ev_[b], s), "event");
+        }
+    }
+    void d2h(void* dst, const void* src, size_t n, cudaStream_t s) {
+        if (n < (1 << 20)) {
+            cuda_check(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s), "D2H");
+            cuda_check(cudaStreamSynchronize(s), "D2H sync");
+            return;
+        }
+        // two chunks in flight: copy k+1 runs while k is unpacked
+        const size_t chunks = (n + kChunk - 1) / kChunk;
+        auto issue = [&](size_t k) {
+            const int b = int(k & 1);
+            const size_t off = k * kChunk, len = std::min(kChunk, n - off);
+            cuda_check(cudaMemcpyAsync(buf_[b], static_cast<const uint8_t*>(src) + off, len, cudaMemcpyDeviceToHost, s), "D2H");
+            cuda_check(cudaEventRecord(ev_[b], s), "event");
+        };
+        issue(0);
+        for (size_t k = 0; k < chunks; ++k) {
+            if (k + 1 < chunks) issue(k + 1);
+            const int b = int(k & 1);
+            cuda_check(cudaEventSynchronize(ev_[b]), "D2H wait");
+            const size_t off = k * kChunk, len = std::min(kChunk, n - off);
+            par_memcpy(static_cast<uint8_t*>(dst) + off, buf_[b], len);
+        }
+    }
+
+private:
+    void* buf_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_[2];
+};
+
+// One per device: context, stream, cached plan and arenas.
+struct Engine {
+    int device = 0;
+    pulse_context* ctx = nullptr;
+    cudaStream_t stream = nullptr;
+    Stager stager;
+    pulse_plan* plan = nullptr;
+    std::vector<pulse_tensor_geom> plan_geom;
+    uint64_t plan_cap = 0;
+    DevBuf arena_a, arena_b, idx64, vals, body, entries, result, misc, out64;
+    std::mutex mu;
+
+    explicit Engine(int dev) : device(dev) {
+        cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+        if (pulse_context_create(dev, &ctx) != PULSE_OK) raise(PULSE_E_CUDA, "context");
+        cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+    }
+
+    pulse_plan* get_plan(const std::vector<pulse_tensor_geom>& geom, uint64_t cap) {
+        const bool same = plan && geom.size() == plan_geom.size() &&
+                          std::equal(geom.begin(), geom.end(), plan_geom.begin(), [](auto& a, auto& b) {
+                              return a.numel == b.numel && a.cols == b.cols;
+                          });
+        if (same && cap <= plan_cap) return plan;
+        if (plan) {
+            cudaStreamSynchronize(stream);
+            pulse_plan_destroy(plan);
+            plan = nullptr;
+        }
+        const uint64_t c = std::max<uint64_t>(cap, 1024);
+        if (pulse_plan_create(ctx, geom.data(), uint32_t(geom.size()), c, &plan) != PULSE_OK)
+            raise(PULSE_E_CUDA, std::string("plan: ") + pulse_last_error());
+        plan_geom = geom;
+        plan_cap = c;
+        return plan;
+    }
+
+    void sync() { cuda_check(cudaStreamSynchronize(stream), "stream sync"); }
+};
+
+Engine& engine() {
+    static std::mutex mu;
+    static std::unordered_map<int, std::unique_ptr<Engine>> engines;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto& e = engines[dev];
+    if (!e) e = std::make_unique<Engine>(dev);
+    cudaSetDevice(dev);
+    return *e;
+}
+
+// ---- checkpoint helpers (checkpoint.hpp:54-80) -----------------------------------------------
+uint64_t shape_numel(const int64_t* shape, uint32_t rank) {
+    uint64_t n = 1;
+    for (uint32_t i = 0; i < rank; ++i) n *= uint64_t(shape[i]);
+    return n;
+}
+
+void validate_checkpoint(const pulse_checkpoint* c) {
+    std::vector<std::string_view> seen;
+    seen.reserve(c->n_tensors);
+    for (uint32_t i = 0; i < c->n_tensors; ++i) {
+        const pulse_tensor& t = c->tensors[i];
+        const std::string name = t.name ? t.name : "";
+        if (name.empty()) raise(PULSE_E_ARGUMENT, "tensor with empty name");
+        if (std::find(seen.begin(), seen.end(), std::string_view(t.name)) != seen.end())
+            raise(PULSE_E_ARGUMENT, "duplicate tensor name: " + name);
+        seen.emplace_back(t.name);
+        if (t.rank == 0) raise(PULSE_E_ARGUMENT, "tensor " + name + " has empty shape");
+        uint64_t n = 1;
+        for (uint32_t k = 0; k < t.rank; ++k) {
+            if (t.shape[k] <= 0) raise(PULSE_E_ARGUMENT, "tensor " + name + " has non-positive extent");
+            n *= uint64_t(t.shape[k]);
+        }
+        if (n != t.numel) raise(PULSE_E_ARGUMENT, "tensor " + name + " shape/data length mismatch");
+    }
+}
+
+std::vector<uint32_t> sorted_order(const pulse_checkpoint* c) {
+    std::vector<uint32_t> o(c->n_tensors);
+    for (uint32_t i = 0; i < c->n_tensors; ++i) o[i] = i;
+    std::stable_sort(o.begin(), o.end(),
+                     [&](uint32_t a, uint32_t b) { return std::strcmp(c->tensors[a].name, c->tensors[b].name) < 0; });
+    return o;
+}
+
+// SHA-256 over raw LE bf16 bytes, tensors in name order (sha256.hpp:93-116).
+void hash_tensors(const std::vector<std::pair<const uint16_t*, uint64_t>>& parts, uint8_t out[32]) {
+    EVP_MD_CTX* ctx = EVP_MD_CTX_new();
+    if (!ctx || EVP_DigestInit_ex(ctx, EVP_sha256(), nullptr) != 1) raise(PULSE_E_ERROR, "failed to initialize SHA-256 context");
+    for (auto& [p, n] : parts)
+        if (n && EVP_DigestUpdate(ctx, p, n * 2) != 1) raise(PULSE_E_ERROR, "SHA-256 update failed");
+    unsigned int len = 0;
+    if (EVP_DigestFinal_ex(ctx, out, &len) != 1 || len != 32) raise(PULSE_E_ERROR, "SHA-256 finalize failed");
+    EVP_MD_CTX_free(ctx);
+}
+
+void hash_checkpoint(const pulse_checkpoint* c, uint8_t out[32]) {
+    std::vector<std::pair<const uint16_t*, uint64_t>> parts;
+    for (uint32_t i : sorted_order(c)) parts.emplace_back(c->tensors[i].data, c->tensors[i].numel);
+    hash_tensors(parts, out);
+}
+
+std::string hex(const uint8_t* h) {
+    static const char* d = "0123456789abcdef";
+    std::string s;
+    for (int i = 0; i < 32; ++i) {
+        s.push_back(d[h[i] >> 4]);
+        s.push_back(d[h[i] & 15]);
+    }
+    return s;
+}
+
+// Arena layout: tensors packed at 16-byte aligned element offsets.
+std::vector<uint64_t> arena_offsets(const std::vector<uint64_t>& numel, uint64_t& total) {
+    std::vector<uint64_t> off(numel.size());
+    uint64_t o = 0;
+    for (size_t i = 0; i < numel.size(); ++i) {
+        off[i] = o;
+        o += (numel[i] + 7) & ~7ull;
+    }
+    total = o;
+    return off;
+}
+
+pulse_result fetch_result(Engine& E, const void* dev_result) {
+    pulse_result r{};
+    cuda_check(cudaMemcpyAsync(&r, dev_result, sizeof(r), cudaMemcpyDeviceToHost, E.stream), "result");
+    E.sync();
+    uint64_t wd[7];
+    if (pulse_watchdog(wd)) raise(PULSE_E_CUDA, "device watchdog fired (kind " + std::to_string(wd[1]) + ")");
+    return r;
+}
+
+// Exception text for a device-detected failure, in the reference's words.
+std::string device_message(const pulse_result& r, const std::string& name, const std::vector<int64_t>* idx) {
+    switch (r.err_check) {
+        case PULSE_CHECK_TRUNCATED: return "unexpected end of data";
+        case PULSE_CHECK_ZERO_GAP: return "zero index gap in tensor '" + name + "'";
+        case PULSE_CHECK_ZERO_COL_GAP: return "non-positive column gap within a row";
+        case PULSE_CHECK_COL_RANGE: return "column index out of range in tensor '" + name + "'";
+        case PULSE_CHECK_INDEX_RANGE: return "index out of range in tensor '" + name + "'";
+        case PULSE_CHECK_TRAILING:
+            return r.err_stage == 3 ? "index payload has trailing bytes" : "downscaled payload has trailing bytes";
+        case PULSE_CHECK_NEGATIVE: return "indices must be non-negative";
+        case PULSE_CHECK_ORDER: return "indices must be strictly increasing";
+        case PULSE_CHECK_FLAT_GAP: return "index gap exceeds 32 bits";
+        case PULSE_CHECK_ROW_GAP: return "row gap exceeds 32 bits";
+        case PULSE_CHECK_COL_ENTRY: return "column entry exceeds 32 bits";
+        case PULSE_CHECK_INT32: return "tensor '" + name + "' is too large for 32-bit indices";
+        case PULSE_CHECK_APPLY_ORDER: return "tensor '" + name + "' indices are not strictly increasing";
+        case PULSE_CHECK_APPLY_RANGE: {
+            std::string v = idx && r.err_elem < idx->size() ? std::to_string((*idx)[r.err_elem]) : "?";
+            return "tensor '" + name + "' index " + v + " out of range";
+        }
+        default: return "capacity exceeded";
+    }
+}
+
+// ---- codecs (compression.hpp:71-204, same libraries and calls) -----------------------------
+std::vector<uint8_t> codec_compress(const uint8_t* raw, size_t n, uint32_t codec) {
+    if (codec == PULSE_IDENTITY) return std::vector<uint8_t>(raw, raw + n);
+    std::vector<uint8_t> out(8);
+    for (int i = 0; i < 8; ++i) out[i] = uint8_t(uint64_t(n) >> (8 * i));
+    if (n == 0) return out;
+    size_t produced = 0;
+    std::vector<uint8_t> stream;
+    switch (codec) {
+        case PULSE_LZ4: {
+            if (n > 0x7E000000) raise(PULSE_E_ARGUMENT, "input too large for lz4 block format");
+            stream.resize(size_t(LZ4_compressBound(int(n))));
+            const int r = LZ4_compress_default(reinterpret_cast<const char*>(raw), reinterpret_cast<char*>(stream.data()),
+                                               int(n), int(stream.size()));
+            if (r <= 0) raise(PULSE_E_ERROR, "lz4 compression failed");
+            produced = size_t(r);
+            break;
+        }
+        case PULSE_ZSTD1:
+        case PULSE_ZSTD3: {
+            stream.resize(ZSTD_compressBound(n));
+            produced = ZSTD_compress(stream.data(), stream.size(), raw, n, codec == PULSE_ZSTD1 ? 1 : 3);
+            if (ZSTD_isError(produced)) raise(PULSE_E_ERROR, "zstd compression failed");
+            break;
+        }
+        case PULSE_GZIP6: {
+            uLongf p = compressBound(uLong(n));
+            stream.resize(size_t(p));
+            if (compress2(stream.data(), &p, raw, uLong(n), 6) != Z_OK) raise(PULSE_E_ERROR, "deflate compression failed");
+            produced = size_t(p);
+            break;
+        }
+        default: raise(PULSE_E_ARGUMENT, "unknown codec");
+    }
+    out.insert(out.end(), stream.begin(), stream.begin() + produced);
+    return out;
+}
+
+std::vector<uint8_t> codec_decompress(const uint8_t* env, size_t n, uint32_t codec) {
+    if (codec == PULSE_IDENTITY) return std::vector<uint8_t>(env, env + n);
+    if (n < 8) raise(PULSE_E_CORRUPT_STREAM, "codec envelope shorter than its size prefix");
+    uint64_t raw = 0;
+    for (int i = 0; i < 8; ++i) raw |= uint64_t(env[i]) << (8 * i);
+    if (raw > (1ull << 40)) raise(PULSE_E_CORRUPT_STREAM, "declared decompressed size is implausible");
+    const uint8_t* body = env + 8;
+    const size_t bn = n - 8;
+    if (raw == 0) {
+        if (bn) raise(PULSE_E_CORRUPT_STREAM, "codec envelope has trailing bytes");
+        return {};
+    }
+    std::vector<uint8_t> out(raw);
+    switch (codec) {
+        case PULSE_LZ4: {
+            if (bn > 0x7E000000) raise(PULSE_E_CORRUPT_STREAM, "lz4 stream is corrupt");
+            const int r = LZ4_decompress_safe(reinterpret_cast<const char*>(body), reinterpret_cast<char*>(out.data()),
+                                              int(bn), int(out.size()));
+            if (r < 0 || uint64_t(r) != raw) raise(PULSE_E_CORRUPT_STREAM, "lz4 stream is corrupt");
+            break;
+        }
+        case PULSE_ZSTD1:
+        case PULSE_ZSTD3: {
+            const size_t r = ZSTD_decompress(out.data(), out.size(), body, bn);
+            if (ZSTD_isError(r) || r != raw) raise(PULSE_E_CORRUPT_STREAM, "zstd stream is corrupt");
+            break;
+        }
+        case PULSE_GZIP6: {
+            uLongf p = uLongf(raw);
+            const int rc = uncompress(out.data(), &p, body, uLong(bn));
+            if (rc != Z_OK || p != raw) raise(PULSE_E_CORRUPT_STREAM, "deflate stream is corrupt");
+            break;
+        }
+        default: raise(PULSE_E_ARGUMENT, "unknown codec");
+    }
+    return out;
+}
+
+const char* repr_name(uint32_t r) {
+    switch (r) {
+        case PULSE_COO_DOWNSCALED: return "COO_DOWNSCALED";
+        case PULSE_COO_INT32: return "COO_INT32";
+        case PULSE_FLAT_INT32: return "FLAT_INT32";
+    }
+    raise(PULSE_E_ARGUMENT, "unknown representation");
+}
+
+// ---- device index coding over a host patch (patch.hpp:116-174) ----------------------------
+// Returns the body (per tensor [index payload][value payload] for tensors with
+// indices) and, per patch tensor, (index payload offset, length).
+struct Coded {
+    std::vector<uint8_t> body;
+    std::vector<std::pair<uint64_t, uint64_t>> payload;  // per tensor; len 0 if no indices
+    std::vector<uint64_t> val_off;                        // per tensor (valid when indices exist)
+};
+
+Coded device_index_code(Engine& E, const pulse_patch* p, bool with_values) {
+    const uint32_t T = uint32_t(p->tensors.size());
+    Coded out;
+    out.payload.assign(T, {0, 0});
+    out.val_off.assign(T, 0);
+    if (T == 0) return out;
+    // patch.hpp:99-103: int32 representations reject tensors of 2^31+ elements,
+    // checked per tensor before its entries -- the host knows them up front.
+    int64_t host_dim = -1;
+    if (p->representation != PULSE_COO_DOWNSCALED)
+        for (uint32_t t = 0; t < T; ++t)
+            if (shape_numel(p->tensors[t].shape.data(), uint32_t(p->tensors[t].shape.size())) >= (1ull << 31)) {
+                host_dim = t;
+                break;
+            }
+    std::vector<pulse_tensor_geom> geom(T);
+    std::vector<uint64_t> start(T + 1, 0);
+    for (uint32_t t = 0; t < T; ++t) {
+        const auto& tp = p->tensors[t];
+        if (tp.shape.empty()) raise(PULSE_E_ARGUMENT, "tensor '" + tp.name + "' has empty shape");
+        geom[t].numel = shape_numel(tp.shape.data(), uint32_t(tp.shape.size()));
+        geom[t].cols = uint64_t(tp.shape.back());
+        if (geom[t].numel == 0 || geom[t].cols == 0)
+            raise(PULSE_E_ARGUMENT, "tensor '" + tp.name + "' has non-positive extent");
+        start[t + 1] = start[t] + tp.indices.size();
+    }
+    const uint64_t n = start[T];
+    pulse_plan* plan = E.get_plan(geom, std::max<uint64_t>(n, 1));
+    const PlanDev& d = plan->dev;
+    int64_t* didx = E.idx64.as<int64_t>(n);
+    uint16_t* dval = E.vals.as<uint16_t>(n);
+    std::vector<int64_t> flat_idx(n);
+    std::vector<uint16_t> flat_val(n, 0);
+    for (uint32_t t = 0; t < T; ++t) {
+        const auto& tp = p->tensors[t];
+        std::copy(tp.indices.begin(), tp.indices.end(), flat_idx.begin() + start[t]);
+        if (with_values && tp.values.size() == tp.indices.size())
+            std::copy(tp.values.begin(), tp.values.end(), flat_val.begin() + start[t]);
+    }
+    E.stager.h2d(didx, flat_idx.data(), n * 8, E.stream);
+    E.stager.h2d(dval, flat_val.data(), n * 2, E.stream);
+    cuda_check(cudaMemcpyAsync(d.id_start, start.data(), (T + 1) * 8, cudaMemcpyHostToDevice, E.stream), "H2D");
+    const uint64_t cap = 10 * n + 64;
+    uint8_t* dbody = E.body.as<uint8_t>(cap);
+    auto* dent = E.entries.as<pulse_patch_entry>(T);
+    auto* dres = E.result.as<pulse_result>(1);
+    launch_encode_emit_idx64(d, p->representation, didx, dval, dbody, cap, dent, dres, E.stream);
+    const pulse_result r = fetch_result(E, dres);
+    if (host_dim >= 0 && (r.status == PULSE_OK || r.err_tensor >= uint64_t(host_dim)))
+        raise(PULSE_E_DIMENSION, "tensor '" + p->tensors[host_dim].name + "' is too large for 32-bit indices");
+    if (r.status != PULSE_OK) {
+        const std::string nm = r.err_tensor < T ? p->tensors[r.err_tensor].name : "?";
+        raise(pulse_status(r.status), device_message(r, nm, nullptr));
+    }
+    std::vector<pulse_patch_entry> ents(r.n_entries);
+    if (r.n_entries)
+        cuda_check(cudaMemcpyAsync(ents.data(), dent, r.n_entries * sizeof(pulse_patch_entry), cudaMemcpyDeviceToHost,
+                                   E.stream), "D2H");
+    out.body.resize(r.body_bytes);
+    E.stager.d2h(out.body.data(), dbody, r.body_bytes, E.stream);
+    E.sync();
+    for (const auto& e : ents) {
+        out.payload[e.tensor] = {e.idx_off, e.idx_nbytes};
+        out.val_off[e.tensor] = e.val_off;
+    }
+    return out;
+}
+
+// Device decode of raw index payloads into indices (patch.hpp:178-262).
+void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const uint8_t*>& pl,
+                            const std::vector<uint64_t>& lens) {
+    const uint32_t T = uint32_t(p->tensors.size());
+    if (T == 0) return;
+    std::vector<pulse_tensor_geom> geom(T);
+    std::vector<pulse_patch_entry> ents(T);
+    uint64_t body_len = 0, n = 0;
+    for (uint32_t t = 0; t < T; ++t) {
+        const auto& tp = p->tensors[t];
+        geom[t].numel = shape_numel(tp.shape.data(), uint32_t(tp.shape.size()));
+        geom[t].cols = uint64_t(tp.shape.back());
+        ents[t].tensor = t;
+        ents[t].reserved = 0;
+        ents[t].count = tp.values.size();
+        ents[t].idx_off = body_len;
+        ents[t].idx_nbytes = lens[t];
+        ents[t].val_off = body_len + lens[t];
+        body_len += lens[t];
+        n += tp.values.size();
+    }
+    pulse_plan* plan = E.get_plan(geom, std::max<uint64_t>({n, body_len / 3 + 1, 1}));
+    std::vector<uint8_t> body(body_len);
+    for (uint32_t t = 0; t < T; ++t)
+        if (lens[t]) std::memcpy(body.data() + ents[t].idx_off, pl[t], lens[t]);
+    uint8_t* dbody = E.body.as<uint8_t>(body_len + 64);
+    E.stager.h2d(dbody, body.data(), body_len, E.stream);
+    auto* dent = E.entries.as<pulse_patch_entry>(T);
+    cuda_check(cudaMemcpyAsync(dent, ents.data(), T * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice, E.stream), "H2D");
+    int64_t* dout = E.out64.as<int64_t>(n);
+    auto* dres = E.result.as<pulse_result>(1);
+    launch_decode(plan->dev, p->representation, dbody, dent, T, nullptr, -1, dout, dres, E.stream);
+    const pulse_result r = fetch_result(E, dres);
+    if (r.status != PULSE_OK) {
+        const std::string nm = r.err_tensor < T ? p->tensors[r.err_tensor].name : "?";
+        raise(pulse_status(r.status), device_message(r, nm, nullptr));
+    }
+    std::vector<int64_t> flat(n);
+    E.stager.d2h(flat.data(), dout, n * 8, E.stream);
+    uint64_t o = 0;
+    for (auto& tp : p->tensors) {
+        tp.indices.assign(flat.begin() + o, flat.begin() + o + tp.values.size());
+        o += tp.values.size();
+    }
+}
+
+void validate_for_write(const pulse_patch* p) {  // patch_file.hpp:31-42
+    for (size_t i = 0; i < p->tensors.size(); ++i) {
+        const auto& tp = p->tensors[i];
+        if (tp.name.empty()) raise(PULSE_E_ARGUMENT, "tensor patch with empty name");
+        if (i > 0 && !(p->tensors[i - 1].name < tp.name))
+            raise(PULSE_E_ARGUMENT, "tensor patches must be in ascending name order");
+        if (tp.shape.empty()) raise(PULSE_E_ARGUMENT, "tensor '" + tp.name + "' has empty shape");
+        for (auto e : tp.shape)
+            if (e <= 0) raise(PULSE_E_ARGUMENT, "tensor '" + tp.name + "' has non-positive extent");
+        if (tp.indices.size() != tp.values.size())
+            raise(PULSE_E_ARGUMENT, "tensor '" + tp.name + "' has mismatched index and value counts");
+    }
+}
+
+std::vector<uint8_t> value_payload(const std::vector<uint16_t>& v) {  // patch.hpp:78-83 (LE u16)
+    std::vector<uint8_t> out(v.size() * 2);
+    for (size_t i = 0; i < v.size(); ++i) {
+        out[2 * i] = uint8_t(v[i]);
+        out[2 * i + 1] = uint8_t(v[i] >> 8);
+    }
+    return out;
+}
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+// ---- objects --------------------------------------------------------------------------------
+pulse_status pulse_patch_new(pulse_patch** out) {
+    if (!out) return fail(PULSE_E_ARGUMENT, "null output");
+    *out = new pulse_patch();
+    return PULSE_OK;
+}
+void pulse_patch_free(pulse_patch* p) { delete p; }
+
+pulse_status pulse_patch_get_header(const pulse_patch* p, pulse_patch_header* h) {
+    if (!p || !h) return fail(PULSE_E_ARGUMENT, "null argument");
+    h->base_step = p->base_step;
+    h->target_step = p->target_step;
+    h->anchor_step = p->anchor_step;
+    h->representation = p->representation;
+    h->codec = p->codec;
+    std::memcpy(h->target_hash, p->target_hash, 32);
+    return PULSE_OK;
+}
+pulse_status pulse_patch_set_header(pulse_patch* p, const pulse_patch_header* h) {
+    if (!p || !h) return fail(PULSE_E_ARGUMENT, "null argument");
+    p->base_step = h->base_step;
+    p->target_step = h->target_step;
+    p->anchor_step = h->anchor_step;
+    p->representation = h->representation;
+    p->codec = h->codec;
+    std::memcpy(p->target_hash, h->target_hash, 32);
+    return PULSE_OK;
+}
+uint32_t pulse_patch_num_tensors(const pulse_patch* p) { return p ? uint32_t(p->tensors.size()) : 0; }
+pulse_status pulse_patch_get_tensor(const pulse_patch* p, uint32_t i, pulse_tensor_patch* v) {
+    if (!p || !v || i >= p->tensors.size()) return fail(PULSE_E_ARGUMENT, "bad tensor index");
+    const auto& t = p->tensors[i];
+    v->name = t.name.c_str();
+    v->shape = t.shape.data();
+    v->rank = uint32_t(t.shape.size());
+    v->indices = t.indices.data();
+    v->n_indices = t.indices.size();
+    v->values = t.values.data();
+    v->n_values = t.values.size();
+    return PULSE_OK;
+}
+pulse_status pulse_patch_add_tensor(pulse_patch* p, const pulse_tensor_patch* v) {
+    if (!p || !v) return fail(PULSE_E_ARGUMENT, "null argument");
+    PatchTensor t;
+    t.name = v->name ? v->name : "";
+    t.shape.assign(v->shape, v->shape + v->rank);
+    t.indices.assign(v->indices, v->indices + v->n_indices);
+    t.values.assign(v->values, v->values + v->n_values);
+    p->tensors.push_back(std::move(t));
+    return PULSE_OK;
+}
+
+const uint8_t* pulse_bytes_data(const pulse_bytes* b) { return b ? b->v.data() : nullptr; }
+uint64_t pulse_bytes_size(const pulse_bytes* b) { return b ? b->v.size() : 0; }
+void pulse_bytes_free(pulse_bytes* b) { delete b; }
+
+// ---- patch.hpp ------------------------------------------------------------------------------
+pulse_status pulse_encode(const pulse_checkpoint* current, const pulse_checkpoint* previous, uint32_t repr,
+                          uint32_t codec, pulse_patch** out) {
+    return guarded([&] {
+        if (!current || !previous || !out) raise(PULSE_E_ARGUMENT, "null argument");
+        validate_checkpoint(current);
+        validate_checkpoint(previous);
+        const auto co = sorted_order(current), po = sorted_order(previous);
+        if (co.size() != po.size()) raise(PULSE_E_TENSOR_SET, "checkpoints have different tensor counts");
+        auto patch = std::make_unique<pulse_patch>();
+        patch->base_step = int64_t(previous->step);
+        patch->target_step = int64_t(current->step);
+        patch->anchor_step = int64_t(previous->step);
+        patch->representation = repr;
+        patch->codec = codec;
+        repr_name(repr);
+        // target hash on a host thread, overlapping the device work
+        auto hash = std::async(std::launch::async, [&] { hash_checkpoint(current, patch->target_hash); });
+        struct HashJoin {
+            std::future<void>& f;
+            ~HashJoin() {
+                if (f.valid()) f.wait();
+            }
+        } join{hash};
+        const uint32_t T = uint32_t(co.size());
+        std::vector<pulse_tensor_geom> geom(T);
+        std::vector<uint64_t> numel(T);
+        for (uint32_t k = 0; k < T; ++k) {
+            const pulse_tensor& c = current->tensors[co[k]];
+            const pulse_tensor& q = previous->tensors[po[k]];
+            if (std::strcmp(c.name, q.name) != 0)
+                raise(PULSE_E_TENSOR_SET, std::string("tensor sets differ: '") + c.name + "' vs '" + q.name + "'");
+            if (c.rank != q.rank || !std::equal(c.shape, c.shape + c.rank, q.shape))
+                raise(PULSE_E_SHAPE_MISMATCH, std::string("tensor '") + c.name + "' changed shape between checkpoints");
+            geom[k].numel = c.numel;
+            geom[k].cols = uint64_t(c.shape[c.rank - 1]);
+            numel[k] = c.numel;
+        }
+        if (T > 0) {
+            Engine& E = engine();
+            std::lock_guard<std::mutex> lk(E.mu);
+            uint64_t total = 0;
+            const auto off = arena_offsets(numel, total);
+            uint16_t* A = E.arena_a.as<uint16_t>(total);
+            uint16_t* B = E.arena_b.as<uint16_t>(total);
+            for (uint32_t k = 0; k < T; ++k) {
+                E.stager.h2d(A + off[k], previous->tensors[po[k]].data, numel[k] * 2, E.stream);
+                E.stager.h2d(B + off[k], current->tensors[co[k]].data, numel[k] * 2, E.stream);
+            }
+            uint64_t cap = std::max<uint64_t>(total / 64, 1 << 20);
+            pulse_scan_summary sm{};
+            pulse_plan* plan = nullptr;
+            for (int attempt = 0; attempt < 2; ++attempt) {
+                plan = E.get_plan(geom, cap);
+                std::vector<const void*> pa(T), pb(T);
+                for (uint32_t k = 0; k < T; ++k) {
+                    pa[k] = A + off[k];
+                    pb[k] = B + off[k];
+                }
+                if (pulse_plan_bind(plan, 0, pa.data()) || pulse_plan_bind(plan, 1, pb.data()))
+                    raise(PULSE_E_CUDA, pulse_last_error());
+                if (pulse_encode_scan(plan, 1, 0, nullptr, E.stream)) raise(PULSE_E_CUDA, pulse_last_error());
+                cuda_check(cudaMemcpyAsync(&sm, plan->dev.scan, sizeof(sm), cudaMemcpyDeviceToHost, E.stream), "D2H");
+                E.sync();
+                if (sm.status != PULSE_E_CAPACITY) break;
+                cap = sm.n_changes + sm.n_changes / 16 + 1024;
+            }
+            const uint64_t n = sm.n_changes;
+            const PlanDev& d = plan->dev;
+            std::vector<uint64_t> seg_start(d.n_segs + 1);
+            cuda_check(cudaMemcpyAsync(seg_start.data(), d.seg_start, seg_start.size() * 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
+            int64_t* didx = E.out64.as<int64_t>(n);
+            launch_export_indices(d, didx, E.stream);
+            std::vector<int64_t> idx(n);
+            std::vector<uint16_t> val(n);
+            E.stager.d2h(idx.data(), didx, n * 8, E.stream);
+            E.stager.d2h(val.data(), d.val16, n * 2, E.stream);
+            E.sync();
+            // per-tensor ranges: segments of a tensor are consecutive (2^31-element splits)
+            uint32_t sg = 0;
+            for (uint32_t k = 0; k < T; ++k) {
+                const uint64_t nseg = (numel[k] + kSegElems - 1) / kSegElems;
+                const uint64_t lo = seg_start[sg], hi = seg_start[sg + nseg];
+                sg += uint32_t(nseg);
+                if (hi == lo) continue;  // unchanged tensors are omitted (patch.hpp:302-304)
+                const pulse_tensor& c = current->tensors[co[k]];
+                PatchTensor tp;
+                tp.name = c.name;
+                tp.shape.assign(c.shape, c.shape + c.rank);
+                tp.indices.assign(idx.begin() + lo, idx.begin() + hi);
+                tp.values.assign(val.begin() + lo, val.begin() + hi);
+                patch->tensors.push_back(std::move(tp));
+            }
+        }
+        hash.get();
+        *out = patch.release();
+    });
+}
+
+pulse_status pulse_decode(const pulse_checkpoint* previous, const pulse_patch* patch, int verify_hash,
+                          uint16_t* const* out_data, uint64_t* out_step) {
+    return guarded([&] {
+        if (!previous || !patch || (previous->n_tensors && !out_data)) raise(PULSE_E_ARGUMENT, "null argument");
+        const uint32_t T = previous->n_tensors;
+        // host checks in patch order (patch.hpp:314-324); the first failing tensor stops
+        // the device validation there so errors surface in the reference's order
+        const uint32_t P = uint32_t(patch->tensors.size());
+        uint32_t stop = P;
+        Failure host_err{PULSE_OK, ""};
+        std::vector<uint32_t> target(P);
+        for (uint32_t k = 0; k < P && stop == P; ++k) {
+            const auto& tp = patch->tensors[k];
+            int64_t f = -1;
+            for (uint32_t i = 0; i < T; ++i)
+                if (tp.name == previous->tensors[i].name) {
+                    f = i;
+                    break;
+                }
+            if (f < 0) {
+                stop = k;
+                host_err = {PULSE_E_TENSOR_SET, "patch references unknown tensor '" + tp.name + "'"};
+                break;
+            }
+            const pulse_tensor& t = previous->tensors[f];
+            if (t.rank != tp.shape.size() || !std::equal(tp.shape.begin(), tp.shape.end(), t.shape)) {
+                stop = k;
+                host_err = {PULSE_E_SHAPE_MISMATCH, "tensor '" + tp.name + "' shape differs between patch and checkpoint"};
+                break;
+            }
+            if (tp.values.size() != tp.indices.size()) {
+                stop = k;
+                host_err = {PULSE_E_ARGUMENT, "tensor '" + tp.name + "' has mismatched index and value counts"};
+                break;
+            }
+            target[k] = uint32_t(f);
+        }
+        if (T > 0) {
+            Engine& E = engine();
+            std::lock_guard<std::mutex> lk(E.mu);
+            std::vector<pulse_tensor_geom> geom(T);
+            std::vector<uint64_t> numel(T);
+            for (uint32_t i = 0; i < T; ++i) {
+                const pulse_tensor& t = previous->tensors[i];
+                numel[i] = t.numel;
+                geom[i].numel = t.numel ? t.numel : 1;
+                geom[i].cols = t.rank ? uint64_t(std::max<int64_t>(1, t.shape[t.rank - 1])) : 1;
+                if (geom[i].numel % geom[i].cols) geom[i].cols = 1;
+            }
+            uint64_t total = 0, n = 0;
+            const auto off = arena_offsets(numel, total);
+            for (uint32_t k = 0; k < stop; ++k) n += patch->tensors[k].indices.size();
+            uint16_t* A = E.arena_a.as<uint16_t>(total);
+            for (uint32_t i = 0; i < T; ++i) E.stager.h2d(A + off[i], previous->tensors[i].data, numel[i] * 2, E.stream);
+            pulse_plan* plan = E.get_plan(geom, std::max<uint64_t>(n, 1));
+            std::vector<const void*> pa(T);
+            for (uint32_t i = 0; i < T; ++i) pa[i] = A + off[i];
+            if (pulse_plan_bind(plan, 2, pa.data())) raise(PULSE_E_CUDA, pulse_last_error());
+            if (stop > 0 && n > 0) {
+                std::vector<int64_t> idx(n);
+                std::vector<uint16_t> val(n);
+                std::vector<pulse_patch_entry> ents(stop);
+                uint64_t o = 0;
+                for (uint32_t k = 0; k < stop; ++k) {
+                    const auto& tp = patch->tensors[k];
+                    std::copy(tp.indices.begin(), tp.indices.end(), idx.begin() + o);
+                    std::copy(tp.values.begin(), tp.values.end(), val.begin() + o);
+                    ents[k] = pulse_patch_entry{target[k], 0, tp.indices.size(), 0, 0, 0};
+                    o += tp.indices.size();
+                }
+                int64_t* didx = E.idx64.as<int64_t>(n);
+                uint16_t* dval = E.vals.as<uint16_t>(n);
+                E.stager.h2d(didx, idx.data(), n * 8, E.stream);
+                E.stager.h2d(dval, val.data(), n * 2, E.stream);
+                auto* dent = E.entries.as<pulse_patch_entry>(stop);
+                cuda_check(cudaMemcpyAsync(dent, ents.data(), stop * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice,
+                                           E.stream), "H2D");
+                auto* dres = E.result.as<pulse_result>(1);
+                launch_apply_idx64(plan->dev, didx, dval, dent, stop, 2, dres, E.stream);
+                const pulse_result r = fetch_result(E, dres);
+                if (r.status != PULSE_OK) {
+                    const auto& tp = patch->tensors[r.err_tensor];
+                    raise(pulse_status(r.status), device_message(r, tp.name, &tp.indices));
+                }
+            }
+            if (host_err.st != PULSE_OK) raise(host_err.st, host_err.msg);
+            for (uint32_t i = 0; i < T; ++i) E.stager.d2h(out_data[i], A + off[i], numel[i] * 2, E.stream);
+            E.sync();
+        } else if (host_err.st != PULSE_OK) {
+            raise(host_err.st, host_err.msg);
+        }
+        if (out_step) *out_step = uint64_t(patch->target_step);
+        if (verify_hash) {  // patch.hpp:341-346
+            pulse_checkpoint outck{uint64_t(patch->target_step), nullptr, T};
+            std::vector<pulse_tensor> ts(T);
+            for (uint32_t i = 0; i < T; ++i) {
+                ts[i] = previous->tensors[i];
+                ts[i].data = out_data[i];
+            }
+            outck.tensors = ts.data();
+            uint8_t h[32];
+            hash_checkpoint(&outck, h);
+            if (std::memcmp(h, patch->target_hash, 32) != 0)
+                raise(PULSE_E_HASH_MISMATCH, "hash mismatch: expected " + hex(patch->target_hash) + ", actual " + hex(h));
+        }
+    });
+}
+
+pulse_status pulse_encode_index_payloads(const pulse_patch* patch, pulse_bytes** concat, uint64_t* sizes) {
+    return guarded([&] {
+        if (!patch || !concat) raise(PULSE_E_ARGUMENT, "null argument");
+        repr_name(patch->representation);
+        Engine& E = engine();
+        std::lock_guard<std::mutex> lk(E.mu);
+        const Coded c = device_index_code(E, patch, false);
+        auto out = std::make_unique<pulse_bytes>();
+        for (size_t t = 0; t < patch->tensors.size(); ++t) {
+            const auto [o, len] = c.payload[t];
+            if (sizes) sizes[t] = len;
+            out->v.insert(out->v.end(), c.body.begin() + o, c.body.begin() + o + len);
+        }
+        *concat = out.release();
+    });
+}
+
+pulse_status pulse_decode_index_payloads(pulse_patch* patch, const uint8_t* const* payloads, const uint64_t* sizes,
+                                         uint32_t n) {
+    return guarded([&] {
+        if (!patch) raise(PULSE_E_ARGUMENT, "null argument");
+        if (n != patch->tensors.size()) raise(PULSE_E_ARGUMENT, "payload count does not match tensor count");
+        repr_name(patch->representation);
+        Engine& E = engine();
+        std::lock_guard<std::mutex> lk(E.mu);
+        std::vector<const uint8_t*> pl(payloads, payloads + n);
+        std::vector<uint64_t> lens(sizes, sizes + n);
+        device_decode_payloads(E, patch, pl, lens);
+    });
+}
+
+// ---- patch_file.hpp -------------------------------------------------------------------------
+pulse_status pulse_write_patch_bytes(const pulse_patch* p, pulse_bytes** out) {
+    return guarded([&] {
+        if (!p || !out) raise(PULSE_E_ARGUMENT, "null argument");
+        validate_for_write(p);
+        const char* rname = repr_name(p->representation);
+        if (p->codec > PULSE_GZIP6) raise(PULSE_E_ARGUMENT, "unknown codec");
+        Coded c;
+        {
+            Engine& E = engine();
+            std::lock_guard<std::mutex> lk(E.mu);
+            c = device_index_code(E, p, true);
+        }
+        const size_t T = p->tensors.size();
+        std::vector<std::vector<uint8_t>> ib(T), vb(T);
+        pool().parallel_for(T, [&](size_t t) {  // blobs are independent: same bytes in any order
+            const auto [o, len] = c.payload[t];
+            ib[t] = codec_compress(c.body.data() + o, len, p->codec);
+            if (len || p->tensors[t].values.empty()) {
+                const uint8_t* v = c.body.data() + c.val_off[t];
+                vb[t] = codec_compress(v, p->tensors[t].values.size() * 2, p->codec);
+            } else {
+                const auto raw = value_payload(p->tensors[t].values);
+                vb[t] = codec_compress(raw.data(), raw.size(), p->codec);
+            }
+        });
+        nlohmann::json header;
+        header["anchor_step"] = p->anchor_step;
+        header["base_step"] = p->base_step;
+        header["target_step"] = p->target_step;
+        header["target_hash"] = hex(p->target_hash);
+        header["codec"] = p->codec;
+        header["representation"] = rname;
+        auto& table = header["tensors"] = nlohmann::json::array();
+        for (size_t t = 0; t < T; ++t) {
+            const auto& tp = p->tensors[t];
+            nlohmann::json e = {{"name", tp.name},
+                                {"shape", tp.shape},
+                                {"count", tp.indices.size()},
+                                {"index_nbytes", ib[t].size()},
+                                {"value_nbytes", vb[t].size()}};
+            if (p->representation == PULSE_COO_DOWNSCALED) {
+                e["row_bits"] = 8;
+                e["col_bits"] = 16;
+            }
+            table.push_back(std::move(e));
+        }
+        const std::string js = header.dump();
+        auto res = std::make_unique<pulse_bytes>();
+        size_t total = 16 + js.size();
+        for (size_t t = 0; t < T; ++t) total += ib[t].size() + vb[t].size();
+        res->v.resize(total);
+        uint8_t* w = res->v.data();
+        std::memcpy(w, "PULP", 4);
+        const uint32_t ver = 1;
+        const uint64_t hl = js.size();
+        for (int i = 0; i < 4; ++i) w[4 + i] = uint8_t(ver >> (8 * i));
+        for (int i = 0; i < 8; ++i) w[8 + i] = uint8_t(hl >> (8 * i));
+        std::memcpy(w + 16, js.data(), js.size());
+        size_t pos = 16 + js.size();
+        for (size_t t = 0; t < T; ++t) {
+            std::memcpy(w + pos, ib[t].data(), ib[t].size());
+            pos += ib[t].size();
+            std::memcpy(w + pos, vb[t].data(), vb[t].size());
+            pos += vb[t].size();
+        }
+        *out = res.release();
+    });
+}
+
+pulse_status pulse_read_patch_bytes(const uint8_t* bytes, uint64_t n, pulse_patch** out) {
+    return guarded([&] {
+        if (!out || (n && !bytes)) raise(PULSE_E_ARGUMENT, "null argument");
+        uint64_t pos = 0;
+        auto need = [&](uint64_t k) {
+            if (n - pos < k) raise(PULSE_E_TRUNCATION, "unexpected end of data");
+        };
+        if (n < 4) raise(PULSE_E_TRUNCATION, "patch shorter than magic");
+        if (std::memcmp(bytes, "PULP", 4) != 0) raise(PULSE_E_BAD_MAGIC, "not a patch file (bad magic)");
+        pos = 4;
+        need(4);
+        uint32_t version = 0;
+        for (int i = 0; i < 4; ++i) version |= uint32_t(bytes[pos + i]) << (8 * i);
+        pos += 4;
+        if (version != 1) raise(PULSE_E_VERSION, "unsupported patch version " + std::to_string(version));
+        need(8);
+        uint64_t hl = 0;
+        for (int i = 0; i < 8; ++i) hl |= uint64_t(bytes[pos + i]) << (8 * i);
+        pos += 8;
+        if (hl > n - pos) raise(PULSE_E_TRUNCATION, "patch header truncated");
+        nlohmann::json header;
+        try {
+            header = nlohmann::json::parse(bytes + pos, bytes + pos + hl);
+        } catch (const nlohmann::json::exception& e) {
+            raise(PULSE_E_FORMAT, std::string("patch header is not valid JSON: ") + e.what());
+        }
+        pos += hl;
+        auto p = std::make_unique<pulse_patch>();
+        std::vector<std::vector<uint8_t>> payloads;
+        try {
+            p->anchor_step = header.at("anchor_step").get<int64_t>();
+            p->base_step = header.at("base_step").get<int64_t>();
+            p->target_step = header.at("target_step").get<int64_t>();
+            const std::string hx = header.at("target_hash").get<std::string>();
+            if (hx.size() != 64) raise(PULSE_E_FORMAT, "sha256 hex digest must be 64 characters");
+            for (int i = 0; i < 32; ++i) {
+                auto nib = [](char ch) -> int {
+                    if (ch >= '0' && ch <= '9') return ch - '0';
+                    if (ch >= 'a' && ch <= 'f') return ch - 'a' + 10;
+                    if (ch >= 'A' && ch <= 'F') return ch - 'A' + 10;
+                    raise(PULSE_E_FORMAT, "invalid hex character in digest");
+                };
+                p->target_hash[i] = uint8_t(nib(hx[2 * i]) << 4 | nib(hx[2 * i + 1]));
+            }
+            const uint32_t codec = header.at("codec").get<uint32_t>();
+            if (codec > PULSE_GZIP6) raise(PULSE_E_FORMAT, "unknown codec id " + std::to_string(codec));
+            p->codec = codec;
+            const std::string rn = header.at("representation").get<std::string>();
+            if (rn == "COO_DOWNSCALED") p->representation = PULSE_COO_DOWNSCALED;
+            else if (rn == "COO_INT32") p->representation = PULSE_COO_INT32;
+            else if (rn == "FLAT_INT32") p->representation = PULSE_FLAT_INT32;
+            else raise(PULSE_E_FORMAT, "unknown representation name: " + rn);
+            for (const auto& entry : header.at("tensors")) {
+                PatchTensor tp;
+                tp.name = entry.at("name").get<std::string>();
+                tp.shape = entry.at("shape").get<std::vector<int64_t>>();
+                for (auto e : tp.shape)
+                    if (e <= 0) raise(PULSE_E_FORMAT, "non-positive extent in tensor " + tp.name);
+                const auto count = entry.at("count").get<uint64_t>();
+                const auto inb = entry.at("index_nbytes").get<uint64_t>();
+                const auto vnb = entry.at("value_nbytes").get<uint64_t>();
+                if (p->representation == PULSE_COO_DOWNSCALED) {
+                    if (entry.at("row_bits").get<int>() != 8 || entry.at("col_bits").get<int>() != 16)
+                        raise(PULSE_E_FORMAT, "unsupported delta widths for tensor " + tp.name);
+                }
+                if (inb > n - pos) raise(PULSE_E_TRUNCATION, "index blob truncated");
+                auto ip = codec_decompress(bytes + pos, inb, p->codec);
+                pos += inb;
+                if (vnb > n - pos) raise(PULSE_E_TRUNCATION, "value blob truncated");
+                auto vp = codec_decompress(bytes + pos, vnb, p->codec);
+                pos += vnb;
+                if (vp.size() != count * 2)
+                    raise(PULSE_E_FORMAT, "value payload length does not match change count for tensor " + tp.name);
+                tp.values.resize(count);
+                for (uint64_t i = 0; i < count; ++i) tp.values[i] = uint16_t(vp[2 * i] | (vp[2 * i + 1] << 8));
+                payloads.push_back(std::move(ip));
+                p->tensors.push_back(std::move(tp));
+            }
+        } catch (const nlohmann::json::exception& e) {
+            raise(PULSE_E_FORMAT, std::string("patch header schema error: ") + e.what());
+        }
+        if (pos != n) raise(PULSE_E_FORMAT, "patch has trailing bytes");
+        if (!p->tensors.empty()) {
+            Engine& E = engine();
+            std::lock_guard<std::mutex> lk(E.mu);
+            std::vector<const uint8_t*> pl;
+            std::vector<uint64_t> lens;
+            for (auto& v : payloads) {
+                pl.push_back(v.data());
+                lens.push_back(v.size());
+            }
+            device_decode_payloads(E, p.get(), pl, lens);
+        }
+        *out = p.release();
+    });
+}
+
+// ---- sha256.hpp -----------------------------------------------------------------------------
+pulse_status pulse_hash_weights(const pulse_checkpoint* c, uint8_t* out32) {
+    return guarded([&] {
+        if (!c || !out32) raise(PULSE_E_ARGUMENT, "null argument");
+        hash_checkpoint(c, out32);
+    });
+}
+
+pulse_status pulse_sha256_new(pulse_sha256_ctx** out) {
+    return guarded([&] {
+        auto* s = new pulse_sha256_ctx{EVP_MD_CTX_new()};
+        if (!s->ctx || EVP_DigestInit_ex(s->ctx, EVP_sha256(), nullptr) != 1) {
+            delete s;
+            raise(PULSE_E_ERROR, "failed to initialize SHA-256 context");
+        }
+        *out = s;
+    });
+}
+pulse_status pulse_sha256_update(pulse_sha256_ctx* s, const uint8_t* data, uint64_t n) {
+    if (!s) return fail(PULSE_E_ARGUMENT, "null context");
+    if (n && EVP_DigestUpdate(s->ctx, data, n) != 1) return fail(PULSE_E_ERROR, "SHA-256 update failed");
+    return PULSE_OK;
+}
+pulse_status pulse_sha256_final(pulse_sha256_ctx* s, uint8_t* out32) {
+    if (!s) return fail(PULSE_E_ARGUMENT, "null context");
+    unsigned int len = 0;
+    if (EVP_DigestFinal_ex(s->ctx, out32, &len) != 1 || len != 32) return fail(PULSE_E_ERROR, "SHA-256 finalize failed");
+    return PULSE_OK;
+}
+void pulse_sha256_free(pulse_sha256_ctx* s) {
+    if (s) {
+        EVP_MD_CTX_free(s->ctx);
+        delete s;
+    }
+}
+
+// ---- index_coding.hpp -----------------------------------------------------------------------
+pulse_status pulse_delta_encode_indices(const int64_t* in, uint64_t n, int64_t* out) {
+    return guarded([&] {
+        if (n == 0) return;
+        Engine& E = engine();
+        std::lock_guard<std::mutex> lk(E.mu);
+        int64_t* d = E.idx64.as<int64_t>(2 * n);
+        uint64_t* err = E.misc.as<uint64_t>(1);
+        cuda_check(cudaMemsetAsync(err, 0xFF, 8, E.stream), "memset");
+        E.stager.h2d(d, in, n * 8, E.stream);
+        launch_delta_encode(d, n, d + n, err, E.stream);
+        uint64_t k = 0;
+        cuda_check(cudaMemcpyAsync(&k, err, 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
+        E.sync();
+        if (k != kNoError)
+            raise(PULSE_E_ARGUMENT, key_check(k) == kArgNegative ? "indices must be non-negative"
+                                                                  : "indices must be strictly increasing");
+        E.stager.d2h(out, d + n, n * 8, E.stream);
+    });
+}
+
+pulse_status pulse_delta_decode_indices(const int64_t* in, uint64_t n, int64_t* out) {
+    return guarded([&] {
+        if (n == 0) return;
+        Engine& E = engine();
+        std::lock_guard<std::mutex> lk(E.mu);
+        int64_t* d = E.idx64.as<int64_t>(2 * n);
+        uint64_t* err = E.misc.as<uint64_t>(1);
+        cuda_check(cudaMemsetAsync(err, 0xFF, 8, E.stream), "memset");
+        E.stager.h2d(d, in, n * 8, E.stream);
+        launch_delta_decode(d, n, d + n, err, E.stream);
+        uint64_t k = 0;
+        cuda_check(cudaMemcpyAsync(&k, err, 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
+        E.sync();
+        if (k != kNoError)
+            raise(PULSE_E_FORMAT, key_elem(k) == 0 ? "first index gap is negative"
+                                                    : "non-positive index gap after the first element");
+        E.stager.d2h(out, d + n, n * 8, E.stream);
+    });
+}
+
+pulse_status pulse_downscale_coo(const int64_t* rows, uint64_t n_rows, const int64_t* cols, uint64_t n_cols,
+                                 pulse_bytes** out) {
+    return guarded([&] {
+        if (!out) raise(PULSE_E_ARGUMENT, "null argument");
+        if (n_rows != n_cols) raise(PULSE_E_ARGUMENT, "row and column lists differ in length");
+        auto res = std::make_unique<pulse_bytes>();
+        if (n_rows) {
+            Engine& E = engine();
+            std::lock_guard<std::mutex> lk(E.mu);
+            int64_t* d = E.idx64.as<int64_t>(2 * n_rows);
+            uint8_t* dout = E.body.as<uint8_t>(10 * n_rows + 16);
+            uint64_t* misc = E.misc.as<uint64_t>(2);
+            cuda_check(cudaMemsetAsync(misc, 0xFF, 8, E.stream), "memset");
+            E.stager.h2d(d, rows, n_rows * 8, E.stream);
+            E.stager.h2d(d + n_rows, cols, n_rows * 8, E.stream);
+            launch_coo_pack(d, d + n_rows, n_rows, dout, misc + 1, misc, E.stream);
+            uint64_t h[2];
+            cuda_check(cudaMemcpyAsync(h, misc, 16, cudaMemcpyDeviceToHost, E.stream), "D2H");
+            E.sync();
+            if (h[0] != kNoError) {
+                const uint32_t c = key_check(h[0]);
+                if (c == kArgNegative) raise(PULSE_E_ARGUMENT, "coordinates must be non-negative");
+                if (c == kArgOrder) raise(PULSE_E_ARGUMENT, "coordinates must be sorted row-major without duplicates");
+                raise(PULSE_E_DIMENSION, c == kDimRow ? "row gap exceeds 32 bits" : "column entry exceeds 32 bits");
+            }
+            res->v.resize(h[1]);
+            E.stager.d2h(res->v.data(), dout, h[1], E.stream);
+        }
+        *out = res.release();
+    });
+}
+
+pulse_status pulse_upscale_coo(const uint8_t* data, uint64_t n, uint64_t count, int64_t* rows, int64_t* cols) {
+    return guarded([&] {
+        Engine& E = engine();
+        std::lock_guard<std::mutex> lk(E.mu);
+        uint8_t* dp = E.body.as<uint8_t>(n + 16);
+        int64_t* d = E.out64.as<int64_t>(2 * count + 2);
+        uint64_t* err = E.misc.as<uint64_t>(1);
+        cuda_check(cudaMemsetAsync(err, 0xFF, 8, E.stream), "memset");
+        if (n) E.stager.h2d(dp, data, n, E.stream);
+        launch_coo_unpack(dp, n, count, d, d + count, err, E.stream);
+        uint64_t k = 0;
+        cuda_check(cudaMemcpyAsync(&k, err, 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
+        E.sync();
+        if (k != kNoError) {
+            const uint32_t c = key_check(k);
+            if (c == kTrunc) raise(PULSE_E_TRUNCATION, "unexpected end of data");
+            if (c == kZeroColGap) raise(PULSE_E_CORRUPT_STREAM, "non-positive column gap within a row");
+            raise(PULSE_E_CORRUPT_STREAM, "downscaled payload has trailing bytes");
+        }
+        if (count) {
+            E.stager.d2h(rows, d, count * 8, E.stream);
+            E.stager.d2h(cols, d + count, count * 8, E.stream);
+        }
+    });
+}
+
+// ---- compression.hpp ------------------------------------------------------------------------
+pulse_status pulse_compress(const uint8_t* data, uint64_t n, uint32_t codec, pulse_bytes** out) {
+    return guarded([&] {
+        if (!out) raise(PULSE_E_ARGUMENT, "null argument");
+        auto b = std::make_unique<pulse_bytes>();
+        b->v = codec_compress(data, n, codec);
+        *out = b.release();
+    });
+}
+pulse_status pulse_decompress(const uint8_t* data, uint64_t n, uint32_t codec, pulse_bytes** out) {
+    return guarded([&] {
+        if (!out) raise(PULSE_E_ARGUMENT, "null argument");
+        auto b = std::make_unique<pulse_bytes>();
+        b->v = codec_decompress(data, n, codec);
+        *out = b.release();
+    });
+}
+
+}  // extern "C"

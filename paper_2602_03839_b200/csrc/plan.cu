@@ -61,7 +61,9 @@ static unsigned long long* g_wd_host = nullptr;
 static unsigned long long* g_wd_dev = nullptr;
 static std::mutex g_wd_mu;
 
-static void install_watchdog(int device) {
+void pulse_install_watchdog(int device);
+static void install_watchdog(int device) { pulse_install_watchdog(device); }
+void pulse_install_watchdog(int device) {
     std::lock_guard<std::mutex> lk(g_wd_mu);
     if (!g_wd_host) {
         void* h = nullptr;
@@ -79,6 +81,7 @@ static void install_watchdog(int device) {
         set_watchdog_synth(g_wd_dev);
         set_watchdog_index(g_wd_dev);
         set_watchdog_apply(g_wd_dev);
+        set_watchdog_helpers(g_wd_dev);
         done[device] = true;
     }
 }
