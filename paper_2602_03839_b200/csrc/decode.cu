@@ -44,6 +44,7 @@ enum Totals : int {
 };
 
 constexpr uint32_t kParseChunksPerTile = kThreads;  // one 16-byte chunk per thread
+constexpr uint32_t kNoPayload = 0xFF;  // d_layout "representation" for int64-index applies
 
 __device__ __forceinline__ uint64_t take_ticket(uint64_t* totals, int which) {
     return atomicAdd(reinterpret_cast<unsigned long long*>(totals + kTicket0 + which), 1ull);
@@ -125,8 +126,12 @@ d_layout(const pulse_patch_entry* __restrict__ entries, uint32_t n_e, const uint
             es[e] = L.es;
             ck[e] = L.ck;
             // fixed-layout fast path (apply_fast.cu) only if no entry needs escapes
-            if (pe.idx_nbytes != (repr == PULSE_COO_DOWNSCALED ? 3 : 4) * pe.count) atomicExch(flags, 1u);
-            if (repr != PULSE_COO_DOWNSCALED) {
+            if (repr <= PULSE_FLAT_INT32 &&
+                pe.idx_nbytes != (repr == PULSE_COO_DOWNSCALED ? 3 : 4) * pe.count)
+                atomicExch(flags, 1u);
+            if (repr > PULSE_FLAT_INT32) {
+                // caller-provided int64 indices: no payload to check
+            } else if (repr != PULSE_COO_DOWNSCALED) {
                 // patch.hpp:193,217: require_int32_indexable; then u32 reads of `count`
                 // entries (truncation) and the trailing-bytes check.
                 if (ne >= (1ull << 31)) report(err, error_key(e, kStageTensor, 0, kDimInt32));
@@ -586,7 +591,7 @@ void launch_decode(const PlanDev& p, uint32_t repr, const uint8_t* body,
 void launch_apply_idx64(const PlanDev& p, const int64_t* idx64, const uint16_t* vals,
                         const pulse_patch_entry* entries, uint32_t n_entries, int weights_slot,
                         pulse_result* result, cudaStream_t s) {
-    decode_prologue(p, entries, n_entries, PULSE_COO_DOWNSCALED, s);
+    decode_prologue(p, entries, n_entries, kNoPayload, s);
     const unsigned g = persistent_grid();
     if (n_entries > 0) {
         d_validate_idx64<<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, idx64, p.d_totals, p.err);

@@ -112,30 +112,31 @@ public:
         cv_.notify_all();
         for (auto& t : workers_) t.join();
     }
-    // f(i) for i in [0, n), parallel; returns when all are done.
+    // f(i) for i in [0, n), parallel.  Returns only after every helper has left
+    // the loop, so the shared counters may live on the caller's stack.
     void parallel_for(size_t n, const std::function<void(size_t)>& f) {
         if (n <= 1 || workers_.empty()) {
             for (size_t i = 0; i < n; ++i) f(i);
             return;
         }
-        std::atomic<size_t> next{0}, done{0};
+        std::atomic<size_t> next{0};
         std::mutex m;
         std::condition_variable c;
-        auto body = [&] {
+        size_t helpers = std::min<size_t>(workers_.size(), n - 1);
+        size_t running = helpers;
+        auto loop = [&] {
             size_t i;
-            while ((i = next.fetch_add(1)) < n) {
-                f(i);
-                if (done.fetch_add(1) + 1 == n) {
-                    std::lock_guard<std::mutex> lk(m);
-                    c.notify_all();
-                }
-            }
+            while ((i = next.fetch_add(1)) < n) f(i);
         };
-        const size_t helpers = std::min<size_t>(workers_.size(), n - 1);
-        for (size_t h = 0; h < helpers; ++h) submit(body);
-        body();
+        for (size_t h = 0; h < helpers; ++h)
+            submit([&] {
+                loop();
+                std::lock_guard<std::mutex> lk(m);
+                if (--running == 0) c.notify_all();
+            });
+        loop();
         std::unique_lock<std::mutex> lk(m);
-        c.wait(lk, [&] { return done.load() == n; });
+        c.wait(lk, [&] { return running == 0; });
     }
 
 private:
