@@ -286,6 +286,11 @@ pulse_status pulse_decode_index_payloads(pulse_patch* patch, const uint8_t* cons
 pulse_status pulse_write_patch_bytes(const pulse_patch* patch, pulse_bytes** out);
 pulse_status pulse_read_patch_bytes(const uint8_t* data, uint64_t n, pulse_patch** out);
 
+/* Bytes the host-buffer API has copied host->device and device->host in this
+ * process (all threads); a benchmark/diagnostic aid with no reference
+ * counterpart.  reset != 0 zeroes the counters after reading them. */
+void pulse_transfer_stats(uint64_t* h2d_bytes, uint64_t* d2h_bytes, int reset);
+
 /* hash_weights -- sha256.hpp:93-116; Sha256 -- sha256.hpp:51-87. */
 pulse_status pulse_hash_weights(const pulse_checkpoint* checkpoint, uint8_t* out32);
 typedef struct pulse_sha256_ctx pulse_sha256_ctx;

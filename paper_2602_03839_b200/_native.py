@@ -92,6 +92,26 @@ CHECK_NAMES = {
     15: "capacity",
 }
 
+class Tensor(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("shape", C.POINTER(C.c_int64)), ("rank", C.c_uint32),
+                ("data", C.c_void_p), ("numel", C.c_uint64)]
+
+
+class CheckpointC(C.Structure):
+    _fields_ = [("step", C.c_uint64), ("tensors", C.POINTER(Tensor)), ("n_tensors", C.c_uint32)]
+
+
+class PatchHeader(C.Structure):
+    _fields_ = [("base_step", C.c_int64), ("target_step", C.c_int64), ("anchor_step", C.c_int64),
+                ("representation", C.c_uint32), ("codec", C.c_uint32), ("target_hash", C.c_uint8 * 32)]
+
+
+class TensorPatchC(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("shape", C.POINTER(C.c_int64)), ("rank", C.c_uint32),
+                ("indices", C.POINTER(C.c_int64)), ("n_indices", C.c_uint64),
+                ("values", C.POINTER(C.c_uint16)), ("n_values", C.c_uint64)]
+
+
 vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32
 _SIGS = {
     "pulse_last_error": (C.c_char_p, []),
@@ -110,6 +130,35 @@ _SIGS = {
     "pulse_decode_indices": (i32, [vp, u32, vp, vp, u32, vp, vp, vp, vp]),
     "pulse_synth_base": (i32, [vp, u64, u64, C.c_double, C.c_double, vp]),
     "pulse_synth_mutate": (i32, [vp, vp, vp, u64, C.c_double, u64, u64, C.POINTER(u64), vp]),
+    # host-buffer API
+    "pulse_patch_new": (i32, [C.POINTER(vp)]),
+    "pulse_patch_free": (None, [vp]),
+    "pulse_patch_get_header": (i32, [vp, C.POINTER(PatchHeader)]),
+    "pulse_patch_set_header": (i32, [vp, C.POINTER(PatchHeader)]),
+    "pulse_patch_num_tensors": (u32, [vp]),
+    "pulse_patch_get_tensor": (i32, [vp, u32, C.POINTER(TensorPatchC)]),
+    "pulse_patch_add_tensor": (i32, [vp, C.POINTER(TensorPatchC)]),
+    "pulse_bytes_data": (vp, [vp]),
+    "pulse_bytes_size": (u64, [vp]),
+    "pulse_bytes_free": (None, [vp]),
+    "pulse_encode": (i32, [C.POINTER(CheckpointC), C.POINTER(CheckpointC), u32, u32, C.POINTER(vp)]),
+    "pulse_decode": (i32, [C.POINTER(CheckpointC), vp, C.c_int, C.POINTER(vp), C.POINTER(u64)]),
+    "pulse_encode_index_payloads": (i32, [vp, C.POINTER(vp), C.POINTER(u64)]),
+    "pulse_decode_index_payloads": (i32, [vp, C.POINTER(vp), C.POINTER(u64), u32]),
+    "pulse_write_patch_bytes": (i32, [vp, C.POINTER(vp)]),
+    "pulse_read_patch_bytes": (i32, [C.c_char_p, u64, C.POINTER(vp)]),
+    "pulse_transfer_stats": (None, [C.POINTER(u64), C.POINTER(u64), C.c_int]),
+    "pulse_hash_weights": (i32, [C.POINTER(CheckpointC), C.c_char_p]),
+    "pulse_sha256_new": (i32, [C.POINTER(vp)]),
+    "pulse_sha256_update": (i32, [vp, C.c_char_p, u64]),
+    "pulse_sha256_final": (i32, [vp, C.c_char_p]),
+    "pulse_sha256_free": (None, [vp]),
+    "pulse_delta_encode_indices": (i32, [C.POINTER(C.c_int64), u64, C.POINTER(C.c_int64)]),
+    "pulse_delta_decode_indices": (i32, [C.POINTER(C.c_int64), u64, C.POINTER(C.c_int64)]),
+    "pulse_downscale_coo": (i32, [C.POINTER(C.c_int64), u64, C.POINTER(C.c_int64), u64, C.POINTER(vp)]),
+    "pulse_upscale_coo": (i32, [C.c_char_p, u64, u64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "pulse_compress": (i32, [C.c_char_p, u64, u32, C.POINTER(vp)]),
+    "pulse_decompress": (i32, [C.c_char_p, u64, u32, C.POINTER(vp)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)

@@ -185,6 +185,27 @@ void par_memcpy(void* dst, const void* src, size_t n) {
     });
 }
 
+// Every host<->device copy the host API issues goes through here, so the
+// end-to-end benchmark can report the bytes it really moved.
+std::atomic<uint64_t> g_h2d_bytes{0}, g_d2h_bytes{0};
+
+cudaError_t counted_copy(void* dst, const void* src, size_t n, cudaMemcpyKind kind, cudaStream_t s) {
+    if (kind == cudaMemcpyHostToDevice) g_h2d_bytes += n;
+    else if (kind == cudaMemcpyDeviceToHost) g_d2h_bytes += n;
+    return cudaMemcpyAsync(dst, src, n, kind, s);
+}
+
+// Page-locked (cudaHostAlloc'd or registered) host memory can be the DMA
+// source/target directly; pageable memory goes through the staging buffers.
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 // ---- device buffers + staging ----------------------------------------------------------------
 struct DevBuf {
     void* p = nullptr;
@@ -215,8 +236,8 @@ public:
         }
     }
     void h2d(void* dst, const void* src, size_t n, cudaStream_t s) {
-        if (n < (1 << 20)) {
-            cuda_check(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s), "H2D");
+        if (n < (1 << 20) || is_pinned(src)) {
+            cuda_check(counted_copy(dst, src, n, cudaMemcpyHostToDevice, s), "H2D");
             return;
         }
         for (size_t off = 0, k = 0; off < n; off += kChunk, ++k) {
@@ -224,13 +245,13 @@ public:
             const size_t len = std::min(kChunk, n - off);
             cuda_check(cudaEventSynchronize(ev_[b]), "staging wait");
             par_memcpy(buf_[b], static_cast<const uint8_t*>(src) + off, len);
-            cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, buf_[b], len, cudaMemcpyHostToDevice, s), "H2D");
+            cuda_check(counted_copy(static_cast<uint8_t*>(dst) + off, buf_[b], len, cudaMemcpyHostToDevice, s), "H2D");
             cuda_check(cudaEventRecord(ev_[b], s), "event");
         }
     }
     void d2h(void* dst, const void* src, size_t n, cudaStream_t s) {
-        if (n < (1 << 20)) {
-            cuda_check(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s), "D2H");
+        if (n < (1 << 20) || is_pinned(dst)) {
+            cuda_check(counted_copy(dst, src, n, cudaMemcpyDeviceToHost, s), "D2H");
             cuda_check(cudaStreamSynchronize(s), "D2H sync");
             return;
         }
@@ -239,7 +260,7 @@ public:
         auto issue = [&](size_t k) {
             const int b = int(k & 1);
             const size_t off = k * kChunk, len = std::min(kChunk, n - off);
-            cuda_check(cudaMemcpyAsync(buf_[b], static_cast<const uint8_t*>(src) + off, len, cudaMemcpyDeviceToHost, s), "D2H");
+            cuda_check(counted_copy(buf_[b], static_cast<const uint8_t*>(src) + off, len, cudaMemcpyDeviceToHost, s), "D2H");
             cuda_check(cudaEventRecord(ev_[b], s), "event");
         };
         issue(0);
@@ -385,7 +406,7 @@ std::vector<uint64_t> arena_offsets(const std::vector<uint64_t>& numel, uint64_t
 
 pulse_result fetch_result(Engine& E, const void* dev_result) {
     pulse_result r{};
-    cuda_check(cudaMemcpyAsync(&r, dev_result, sizeof(r), cudaMemcpyDeviceToHost, E.stream), "result");
+    cuda_check(counted_copy(&r, dev_result, sizeof(r), cudaMemcpyDeviceToHost, E.stream), "result");
     E.sync();
     uint64_t wd[7];
     if (pulse_watchdog(wd)) raise(PULSE_E_CUDA, "device watchdog fired (kind " + std::to_string(wd[1]) + ")");
@@ -552,7 +573,7 @@ Coded device_index_code(Engine& E, const pulse_patch* p, bool with_values) {
     }
     E.stager.h2d(didx, flat_idx.data(), n * 8, E.stream);
     E.stager.h2d(dval, flat_val.data(), n * 2, E.stream);
-    cuda_check(cudaMemcpyAsync(d.id_start, start.data(), (T + 1) * 8, cudaMemcpyHostToDevice, E.stream), "H2D");
+    cuda_check(counted_copy(d.id_start, start.data(), (T + 1) * 8, cudaMemcpyHostToDevice, E.stream), "H2D");
     const uint64_t cap = 10 * n + 64;
     uint8_t* dbody = E.body.as<uint8_t>(cap);
     auto* dent = E.entries.as<pulse_patch_entry>(T);
@@ -567,7 +588,7 @@ Coded device_index_code(Engine& E, const pulse_patch* p, bool with_values) {
     }
     std::vector<pulse_patch_entry> ents(r.n_entries);
     if (r.n_entries)
-        cuda_check(cudaMemcpyAsync(ents.data(), dent, r.n_entries * sizeof(pulse_patch_entry), cudaMemcpyDeviceToHost,
+        cuda_check(counted_copy(ents.data(), dent, r.n_entries * sizeof(pulse_patch_entry), cudaMemcpyDeviceToHost,
                                    E.stream), "D2H");
     out.body.resize(r.body_bytes);
     E.stager.d2h(out.body.data(), dbody, r.body_bytes, E.stream);
@@ -607,7 +628,7 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
     uint8_t* dbody = E.body.as<uint8_t>(body_len + 64);
     E.stager.h2d(dbody, body.data(), body_len, E.stream);
     auto* dent = E.entries.as<pulse_patch_entry>(T);
-    cuda_check(cudaMemcpyAsync(dent, ents.data(), T * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice, E.stream), "H2D");
+    cuda_check(counted_copy(dent, ents.data(), T * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice, E.stream), "H2D");
     int64_t* dout = E.out64.as<int64_t>(n);
     auto* dres = E.result.as<pulse_result>(1);
     launch_decode(plan->dev, p->representation, dbody, dent, T, nullptr, -1, dout, dres, E.stream);
@@ -773,7 +794,7 @@ pulse_status pulse_encode(const pulse_checkpoint* current, const pulse_checkpoin
                 if (pulse_plan_bind(plan, 0, pa.data()) || pulse_plan_bind(plan, 1, pb.data()))
                     raise(PULSE_E_CUDA, pulse_last_error());
                 if (pulse_encode_scan(plan, 1, 0, nullptr, E.stream)) raise(PULSE_E_CUDA, pulse_last_error());
-                cuda_check(cudaMemcpyAsync(&sm, plan->dev.scan, sizeof(sm), cudaMemcpyDeviceToHost, E.stream), "D2H");
+                cuda_check(counted_copy(&sm, plan->dev.scan, sizeof(sm), cudaMemcpyDeviceToHost, E.stream), "D2H");
                 E.sync();
                 if (sm.status != PULSE_E_CAPACITY) break;
                 cap = sm.n_changes + sm.n_changes / 16 + 1024;
@@ -781,7 +802,7 @@ pulse_status pulse_encode(const pulse_checkpoint* current, const pulse_checkpoin
             const uint64_t n = sm.n_changes;
             const PlanDev& d = plan->dev;
             std::vector<uint64_t> seg_start(d.n_segs + 1);
-            cuda_check(cudaMemcpyAsync(seg_start.data(), d.seg_start, seg_start.size() * 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
+            cuda_check(counted_copy(seg_start.data(), d.seg_start, seg_start.size() * 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
             int64_t* didx = E.out64.as<int64_t>(n);
             launch_export_indices(d, didx, E.stream);
             std::vector<int64_t> idx(n);
@@ -885,7 +906,7 @@ pulse_status pulse_decode(const pulse_checkpoint* previous, const pulse_patch* p
                 E.stager.h2d(didx, idx.data(), n * 8, E.stream);
                 E.stager.h2d(dval, val.data(), n * 2, E.stream);
                 auto* dent = E.entries.as<pulse_patch_entry>(stop);
-                cuda_check(cudaMemcpyAsync(dent, ents.data(), stop * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice,
+                cuda_check(counted_copy(dent, ents.data(), stop * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice,
                                            E.stream), "H2D");
                 auto* dres = E.result.as<pulse_result>(1);
                 launch_apply_idx64(plan->dev, didx, dval, dent, stop, 2, dres, E.stream);
@@ -1116,6 +1137,15 @@ pulse_status pulse_read_patch_bytes(const uint8_t* bytes, uint64_t n, pulse_patc
     });
 }
 
+void pulse_transfer_stats(uint64_t* h2d, uint64_t* d2h, int reset) {
+    if (h2d) *h2d = g_h2d_bytes.load();
+    if (d2h) *d2h = g_d2h_bytes.load();
+    if (reset) {
+        g_h2d_bytes = 0;
+        g_d2h_bytes = 0;
+    }
+}
+
 // ---- sha256.hpp -----------------------------------------------------------------------------
 pulse_status pulse_hash_weights(const pulse_checkpoint* c, uint8_t* out32) {
     return guarded([&] {
@@ -1164,7 +1194,7 @@ pulse_status pulse_delta_encode_indices(const int64_t* in, uint64_t n, int64_t* 
         E.stager.h2d(d, in, n * 8, E.stream);
         launch_delta_encode(d, n, d + n, err, E.stream);
         uint64_t k = 0;
-        cuda_check(cudaMemcpyAsync(&k, err, 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
+        cuda_check(counted_copy(&k, err, 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
         E.sync();
         if (k != kNoError)
             raise(PULSE_E_ARGUMENT, key_check(k) == kArgNegative ? "indices must be non-negative"
@@ -1184,7 +1214,7 @@ pulse_status pulse_delta_decode_indices(const int64_t* in, uint64_t n, int64_t* 
         E.stager.h2d(d, in, n * 8, E.stream);
         launch_delta_decode(d, n, d + n, err, E.stream);
         uint64_t k = 0;
-        cuda_check(cudaMemcpyAsync(&k, err, 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
+        cuda_check(counted_copy(&k, err, 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
         E.sync();
         if (k != kNoError)
             raise(PULSE_E_FORMAT, key_elem(k) == 0 ? "first index gap is negative"
@@ -1210,7 +1240,7 @@ pulse_status pulse_downscale_coo(const int64_t* rows, uint64_t n_rows, const int
             E.stager.h2d(d + n_rows, cols, n_rows * 8, E.stream);
             launch_coo_pack(d, d + n_rows, n_rows, dout, misc + 1, misc, E.stream);
             uint64_t h[2];
-            cuda_check(cudaMemcpyAsync(h, misc, 16, cudaMemcpyDeviceToHost, E.stream), "D2H");
+            cuda_check(counted_copy(h, misc, 16, cudaMemcpyDeviceToHost, E.stream), "D2H");
             E.sync();
             if (h[0] != kNoError) {
                 const uint32_t c = key_check(h[0]);
@@ -1236,7 +1266,7 @@ pulse_status pulse_upscale_coo(const uint8_t* data, uint64_t n, uint64_t count, 
         if (n) E.stager.h2d(dp, data, n, E.stream);
         launch_coo_unpack(dp, n, count, d, d + count, err, E.stream);
         uint64_t k = 0;
-        cuda_check(cudaMemcpyAsync(&k, err, 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
+        cuda_check(counted_copy(&k, err, 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
         E.sync();
         if (k != kNoError) {
             const uint32_t c = key_check(k);

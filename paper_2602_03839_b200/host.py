@@ -1,0 +1,324 @@
+"""Python mirror of the reference's host-buffer API (patch.hpp, patch_file.hpp,
+index_coding.hpp, compression.hpp, sha256.hpp) over the C ABI of
+libpulse_cuda.so -- the same functions the C++ drop-in headers
+(include/pulse/*.hpp) wrap.  Per-element work runs in the CUDA kernels.
+
+Checkpoints are lists of (name, shape, uint16 ndarray of bf16 bit patterns).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from ._native import COO_DOWNSCALED, COO_INT32, FLAT_INT32, IDENTITY, LZ4, ZSTD1, ZSTD3, GZIP6, PulseError  # noqa: F401
+
+
+@dataclass
+class Tensor:
+    name: str
+    shape: tuple
+    data: np.ndarray  # uint16, flat
+
+
+@dataclass
+class Checkpoint:
+    step: int = 0
+    tensors: list = field(default_factory=list)
+
+
+@dataclass
+class TensorPatch:
+    name: str
+    shape: tuple
+    indices: np.ndarray  # int64
+    values: np.ndarray   # uint16
+
+
+@dataclass
+class SparsePatch:
+    base_step: int = 0
+    target_step: int = 0
+    anchor_step: int = 0
+    representation: int = COO_DOWNSCALED
+    codec: int = ZSTD1
+    target_hash: bytes = b"\0" * 32
+    tensors: list = field(default_factory=list)
+
+    def total_changes(self) -> int:
+        return sum(int(t.indices.size) for t in self.tensors)
+
+
+# ---- C views ----------------------------------------------------------------------------------
+class CheckpointView:
+    """pulse_checkpoint over Python/numpy memory (kept alive by this object)."""
+
+    def __init__(self, ck: Checkpoint):
+        self._keep = []
+        arr = (N.Tensor * max(1, len(ck.tensors)))()
+        for i, t in enumerate(ck.tensors):
+            shp = np.ascontiguousarray(t.shape, dtype=np.int64)
+            data = np.ascontiguousarray(t.data).view(np.uint16)
+            name = t.name.encode()
+            self._keep += [shp, data, name]
+            arr[i] = N.Tensor(name, shp.ctypes.data_as(C.POINTER(C.c_int64)), len(t.shape), data.ctypes.data, data.size)
+        self._arr = arr
+        self.c = N.CheckpointC(ck.step, arr, len(ck.tensors))
+
+
+class PatchHandle:
+    """Owns a library pulse_patch*."""
+
+    def __init__(self, ptr=None):
+        if ptr is None:
+            ptr = C.c_void_p()
+            N.check(N.lib.pulse_patch_new(C.byref(ptr)))
+        self.ptr = ptr
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            N.lib.pulse_patch_free(self.ptr)
+            self.ptr = None
+
+    @classmethod
+    def from_patch(cls, p: SparsePatch, with_indices=True):
+        h = cls()
+        hd = N.PatchHeader(p.base_step, p.target_step, p.anchor_step, p.representation, p.codec,
+                           (C.c_uint8 * 32)(*bytes(p.target_hash)))
+        N.check(N.lib.pulse_patch_set_header(h.ptr, C.byref(hd)))
+        for tp in p.tensors:
+            shp = np.ascontiguousarray(tp.shape, dtype=np.int64)
+            idx = np.ascontiguousarray(tp.indices, dtype=np.int64)
+            val = np.ascontiguousarray(tp.values, dtype=np.uint16)
+            v = N.TensorPatchC(tp.name.encode(), shp.ctypes.data_as(C.POINTER(C.c_int64)), len(tp.shape),
+                               idx.ctypes.data_as(C.POINTER(C.c_int64)), idx.size if with_indices else 0,
+                               val.ctypes.data_as(C.POINTER(C.c_uint16)), val.size)
+            N.check(N.lib.pulse_patch_add_tensor(h.ptr, C.byref(v)))
+        return h
+
+    def to_patch(self) -> SparsePatch:
+        hd = N.PatchHeader()
+        N.check(N.lib.pulse_patch_get_header(self.ptr, C.byref(hd)))
+        p = SparsePatch(hd.base_step, hd.target_step, hd.anchor_step, hd.representation, hd.codec, bytes(hd.target_hash))
+        for i in range(N.lib.pulse_patch_num_tensors(self.ptr)):
+            v = N.TensorPatchC()
+            N.check(N.lib.pulse_patch_get_tensor(self.ptr, i, C.byref(v)))
+            idx = np.ctypeslib.as_array(v.indices, (v.n_indices,)).copy() if v.n_indices else np.zeros(0, np.int64)
+            val = np.ctypeslib.as_array(v.values, (v.n_values,)).copy() if v.n_values else np.zeros(0, np.uint16)
+            p.tensors.append(TensorPatch(v.name.decode(), tuple(v.shape[k] for k in range(v.rank)), idx, val))
+        return p
+
+
+def _take(b) -> bytes:
+    n = N.lib.pulse_bytes_size(b)
+    out = C.string_at(N.lib.pulse_bytes_data(b), n) if n else b""
+    N.lib.pulse_bytes_free(b)
+    return out
+
+
+# ---- the reference API ---------------------------------------------------------------------------
+def encode_handle(current: Checkpoint, previous: Checkpoint, representation=COO_DOWNSCALED, codec=ZSTD1,
+                  views=None) -> PatchHandle:
+    cv, pv = views or (CheckpointView(current), CheckpointView(previous))
+    out = C.c_void_p()
+    N.check(N.lib.pulse_encode(C.byref(cv.c), C.byref(pv.c), representation, codec, C.byref(out)))
+    return PatchHandle(out)
+
+
+def encode(current: Checkpoint, previous: Checkpoint, representation=COO_DOWNSCALED, codec=ZSTD1) -> SparsePatch:
+    """patch.hpp:264-307"""
+    return encode_handle(current, previous, representation, codec).to_patch()
+
+
+def decode_into(previous: Checkpoint, patch, out_arrays, verify_hash=True, view=None) -> int:
+    """patch.hpp:309-348 into caller arrays (one per tensor of `previous`); returns the step."""
+    pv = view or CheckpointView(previous)
+    h = patch if isinstance(patch, PatchHandle) else PatchHandle.from_patch(patch)
+    ptrs = (C.c_void_p * max(1, len(out_arrays)))(*[a.ctypes.data for a in out_arrays])
+    step = C.c_uint64()
+    N.check(N.lib.pulse_decode(C.byref(pv.c), h.ptr, int(verify_hash), ptrs, C.byref(step)))
+    return step.value
+
+
+def decode(previous: Checkpoint, patch, verify_hash=True) -> Checkpoint:
+    outs = [np.empty(t.data.size, np.uint16) for t in previous.tensors]
+    step = decode_into(previous, patch, outs, verify_hash)
+    return Checkpoint(step, [Tensor(t.name, t.shape, o) for t, o in zip(previous.tensors, outs)])
+
+
+def encode_index_payloads(patch: SparsePatch) -> list:
+    """patch.hpp:116-174"""
+    h = PatchHandle.from_patch(patch)
+    sizes = (C.c_uint64 * max(1, len(patch.tensors)))()
+    b = C.c_void_p()
+    N.check(N.lib.pulse_encode_index_payloads(h.ptr, C.byref(b), sizes))
+    blob = _take(b)
+    out, off = [], 0
+    for i in range(len(patch.tensors)):
+        out.append(blob[off:off + sizes[i]])
+        off += sizes[i]
+    return out
+
+
+def decode_index_payloads(patch: SparsePatch, payloads: list) -> SparsePatch:
+    """patch.hpp:178-262 (counts = len(values)); returns the patch with indices."""
+    h = PatchHandle.from_patch(patch, with_indices=False)
+    bufs = [C.create_string_buffer(p, len(p)) for p in payloads]
+    ptrs = (C.c_void_p * max(1, len(bufs)))(*[C.addressof(b) for b in bufs])
+    sizes = (C.c_uint64 * max(1, len(bufs)))(*[len(p) for p in payloads])
+    N.check(N.lib.pulse_decode_index_payloads(h.ptr, ptrs, sizes, len(payloads)))
+    return h.to_patch()
+
+
+def write_patch_bytes(patch) -> bytes:
+    """patch_file.hpp:30-83"""
+    h = patch if isinstance(patch, PatchHandle) else PatchHandle.from_patch(patch)
+    b = C.c_void_p()
+    N.check(N.lib.pulse_write_patch_bytes(h.ptr, C.byref(b)))
+    return _take(b)
+
+
+def read_patch_handle(data: bytes) -> PatchHandle:
+    out = C.c_void_p()
+    N.check(N.lib.pulse_read_patch_bytes(data, len(data), C.byref(out)))
+    return PatchHandle(out)
+
+
+def read_patch_bytes(data: bytes) -> SparsePatch:
+    """patch_file.hpp:85-147"""
+    return read_patch_handle(data).to_patch()
+
+
+def hash_weights(ck: Checkpoint) -> bytes:
+    """sha256.hpp:93-116"""
+    v = CheckpointView(ck)
+    out = C.create_string_buffer(32)
+    N.check(N.lib.pulse_hash_weights(C.byref(v.c), out))
+    return out.raw
+
+
+def delta_encode_indices(idx) -> np.ndarray:
+    a = np.ascontiguousarray(idx, np.int64)
+    out = np.empty_like(a)
+    N.check(N.lib.pulse_delta_encode_indices(a.ctypes.data_as(C.POINTER(C.c_int64)), a.size,
+                                             out.ctypes.data_as(C.POINTER(C.c_int64))))
+    return out
+
+
+def delta_decode_indices(gaps) -> np.ndarray:
+    a = np.ascontiguousarray(gaps, np.int64)
+    out = np.empty_like(a)
+    N.check(N.lib.pulse_delta_decode_indices(a.ctypes.data_as(C.POINTER(C.c_int64)), a.size,
+                                             out.ctypes.data_as(C.POINTER(C.c_int64))))
+    return out
+
+
+def downscale_coo(rows, cols) -> bytes:
+    r = np.ascontiguousarray(rows, np.int64)
+    c = np.ascontiguousarray(cols, np.int64)
+    b = C.c_void_p()
+    N.check(N.lib.pulse_downscale_coo(r.ctypes.data_as(C.POINTER(C.c_int64)), r.size,
+                                      c.ctypes.data_as(C.POINTER(C.c_int64)), c.size, C.byref(b)))
+    return _take(b)
+
+
+def upscale_coo(data: bytes, count: int):
+    rows = np.empty(count, np.int64)
+    cols = np.empty(count, np.int64)
+    N.check(N.lib.pulse_upscale_coo(data, len(data), count, rows.ctypes.data_as(C.POINTER(C.c_int64)),
+                                    cols.ctypes.data_as(C.POINTER(C.c_int64))))
+    return rows, cols
+
+
+def compress(data: bytes, codec: int) -> bytes:
+    b = C.c_void_p()
+    N.check(N.lib.pulse_compress(data, len(data), codec, C.byref(b)))
+    return _take(b)
+
+
+def decompress(data: bytes, codec: int) -> bytes:
+    b = C.c_void_p()
+    N.check(N.lib.pulse_decompress(data, len(data), codec, C.byref(b)))
+    return _take(b)
+
+
+def transfer_stats(reset=False):
+    """(h2d_bytes, d2h_bytes) the host API has copied so far in this process."""
+    a, b = C.c_uint64(), C.c_uint64()
+    N.lib.pulse_transfer_stats(C.byref(a), C.byref(b), int(reset))
+    return a.value, b.value
+
+
+# ---- end-to-end benchmark leg ---------------------------------------------------------------------
+def bench_e2e(args, mine, prev_dev, curr_dev, world, rank, steps=None, warmup=3):
+    """The benchmark metric measured end to end through the public host API.
+
+    Every step runs encode -> write_patch_bytes -> read_patch_bytes ->
+    decode(verify_hash=False) on snapshots held in pinned host memory, so it
+    includes all host->device copies of the inputs and device->host reads of
+    the results (and encode's SHA-256 target hash, as the reference's encode
+    does).  The snapshots are the same bytes as the device-resident run
+    (copied out once, untimed).  Wall-clock per step, max over ranks; the
+    bytes moved are the library's own counters (pulse_transfer_stats)."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from .shapes import numel
+
+    sizes = [numel(s) for _, s in mine]
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    hp = torch.empty(prev_dev.numel(), dtype=torch.int16).pin_memory()
+    hc = torch.empty(curr_dev.numel(), dtype=torch.int16).pin_memory()
+    ho = torch.empty(prev_dev.numel(), dtype=torch.int16).pin_memory()
+    hp.copy_(prev_dev.view(torch.int16))
+    hc.copy_(curr_dev.view(torch.int16))
+    a_prev, a_curr, a_out = (t.numpy().view(np.uint16) for t in (hp, hc, ho))
+
+    def mk(a, step):
+        return Checkpoint(step, [Tensor(n, s, a[int(offs[i]):int(offs[i + 1])]) for i, (n, s) in enumerate(mine)])
+
+    ck = {0: mk(a_prev, 0), 1: mk(a_curr, 1)}
+    views = {k: CheckpointView(v) for k, v in ck.items()}
+    outs = [a_out[int(offs[i]):int(offs[i + 1])] for i in range(len(sizes))]
+    steps = steps or max(1, min(args.steps, 3))
+
+    def step(k):
+        # alternate direction like the device run: prev->curr, then curr->prev
+        c, p = (1, 0) if k % 2 == 0 else (0, 1)
+        h = encode_handle(ck[c], ck[p], args.repr, IDENTITY, views=(views[c], views[p]))
+        wire = write_patch_bytes(h)
+        back = read_patch_handle(wire)
+        decode_into(ck[p], back, outs, verify_hash=False, view=views[p])
+        return c
+
+    for k in range(warmup):
+        step(k)
+    if world > 1:
+        dist.barrier()
+    transfer_stats(reset=True)
+    t0 = time.perf_counter()
+    for k in range(steps):
+        last = step(k)
+    dt = time.perf_counter() - t0
+    h2d, d2h = transfer_stats()
+    ok = bool(np.array_equal(a_out, (a_curr if last == 1 else a_prev)))
+    t = torch.tensor([dt / steps, float(offs[-1]), float(ok)], dtype=torch.float64)
+    if world > 1:
+        t = t.cuda()
+        mx = t[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot = t[1:].clone()
+        dist.all_reduce(tot)
+        s_step, d_total, n_ok = float(mx.item()), float(tot[0].item()), int(tot[1].item())
+        ok = n_ok == world
+    else:
+        s_step, d_total = float(t[0]), float(t[1])
+    return {"value": round(2 * d_total / s_step / 1e9, 4), "unit": "GB/s",
+            "h2d_bytes_per_step": int(h2d // steps), "d2h_bytes_per_step": int(d2h // steps),
+            "steps": steps, "warmup": warmup, "s_per_step": round(s_step, 4), "verified": ok,
+            "path": "pulse_encode -> pulse_write_patch_bytes -> pulse_read_patch_bytes -> "
+                    "pulse_decode(verify_hash=false); identity codec; pinned host snapshots; wall clock"}

@@ -1,0 +1,147 @@
+"""The Python mirror of the reference API (paper_2602_03839_b200.host) over the
+host-buffer C ABI, against the reference's own bytes: full PULP files (every
+representation x codec) from encode -> write_patch_bytes, read -> decode
+round trips, index payload coding, and the host-only helpers (hash, codecs)."""
+import numpy as np
+import pytest
+
+from oracle.oracle import have_reference, reference
+
+H = pytest.importorskip("paper_2602_03839_b200.host")
+
+CODECS = [0, 1, 2, 3, 4]
+
+
+def mirror(ck):
+    return H.Checkpoint(ck.step, [H.Tensor(t.name, t.shape, t.data) for t in ck.tensors])
+
+
+def as_ref_patch(p):
+    from oracle.oracle import Patch, TensorPatch
+    return Patch(p.base_step, p.target_step, p.anchor_step, p.representation, p.codec, p.target_hash,
+                 [TensorPatch(t.name, t.shape, t.indices, t.values) for t in p.tensors])
+
+
+# ---- host-only (CPU) --------------------------------------------------------------------------
+def test_hash_weights_matches_golden(golden):
+    for name in golden.names:
+        _, curr, m = golden.case(name)
+        assert H.hash_weights(mirror(curr)).hex() == m["target_hash"], name
+
+
+@pytest.mark.parametrize("codec", CODECS)
+def test_codec_round_trip_and_bytes(codec):
+    rng = np.random.default_rng(codec)
+    data = (rng.integers(0, 4, 200_000, dtype=np.uint8)).tobytes()
+    z = H.compress(data, codec)
+    assert H.decompress(z, codec) == data
+    if have_reference():
+        assert z == reference().compress(data, codec)
+
+
+def test_transfer_stats_exported():
+    h2d, d2h = H.transfer_stats()
+    assert h2d >= 0 and d2h >= 0
+
+
+# ---- device compute through the host API --------------------------------------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("repr_", [0, 1, 2])
+def test_encode_write_matches_reference_pulp(golden, repr_):
+    for name in golden.names:
+        prev, curr, m = golden.case(name)
+        for codec in CODECS:
+            want = golden.pulp(name, repr_, codec)
+            if want is None:
+                continue
+            h = H.encode_handle(mirror(curr), mirror(prev), repr_, codec)
+            assert H.write_patch_bytes(h) == want, (name, repr_, codec)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("repr_", [0, 1, 2])
+def test_read_decode_round_trip(golden, repr_):
+    for name in golden.names:
+        prev, curr, m = golden.case(name)
+        for codec in CODECS:
+            wire = golden.pulp(name, repr_, codec)
+            if wire is None:
+                continue
+            p = H.read_patch_bytes(wire)
+            assert p.total_changes() == m["patches"][f"{repr_}/{codec}"]["changes"]
+            out = H.decode(mirror(prev), p, verify_hash=True)
+            for a, b in zip(sorted(out.tensors, key=lambda t: t.name), curr.sorted()):
+                assert np.array_equal(a.data, b.data), (name, repr_, codec, a.name)
+
+
+@pytest.mark.gpu
+def test_patch_object_matches_reference_encode(golden):
+    if not have_reference():
+        pytest.skip("oracle/_ref not built")
+    R = reference()
+    for name in golden.names[:6]:
+        prev, curr, _ = golden.case(name)
+        for repr_ in (0, 1, 2):
+            mine = H.encode(mirror(curr), mirror(prev), repr_, 2)
+            ref = R.encode(curr, prev, repr_, 2)
+            assert mine.target_hash == ref.target_hash
+            assert [t.name for t in mine.tensors] == [t.name for t in ref.tensors]
+            for a, b in zip(mine.tensors, ref.tensors):
+                assert np.array_equal(a.indices, b.indices) and np.array_equal(a.values, b.values)
+            pay = H.encode_index_payloads(mine)
+            assert pay == R.encode_index_payloads(ref), (name, repr_)
+            back = H.decode_index_payloads(H.SparsePatch(mine.base_step, mine.target_step, mine.anchor_step,
+                                                         repr_, 2, mine.target_hash,
+                                                         [H.TensorPatch(t.name, t.shape, np.zeros(0, np.int64),
+                                                                        t.values) for t in mine.tensors]), pay)
+            for a, b in zip(back.tensors, mine.tensors):
+                assert np.array_equal(a.indices, b.indices)
+
+
+@pytest.mark.gpu
+def test_index_helpers_match_reference():
+    if not have_reference():
+        pytest.skip("oracle/_ref not built")
+    R = reference()
+    rng = np.random.default_rng(3)
+    idx = np.unique(rng.integers(0, 1 << 40, 50_000)).astype(np.int64)
+    g = H.delta_encode_indices(idx)
+    assert np.array_equal(g, R.delta_encode(idx))
+    assert np.array_equal(H.delta_decode_indices(g), idx)
+    rows = np.sort(rng.integers(0, 1 << 20, 20_000)).astype(np.int64)
+    cols = rng.integers(0, 1 << 18, 20_000).astype(np.int64)
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    keep = np.concatenate([[True], (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])])
+    rows, cols = rows[keep], cols[keep]
+    b = H.downscale_coo(rows, cols)
+    assert b == R.downscale_coo(rows, cols)
+    r2, c2 = H.upscale_coo(b, rows.size)
+    assert np.array_equal(r2, rows) and np.array_equal(c2, cols)
+
+
+@pytest.mark.gpu
+def test_errors_map_to_reference_kinds(golden):
+    from oracle.oracle import OracleError, Tensor
+
+    prev, curr, _ = golden.case("roundtrip_s0")
+    R = reference() if have_reference() else None
+    for codec in CODECS:
+        wire = golden.pulp("roundtrip_s0", 0, codec)
+        for cut in (3, 40, len(wire) - 10):
+            with pytest.raises(H.PulseError) as e:
+                H.read_patch_bytes(wire[:-cut])
+            if R is not None:
+                with pytest.raises(OracleError) as r:
+                    R.read_patch_bytes(wire[:-cut])
+                assert e.value.kind == r.value.kind, (codec, cut)
+    wire = golden.pulp("roundtrip_s0", 0, 2)
+    bad = mirror(prev)
+    bad.tensors[0] = H.Tensor(bad.tensors[0].name, (1,), bad.tensors[0].data[:1])
+    with pytest.raises(H.PulseError) as e:
+        H.decode(bad, H.read_patch_bytes(wire))
+    if R is not None:
+        rb = type(prev)(prev.step, [Tensor(t.name, t.shape, t.data) for t in bad.tensors])
+        with pytest.raises(OracleError) as r:
+            R.decode(rb, R.read_patch_bytes(wire))
+        assert e.value.kind == r.value.kind
