@@ -65,56 +65,93 @@ def measured_peaks():
 # clocks during the timed region
 # ------------------------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event reasons sampled DURING the timed region: NVML
+    polled every 5 ms from a thread (nvidia-smi -lms 100 as a fallback)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, device_index: int):
+    def __init__(self, device_index: int, period_s: float = 0.005):
         self.dev = device_index
+        self.period = period_s
+        self.sm, self.mx, self.reasons = [], None, set()
         self.proc = None
-        self.lines = []
+        self.stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.FIELDS,
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self._nvml_index(nv))
+            self.mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def poll():
+                while not self.stop.is_set():
+                    self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                    r = int(get_reasons(h))
+                    for name, bit in self.REASONS.items():
+                        if r & bit:
+                            self.reasons.add(name)
+                    time.sleep(self.period)
+            self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+            self.mode = "nvml"
+        except Exception:
+            self.mode = "nvidia-smi"
+            self._start_smi()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _nvml_index(self, nv):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            ids = [v.strip() for v in vis.split(",")]
+            if self.dev < len(ids) and ids[self.dev].isdigit():
+                return int(ids[self.dev])
+        return self.dev
+
+    def _start_smi(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + fields,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            return
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+        def read():
+            for line in self.proc.stdout:
+                parts = [p.strip() for p in line.split(",")]
+                try:
+                    self.sm.append(float(parts[0]))
+                    self.mx = float(parts[1])
+                except (ValueError, IndexError):
+                    continue
+                for name, v in zip(names, parts[2:6]):
+                    if v.lower().startswith("active"):
+                        self.reasons.add(name)
+        self.t = threading.Thread(target=read, daemon=True)
+        self.t.start()
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        elif getattr(self, "t", None):
+            self.t.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for name, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": self.mode}
 
 
 # ------------------------------------------------------------------------------------------
@@ -359,7 +396,8 @@ def run_pulse(args):
             "encode_ms": round(scan_max, 4), "apply_ms": round(apply_max, 4),
             "patch_mb": round(body_total / 1e6, 3), "changes": int(changes_total),
             "roofline": {"kernel": "k1_diff_compact", "bound": "hbm", "achieved": round(k1_gbs, 2),
-                         "peak": peak, "unit": "GB/s", "frac": round(k1_gbs / peak, 4), "traffic": None,
+                         "peak": peak, "unit": "GB/s", "frac": round(k1_gbs / peak, 4),
+                         "traffic": profiled_traffic(args, world),
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": k1_bytes},
             "gpu_launches": (2 + n_emit + n_apply) * args.steps,
@@ -373,6 +411,20 @@ def run_pulse(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def profiled_traffic(args, world):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one K1 launch from the
+    committed `ncu --set full` capture of this same configuration, else None."""
+    path = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)["k1_diff_compact"]
+    except (OSError, KeyError, ValueError):
+        return None
+    same = (t.get("workload") == args.workload and t.get("n_gpus") == world and
+            t.get("representation") == REPR_NAMES[args.repr] and abs(t.get("sparsity", -1) - args.sparsity) < 1e-9)
+    return t["dram_bytes_per_launch"] if same else None
 
 
 def run_e2e(args, mine, prev, curr, views, world, rank):

@@ -8,13 +8,27 @@
 // patch.hpp:120-156).  Decoding is then a pair of segmented prefix sums over
 // the entries, read straight from the body:
 //
-//   F1 f_range_agg   per warp range of 4096 entries: segmented-sum aggregates
+//   F1 f_agg<0>      per warp range of 4096 entries: segmented-sum aggregates
 //                    (rows: restart at each tensor; columns: restart at each new
 //                    row, index_coding.hpp:141-153); flags escape markers.
 //   F2 f_range_scan  one CTA: exclusive scan of the range aggregates.
-//   F3 f_validate    recompute every (row, col) / index and apply the reference
+//   F3 f_agg<1>      recompute every (row, col) / index and apply the reference
 //                    checks (zero gap, column range, index range) -- no writes.
-//   F4 f_scatter     only if nothing failed: recompute and W[flat] = value.
+//   F4 f_agg<2>      only if nothing failed: recompute and W[flat] = value.
+//
+// Data movement.  A warp works on 1024-entry chunks.  It stages a chunk's row
+// bytes / column units / u32 gaps (and, for F4, its values) from the body into
+// its own shared memory with coalesced 16-byte loads, funnel-shifting the
+// arbitrary byte alignment of the payload away; each lane then decodes 32
+// CONSECUTIVE entries serially from shared memory (one warp segmented scan per
+// chunk, not per 32 entries).  Shared-memory vectors are XOR-swizzled so both
+// the staging stores and the per-lane 16-byte reads are bank-conflict free.
+// F4 transposes the decoded indices back to entry order through shared memory
+// so each warp store instruction covers 32 consecutive changes (a few sectors
+// for clustered updates) rather than 32 scattered ones.
+//
+// A chunk that straddles two patch entries (at most one per changed tensor) or
+// a tensor with >= 2^32 elements takes the per-round walker path instead.
 //
 // If d_layout or F1 finds anything the fixed layout cannot express (escapes,
 // short/long payloads, marker bytes), `flags[0]` routes the patch to the
@@ -27,8 +41,18 @@ namespace dev {
 
 namespace {
 
-constexpr uint32_t kRange = 4096;  // entries per warp range
+constexpr uint32_t kRange = 4096;  // entries per warp range (aggregate granularity)
+constexpr uint32_t kChunk = 1024;  // entries staged per warp step
+constexpr uint32_t kPer = kChunk / 32;  // consecutive entries per lane
 constexpr uint64_t H = SegSumOp::kHead;
+
+enum Repr : int { kCoo = 0, kI32 = 1, kFlat = 2 };
+enum Pass : int { kAgg = 0, kValidate = 1, kScatter = 2 };
+
+// Per-warp staging area (bytes).  a: COO rows (1 KiB used) or u32 gaps (4 KiB);
+// b: COO column units; v: values; x: decoded tensor-local indices.
+constexpr uint32_t kABytes = kChunk * 4, kBBytes = kChunk * 2, kVBytes = kChunk * 2, kXBytes = kChunk * 4;
+__host__ __device__ constexpr uint32_t warp_smem(int pass) { return kABytes + kBBytes + (pass == kScatter ? kVBytes + kXBytes : 0); }
 
 __device__ __forceinline__ uint32_t lanemask_le() {
     uint32_t m;
@@ -36,34 +60,121 @@ __device__ __forceinline__ uint32_t lanemask_le() {
     return m;
 }
 
-// Warp-uniform context: the patch entry a round starts in.
+// XOR swizzle of 16-byte vector slots for buffers read as V consecutive vectors
+// per lane: within every group of 8 lanes the slots hit 8 distinct bank quads,
+// and 8 consecutive slots (a staging store) stay a permutation of one 128 B row.
+template <int V>
+__device__ __forceinline__ uint32_t swz(uint32_t q) {
+    return V == 1 ? q : (q ^ ((q >> 3) & (V - 1)));
+}
+
+__device__ __forceinline__ uint32_t shr_pair(uint32_t lo, uint32_t hi, uint32_t sh) {
+    return __funnelshift_r(lo, hi, sh);
+}
+
+// Copies bytes [g, g+len) (len <= 512 * R) into shared vectors dst[swz(q)],
+// packed from byte 0.  All loads are issued before any store.  Reads at most
+// the 16-byte-aligned blocks that contain payload bytes (never past a page).
+template <int R, int V>
+__device__ __forceinline__ void stage_piece(uint4* dst, const uint8_t* g, uint32_t len, uint32_t q_base) {
+    const int lane = threadIdx.x & 31;
+    const uintptr_t ga = reinterpret_cast<uintptr_t>(g);
+    const uint32_t s = uint32_t(ga & 15);
+    const uint4* src = reinterpret_cast<const uint4*>(ga - s);
+    const uint32_t nv_in = (s + len + 15) >> 4;
+    const uint32_t nv_out = (len + 15) >> 4;
+    uint4 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t q = lane + 32 * r;
+        v[r] = q < nv_in ? ld_stream(src + q) : make_uint4(0, 0, 0, 0);
+    }
+    if (s == 0) {  // aligned: straight copy
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t q = lane + 32 * r;
+            if (q < nv_out) dst[swz<V>(q_base + q)] = v[r];
+        }
+        return;
+    }
+    uint4 extra = make_uint4(0, 0, 0, 0);
+    if (lane == 0 && 32u * R < nv_in) extra = ld_stream(src + 32 * R);
+    const uint32_t sw = s >> 2, sh = (s & 3) * 8;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        uint4 nx;
+        nx.x = __shfl_down_sync(0xffffffffu, v[r].x, 1);
+        nx.y = __shfl_down_sync(0xffffffffu, v[r].y, 1);
+        nx.z = __shfl_down_sync(0xffffffffu, v[r].z, 1);
+        nx.w = __shfl_down_sync(0xffffffffu, v[r].w, 1);
+        const uint4 n0 = r + 1 < R ? v[r + 1 < R ? r + 1 : r] : extra;
+        const uint32_t w0 = __shfl_sync(0xffffffffu, n0.x, 0), w1 = __shfl_sync(0xffffffffu, n0.y, 0);
+        const uint32_t w2 = __shfl_sync(0xffffffffu, n0.z, 0), w3 = __shfl_sync(0xffffffffu, n0.w, 0);
+        if (lane == 31) nx = make_uint4(w0, w1, w2, w3);
+        const uint32_t W[8] = {v[r].x, v[r].y, v[r].z, v[r].w, nx.x, nx.y, nx.z, nx.w};
+        uint4 o;
+        switch (sw) {
+            case 0: o = make_uint4(shr_pair(W[0], W[1], sh), shr_pair(W[1], W[2], sh), shr_pair(W[2], W[3], sh), shr_pair(W[3], W[4], sh)); break;
+            case 1: o = make_uint4(shr_pair(W[1], W[2], sh), shr_pair(W[2], W[3], sh), shr_pair(W[3], W[4], sh), shr_pair(W[4], W[5], sh)); break;
+            case 2: o = make_uint4(shr_pair(W[2], W[3], sh), shr_pair(W[3], W[4], sh), shr_pair(W[4], W[5], sh), shr_pair(W[5], W[6], sh)); break;
+            default: o = make_uint4(shr_pair(W[3], W[4], sh), shr_pair(W[4], W[5], sh), shr_pair(W[5], W[6], sh), shr_pair(W[6], W[7], sh)); break;
+        }
+        const uint32_t q = lane + 32 * r;
+        if (q < nv_out) dst[swz<V>(q_base + q)] = o;
+    }
+}
+
+// Stages up to `len` bytes (len <= cap) in pieces of 2 KiB (16 B aligned pieces
+// keep the source alignment, so the swizzled slot index just continues).
+template <int V>
+__device__ __forceinline__ void stage(uint4* dst, const uint8_t* g, uint32_t len) {
+    for (uint32_t off = 0; off < len; off += 2048)
+        stage_piece<4, V>(dst, g + off, min(2048u, len - off), off >> 4);
+}
+
+// Reads lane-consecutive vector i (of V) of a swizzled buffer.
+template <int V>
+__device__ __forceinline__ uint4 lane_vec(const uint4* buf, int i) {
+    const int lane = threadIdx.x & 31;
+    return buf[swz<V>(uint32_t(lane * V + i))];
+}
+
+// Inclusive SegSum scan over lanes of a (rows, cols) pair.
+__device__ __forceinline__ void warp_segscan2(uint64_t& r, uint64_t& c) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t pr = __shfl_up_sync(0xffffffffu, r, off);
+        const uint64_t pc = __shfl_up_sync(0xffffffffu, c, off);
+        if (lane >= off) {
+            r = SegSumOp::op(pr, r);
+            c = SegSumOp::op(pc, c);
+        }
+    }
+}
+
+// ---- per-round walker (fallback for chunks that straddle patch entries) -------------------
 struct ECtx {
     uint32_t e;
-    uint64_t lo, hi;   // entries [lo, hi) belong to e
+    uint64_t lo, hi;  // entries [lo, hi) belong to e
     EntryLayout L;
-    uint32_t magic, shift;
 };
 
-__device__ __forceinline__ ECtx load_ectx(const EntryLayout* el, const uint64_t* es, const ColDiv* cdv, uint32_t e) {
+__device__ __forceinline__ ECtx load_ectx(const EntryLayout* el, const uint64_t* es, uint32_t e) {
     ECtx c;
     c.e = e;
     c.lo = es[e];
     c.hi = es[e + 1];
     c.L = el[e];
-    const ColDiv d = cdv[c.L.tensor];
-    c.magic = d.magic;
-    c.shift = d.shift;
     return c;
 }
 
-// One round of 32 consecutive entries: per-lane entry, ordinal and raw fields.
 struct Fields {
     bool valid;
     uint32_t e;
     uint64_t o;
     uint32_t a;  // COO: row gap byte; int32: the u32 gap
     uint32_t b;  // COO: column entry (u16)
-    // this lane's entry layout (by value: the warp context may move on)
     uint32_t tensor;
     uint64_t val_off, numel, cols, flat_base;
 };
@@ -71,19 +182,15 @@ struct Fields {
 struct EWalker {
     const EntryLayout* el;
     const uint64_t* es;
-    const ColDiv* cdv;
     uint32_t n_e;
     uint64_t base, end;
     ECtx ctx;
 
-    __device__ EWalker(const EntryLayout* el_, const uint64_t* es_, const ColDiv* cdv_, uint32_t n_e_, uint64_t first,
-                       uint64_t last)
-        : el(el_), es(es_), cdv(cdv_), n_e(n_e_), base(first), end(last) {
-        const uint64_t f = first < end ? first : first;
-        ctx = load_ectx(el, es, cdv, upper_index<uint64_t>(es, 0, n_e, f));
+    __device__ EWalker(const EntryLayout* el_, const uint64_t* es_, uint32_t n_e_, uint64_t first, uint64_t last)
+        : el(el_), es(es_), n_e(n_e_), base(first), end(last) {
+        ctx = load_ectx(el, es, upper_index<uint64_t>(es, 0, n_e, first));
     }
 
-    // Reads this lane's fields for `repr`; entries past a boundary walk per lane.
     __device__ __forceinline__ Fields next(const uint8_t* __restrict__ body, bool coo) {
         const int lane = threadIdx.x & 31;
         Fields f;
@@ -123,14 +230,13 @@ struct EWalker {
         }
         if (crosses) {
             const uint32_t last_e = __shfl_sync(0xffffffffu, e, 31);
-            if (last_e != ctx.e) ctx = load_ectx(el, es, cdv, last_e);
+            if (last_e != ctx.e) ctx = load_ectx(el, es, last_e);
         }
         base += 32;
         return f;
     }
 };
 
-// Segmented warp aggregate of (head, value) items in lane order.
 __device__ __forceinline__ uint64_t seg_round_agg(bool head, uint64_t v) {
     const uint32_t hm = __ballot_sync(0xffffffffu, head);
     const int lane = threadIdx.x & 31;
@@ -141,8 +247,6 @@ __device__ __forceinline__ uint64_t seg_round_agg(bool head, uint64_t v) {
     return x | (hm ? H : 0);
 }
 
-// Inclusive segmented scan within the round, continuing `carry` (a plain
-// running value).  Returns this lane's value; updates carry to lane 31's.
 __device__ __forceinline__ uint64_t seg_round_scan(bool head, uint64_t v, uint64_t& carry) {
     const int lane = threadIdx.x & 31;
     uint64_t inc = v;
@@ -161,27 +265,31 @@ __device__ __forceinline__ uint64_t seg_round_scan(bool head, uint64_t v, uint64
 
 __device__ __forceinline__ bool fast_blocked(const uint32_t* flags) { return *(volatile const uint32_t*)flags != 0; }
 
-}  // namespace
+struct ApplyArgs {
+    const EntryLayout* el;
+    const uint64_t* es;
+    uint32_t n_e;
+    const uint8_t* body;
+    const pulse_flat_carry* carry;
+    const uint64_t* totals;
+    ulonglong2* agg;  // F1 out / F2 in-out / F3-F4 in
+    uint32_t* flags;
+    uint64_t* err;
+    uint16_t* const* weights;
+    int64_t* out_idx;
+};
 
-// =============================================================================================
-// F1
-// =============================================================================================
-__global__ void __launch_bounds__(kThreads)
-f_range_agg(const EntryLayout* __restrict__ el, const uint64_t* __restrict__ es, const ColDiv* __restrict__ cdv,
-            uint32_t n_e, const uint8_t* __restrict__ body, uint32_t repr, const uint64_t* __restrict__ totals,
-            ulonglong2* __restrict__ agg, uint32_t* __restrict__ flags) {
-    if (fast_blocked(flags)) return;
-    const uint64_t n = totals[0];
-    const uint64_t n_ranges = (n + kRange - 1) / kRange;
-    const bool coo = repr == PULSE_COO_DOWNSCALED;
-    const uint64_t stride = uint64_t(gridDim.x) * kWarps;
-    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5); rg < n_ranges; rg += stride) {
-        const uint64_t first = rg * kRange;
-        EWalker w(el, es, cdv, n_e, first, min(first + kRange, n));
-        uint64_t ar = 0, ac = 0;  // SegSum aggregates (earlier ⊕ later)
-        bool marker = false;
-        while (w.base < w.end) {
-            const Fields f = w.next(body, coo);
+// Walker path over entries [first, last) for one pass.  (ar, ac): aggregates
+// (kAgg) or running values (validate / scatter); updated in place.
+template <int kRepr, int kPass>
+__device__ __noinline__ void slow_span(const ApplyArgs& A, uint64_t first, uint64_t last, uint64_t& ar, uint64_t& ac,
+                                       bool& marker, bool has_prev, uint64_t gap_base) {
+    constexpr bool coo = kRepr == kCoo;
+    EWalker w(A.el, A.es, A.n_e, first, last);
+    while (w.base < w.end) {
+        const uint64_t i = w.base + (threadIdx.x & 31);
+        const Fields f = w.next(A.body, coo);
+        if (kPass == kAgg) {
             if (coo) {
                 marker |= f.valid && (f.a == 0xFF || f.b == 0xFFFF);
                 const bool hr = f.valid && f.o == 0;
@@ -189,12 +297,238 @@ f_range_agg(const EntryLayout* __restrict__ el, const uint64_t* __restrict__ es,
                 ar = SegSumOp::op(ar, seg_round_agg(hr, f.a));
                 ac = SegSumOp::op(ac, seg_round_agg(hc, f.b));
             } else {
-                const bool hr = repr == PULSE_COO_INT32 && f.valid && f.o == 0;
+                const bool hr = kRepr == kI32 && f.valid && f.o == 0;
                 ar = SegSumOp::op(ar, seg_round_agg(hr, f.a));
             }
+            continue;
         }
-        if (__any_sync(0xffffffffu, marker) && (threadIdx.x & 31) == 0) atomicExch(flags, 1u);
-        if ((threadIdx.x & 31) == 0) agg[rg] = make_ulonglong2(ar, ac);
+        constexpr bool kScat = kPass == kScatter;
+        if (coo) {
+            const bool hr = f.valid && f.o == 0;
+            const bool nr = f.valid && (f.o == 0 || f.a != 0);
+            const uint64_t row = seg_round_scan(hr, f.a, ar);
+            const uint64_t col = seg_round_scan(nr, f.b, ac);
+            if (!f.valid) continue;
+            if (!kScat) {
+                if (!nr && f.b == 0) { report(A.err, error_key(f.e, kStageCols, f.o, kZeroColGap)); continue; }
+                if (col >= f.cols) { report(A.err, error_key(f.e, kStageRange, f.o, kColRange)); continue; }
+            }
+            const uint64_t flat = row * f.cols + col;
+            if (!kScat) {
+                if (flat >= f.numel) report(A.err, error_key(f.e, kStageRange, f.o, kIdxRange));
+            } else if (A.out_idx) {
+                A.out_idx[i] = int64_t(flat);
+            } else {
+                A.weights[f.tensor][flat] = uint16_t(rd_u16(A.body + f.val_off + 2 * f.o));
+            }
+        } else if (kRepr == kI32) {
+            const bool hr = f.valid && f.o == 0;
+            const uint64_t idx = seg_round_scan(hr, f.a, ar);
+            if (!f.valid) continue;
+            if (!kScat) {
+                if (f.o > 0 && f.a == 0) { report(A.err, error_key(f.e, kStageRows, f.o, kZeroGap)); continue; }
+                if (idx >= f.numel) report(A.err, error_key(f.e, kStageRows, f.o, kIdxRange));
+            } else if (A.out_idx) {
+                A.out_idx[i] = int64_t(idx);
+            } else {
+                A.weights[f.tensor][idx] = uint16_t(rd_u16(A.body + f.val_off + 2 * f.o));
+            }
+        } else {  // FLAT_INT32: one running global sum (patch.hpp:219-237)
+            const uint64_t S = seg_round_scan(false, f.a, ar);
+            if (!f.valid) continue;
+            const int64_t local = int64_t(S) - int64_t(gap_base) - int64_t(f.flat_base);
+            if (!kScat) {
+                if (f.a == 0 && (i > 0 || has_prev)) { report(A.err, error_key(f.e, kStageRows, f.o, kZeroGap)); continue; }
+                if (local < 0 || uint64_t(local) >= f.numel) report(A.err, error_key(f.e, kStageRows, f.o, kIdxRange));
+            } else if (A.out_idx) {
+                A.out_idx[i] = local;
+            } else {
+                A.weights[f.tensor][local] = uint16_t(rd_u16(A.body + f.val_off + 2 * f.o));
+            }
+        }
+    }
+}
+
+}  // namespace
+
+// =============================================================================================
+// F1 / F3 / F4: one kernel body, three passes
+// =============================================================================================
+template <int kRepr, int kPass>
+__global__ void __launch_bounds__(kThreads)
+f_pass(ApplyArgs A) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    if (fast_blocked(A.flags)) return;
+    if (kPass == kScatter && *(volatile const uint64_t*)A.err != kNoError) return;
+    constexpr bool coo = kRepr == kCoo;
+    constexpr int VA = coo ? 2 : 8;  // vectors per lane of the a buffer
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* ws = smem + warp * warp_smem(kPass);
+    uint4* sa = reinterpret_cast<uint4*>(ws);
+    uint4* sb = reinterpret_cast<uint4*>(ws + kABytes);
+    uint16_t* sv = reinterpret_cast<uint16_t*>(ws + kABytes + kBBytes);
+    uint4* sx = reinterpret_cast<uint4*>(ws + kABytes + kBBytes + kVBytes);
+
+    const uint64_t n = A.totals[0];
+    const uint64_t n_ranges = (n + kRange - 1) / kRange;
+    const bool has_prev = A.carry && A.carry->has_prev;
+    const uint64_t gap_base = has_prev ? A.carry->gap_base : 0;
+    const uint64_t stride = uint64_t(gridDim.x) * kWarps;
+
+    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + warp; rg < n_ranges; rg += stride) {
+        const uint64_t r0 = rg * kRange, r1 = min(r0 + kRange, n);
+        uint64_t ar = 0, ac = 0;  // kAgg: aggregates; else running (row, col) / sums
+        if (kPass != kAgg) {
+            const ulonglong2 p = A.agg[rg];
+            ar = p.x;
+            ac = p.y;
+        }
+        bool marker = false;
+        uint32_t e = upper_index<uint64_t>(A.es, 0, A.n_e, r0);
+        for (uint64_t c0 = r0; c0 < r1; c0 += kChunk) {
+            const uint32_t len = uint32_t(r1 - c0 < kChunk ? r1 - c0 : kChunk);
+            while (A.es[e + 1] <= c0) ++e;
+            const uint64_t lo = A.es[e], hi = A.es[e + 1];
+            const EntryLayout L = A.el[e];
+            if (hi < c0 + len || L.numel >= (1ull << 32)) {
+                slow_span<kRepr, kPass>(A, c0, c0 + len, ar, ac, marker, has_prev, gap_base);
+                continue;
+            }
+            const uint64_t o0 = c0 - lo;
+            // ---- stage ----
+            if (coo) {
+                stage<2>(sa, A.body + L.idx_off + o0, len);
+                stage<4>(sb, A.body + L.idx_off + L.count + 2 * o0, 2 * len);
+            } else {
+                stage<8>(sa, A.body + L.idx_off + 4 * o0, 4 * len);
+            }
+            if (kPass == kScatter && !A.out_idx) stage<1>(reinterpret_cast<uint4*>(sv), A.body + L.val_off + 2 * o0, 2 * len);
+            __syncwarp();
+            // ---- this lane's kPer consecutive entries, straight from shared memory ----
+            const int nv = max(0, min(int(kPer), int(len) - lane * int(kPer)));
+            // packed fields: COO rows 4 per word, columns 2 per word; int32 one per word
+            constexpr int kAW = coo ? 8 : 32, kBW = coo ? 16 : 1;
+            uint32_t aw[kAW], bw[kBW];
+            if (coo) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const uint4 q = lane_vec<2>(sa, i);
+                    aw[4 * i] = q.x; aw[4 * i + 1] = q.y; aw[4 * i + 2] = q.z; aw[4 * i + 3] = q.w;
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint4 q = lane_vec<4>(sb, i);
+                    bw[4 * i] = q.x; bw[4 * i + 1] = q.y; bw[4 * i + 2] = q.z; bw[4 * i + 3] = q.w;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint4 q = lane_vec<8>(sa, i);
+                    aw[4 * i] = q.x; aw[4 * i + 1] = q.y; aw[4 * i + 2] = q.z; aw[4 * i + 3] = q.w;
+                }
+                bw[0] = 0;
+            }
+#define PULSE_AV(j) (coo ? (aw[(j) >> 2] >> (8 * ((j) & 3))) & 0xFFu : aw[(j) % kAW])
+#define PULSE_BV(j) (coo ? (bw[((j) >> 1) % kBW] >> (16 * ((j) & 1))) & 0xFFFFu : 0u)
+            const uint64_t ol = o0 + uint64_t(lane) * kPer;  // ordinal of this lane's first entry
+            // lane aggregates
+            uint64_t lr = 0, lc = 0;
+            bool lmark = false;
+#pragma unroll
+            for (int j = 0; j < int(kPer); ++j) {
+                if (j < nv) {
+                    const uint32_t a = PULSE_AV(j), b = PULSE_BV(j);
+                    const bool hr = kRepr != kFlat && ol + j == 0;
+                    if (coo) {
+                        const bool hc = ol + j == 0 || a != 0;
+                        lmark |= a == 0xFF || b == 0xFFFF;
+                        lc = hc ? (H | b) : lc + b;
+                    }
+                    lr = hr ? (H | a) : lr + a;
+                }
+            }
+            uint64_t ir = lr, ic = lc;
+            warp_segscan2(ir, ic);
+            const uint64_t tr = __shfl_sync(0xffffffffu, ir, 31), tc = __shfl_sync(0xffffffffu, ic, 31);
+            if (kPass == kAgg) {
+                marker |= lmark;
+                ar = SegSumOp::op(ar, tr);
+                ac = SegSumOp::op(ac, tc);
+                continue;
+            }
+            uint64_t er = __shfl_up_sync(0xffffffffu, ir, 1), ec = __shfl_up_sync(0xffffffffu, ic, 1);
+            if (lane == 0) er = ec = 0;
+            uint64_t row = SegSumOp::op(ar, er) & (H - 1), col = SegSumOp::op(ac, ec) & (H - 1);
+            ar = SegSumOp::op(ar, tr) & (H - 1);
+            ac = SegSumOp::op(ac, tc) & (H - 1);
+#pragma unroll
+            for (int i = 0; i < int(kPer) / 4; ++i) {
+                uint32_t xv[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int j = 4 * i + c;
+                    xv[c] = 0;
+                    if (j >= nv) continue;
+                    const uint32_t a = PULSE_AV(j), b = PULSE_BV(j);
+                    const uint64_t o = ol + j;
+                    if (coo) {
+                        const bool nr = o == 0 || a != 0;
+                        row = o == 0 ? a : row + a;
+                        col = nr ? b : col + b;
+                        if (kPass == kValidate) {
+                            if (!nr && b == 0) { report(A.err, error_key(e, kStageCols, o, kZeroColGap)); continue; }
+                            if (col >= L.cols) { report(A.err, error_key(e, kStageRange, o, kColRange)); continue; }
+                        }
+                        const uint64_t flat = row * L.cols + col;
+                        if (kPass == kValidate) {
+                            if (flat >= L.numel) report(A.err, error_key(e, kStageRange, o, kIdxRange));
+                        }
+                        xv[c] = uint32_t(flat);
+                    } else if (kRepr == kI32) {
+                        row = o == 0 ? a : row + a;
+                        if (kPass == kValidate) {
+                            if (o > 0 && a == 0) { report(A.err, error_key(e, kStageRows, o, kZeroGap)); continue; }
+                            if (row >= L.numel) report(A.err, error_key(e, kStageRows, o, kIdxRange));
+                        }
+                        xv[c] = uint32_t(row);
+                    } else {
+                        row += a;
+                        const int64_t local = int64_t(row) - int64_t(gap_base) - int64_t(L.flat_base);
+                        if (kPass == kValidate) {
+                            const uint64_t gi = c0 + uint64_t(lane) * kPer + j;
+                            if (a == 0 && (gi > 0 || has_prev)) { report(A.err, error_key(e, kStageRows, o, kZeroGap)); continue; }
+                            if (local < 0 || uint64_t(local) >= L.numel) report(A.err, error_key(e, kStageRows, o, kIdxRange));
+                        }
+                        xv[c] = uint32_t(local);
+                    }
+                }
+                if (kPass == kScatter) sx[swz<8>(uint32_t(lane * 8 + i))] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
+            }
+#undef PULSE_AV
+#undef PULSE_BV
+            if (kPass != kScatter) continue;
+            // ---- indices are in shared memory in entry order: coalesced scatter ----
+            __syncwarp();
+            const uint32_t* xs = reinterpret_cast<const uint32_t*>(sx);
+            if (A.out_idx) {
+                for (uint32_t k = lane; k < len; k += 32) {
+                    const uint32_t q = k >> 2;
+                    A.out_idx[c0 + k] = int64_t(xs[swz<8>(q) * 4 + (k & 3)]);
+                }
+            } else {
+                uint16_t* W = A.weights[L.tensor];
+#pragma unroll 4
+                for (uint32_t k = lane; k < len; k += 32) {
+                    const uint32_t q = k >> 2;
+                    W[xs[swz<8>(q) * 4 + (k & 3)]] = sv[k];
+                }
+            }
+            __syncwarp();
+        }
+        if (kPass == kAgg) {
+            if (__any_sync(0xffffffffu, marker) && lane == 0) atomicExch(A.flags, 1u);
+            if (lane == 0) A.agg[rg] = make_ulonglong2(ar, ac);
+        }
     }
 }
 
@@ -202,19 +536,12 @@ f_range_agg(const EntryLayout* __restrict__ el, const uint64_t* __restrict__ es,
 // F2: exclusive SegSum scan of the range aggregates (one CTA of 1024)
 // =============================================================================================
 constexpr int kScanThreads = 1024;
+constexpr int kScanPer = 8;  // items held in registers per thread per block
 
 __device__ __forceinline__ void cta_seg_exclusive(uint64_t& vr, uint64_t& vc, uint64_t* s_r, uint64_t* s_c) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint64_t ir = vr, ic = vc;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint64_t o1 = __shfl_up_sync(0xffffffffu, ir, off);
-        const uint64_t o2 = __shfl_up_sync(0xffffffffu, ic, off);
-        if (lane >= off) {
-            ir = SegSumOp::op(o1, ir);
-            ic = SegSumOp::op(o2, ic);
-        }
-    }
+    warp_segscan2(ir, ic);
     if (lane == 31) {
         s_r[warp] = ir;
         s_c[warp] = ic;
@@ -238,119 +565,87 @@ __device__ __forceinline__ void cta_seg_exclusive(uint64_t& vr, uint64_t& vc, ui
 __global__ void __launch_bounds__(kScanThreads, 1)
 f_range_scan(const uint64_t* __restrict__ totals, ulonglong2* __restrict__ agg, const uint32_t* __restrict__ flags) {
     __shared__ uint64_t s_r[32], s_c[32];
+    __shared__ uint64_t s_carry[2];
     if (fast_blocked(flags)) return;
     const uint64_t n = totals[0];
     const uint64_t n_ranges = (n + kRange - 1) / kRange;
-    const uint64_t per = (n_ranges + kScanThreads - 1) / kScanThreads;
-    const uint64_t q0 = min(n_ranges, per * threadIdx.x), q1 = min(n_ranges, q0 + per);
-    uint64_t sr = 0, sc = 0;
-    for (uint64_t q = q0; q < q1; ++q) {
-        const ulonglong2 v = agg[q];
-        sr = SegSumOp::op(sr, v.x);
-        sc = SegSumOp::op(sc, v.y);
-    }
-    cta_seg_exclusive(sr, sc, s_r, s_c);
-    for (uint64_t q = q0; q < q1; ++q) {  // in place: aggregate -> exclusive prefix
-        const ulonglong2 v = agg[q];
-        agg[q] = make_ulonglong2(sr & (H - 1), sc & (H - 1));
-        sr = SegSumOp::op(sr, v.x);
-        sc = SegSumOp::op(sc, v.y);
-    }
-}
-
-// =============================================================================================
-// F3 / F4: recompute per entry; validate, then scatter
-// =============================================================================================
-template <bool kScatter>
-__global__ void __launch_bounds__(kThreads)
-f_apply(const EntryLayout* __restrict__ el, const uint64_t* __restrict__ es, const ColDiv* __restrict__ cdv,
-        uint32_t n_e, const uint8_t* __restrict__ body, uint32_t repr, const pulse_flat_carry* __restrict__ carry,
-        const uint64_t* __restrict__ totals, const ulonglong2* __restrict__ pre, const uint32_t* __restrict__ flags,
-        uint64_t* __restrict__ err, uint16_t* const* __restrict__ weights, int64_t* __restrict__ out_idx) {
-    if (fast_blocked(flags)) return;
-    if (kScatter && *(volatile const uint64_t*)err != kNoError) return;
-    const uint64_t n = totals[0];
-    const uint64_t n_ranges = (n + kRange - 1) / kRange;
-    const bool coo = repr == PULSE_COO_DOWNSCALED;
-    const bool has_prev = carry && carry->has_prev;
-    const uint64_t gap_base = has_prev ? carry->gap_base : 0;
-    const uint64_t stride = uint64_t(gridDim.x) * kWarps;
-    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5); rg < n_ranges; rg += stride) {
-        const uint64_t first = rg * kRange;
-        EWalker w(el, es, cdv, n_e, first, min(first + kRange, n));
-        const ulonglong2 p = pre[rg];
-        uint64_t cr = p.x, cc = p.y;  // running (row, col) or running index / global sum
-        while (w.base < w.end) {
-            const uint64_t i = w.base + (threadIdx.x & 31);
-            const Fields f = w.next(body, coo);
-            if (coo) {
-                const bool hr = f.valid && f.o == 0;
-                const bool nr = f.valid && (f.o == 0 || f.a != 0);
-                const uint64_t row = seg_round_scan(hr, f.a, cr);
-                const uint64_t col = seg_round_scan(nr, f.b, cc);
-                if (!f.valid) continue;
-                if (!kScatter) {
-                    if (!nr && f.b == 0) { report(err, error_key(f.e, kStageCols, f.o, kZeroColGap)); continue; }
-                    if (col >= f.cols) { report(err, error_key(f.e, kStageRange, f.o, kColRange)); continue; }
-                }
-                uint64_t flat;
-                if (f.cols < (1ull << 32) && row < (1ull << 32)) {
-                    flat = uint64_t(uint32_t(row)) * uint32_t(f.cols) + col;
-                } else {
-                    flat = row * f.cols + col;
-                }
-                if (!kScatter) {
-                    if (flat >= f.numel) report(err, error_key(f.e, kStageRange, f.o, kIdxRange));
-                } else if (out_idx) {
-                    out_idx[i] = int64_t(flat);
-                } else {
-                    weights[f.tensor][flat] = uint16_t(rd_u16(body + f.val_off + 2 * f.o));
-                }
-            } else if (repr == PULSE_COO_INT32) {
-                const bool hr = f.valid && f.o == 0;
-                const uint64_t idx = seg_round_scan(hr, f.a, cr);
-                if (!f.valid) continue;
-                if (!kScatter) {
-                    if (f.o > 0 && f.a == 0) { report(err, error_key(f.e, kStageRows, f.o, kZeroGap)); continue; }
-                    if (idx >= f.numel) report(err, error_key(f.e, kStageRows, f.o, kIdxRange));
-                } else if (out_idx) {
-                    out_idx[i] = int64_t(idx);
-                } else {
-                    weights[f.tensor][idx] = uint16_t(rd_u16(body + f.val_off + 2 * f.o));
-                }
-            } else {  // FLAT_INT32: one running global sum (patch.hpp:219-237)
-                const uint64_t S = seg_round_scan(false, f.a, cr);
-                if (!f.valid) continue;
-                const int64_t local = int64_t(S) - int64_t(gap_base) - int64_t(f.flat_base);
-                if (!kScatter) {
-                    if (f.a == 0 && (i > 0 || has_prev)) { report(err, error_key(f.e, kStageRows, f.o, kZeroGap)); continue; }
-                    if (local < 0 || uint64_t(local) >= f.numel) report(err, error_key(f.e, kStageRows, f.o, kIdxRange));
-                } else if (out_idx) {
-                    out_idx[i] = local;
-                } else {
-                    weights[f.tensor][local] = uint16_t(rd_u16(body + f.val_off + 2 * f.o));
-                }
-            }
+    if (threadIdx.x == 0) s_carry[0] = s_carry[1] = 0;
+    __syncthreads();
+    constexpr uint64_t kBlock = uint64_t(kScanThreads) * kScanPer;
+    for (uint64_t b0 = 0; b0 < n_ranges; b0 += kBlock) {
+        const uint64_t q0 = b0 + uint64_t(threadIdx.x) * kScanPer;
+        ulonglong2 v[kScanPer];
+#pragma unroll
+        for (int j = 0; j < kScanPer; ++j) v[j] = q0 + j < n_ranges ? agg[q0 + j] : make_ulonglong2(0, 0);
+        uint64_t sr = 0, sc = 0;
+#pragma unroll
+        for (int j = 0; j < kScanPer; ++j) {
+            sr = SegSumOp::op(sr, v[j].x);
+            sc = SegSumOp::op(sc, v[j].y);
         }
+        cta_seg_exclusive(sr, sc, s_r, s_c);
+        const uint64_t cr = s_carry[0], cc = s_carry[1];
+        sr = SegSumOp::op(cr, sr);
+        sc = SegSumOp::op(cc, sc);
+#pragma unroll
+        for (int j = 0; j < kScanPer; ++j) {  // in place: aggregate -> exclusive prefix
+            if (q0 + j < n_ranges) agg[q0 + j] = make_ulonglong2(sr & (H - 1), sc & (H - 1));
+            sr = SegSumOp::op(sr, v[j].x);
+            sc = SegSumOp::op(sc, v[j].y);
+        }
+        __syncthreads();
+        if (threadIdx.x == kScanThreads - 1) {
+            s_carry[0] = sr & (H - 1);
+            s_carry[1] = sc & (H - 1);
+        }
+        __syncthreads();
     }
 }
 
 // =============================================================================================
 // launcher (called from launch_decode after d_layout)
 // =============================================================================================
+namespace {
+template <int kRepr, int kPass>
+void launch_pass(const ApplyArgs& a, cudaStream_t s) {
+    const uint32_t smem = kWarps * warp_smem(kPass);
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        cudaFuncSetAttribute(f_pass<kRepr, kPass>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        configured = true;
+    }
+    const int per_sm = kPass == kScatter ? 2 : 4;
+    f_pass<kRepr, kPass><<<unsigned(sm_count() * per_sm), kThreads, smem, s>>>(a);
+}
+
+template <int kRepr>
+void launch_all(const ApplyArgs& a, bool scatter, cudaStream_t s) {
+    launch_pass<kRepr, kAgg>(a, s);
+    f_range_scan<<<1, kScanThreads, 0, s>>>(a.totals, a.agg, a.flags);
+    launch_pass<kRepr, kValidate>(a, s);
+    if (scatter) launch_pass<kRepr, kScatter>(a, s);
+}
+}  // namespace
+
 void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uint32_t n_entries,
                        const pulse_flat_carry* carry, int weights_slot, int64_t* out_indices, uint32_t* flags,
                        cudaStream_t s) {
-    const unsigned grid = unsigned(sm_count() * 4);
-    ulonglong2* agg = reinterpret_cast<ulonglong2*>(p.flat);  // flat scratch is free on this path
-    f_range_agg<<<grid, kThreads, 0, s>>>(p.elay, p.d_es, p.coldiv, n_entries, body, repr, p.d_totals, agg, flags);
-    f_range_scan<<<1, kScanThreads, 0, s>>>(p.d_totals, agg, flags);
-    f_apply<false><<<grid, kThreads, 0, s>>>(p.elay, p.d_es, p.coldiv, n_entries, body, repr, carry, p.d_totals, agg,
-                                             flags, p.err, nullptr, nullptr);
-    if (weights_slot >= 0 || out_indices)
-        f_apply<true><<<grid, kThreads, 0, s>>>(p.elay, p.d_es, p.coldiv, n_entries, body, repr, carry, p.d_totals,
-                                                agg, flags, p.err, weights_slot >= 0 ? p.slot[weights_slot] : nullptr,
-                                                out_indices);
+    ApplyArgs a;
+    a.el = p.elay;
+    a.es = p.d_es;
+    a.n_e = n_entries;
+    a.body = body;
+    a.carry = carry;
+    a.totals = p.d_totals;
+    a.agg = reinterpret_cast<ulonglong2*>(p.flat);  // flat scratch is free on this path
+    a.flags = flags;
+    a.err = p.err;
+    a.weights = weights_slot >= 0 ? p.slot[weights_slot] : nullptr;
+    a.out_idx = out_indices;
+    const bool scatter = weights_slot >= 0 || out_indices;
+    if (repr == PULSE_COO_DOWNSCALED) launch_all<kCoo>(a, scatter, s);
+    else if (repr == PULSE_COO_INT32) launch_all<kI32>(a, scatter, s);
+    else launch_all<kFlat>(a, scatter, s);
 }
 
 PULSE_DEFINE_WATCHDOG_SETTER(set_watchdog_apply)
