@@ -35,6 +35,7 @@
 // general parser in decode.cu instead; every kernel checks it on entry.
 #include "device.cuh"
 #include "internal.hpp"
+#include "stage.cuh"
 
 namespace pulse {
 namespace dev {
@@ -58,85 +59,6 @@ __device__ __forceinline__ uint32_t lanemask_le() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
     return m;
-}
-
-// XOR swizzle of 16-byte vector slots for buffers read as V consecutive vectors
-// per lane: within every group of 8 lanes the slots hit 8 distinct bank quads,
-// and 8 consecutive slots (a staging store) stay a permutation of one 128 B row.
-template <int V>
-__device__ __forceinline__ uint32_t swz(uint32_t q) {
-    return V == 1 ? q : (q ^ ((q >> 3) & (V - 1)));
-}
-
-__device__ __forceinline__ uint32_t shr_pair(uint32_t lo, uint32_t hi, uint32_t sh) {
-    return __funnelshift_r(lo, hi, sh);
-}
-
-// Copies bytes [g, g+len) (len <= 512 * R) into shared vectors dst[swz(q)],
-// packed from byte 0.  All loads are issued before any store.  Reads at most
-// the 16-byte-aligned blocks that contain payload bytes (never past a page).
-template <int R, int V>
-__device__ __forceinline__ void stage_piece(uint4* dst, const uint8_t* g, uint32_t len, uint32_t q_base) {
-    const int lane = threadIdx.x & 31;
-    const uintptr_t ga = reinterpret_cast<uintptr_t>(g);
-    const uint32_t s = uint32_t(ga & 15);
-    const uint4* src = reinterpret_cast<const uint4*>(ga - s);
-    const uint32_t nv_in = (s + len + 15) >> 4;
-    const uint32_t nv_out = (len + 15) >> 4;
-    uint4 v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const uint32_t q = lane + 32 * r;
-        v[r] = q < nv_in ? ld_stream(src + q) : make_uint4(0, 0, 0, 0);
-    }
-    if (s == 0) {  // aligned: straight copy
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const uint32_t q = lane + 32 * r;
-            if (q < nv_out) dst[swz<V>(q_base + q)] = v[r];
-        }
-        return;
-    }
-    uint4 extra = make_uint4(0, 0, 0, 0);
-    if (lane == 0 && 32u * R < nv_in) extra = ld_stream(src + 32 * R);
-    const uint32_t sw = s >> 2, sh = (s & 3) * 8;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        uint4 nx;
-        nx.x = __shfl_down_sync(0xffffffffu, v[r].x, 1);
-        nx.y = __shfl_down_sync(0xffffffffu, v[r].y, 1);
-        nx.z = __shfl_down_sync(0xffffffffu, v[r].z, 1);
-        nx.w = __shfl_down_sync(0xffffffffu, v[r].w, 1);
-        const uint4 n0 = r + 1 < R ? v[r + 1 < R ? r + 1 : r] : extra;
-        const uint32_t w0 = __shfl_sync(0xffffffffu, n0.x, 0), w1 = __shfl_sync(0xffffffffu, n0.y, 0);
-        const uint32_t w2 = __shfl_sync(0xffffffffu, n0.z, 0), w3 = __shfl_sync(0xffffffffu, n0.w, 0);
-        if (lane == 31) nx = make_uint4(w0, w1, w2, w3);
-        const uint32_t W[8] = {v[r].x, v[r].y, v[r].z, v[r].w, nx.x, nx.y, nx.z, nx.w};
-        uint4 o;
-        switch (sw) {
-            case 0: o = make_uint4(shr_pair(W[0], W[1], sh), shr_pair(W[1], W[2], sh), shr_pair(W[2], W[3], sh), shr_pair(W[3], W[4], sh)); break;
-            case 1: o = make_uint4(shr_pair(W[1], W[2], sh), shr_pair(W[2], W[3], sh), shr_pair(W[3], W[4], sh), shr_pair(W[4], W[5], sh)); break;
-            case 2: o = make_uint4(shr_pair(W[2], W[3], sh), shr_pair(W[3], W[4], sh), shr_pair(W[4], W[5], sh), shr_pair(W[5], W[6], sh)); break;
-            default: o = make_uint4(shr_pair(W[3], W[4], sh), shr_pair(W[4], W[5], sh), shr_pair(W[5], W[6], sh), shr_pair(W[6], W[7], sh)); break;
-        }
-        const uint32_t q = lane + 32 * r;
-        if (q < nv_out) dst[swz<V>(q_base + q)] = o;
-    }
-}
-
-// Stages up to `len` bytes (len <= cap) in pieces of 2 KiB (16 B aligned pieces
-// keep the source alignment, so the swizzled slot index just continues).
-template <int V>
-__device__ __forceinline__ void stage(uint4* dst, const uint8_t* g, uint32_t len) {
-    for (uint32_t off = 0; off < len; off += 2048)
-        stage_piece<4, V>(dst, g + off, min(2048u, len - off), off >> 4);
-}
-
-// Reads lane-consecutive vector i (of V) of a swizzled buffer.
-template <int V>
-__device__ __forceinline__ uint4 lane_vec(const uint4* buf, int i) {
-    const int lane = threadIdx.x & 31;
-    return buf[swz<V>(uint32_t(lane * V + i))];
 }
 
 // Inclusive SegSum scan over lanes of a (rows, cols) pair.
@@ -609,12 +531,12 @@ namespace {
 template <int kRepr, int kPass>
 void launch_pass(const ApplyArgs& a, cudaStream_t s) {
     const uint32_t smem = kWarps * warp_smem(kPass);
-    static bool configured = false;  // per instantiation
-    if (!configured) {
+    static int per_sm = 0;  // per instantiation: resident CTAs per SM (persistent grid)
+    if (!per_sm) {
         cudaFuncSetAttribute(f_pass<kRepr, kPass>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        configured = true;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f_pass<kRepr, kPass>, kThreads, smem);
+        per_sm = per_sm > 0 ? per_sm : 1;
     }
-    const int per_sm = kPass == kScatter ? 2 : 4;
     f_pass<kRepr, kPass><<<unsigned(sm_count() * per_sm), kThreads, smem, s>>>(a);
 }
 

@@ -21,6 +21,7 @@
 
 #include "device.cuh"
 #include "internal.hpp"
+#include "stage.cuh"
 
 namespace pulse {
 namespace dev {
@@ -226,94 +227,222 @@ struct CooWalker {
 };
 
 // =============================================================================================
+// Staged fast path shared by K2a / K2b.  A warp takes 1024-entry chunks that lie
+// inside one segment of a tensor with < 2^32 elements (compacted K1 input):
+// the chunk's u32 indices are staged into shared memory with coalesced 16-byte
+// loads and each lane derives 32 CONSECUTIVE entries serially -- the
+// predecessor of its first entry is the previous lane's last one (shared
+// memory; the global entry before the chunk for lane 0).  Everything else
+// (segment boundaries, caller int64 indices, and in K2b chunks with escapes)
+// takes the per-round walker path.
+// =============================================================================================
+constexpr uint32_t kChunkE = 1024;                 // entries per staged chunk
+constexpr uint32_t kLaneE = kChunkE / 32;          // consecutive entries per lane
+constexpr uint32_t kSIdx = kChunkE * 4, kSRow = kChunkE, kSCol = kChunkE * 2, kSVal = kChunkE * 2;
+constexpr uint32_t kScanWarpSmem = kSIdx;
+constexpr uint32_t kEmitWarpSmem = kSIdx + kSRow + kSCol + kSVal;
+
+struct FastCtx {
+    bool fast;
+    uint32_t t;
+    uint64_t ts;        // first entry of the tensor
+    uint32_t elem_off;  // segment offset inside the tensor (< 2^32 on the fast path)
+    uint32_t cols32, magic, shift;
+};
+
+// Segment of chunk [c0, c0+len) (sg walks forward monotonically) and whether
+// the staged path applies.
+__device__ __forceinline__ FastCtx fast_ctx(const EntryMap& em, uint64_t c0, uint32_t len, uint32_t& sg) {
+    FastCtx c;
+    while (em.seg_start[sg + 1] <= c0) ++sg;
+    const SegDesc d = em.segs[sg];
+    const ColDiv cd = em.coldiv[d.tensor];
+    c.t = d.tensor;
+    c.ts = em.seg_start[em.seg_first[d.tensor]];
+    c.elem_off = uint32_t(d.elem_off);
+    c.cols32 = cd.cols32;
+    c.magic = cd.magic;
+    c.shift = cd.shift;
+    c.fast = !em.idx64 && em.seg_start[sg + 1] >= c0 + len && !cd.wide && em.numel[d.tensor] < (1ull << 32);
+    return c;
+}
+
+// Local index of the predecessor of this lane's first entry (meaningful when
+// that entry is not the tensor's first): the previous lane's last staged index,
+// or for lane 0 the global entry before the chunk (same tensor, maybe the
+// previous segment).
+__device__ __forceinline__ uint32_t lane_pred(const EntryMap& em, const uint4* sidx, uint64_t c0, const FastCtx& c) {
+    const int lane = threadIdx.x & 31;
+    if (lane > 0) return c.elem_off + smem_word<8>(sidx, uint32_t(lane) * kLaneE - 1);
+    if (c0 > c.ts) {
+        const uint32_t sp = upper_index<uint64_t>(em.seg_start, 0, em.n_segs, c0 - 1);
+        return uint32_t(em.segs[sp].elem_off + em.idx32[c0 - 1]);
+    }
+    return 0;
+}
+
+// Local index of staged entry 4*i + k of this lane (compile-time i, k).
+#define PULSE_LANE_L(q, k) (c.elem_off + ((k) == 0 ? (q).x : (k) == 1 ? (q).y : (k) == 2 ? (q).z : (q).w))
+
+__device__ __forceinline__ void st_u16_any(uint8_t* p, uint32_t v) {
+    if ((reinterpret_cast<uintptr_t>(p) & 1) == 0) *reinterpret_cast<uint16_t*>(p) = uint16_t(v);
+    else wr_u16(p, v);
+}
+__device__ __forceinline__ void st_u32_any(uint8_t* p, uint32_t v) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    if ((a & 3) == 0) {
+        *reinterpret_cast<uint32_t*>(p) = v;
+    } else if ((a & 1) == 0) {
+        reinterpret_cast<uint16_t*>(p)[0] = uint16_t(v);
+        reinterpret_cast<uint16_t*>(p)[1] = uint16_t(v >> 16);
+    } else {
+        wr_u32(p, v);
+    }
+}
+
+// Per-round walker path of K2a over entries [first, last).
+__device__ __noinline__ void k2a_span(const EntryMap& em, uint32_t repr, uint64_t n, uint64_t first, uint64_t last,
+                                      uint32_t* __restrict__ t_resc, uint32_t* __restrict__ t_cesc,
+                                      uint64_t* __restrict__ err, uint32_t& re, uint32_t& ce) {
+    const bool coo = repr == PULSE_COO_DOWNSCALED;
+    const int lane = threadIdx.x & 31;
+    Walker w(em, n, first, last);
+    CooWalker cw;
+    bool seeded = false;
+    while (!w.done()) {
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) {
+        if (seeded && w.fast_round()) {
+            if (coo) {
+                uint32_t j, L, Lp;
+                bool valid;
+                w.fast_step(rr, j, L, Lp, valid);
+                const uint32_t row = div_magic(L, w.ctx.magic, w.ctx.shift);
+                const uint32_t col = L - row * w.ctx.cols32;
+                uint32_t prow = __shfl_up_sync(0xffffffffu, row, 1), pcol = __shfl_up_sync(0xffffffffu, col, 1);
+                if (lane == 0) {
+                    prow = uint32_t(cw.carry_row);
+                    pcol = uint32_t(cw.carry_col);
+                }
+                cw.carry_row = __shfl_sync(0xffffffffu, row, 31);
+                cw.carry_col = __shfl_sync(0xffffffffu, col, 31);
+                const bool nr = j == 0 || row != prow;
+                const uint32_t rgap = j == 0 ? row : row - prow;
+                const uint32_t cval = nr ? col : col - pcol;
+                const bool rf = valid && rgap >= 0xFF, cf = valid && cval >= 0xFFFF;
+                if (rf) atomicAdd(t_resc + w.ctx.t, 1u);
+                if (cf) atomicAdd(t_cesc + w.ctx.t, 1u);
+                re += __popc(__ballot_sync(0xffffffffu, rf));
+                ce += __popc(__ballot_sync(0xffffffffu, cf));
+            } else {
+                uint32_t j, L, Lp;
+                bool valid;
+                w.fast_step(rr, j, L, Lp, valid);
+            }
+            continue;
+        }
+        const Ent r = w.next(rr);
+        const ColDiv cd = em.coldiv[r.t];
+        if (!seeded) {  // predecessor (row, col) of the span's first entry
+            seeded = true;
+            const int64_t Lp0 = __shfl_sync(0xffffffffu, r.Lp, 0);
+            const uint32_t t0 = __shfl_sync(0xffffffffu, r.t, 0);
+            if (coo && Lp0 >= 0) coo_split(Lp0, em.coldiv[t0], cw.carry_row, cw.carry_col);
+        }
+        bool rf = false, cf = false;
+        if (em.idx64 && r.valid) {  // argument checks, in the reference's order
+            if (repr == PULSE_COO_INT32) {  // delta_encode_indices, index_coding.hpp:18-25
+                if (r.L < 0) report(err, error_key(r.t, kStageRows, r.j, kArgNegative));
+                else if (r.j > 0 && r.L <= r.Lp) report(err, error_key(r.t, kStageRows, r.j, kArgOrder));
+            } else if (repr == PULSE_FLAT_INT32) {  // patch.hpp:139-147 (first entry: k2_layout)
+                if (r.j > 0 && r.L <= r.Lp) report(err, error_key(r.t, kStageRows, r.j, kArgOrder));
+                else if (r.j > 0 && r.L - r.Lp > 0xFFFFFFFFll)
+                    report(err, error_key(r.t, kStageRows, r.j, kDimFlatGap));
+            }
+        }
+        if (coo) {
+            const Coo f = cw.fields(r, cd);
+            if (r.valid) {
+                if (em.idx64) {  // downscale_coo, index_coding.hpp:117-121
+                    int64_t row, col;
+                    coo_split(r.L, cd, row, col);
+                    if (row < 0 || col < 0) report(err, error_key(r.t, kStageRows, r.j, kArgNegative));
+                    else if (r.j > 0 && r.L <= r.Lp) report(err, error_key(r.t, kStageRows, r.j, kArgOrder));
+                }
+                if (f.rg > 0xFFFFFFFFll) report(err, error_key(r.t, kStageRows, r.j, kDimRow));
+                if (f.cv > 0xFFFFFFFFll) report(err, error_key(r.t, kStageCols, r.j, kDimCol));
+                rf = f.rg >= 0xFF;
+                cf = f.cv >= 0xFFFF;
+                if (rf) atomicAdd(t_resc + r.t, 1u);
+                if (cf) atomicAdd(t_cesc + r.t, 1u);
+            }
+        }
+        re += __popc(__ballot_sync(0xffffffffu, rf));
+        ce += __popc(__ballot_sync(0xffffffffu, cf));
+      }
+      w.rotate();
+    }
+}
+
+// =============================================================================================
 // K2a
 // =============================================================================================
 __global__ void __launch_bounds__(kThreads)
 k2_scan_escapes(EntryMap em, uint32_t repr, uint64_t* __restrict__ range_cnt, uint32_t* __restrict__ t_resc,
                 uint32_t* __restrict__ t_cesc, uint64_t* __restrict__ err) {
+    extern __shared__ __align__(16) uint8_t smem[];
     const uint64_t n = em.seg_start[em.n_segs];
     const uint64_t n_ranges = (n + kRangeEntries - 1) / kRangeEntries;
     const bool coo = repr == PULSE_COO_DOWNSCALED;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint4* sidx = reinterpret_cast<uint4*>(smem + warp * kScanWarpSmem);
     const uint64_t stride = uint64_t(gridDim.x) * kWarps;
-    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5); rg < n_ranges; rg += stride) {
-        const uint64_t first = rg * kRangeEntries;
-        Walker w(em, n, first, first + kRangeEntries);
-        CooWalker cw;
+    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + warp; rg < n_ranges; rg += stride) {
+        const uint64_t r0 = rg * kRangeEntries, r1 = min(r0 + kRangeEntries, n);
         uint32_t re = 0, ce = 0;
-        bool seeded = false;
-        while (!w.done()) {
-#pragma unroll
-          for (int rr = 0; rr < 8; ++rr) {
-            if (seeded && w.fast_round()) {
-                if (coo) {
-                    uint32_t j, L, Lp;
-                    bool valid;
-                    w.fast_step(rr, j, L, Lp, valid);
-                    const uint32_t row = div_magic(L, w.ctx.magic, w.ctx.shift);
-                    const uint32_t col = L - row * w.ctx.cols32;
-                    uint32_t prow = __shfl_up_sync(0xffffffffu, row, 1), pcol = __shfl_up_sync(0xffffffffu, col, 1);
-                    if (lane == 0) {
-                        prow = uint32_t(cw.carry_row);
-                        pcol = uint32_t(cw.carry_col);
-                    }
-                    cw.carry_row = __shfl_sync(0xffffffffu, row, 31);
-                    cw.carry_col = __shfl_sync(0xffffffffu, col, 31);
-                    const bool nr = j == 0 || row != prow;
-                    const uint32_t rgap = j == 0 ? row : row - prow;
-                    const uint32_t cval = nr ? col : col - pcol;
-                    const bool rf = valid && rgap >= 0xFF, cf = valid && cval >= 0xFFFF;
-                    if (rf) atomicAdd(t_resc + w.ctx.t, 1u);
-                    if (cf) atomicAdd(t_cesc + w.ctx.t, 1u);
-                    re += __popc(__ballot_sync(0xffffffffu, rf));
-                    ce += __popc(__ballot_sync(0xffffffffu, cf));
-                } else {
-                    uint32_t j, L, Lp;
-                    bool valid;
-                    w.fast_step(rr, j, L, Lp, valid);
-                }
+        uint32_t sg = em.n_segs ? upper_index<uint64_t>(em.seg_start, 0, em.n_segs, r0) : 0;
+        for (uint64_t c0 = r0; c0 < r1; c0 += kChunkE) {
+            const uint32_t len = uint32_t(r1 - c0 < kChunkE ? r1 - c0 : kChunkE);
+            const FastCtx c = fast_ctx(em, c0, len, sg);
+            if (!coo || !c.fast) {
+                k2a_span(em, repr, n, c0, c0 + len, t_resc, t_cesc, err, re, ce);
                 continue;
             }
-            const Ent r = w.next(rr);
-            const ColDiv cd = em.coldiv[r.t];
-            if (!seeded) {  // predecessor (row, col) of the range's first entry
-                seeded = true;
-                const int64_t Lp0 = __shfl_sync(0xffffffffu, r.Lp, 0);
-                const uint32_t t0 = __shfl_sync(0xffffffffu, r.t, 0);
-                if (coo && Lp0 >= 0) coo_split(Lp0, em.coldiv[t0], cw.carry_row, cw.carry_col);
-            }
-            bool rf = false, cf = false;
-            if (em.idx64 && r.valid) {  // argument checks, in the reference's order
-                if (repr == PULSE_COO_INT32) {  // delta_encode_indices, index_coding.hpp:18-25
-                    if (r.L < 0) report(err, error_key(r.t, kStageRows, r.j, kArgNegative));
-                    else if (r.j > 0 && r.L <= r.Lp) report(err, error_key(r.t, kStageRows, r.j, kArgOrder));
-                } else if (repr == PULSE_FLAT_INT32) {  // patch.hpp:139-147 (first entry: k2_layout)
-                    if (r.j > 0 && r.L <= r.Lp) report(err, error_key(r.t, kStageRows, r.j, kArgOrder));
-                    else if (r.j > 0 && r.L - r.Lp > 0xFFFFFFFFll)
-                        report(err, error_key(r.t, kStageRows, r.j, kDimFlatGap));
+            stage<8>(sidx, reinterpret_cast<const uint8_t*>(em.idx32 + c0), 4 * len);
+            __syncwarp();
+            const uint32_t Lp = lane_pred(em, sidx, c0, c);
+            const int nv = max(0, min(int(kLaneE), int(len) - lane * int(kLaneE)));
+            const uint64_t jf = c0 - c.ts + uint64_t(lane) * kLaneE;  // ordinal of the lane's first entry
+            uint32_t prow = div_magic(Lp, c.magic, c.shift), pcol = Lp - prow * c.cols32;
+            uint32_t lre = 0, lce = 0;
+#pragma unroll
+            for (int j = 0; j < int(kLaneE); ++j) {
+                if (j < nv) {
+                    const uint4 q = lane_vec<8>(sidx, j >> 2);
+                    const uint32_t Lj = PULSE_LANE_L(q, j & 3);
+                    const uint32_t row = div_magic(Lj, c.magic, c.shift), col = Lj - row * c.cols32;
+                    const bool first = jf + j == 0;
+                    const bool nr = first || row != prow;
+                    const uint32_t rgap = first ? row : row - prow;
+                    const uint32_t cval = nr ? col : col - pcol;
+                    lre += rgap >= 0xFF;
+                    lce += cval >= 0xFFFF;
+                    prow = row;
+                    pcol = col;
                 }
             }
-            if (coo) {
-                const Coo f = cw.fields(r, cd);
-                if (r.valid) {
-                    if (em.idx64) {  // downscale_coo, index_coding.hpp:117-121
-                        int64_t row, col;
-                        coo_split(r.L, cd, row, col);
-                        if (row < 0 || col < 0) report(err, error_key(r.t, kStageRows, r.j, kArgNegative));
-                        else if (r.j > 0 && r.L <= r.Lp) report(err, error_key(r.t, kStageRows, r.j, kArgOrder));
-                    }
-                    if (f.rg > 0xFFFFFFFFll) report(err, error_key(r.t, kStageRows, r.j, kDimRow));
-                    if (f.cv > 0xFFFFFFFFll) report(err, error_key(r.t, kStageCols, r.j, kDimCol));
-                    rf = f.rg >= 0xFF;
-                    cf = f.cv >= 0xFFFF;
-                    if (rf) atomicAdd(t_resc + r.t, 1u);
-                    if (cf) atomicAdd(t_cesc + r.t, 1u);
-                }
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                lre += __shfl_xor_sync(0xffffffffu, lre, off);
+                lce += __shfl_xor_sync(0xffffffffu, lce, off);
             }
-            re += __popc(__ballot_sync(0xffffffffu, rf));
-            ce += __popc(__ballot_sync(0xffffffffu, cf));
-          }
-          w.rotate();
+            if (lane == 0) {
+                if (lre) atomicAdd(t_resc + c.t, lre);
+                if (lce) atomicAdd(t_cesc + c.t, lce);
+            }
+            re += lre;
+            ce += lce;
+            __syncwarp();
         }
         if (coo && lane == 0) range_cnt[rg] = uint64_t(re) | (uint64_t(ce) << 32);
     }
@@ -547,19 +676,113 @@ __global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
 // =============================================================================================
 // K2b: emit
 // =============================================================================================
-__device__ __forceinline__ void st_u16_any(uint8_t* p, uint32_t v) {
-    if ((reinterpret_cast<uintptr_t>(p) & 1) == 0) *reinterpret_cast<uint16_t*>(p) = uint16_t(v);
-    else wr_u16(p, v);
-}
-__device__ __forceinline__ void st_u32_any(uint8_t* p, uint32_t v) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    if ((a & 3) == 0) {
-        *reinterpret_cast<uint32_t*>(p) = v;
-    } else if ((a & 1) == 0) {
-        reinterpret_cast<uint16_t*>(p)[0] = uint16_t(v);
-        reinterpret_cast<uint16_t*>(p)[1] = uint16_t(v >> 16);
-    } else {
-        wr_u32(p, v);
+// Per-round walker path of K2b over entries [first, last); (R, Cc): global row /
+// column escapes before `first` (COO_DOWNSCALED), advanced in place.
+__device__ __noinline__ void k2b_span(const EntryMap& em, uint32_t repr, uint64_t n, uint64_t first, uint64_t last,
+                                      const TensorLayout* __restrict__ tlay, const uint16_t* __restrict__ vals,
+                                      uint8_t* __restrict__ body, uint64_t& R, uint64_t& Cc) {
+    const int lane = threadIdx.x & 31;
+    const bool coo = repr == PULSE_COO_DOWNSCALED;
+    Walker w(em, n, first, last);
+    CooWalker cw;
+    bool seeded = false;
+    while (!w.done()) {
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) {
+        if (seeded && w.fast_round()) {
+            const TensorLayout& tl = w.ctx.tl;
+            const uint64_t i = w.base + lane;
+            uint32_t j, L, Lp;
+            bool valid;
+            w.fast_step(rr, j, L, Lp, valid);
+            if (coo) {
+                const uint32_t row = div_magic(L, w.ctx.magic, w.ctx.shift);
+                const uint32_t col = L - row * w.ctx.cols32;
+                uint32_t prow = __shfl_up_sync(0xffffffffu, row, 1), pcol = __shfl_up_sync(0xffffffffu, col, 1);
+                if (lane == 0) {
+                    prow = uint32_t(cw.carry_row);
+                    pcol = uint32_t(cw.carry_col);
+                }
+                cw.carry_row = __shfl_sync(0xffffffffu, row, 31);
+                cw.carry_col = __shfl_sync(0xffffffffu, col, 31);
+                const bool nr = j == 0 || row != prow;
+                const uint32_t rgap = j == 0 ? row : row - prow;
+                const uint32_t cval = nr ? col : col - pcol;
+                const bool rf = valid && rgap >= 0xFF, cf = valid && cval >= 0xFFFF;
+                const uint32_t br = __ballot_sync(0xffffffffu, rf), bc = __ballot_sync(0xffffffffu, cf);
+                if (valid) {
+                    const uint64_t Ri = R + __popc(br & lanemask_lt());
+                    const uint64_t Ci = Cc + __popc(bc & lanemask_lt());
+                    uint8_t* rp = body + tl.idx_off + j + 4 * (Ri - tl.rts);
+                    if (rf) {
+                        rp[0] = 0xFF;
+                        wr_u32(rp + 1, rgap);
+                    } else {
+                        rp[0] = uint8_t(rgap);
+                    }
+                    uint8_t* cq = body + tl.idx_off + tl.row_bytes + 2ull * j + 4 * (Ci - tl.cts);
+                    if (cf) {
+                        wr_u16(cq, 0xFFFF);
+                        wr_u32(cq + 2, cval);
+                    } else {
+                        st_u16_any(cq, cval);
+                    }
+                    st_u16_any(body + tl.val_off + 2ull * j, vals[i]);
+                }
+                R += __popc(br);
+                Cc += __popc(bc);
+            } else if (valid) {
+                uint64_t g;
+                if (j > 0) g = L - Lp;
+                else g = uint64_t(L) + (repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0);
+                st_u32_any(body + tl.idx_off + 4ull * j, uint32_t(g));
+                st_u16_any(body + tl.val_off + 2ull * j, vals[i]);
+            }
+            continue;
+        }
+        const Ent r = w.next(rr);
+        const TensorLayout& tl = tlay[r.t];
+        if (coo) {
+            const ColDiv cd = em.coldiv[r.t];
+            if (!seeded) {
+                const int64_t Lp0 = __shfl_sync(0xffffffffu, r.Lp, 0);
+                const uint32_t t0 = __shfl_sync(0xffffffffu, r.t, 0);
+                if (Lp0 >= 0) coo_split(Lp0, em.coldiv[t0], cw.carry_row, cw.carry_col);
+            }
+            const Coo f = cw.fields(r, cd);
+            const bool rf = r.valid && f.rg >= 0xFF, cf = r.valid && f.cv >= 0xFFFF;
+            const uint32_t br = __ballot_sync(0xffffffffu, rf), bc = __ballot_sync(0xffffffffu, cf);
+            if (r.valid) {
+                const uint64_t Ri = R + __popc(br & lanemask_lt());
+                const uint64_t Ci = Cc + __popc(bc & lanemask_lt());
+                uint8_t* rp = body + tl.idx_off + r.j + 4 * (Ri - tl.rts);
+                if (rf) {
+                    rp[0] = 0xFF;
+                    wr_u32(rp + 1, uint32_t(f.rg));
+                } else {
+                    rp[0] = uint8_t(f.rg);
+                }
+                uint8_t* cq = body + tl.idx_off + tl.row_bytes + 2 * r.j + 4 * (Ci - tl.cts);
+                if (cf) {
+                    wr_u16(cq, 0xFFFF);
+                    wr_u32(cq + 2, uint32_t(f.cv));
+                } else {
+                    st_u16_any(cq, uint32_t(f.cv));
+                }
+                st_u16_any(body + tl.val_off + 2 * r.j, vals[r.i]);
+            }
+            R += __popc(br);
+            Cc += __popc(bc);
+        } else if (r.valid) {
+            uint64_t g;
+            if (r.j > 0) g = uint64_t(r.L - r.Lp);
+            else g = uint64_t(r.L) + (repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0);
+            st_u32_any(body + tl.idx_off + 4 * r.j, uint32_t(g));
+            st_u16_any(body + tl.val_off + 2 * r.j, vals[r.i]);
+        }
+        seeded = true;
+      }
+      w.rotate();
     }
 }
 
@@ -567,120 +790,101 @@ __global__ void __launch_bounds__(kThreads)
 k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
         const ulonglong2* __restrict__ range_pre, const uint16_t* __restrict__ vals,
         const pulse_result* __restrict__ result, uint8_t* __restrict__ body) {
+    extern __shared__ __align__(16) uint8_t smem[];
     if (result->status != 0) return;
     const uint64_t n = em.seg_start[em.n_segs];
     const uint64_t n_ranges = (n + kRangeEntries - 1) / kRangeEntries;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool coo = repr == PULSE_COO_DOWNSCALED;
+    uint8_t* ws = smem + warp * kEmitWarpSmem;
+    uint4* sidx = reinterpret_cast<uint4*>(ws);
+    uint4* srow = reinterpret_cast<uint4*>(ws + kSIdx);
+    uint4* scol = reinterpret_cast<uint4*>(ws + kSIdx + kSRow);
+    uint4* sval = reinterpret_cast<uint4*>(ws + kSIdx + kSRow + kSCol);
     const uint64_t stride = uint64_t(gridDim.x) * kWarps;
-    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5); rg < n_ranges; rg += stride) {
-        const uint64_t first = rg * kRangeEntries;
-        Walker w(em, n, first, first + kRangeEntries);
-        CooWalker cw;
+    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + warp; rg < n_ranges; rg += stride) {
+        const uint64_t r0 = rg * kRangeEntries, r1 = min(r0 + kRangeEntries, n);
         uint64_t R = 0, Cc = 0;
         if (coo) {
             const ulonglong2 p = range_pre[rg];
             R = p.x;
             Cc = p.y;
         }
-        bool seeded = false;
-        while (!w.done()) {
-#pragma unroll
-          for (int rr = 0; rr < 8; ++rr) {
-            if (seeded && w.fast_round()) {
-                const TensorLayout& tl = w.ctx.tl;
-                const uint64_t i = w.base + lane;
-                uint32_t j, L, Lp;
-                bool valid;
-                w.fast_step(rr, j, L, Lp, valid);
-                if (coo) {
-                    const uint32_t row = div_magic(L, w.ctx.magic, w.ctx.shift);
-                    const uint32_t col = L - row * w.ctx.cols32;
-                    uint32_t prow = __shfl_up_sync(0xffffffffu, row, 1), pcol = __shfl_up_sync(0xffffffffu, col, 1);
-                    if (lane == 0) {
-                        prow = uint32_t(cw.carry_row);
-                        pcol = uint32_t(cw.carry_col);
-                    }
-                    cw.carry_row = __shfl_sync(0xffffffffu, row, 31);
-                    cw.carry_col = __shfl_sync(0xffffffffu, col, 31);
-                    const bool nr = j == 0 || row != prow;
-                    const uint32_t rgap = j == 0 ? row : row - prow;
-                    const uint32_t cval = nr ? col : col - pcol;
-                    const bool rf = valid && rgap >= 0xFF, cf = valid && cval >= 0xFFFF;
-                    const uint32_t br = __ballot_sync(0xffffffffu, rf), bc = __ballot_sync(0xffffffffu, cf);
-                    if (valid) {
-                        const uint64_t Ri = R + __popc(br & lanemask_lt());
-                        const uint64_t Ci = Cc + __popc(bc & lanemask_lt());
-                        uint8_t* rp = body + tl.idx_off + j + 4 * (Ri - tl.rts);
-                        if (rf) {
-                            rp[0] = 0xFF;
-                            wr_u32(rp + 1, rgap);
-                        } else {
-                            rp[0] = uint8_t(rgap);
-                        }
-                        uint8_t* cq = body + tl.idx_off + tl.row_bytes + 2ull * j + 4 * (Ci - tl.cts);
-                        if (cf) {
-                            wr_u16(cq, 0xFFFF);
-                            wr_u32(cq + 2, cval);
-                        } else {
-                            st_u16_any(cq, cval);
-                        }
-                        st_u16_any(body + tl.val_off + 2ull * j, vals[i]);
-                    }
-                    R += __popc(br);
-                    Cc += __popc(bc);
-                } else if (valid) {
-                    uint64_t g;
-                    if (j > 0) g = L - Lp;
-                    else g = uint64_t(L) + (repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0);
-                    st_u32_any(body + tl.idx_off + 4ull * j, uint32_t(g));
-                    st_u16_any(body + tl.val_off + 2ull * j, vals[i]);
-                }
+        uint32_t sg = em.n_segs ? upper_index<uint64_t>(em.seg_start, 0, em.n_segs, r0) : 0;
+        for (uint64_t c0 = r0; c0 < r1; c0 += kChunkE) {
+            const uint32_t len = uint32_t(r1 - c0 < kChunkE ? r1 - c0 : kChunkE);
+            const FastCtx c = fast_ctx(em, c0, len, sg);
+            if (!c.fast) {
+                k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
                 continue;
             }
-            const Ent r = w.next(rr);
-            const TensorLayout& tl = tlay[r.t];
+            stage<8>(sidx, reinterpret_cast<const uint8_t*>(em.idx32 + c0), 4 * len);
+            stage<1>(sval, reinterpret_cast<const uint8_t*>(vals + c0), 2 * len);
+            __syncwarp();
+            const uint32_t Lp = lane_pred(em, sidx, c0, c);
+            const int nv = max(0, min(int(kLaneE), int(len) - lane * int(kLaneE)));
+            const uint64_t j0 = c0 - c.ts;                          // ordinal of the chunk's first entry
+            const uint64_t jf = j0 + uint64_t(lane) * kLaneE;       // ... and of this lane's
+            const TensorLayout tl = tlay[c.t];
             if (coo) {
-                const ColDiv cd = em.coldiv[r.t];
-                if (!seeded) {
-                    const int64_t Lp0 = __shfl_sync(0xffffffffu, r.Lp, 0);
-                    const uint32_t t0 = __shfl_sync(0xffffffffu, r.t, 0);
-                    if (Lp0 >= 0) coo_split(Lp0, em.coldiv[t0], cw.carry_row, cw.carry_col);
-                }
-                const Coo f = cw.fields(r, cd);
-                const bool rf = r.valid && f.rg >= 0xFF, cf = r.valid && f.cv >= 0xFFFF;
-                const uint32_t br = __ballot_sync(0xffffffffu, rf), bc = __ballot_sync(0xffffffffu, cf);
-                if (r.valid) {
-                    const uint64_t Ri = R + __popc(br & lanemask_lt());
-                    const uint64_t Ci = Cc + __popc(bc & lanemask_lt());
-                    uint8_t* rp = body + tl.idx_off + r.j + 4 * (Ri - tl.rts);
-                    if (rf) {
-                        rp[0] = 0xFF;
-                        wr_u32(rp + 1, uint32_t(f.rg));
-                    } else {
-                        rp[0] = uint8_t(f.rg);
+                uint32_t prow = div_magic(Lp, c.magic, c.shift), pcol = Lp - prow * c.cols32;
+                uint32_t rw[kLaneE / 4], cw2[kLaneE / 2];
+                bool esc = false;
+#pragma unroll
+                for (int q = 0; q < int(kLaneE / 4); ++q) rw[q] = 0;
+#pragma unroll
+                for (int q = 0; q < int(kLaneE / 2); ++q) cw2[q] = 0;
+#pragma unroll
+                for (int j = 0; j < int(kLaneE); ++j) {
+                    if (j < nv) {
+                        const uint4 q = lane_vec<8>(sidx, j >> 2);
+                        const uint32_t Lj = PULSE_LANE_L(q, j & 3);
+                        const uint32_t row = div_magic(Lj, c.magic, c.shift), col = Lj - row * c.cols32;
+                        const bool first = jf + j == 0;
+                        const bool nr = first || row != prow;
+                        const uint32_t rgap = first ? row : row - prow;
+                        const uint32_t cval = nr ? col : col - pcol;
+                        esc |= rgap >= 0xFF || cval >= 0xFFFF;
+                        rw[j >> 2] |= (rgap & 0xFF) << (8 * (j & 3));
+                        cw2[j >> 1] |= (cval & 0xFFFF) << (16 * (j & 1));
+                        prow = row;
+                        pcol = col;
                     }
-                    uint8_t* cq = body + tl.idx_off + tl.row_bytes + 2 * r.j + 4 * (Ci - tl.cts);
-                    if (cf) {
-                        wr_u16(cq, 0xFFFF);
-                        wr_u32(cq + 2, uint32_t(f.cv));
-                    } else {
-                        st_u16_any(cq, uint32_t(f.cv));
-                    }
-                    st_u16_any(body + tl.val_off + 2 * r.j, vals[r.i]);
                 }
-                R += __popc(br);
-                Cc += __popc(bc);
-            } else if (r.valid) {
-                uint64_t g;
-                if (r.j > 0) g = uint64_t(r.L - r.Lp);
-                else g = uint64_t(r.L) + (repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0);
-                st_u32_any(body + tl.idx_off + 4 * r.j, uint32_t(g));
-                st_u16_any(body + tl.val_off + 2 * r.j, vals[r.i]);
+                if (__any_sync(0xffffffffu, esc)) {  // escapes: variable-size entries
+                    __syncwarp();
+                    k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
+                    continue;
+                }
+#pragma unroll
+                for (int i = 0; i < 2; ++i) srow[swz<2>(uint32_t(lane * 2 + i))] = make_uint4(rw[4 * i], rw[4 * i + 1], rw[4 * i + 2], rw[4 * i + 3]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) scol[swz<4>(uint32_t(lane * 4 + i))] = make_uint4(cw2[4 * i], cw2[4 * i + 1], cw2[4 * i + 2], cw2[4 * i + 3]);
+                __syncwarp();
+                unstage<2>(body + tl.idx_off + j0 + 4 * (R - tl.rts), srow, len);
+                unstage<4>(body + tl.idx_off + tl.row_bytes + 2 * j0 + 4 * (Cc - tl.cts), scol, 2 * len);
+            } else {
+                const uint64_t first_add = repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0;
+                uint32_t prev = Lp;
+                __syncwarp();  // every lane has read its predecessor before gaps overwrite indices
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {  // in place: each lane rewrites only its own slots
+                    const uint32_t slot = swz<8>(uint32_t(lane * 8 + i));
+                    const uint4 q = sidx[slot];
+                    uint32_t g[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t Lj = PULSE_LANE_L(q, k);
+                        g[k] = jf + 4 * i + k == 0 ? uint32_t(uint64_t(Lj) + first_add) : Lj - prev;
+                        prev = Lj;
+                    }
+                    sidx[slot] = make_uint4(g[0], g[1], g[2], g[3]);
+                }
+                __syncwarp();
+                unstage<8>(body + tl.idx_off + 4 * j0, sidx, 4 * len);
             }
-            seeded = true;
-          }
-          w.rotate();
+            unstage<1>(body + tl.val_off + 2 * j0, sval, 2 * len);
+            __syncwarp();
         }
     }
 }
@@ -692,12 +896,24 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
                         const pulse_scan_summary* gathered, uint32_t n_ranks, uint32_t rank,
                         const uint16_t* vals, uint8_t* body, uint64_t body_cap, pulse_patch_entry* entries,
                         pulse_result* result, uint64_t cap, cudaStream_t s) {
-    const unsigned grid = unsigned(sm_count() * 4);
     cudaMemsetAsync(p.t_resc, 0, p.n_tensors * sizeof(uint32_t), s);
     cudaMemsetAsync(p.t_cesc, 0, p.n_tensors * sizeof(uint32_t), s);
     cudaMemsetAsync(p.err, 0xFF, sizeof(uint64_t), s);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k2_scan_escapes, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWarps * kScanWarpSmem));
+        cudaFuncSetAttribute(k2_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWarps * kEmitWarpSmem));
+        configured = true;
+    }
+    static int occ_scan = 0, occ_emit = 0;
+    if (!occ_scan) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_scan, k2_scan_escapes, kThreads, kWarps * kScanWarpSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_emit, k2_emit, kThreads, kWarps * kEmitWarpSmem);
+        occ_scan = std::max(occ_scan, 1);
+        occ_emit = std::max(occ_emit, 1);
+    }
     if (repr == PULSE_COO_DOWNSCALED || validate_args)
-        k2_scan_escapes<<<grid, kThreads, 0, s>>>(em, repr, p.range_cnt, p.t_resc, p.t_cesc, p.err);
+        k2_scan_escapes<<<unsigned(sm_count() * occ_scan), kThreads, kWarps * kScanWarpSmem, s>>>(em, repr, p.range_cnt, p.t_resc, p.t_cesc, p.err);
     LayoutArgs a;
     a.range_cnt = p.range_cnt;
     a.range_pre = p.range_pre;
@@ -717,7 +933,8 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
     a.err = p.err;
     a.cap = cap;
     k2_layout<<<1, kLayoutThreads, 0, s>>>(a);
-    k2_emit<<<grid, kThreads, 0, s>>>(em, repr, p.tlay, p.range_pre, vals, result, body);
+    k2_emit<<<unsigned(sm_count() * occ_emit), kThreads, kWarps * kEmitWarpSmem, s>>>(em, repr, p.tlay, p.range_pre, vals,
+                                                                             result, body);
 }
 
 void launch_encode_emit(const PlanDev& p, uint32_t repr, const pulse_scan_summary* gathered, uint32_t n_ranks,
