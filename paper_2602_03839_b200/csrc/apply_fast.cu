@@ -185,6 +185,10 @@ __device__ __forceinline__ uint64_t seg_round_scan(bool head, uint64_t v, uint64
     return r;
 }
 
+// Error reporting stays out of line: the unrolled per-entry loops then keep a
+// small instruction footprint (the checks almost never fire).
+__device__ __noinline__ void report_cold(uint64_t* err, uint64_t key) { report(err, key); }
+
 __device__ __forceinline__ bool fast_blocked(const uint32_t* flags) { return *(volatile const uint32_t*)flags != 0; }
 
 struct ApplyArgs {
@@ -352,7 +356,8 @@ f_pass(ApplyArgs A) {
             }
 #define PULSE_AV(j) (coo ? (aw[(j) >> 2] >> (8 * ((j) & 3))) & 0xFFu : aw[(j) % kAW])
 #define PULSE_BV(j) (coo ? (bw[((j) >> 1) % kBW] >> (16 * ((j) & 1))) & 0xFFFFu : 0u)
-            const uint64_t ol = o0 + uint64_t(lane) * kPer;  // ordinal of this lane's first entry
+            const uint64_t ol = o0 + uint64_t(lane) * kPer;
+            const uint64_t nrows = coo && kPass == kValidate ? L.numel / L.cols : 0;  // ordinal of this lane's first entry
             // lane aggregates
             uint64_t lr = 0, lc = 0;
             bool lmark = false;
@@ -398,19 +403,17 @@ f_pass(ApplyArgs A) {
                         row = o == 0 ? a : row + a;
                         col = nr ? b : col + b;
                         if (kPass == kValidate) {
-                            if (!nr && b == 0) { report(A.err, error_key(e, kStageCols, o, kZeroColGap)); continue; }
-                            if (col >= L.cols) { report(A.err, error_key(e, kStageRange, o, kColRange)); continue; }
+                            // patch.hpp:247-254; with col < cols, flat >= numel <=> row >= numel / cols
+                            if (!nr && b == 0) { report_cold(A.err, error_key(e, kStageCols, o, kZeroColGap)); continue; }
+                            if (col >= L.cols) { report_cold(A.err, error_key(e, kStageRange, o, kColRange)); continue; }
+                            if (row >= nrows) report_cold(A.err, error_key(e, kStageRange, o, kIdxRange));
                         }
-                        const uint64_t flat = row * L.cols + col;
-                        if (kPass == kValidate) {
-                            if (flat >= L.numel) report(A.err, error_key(e, kStageRange, o, kIdxRange));
-                        }
-                        xv[c] = uint32_t(flat);
+                        if (kPass == kScatter) xv[c] = uint32_t(row) * uint32_t(L.cols) + uint32_t(col);
                     } else if (kRepr == kI32) {
                         row = o == 0 ? a : row + a;
                         if (kPass == kValidate) {
-                            if (o > 0 && a == 0) { report(A.err, error_key(e, kStageRows, o, kZeroGap)); continue; }
-                            if (row >= L.numel) report(A.err, error_key(e, kStageRows, o, kIdxRange));
+                            if (o > 0 && a == 0) { report_cold(A.err, error_key(e, kStageRows, o, kZeroGap)); continue; }
+                            if (row >= L.numel) report_cold(A.err, error_key(e, kStageRows, o, kIdxRange));
                         }
                         xv[c] = uint32_t(row);
                     } else {
@@ -418,8 +421,8 @@ f_pass(ApplyArgs A) {
                         const int64_t local = int64_t(row) - int64_t(gap_base) - int64_t(L.flat_base);
                         if (kPass == kValidate) {
                             const uint64_t gi = c0 + uint64_t(lane) * kPer + j;
-                            if (a == 0 && (gi > 0 || has_prev)) { report(A.err, error_key(e, kStageRows, o, kZeroGap)); continue; }
-                            if (local < 0 || uint64_t(local) >= L.numel) report(A.err, error_key(e, kStageRows, o, kIdxRange));
+                            if (a == 0 && (gi > 0 || has_prev)) { report_cold(A.err, error_key(e, kStageRows, o, kZeroGap)); continue; }
+                            if (local < 0 || uint64_t(local) >= L.numel) report_cold(A.err, error_key(e, kStageRows, o, kIdxRange));
                         }
                         xv[c] = uint32_t(local);
                     }
@@ -538,12 +541,14 @@ void launch_pass(const ApplyArgs& a, cudaStream_t s) {
         per_sm = per_sm > 0 ? per_sm : 1;
     }
     f_pass<kRepr, kPass><<<unsigned(sm_count() * per_sm), kThreads, smem, s>>>(a);
+    PULSE_LAUNCHED("f_pass", s);
 }
 
 template <int kRepr>
 void launch_all(const ApplyArgs& a, bool scatter, cudaStream_t s) {
     launch_pass<kRepr, kAgg>(a, s);
     f_range_scan<<<1, kScanThreads, 0, s>>>(a.totals, a.agg, a.flags);
+    PULSE_LAUNCHED("f_range_scan", s);
     launch_pass<kRepr, kValidate>(a, s);
     if (scatter) launch_pass<kRepr, kScatter>(a, s);
 }

@@ -713,6 +713,17 @@ __global__ void k1_finalize(const SegDesc* __restrict__ segs, uint32_t n_segs,
 // launchers
 // =============================================================================================
 static int g_sms = 0;
+void debug_sync(const char* kernel, cudaStream_t s) {
+    static const bool on = [] {
+        const char* e = getenv("PULSE_DEBUG_SYNC");
+        return e && *e && *e != '0';
+    }();
+    if (!on) return;
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) fprintf(stderr, "[pulse debug] %s: %s\n", kernel, cudaGetErrorString(e));
+}
+
 int sm_count() {
     if (!g_sms) {
         int dev = 0;
@@ -760,6 +771,7 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
             kt.tile_seg = p.tma_tile_seg;
             const uint64_t grid = std::min<uint64_t>(uint64_t(sm_count()), p.tma_tiles);
             k1_tma<<<unsigned(grid), tma::kThreadsTotal, sizeof(tma::Smem), s>>>(kt);
+            PULSE_LAUNCHED("k1_tma", s);
             launched = true;
         }
         if (!launched && k1_variant() == 2 && per_sm_static > 0) {
@@ -772,9 +784,11 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
         if (!launched) {
             const uint64_t grid = std::min<uint64_t>(uint64_t(std::max(1, per_sm_ticket)) * sm_count(), p.n_tiles);
             k1_ticket<<<unsigned(grid), kThreads, 0, s>>>(k);
+            PULSE_LAUNCHED("k1_ticket", s);
         }
     }
     k1_finalize<<<1, 32, 0, s>>>(p.segs, p.n_segs, p.numel, p.seg_start, p.idx32, p.cap, p.scan, copy_out);
+    PULSE_LAUNCHED("k1_finalize", s);
 }
 
 PULSE_DEFINE_WATCHDOG_SETTER(set_watchdog_encode)

@@ -193,20 +193,25 @@ __global__ void k_coo_unpack(const uint8_t* __restrict__ p, uint64_t len, uint64
 
 void launch_export_indices(const PlanDev& p, int64_t* out, cudaStream_t s) {
     k_export_indices<<<sm_count() * 4, 256, 0, s>>>(p.segs, p.seg_start, p.n_segs, p.idx32, out);
+    PULSE_LAUNCHED("k_export_indices", s);
 }
 void launch_delta_encode(const int64_t* in, uint64_t n, int64_t* out, uint64_t* err, cudaStream_t s) {
     if (n) k_delta_encode<<<unsigned(std::min<uint64_t>((n + 255) / 256, 4096)), 256, 0, s>>>(in, n, out, err);
+    PULSE_LAUNCHED("k_delta_encode", s);
 }
 void launch_delta_decode(const int64_t* in, uint64_t n, int64_t* out, uint64_t* err, cudaStream_t s) {
     if (n) k_delta_decode<<<1, 1024, 0, s>>>(in, n, out, err);
+    PULSE_LAUNCHED("k_delta_decode", s);
 }
 void launch_coo_pack(const int64_t* rows, const int64_t* cols, uint64_t n, uint8_t* out, uint64_t* nbytes,
                      uint64_t* err, cudaStream_t s) {
     k_coo_pack<<<1, 1024, 0, s>>>(rows, cols, n, out, nbytes, err);
+    PULSE_LAUNCHED("k_coo_pack", s);
 }
 void launch_coo_unpack(const uint8_t* p, uint64_t len, uint64_t count, int64_t* rows, int64_t* cols, uint64_t* err,
                        cudaStream_t s) {
     k_coo_unpack<<<1, 32, 0, s>>>(p, len, count, rows, cols, err);
+    PULSE_LAUNCHED("k_coo_unpack", s);
 }
 
 PULSE_DEFINE_WATCHDOG_SETTER(set_watchdog_helpers)

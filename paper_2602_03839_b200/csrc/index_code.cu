@@ -39,7 +39,15 @@ struct EntryMap {
     const ColDiv* coldiv;       // per tensor
     const uint64_t* numel;      // per tensor
     const TensorLayout* tlay;   // per tensor (emit only; may be null)
+    uint64_t cap;               // entries the idx32/val16 arrays hold (mode A); ~0 for mode B
 };
+
+// Entries K2 may touch: on overflow K1 counted more changes than it stored, and
+// k2_layout reports PULSE_E_CAPACITY -- the kernels must not read past `cap`.
+__device__ __forceinline__ uint64_t k2_entries(const EntryMap& em) {
+    const uint64_t n = em.seg_start[em.n_segs];
+    return n < em.cap ? n : em.cap;
+}
 
 // Division of a local index by the tensor's column extent (patch.hpp:165-166):
 // 32-bit magic multiply when both fit, 64-bit division otherwise.
@@ -238,9 +246,38 @@ struct CooWalker {
 // =============================================================================================
 constexpr uint32_t kChunkE = 1024;                 // entries per staged chunk
 constexpr uint32_t kLaneE = kChunkE / 32;          // consecutive entries per lane
-constexpr uint32_t kSIdx = kChunkE * 4, kSRow = kChunkE, kSCol = kChunkE * 2, kSVal = kChunkE * 2;
-constexpr uint32_t kScanWarpSmem = kSIdx;
-constexpr uint32_t kEmitWarpSmem = kSIdx + kSRow + kSCol + kSVal;
+constexpr uint32_t kSIdx = kChunkE * 4, kSVal = kChunkE * 2;
+// double-buffered (cp.async prefetch of the next chunk): K2a idx; K2b idx + values
+// (K2b's packed row/column output reuses the chunk's own idx buffer)
+constexpr uint32_t kScanWarpSmem = 2 * kSIdx;
+constexpr uint32_t kEmitWarpSmem = 2 * (kSIdx + kSVal);
+
+// A warp's work: ranges rg, rg + stride, ...; each cut into kChunkE chunks.
+struct ChunkIt {
+    bool ok;
+    uint64_t rg, c0, r1;
+    uint32_t len;
+    __device__ __forceinline__ bool range_start() const { return c0 == rg * kRangeEntries; }
+    __device__ __forceinline__ bool range_end() const { return c0 + len >= r1; }
+};
+__device__ __forceinline__ ChunkIt chunk_at(uint64_t rg, uint64_t n_ranges, uint64_t n) {
+    ChunkIt it;
+    it.ok = rg < n_ranges;
+    it.rg = rg;
+    it.c0 = rg * kRangeEntries;
+    it.r1 = min(it.c0 + kRangeEntries, n);
+    it.len = it.ok ? uint32_t(it.r1 - it.c0 < kChunkE ? it.r1 - it.c0 : kChunkE) : 0;
+    return it;
+}
+__device__ __forceinline__ ChunkIt chunk_next(const ChunkIt& it, uint64_t stride, uint64_t n_ranges, uint64_t n) {
+    if (it.c0 + kChunkE < it.r1) {
+        ChunkIt nx = it;
+        nx.c0 += kChunkE;
+        nx.len = uint32_t(nx.r1 - nx.c0 < kChunkE ? nx.r1 - nx.c0 : kChunkE);
+        return nx;
+    }
+    return chunk_at(it.rg + stride, n_ranges, n);
+}
 
 struct FastCtx {
     bool fast;
@@ -271,11 +308,12 @@ __device__ __forceinline__ FastCtx fast_ctx(const EntryMap& em, uint64_t c0, uin
 // that entry is not the tensor's first): the previous lane's last staged index,
 // or for lane 0 the global entry before the chunk (same tensor, maybe the
 // previous segment).
-__device__ __forceinline__ uint32_t lane_pred(const EntryMap& em, const uint4* sidx, uint64_t c0, const FastCtx& c) {
+__device__ __forceinline__ uint32_t lane_pred(const EntryMap& em, const uint4* sidx, uint64_t c0, const FastCtx& c,
+                                              uint32_t sg) {
     const int lane = threadIdx.x & 31;
     if (lane > 0) return c.elem_off + smem_word<8>(sidx, uint32_t(lane) * kLaneE - 1);
     if (c0 > c.ts) {
-        const uint32_t sp = upper_index<uint64_t>(em.seg_start, 0, em.n_segs, c0 - 1);
+        const uint32_t sp = c0 - 1 >= em.seg_start[sg] ? sg : sg - 1;  // same tensor: this or the previous segment
         return uint32_t(em.segs[sp].elem_off + em.idx32[c0 - 1]);
     }
     return 0;
@@ -387,48 +425,62 @@ __device__ __noinline__ void k2a_span(const EntryMap& em, uint32_t repr, uint64_
 // =============================================================================================
 // K2a
 // =============================================================================================
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
 k2_scan_escapes(EntryMap em, uint32_t repr, uint64_t* __restrict__ range_cnt, uint32_t* __restrict__ t_resc,
                 uint32_t* __restrict__ t_cesc, uint64_t* __restrict__ err) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const uint64_t n = em.seg_start[em.n_segs];
+    const uint64_t n = k2_entries(em);
     const uint64_t n_ranges = (n + kRangeEntries - 1) / kRangeEntries;
     const bool coo = repr == PULSE_COO_DOWNSCALED;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint4* sidx = reinterpret_cast<uint4*>(smem + warp * kScanWarpSmem);
+    uint4* bufs = reinterpret_cast<uint4*>(smem + warp * kScanWarpSmem);
     const uint64_t stride = uint64_t(gridDim.x) * kWarps;
-    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + warp; rg < n_ranges; rg += stride) {
-        const uint64_t r0 = rg * kRangeEntries, r1 = min(r0 + kRangeEntries, n);
-        uint32_t re = 0, ce = 0;
-        uint32_t sg = em.n_segs ? upper_index<uint64_t>(em.seg_start, 0, em.n_segs, r0) : 0;
-        for (uint64_t c0 = r0; c0 < r1; c0 += kChunkE) {
-            const uint32_t len = uint32_t(r1 - c0 < kChunkE ? r1 - c0 : kChunkE);
-            const FastCtx c = fast_ctx(em, c0, len, sg);
-            if (!coo || !c.fast) {
-                k2a_span(em, repr, n, c0, c0 + len, t_resc, t_cesc, err, re, ce);
-                continue;
-            }
-            stage<8>(sidx, reinterpret_cast<const uint8_t*>(em.idx32 + c0), 4 * len);
+    const bool staged = coo && !em.idx64;
+    ChunkIt cur = chunk_at(uint64_t(blockIdx.x) * kWarps + warp, n_ranges, n);
+    if (staged && cur.ok) stage_async<8>(bufs, reinterpret_cast<const uint8_t*>(em.idx32 + cur.c0), 4 * cur.len);
+    cp_async_commit();
+    uint32_t re = 0, ce = 0, sg = 0, b = 0;
+    while (cur.ok) {
+        const ChunkIt nx = chunk_next(cur, stride, n_ranges, n);
+        if (staged && nx.ok)  // prefetch the next chunk while this one is decoded
+            stage_async<8>(bufs + (b ^ 1) * (kSIdx / 16), reinterpret_cast<const uint8_t*>(em.idx32 + nx.c0), 4 * nx.len);
+        cp_async_commit();
+        if (cur.range_start()) {
+            re = ce = 0;
+            sg = em.n_segs ? upper_index<uint64_t>(em.seg_start, 0, em.n_segs, cur.c0) : 0;
+        }
+        const uint64_t c0 = cur.c0;
+        const uint32_t len = cur.len;
+        const FastCtx c = fast_ctx(em, c0, len, sg);
+        if (!staged || !c.fast) {
+            k2a_span(em, repr, n, c0, c0 + len, t_resc, t_cesc, err, re, ce);
+        } else {
+            const uint4* sidx = bufs + b * (kSIdx / 16);
+            cp_async_wait<1>();
             __syncwarp();
-            const uint32_t Lp = lane_pred(em, sidx, c0, c);
+            const uint32_t Lp = lane_pred(em, sidx, c0, c, sg);
             const int nv = max(0, min(int(kLaneE), int(len) - lane * int(kLaneE)));
-            const uint64_t jf = c0 - c.ts + uint64_t(lane) * kLaneE;  // ordinal of the lane's first entry
+            const bool lane_first = c0 - c.ts + uint64_t(lane) * kLaneE == 0;  // lane holds the tensor's first entry
             uint32_t prow = div_magic(Lp, c.magic, c.shift), pcol = Lp - prow * c.cols32;
             uint32_t lre = 0, lce = 0;
 #pragma unroll
-            for (int j = 0; j < int(kLaneE); ++j) {
-                if (j < nv) {
-                    const uint4 q = lane_vec<8>(sidx, j >> 2);
-                    const uint32_t Lj = PULSE_LANE_L(q, j & 3);
-                    const uint32_t row = div_magic(Lj, c.magic, c.shift), col = Lj - row * c.cols32;
-                    const bool first = jf + j == 0;
-                    const bool nr = first || row != prow;
-                    const uint32_t rgap = first ? row : row - prow;
-                    const uint32_t cval = nr ? col : col - pcol;
-                    lre += rgap >= 0xFF;
-                    lce += cval >= 0xFFFF;
-                    prow = row;
-                    pcol = col;
+            for (int i = 0; i < int(kLaneE / 4); ++i) {
+                const uint4 q = lane_vec<8>(sidx, i);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int j = 4 * i + k;
+                    if (j < nv) {
+                        const uint32_t Lj = PULSE_LANE_L(q, k);
+                        const uint32_t row = div_magic(Lj, c.magic, c.shift), col = Lj - row * c.cols32;
+                        const bool first = j == 0 && lane_first;
+                        const bool nr = first || row != prow;
+                        const uint32_t rgap = first ? row : row - prow;
+                        const uint32_t cval = nr ? col : col - pcol;
+                        lre += rgap >= 0xFF;
+                        lce += cval >= 0xFFFF;
+                        prow = row;
+                        pcol = col;
+                    }
                 }
             }
 #pragma unroll
@@ -444,8 +496,11 @@ k2_scan_escapes(EntryMap em, uint32_t repr, uint64_t* __restrict__ range_cnt, ui
             ce += lce;
             __syncwarp();
         }
-        if (coo && lane == 0) range_cnt[rg] = uint64_t(re) | (uint64_t(ce) << 32);
+        if (cur.range_end() && coo && lane == 0) range_cnt[cur.rg] = uint64_t(re) | (uint64_t(ce) << 32);
+        cur = nx;
+        b ^= 1;
     }
+    cp_async_wait<0>();
 }
 
 // =============================================================================================
@@ -792,55 +847,75 @@ k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
         const pulse_result* __restrict__ result, uint8_t* __restrict__ body) {
     extern __shared__ __align__(16) uint8_t smem[];
     if (result->status != 0) return;
-    const uint64_t n = em.seg_start[em.n_segs];
+    const uint64_t n = k2_entries(em);
     const uint64_t n_ranges = (n + kRangeEntries - 1) / kRangeEntries;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool coo = repr == PULSE_COO_DOWNSCALED;
-    uint8_t* ws = smem + warp * kEmitWarpSmem;
-    uint4* sidx = reinterpret_cast<uint4*>(ws);
-    uint4* srow = reinterpret_cast<uint4*>(ws + kSIdx);
-    uint4* scol = reinterpret_cast<uint4*>(ws + kSIdx + kSRow);
-    uint4* sval = reinterpret_cast<uint4*>(ws + kSIdx + kSRow + kSCol);
+    uint8_t* ws = smem + warp * kEmitWarpSmem;  // [idx0 | idx1 | val0 | val1]
     const uint64_t stride = uint64_t(gridDim.x) * kWarps;
-    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + warp; rg < n_ranges; rg += stride) {
-        const uint64_t r0 = rg * kRangeEntries, r1 = min(r0 + kRangeEntries, n);
-        uint64_t R = 0, Cc = 0;
-        if (coo) {
-            const ulonglong2 p = range_pre[rg];
-            R = p.x;
-            Cc = p.y;
+    const bool staged = !em.idx64;
+    auto prefetch = [&](const ChunkIt& it, uint32_t bb) {
+        if (staged && it.ok) {
+            stage_async<8>(reinterpret_cast<uint4*>(ws + bb * kSIdx), reinterpret_cast<const uint8_t*>(em.idx32 + it.c0),
+                           4 * it.len);
+            stage_async<1>(reinterpret_cast<uint4*>(ws + 2 * kSIdx + bb * kSVal),
+                           reinterpret_cast<const uint8_t*>(vals + it.c0), 2 * it.len);
         }
-        uint32_t sg = em.n_segs ? upper_index<uint64_t>(em.seg_start, 0, em.n_segs, r0) : 0;
-        for (uint64_t c0 = r0; c0 < r1; c0 += kChunkE) {
-            const uint32_t len = uint32_t(r1 - c0 < kChunkE ? r1 - c0 : kChunkE);
-            const FastCtx c = fast_ctx(em, c0, len, sg);
-            if (!c.fast) {
-                k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
-                continue;
-            }
-            stage<8>(sidx, reinterpret_cast<const uint8_t*>(em.idx32 + c0), 4 * len);
-            stage<1>(sval, reinterpret_cast<const uint8_t*>(vals + c0), 2 * len);
-            __syncwarp();
-            const uint32_t Lp = lane_pred(em, sidx, c0, c);
-            const int nv = max(0, min(int(kLaneE), int(len) - lane * int(kLaneE)));
-            const uint64_t j0 = c0 - c.ts;                          // ordinal of the chunk's first entry
-            const uint64_t jf = j0 + uint64_t(lane) * kLaneE;       // ... and of this lane's
-            const TensorLayout tl = tlay[c.t];
+        cp_async_commit();
+    };
+    ChunkIt cur = chunk_at(uint64_t(blockIdx.x) * kWarps + warp, n_ranges, n);
+    prefetch(cur, 0);
+    uint64_t R = 0, Cc = 0;
+    uint32_t sg = 0, b = 0;
+    while (cur.ok) {
+        const ChunkIt nx = chunk_next(cur, stride, n_ranges, n);
+        prefetch(nx, b ^ 1);
+        if (cur.range_start()) {
+            R = Cc = 0;
             if (coo) {
-                uint32_t prow = div_magic(Lp, c.magic, c.shift), pcol = Lp - prow * c.cols32;
-                uint32_t rw[kLaneE / 4], cw2[kLaneE / 2];
-                bool esc = false;
+                const ulonglong2 p = range_pre[cur.rg];
+                R = p.x;
+                Cc = p.y;
+            }
+            sg = em.n_segs ? upper_index<uint64_t>(em.seg_start, 0, em.n_segs, cur.c0) : 0;
+        }
+        const uint64_t c0 = cur.c0;
+        const uint32_t len = cur.len;
+        const FastCtx c = fast_ctx(em, c0, len, sg);
+        uint4* sidx = reinterpret_cast<uint4*>(ws + b * kSIdx);
+        const uint4* sval = reinterpret_cast<const uint4*>(ws + 2 * kSIdx + b * kSVal);
+        if (!staged || !c.fast) {
+            k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
+            cur = nx;
+            b ^= 1;
+            continue;
+        }
+        cp_async_wait<1>();
+        __syncwarp();
+        const uint32_t Lp = lane_pred(em, sidx, c0, c, sg);
+        const int nv = max(0, min(int(kLaneE), int(len) - lane * int(kLaneE)));
+        const uint64_t j0 = c0 - c.ts;                                     // ordinal of the chunk's first entry
+        const bool lane_first = j0 + uint64_t(lane) * kLaneE == 0;         // lane holds the tensor's first entry
+        const TensorLayout tl = tlay[c.t];
+        bool via_walker = false;
+        if (coo) {
+            uint32_t prow = div_magic(Lp, c.magic, c.shift), pcol = Lp - prow * c.cols32;
+            uint32_t rw[kLaneE / 4], cw2[kLaneE / 2];
+            bool esc = false;
 #pragma unroll
-                for (int q = 0; q < int(kLaneE / 4); ++q) rw[q] = 0;
+            for (int q = 0; q < int(kLaneE / 4); ++q) rw[q] = 0;
 #pragma unroll
-                for (int q = 0; q < int(kLaneE / 2); ++q) cw2[q] = 0;
+            for (int q = 0; q < int(kLaneE / 2); ++q) cw2[q] = 0;
 #pragma unroll
-                for (int j = 0; j < int(kLaneE); ++j) {
+            for (int i = 0; i < int(kLaneE / 4); ++i) {
+                const uint4 q = lane_vec<8>(sidx, i);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int j = 4 * i + k;
                     if (j < nv) {
-                        const uint4 q = lane_vec<8>(sidx, j >> 2);
-                        const uint32_t Lj = PULSE_LANE_L(q, j & 3);
+                        const uint32_t Lj = PULSE_LANE_L(q, k);
                         const uint32_t row = div_magic(Lj, c.magic, c.shift), col = Lj - row * c.cols32;
-                        const bool first = jf + j == 0;
+                        const bool first = j == 0 && lane_first;
                         const bool nr = first || row != prow;
                         const uint32_t rgap = first ? row : row - prow;
                         const uint32_t cval = nr ? col : col - pcol;
@@ -851,11 +926,14 @@ k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
                         pcol = col;
                     }
                 }
-                if (__any_sync(0xffffffffu, esc)) {  // escapes: variable-size entries
-                    __syncwarp();
-                    k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
-                    continue;
-                }
+            }
+            if (__any_sync(0xffffffffu, esc)) {
+                via_walker = true;  // escapes: variable-size entries
+            } else {
+                // packed rows (1 KiB, V=2) and columns (2 KiB, V=4) replace the chunk's indices
+                uint4* srow = sidx;
+                uint4* scol = sidx + kChunkE / 16;
+                __syncwarp();
 #pragma unroll
                 for (int i = 0; i < 2; ++i) srow[swz<2>(uint32_t(lane * 2 + i))] = make_uint4(rw[4 * i], rw[4 * i + 1], rw[4 * i + 2], rw[4 * i + 3]);
 #pragma unroll
@@ -863,30 +941,38 @@ k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
                 __syncwarp();
                 unstage<2>(body + tl.idx_off + j0 + 4 * (R - tl.rts), srow, len);
                 unstage<4>(body + tl.idx_off + tl.row_bytes + 2 * j0 + 4 * (Cc - tl.cts), scol, 2 * len);
-            } else {
-                const uint64_t first_add = repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0;
-                uint32_t prev = Lp;
-                __syncwarp();  // every lane has read its predecessor before gaps overwrite indices
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {  // in place: each lane rewrites only its own slots
-                    const uint32_t slot = swz<8>(uint32_t(lane * 8 + i));
-                    const uint4 q = sidx[slot];
-                    uint32_t g[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint32_t Lj = PULSE_LANE_L(q, k);
-                        g[k] = jf + 4 * i + k == 0 ? uint32_t(uint64_t(Lj) + first_add) : Lj - prev;
-                        prev = Lj;
-                    }
-                    sidx[slot] = make_uint4(g[0], g[1], g[2], g[3]);
-                }
-                __syncwarp();
-                unstage<8>(body + tl.idx_off + 4 * j0, sidx, 4 * len);
             }
-            unstage<1>(body + tl.val_off + 2 * j0, sval, 2 * len);
+        } else {
+            const uint64_t first_add = repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0;
+            uint32_t prev = Lp;
+            __syncwarp();  // every lane has read its predecessor before gaps overwrite indices
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {  // in place: each lane rewrites only its own slots
+                const uint32_t slot = swz<8>(uint32_t(lane * 8 + i));
+                const uint4 q = lds128(sidx + slot);
+                uint32_t g[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t Lj = PULSE_LANE_L(q, k);
+                    g[k] = (i == 0 && k == 0 && lane_first) ? uint32_t(uint64_t(Lj) + first_add) : Lj - prev;
+                    prev = Lj;
+                }
+                sidx[slot] = make_uint4(g[0], g[1], g[2], g[3]);
+            }
             __syncwarp();
+            unstage<8>(body + tl.idx_off + 4 * j0, sidx, 4 * len);
         }
+        if (via_walker) {
+            __syncwarp();
+            k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
+        } else {
+            unstage<1>(body + tl.val_off + 2 * j0, sval, 2 * len);
+        }
+        __syncwarp();
+        cur = nx;
+        b ^= 1;
     }
+    cp_async_wait<0>();
 }
 
 // =============================================================================================
@@ -913,7 +999,10 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
         occ_emit = std::max(occ_emit, 1);
     }
     if (repr == PULSE_COO_DOWNSCALED || validate_args)
+        {
         k2_scan_escapes<<<unsigned(sm_count() * occ_scan), kThreads, kWarps * kScanWarpSmem, s>>>(em, repr, p.range_cnt, p.t_resc, p.t_cesc, p.err);
+        PULSE_LAUNCHED("k2_scan_escapes", s);
+        }
     LayoutArgs a;
     a.range_cnt = p.range_cnt;
     a.range_pre = p.range_pre;
@@ -933,21 +1022,23 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
     a.err = p.err;
     a.cap = cap;
     k2_layout<<<1, kLayoutThreads, 0, s>>>(a);
+    PULSE_LAUNCHED("k2_layout", s);
     k2_emit<<<unsigned(sm_count() * occ_emit), kThreads, kWarps * kEmitWarpSmem, s>>>(em, repr, p.tlay, p.range_pre, vals,
                                                                              result, body);
+    PULSE_LAUNCHED("k2_emit", s);
 }
 
 void launch_encode_emit(const PlanDev& p, uint32_t repr, const pulse_scan_summary* gathered, uint32_t n_ranks,
                         uint32_t rank, uint8_t* body, uint64_t body_cap, pulse_patch_entry* entries,
                         pulse_result* result, cudaStream_t s) {
-    EntryMap em{p.segs, p.seg_first, p.seg_start, p.n_segs, p.idx32, nullptr, p.coldiv, p.numel, p.tlay};
+    EntryMap em{p.segs, p.seg_first, p.seg_start, p.n_segs, p.idx32, nullptr, p.coldiv, p.numel, p.tlay, p.cap};
     emit_common(p, em, repr, false, gathered, n_ranks, rank, p.val16, body, body_cap, entries, result, p.cap, s);
 }
 
 void launch_encode_emit_idx64(const PlanDev& p, uint32_t repr, const int64_t* idx64, const uint16_t* vals,
                               uint8_t* body, uint64_t body_cap, pulse_patch_entry* entries, pulse_result* result,
                               cudaStream_t s) {
-    EntryMap em{p.id_segs, p.id_first, p.id_start, p.n_tensors, nullptr, idx64, p.coldiv, p.numel, p.tlay};
+    EntryMap em{p.id_segs, p.id_first, p.id_start, p.n_tensors, nullptr, idx64, p.coldiv, p.numel, p.tlay, ~0ull};
     emit_common(p, em, repr, true, nullptr, 1, 0, vals, body, body_cap, entries, result, ~0ull, s);
 }
 

@@ -156,6 +156,10 @@ void launch_encode_emit_idx64(const PlanDev& p, uint32_t repr, const int64_t* id
                               pulse_result* result, cudaStream_t s);
 
 int sm_count();
+// PULSE_DEBUG_SYNC=1: synchronise after every launch and report the first
+// failing kernel by name on stderr (debugging aid; off by default).
+void debug_sync(const char* kernel, cudaStream_t s);
+#define PULSE_LAUNCHED(name, stream) ::pulse::dev::debug_sync(name, stream)
 // helpers.cu (host-buffer API support)
 void launch_export_indices(const PlanDev& p, int64_t* out, cudaStream_t s);
 void launch_delta_encode(const int64_t* in, uint64_t n, int64_t* out, uint64_t* err, cudaStream_t s);

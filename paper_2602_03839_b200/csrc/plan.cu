@@ -168,7 +168,8 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
 #define A(ptr, n) if (e == cudaSuccess) e = dalloc(o, &(ptr), (n))
     A(segs_d, S); A(first_d, T + 1); A(numel_d, T); A(cols_d, T); A(tile_seg_d, tiles); A(ticket_seg_d, tickets);
     for (int s = 0; s < PULSE_MAX_SLOTS; ++s) { uint16_t** sp = nullptr; A(sp, T); p.slot[s] = sp; }
-    A(p.idx32, cap); A(p.val16, cap); A(p.seg_start, S + 1); A(p.k1_status, tiles + 1);
+    // idx32 / val16: +8 entries so 16-byte async copies of a partial last chunk stay in bounds
+    A(p.idx32, cap + 8); A(p.val16, cap + 8); A(p.seg_start, S + 1); A(p.k1_status, tiles + 1);
     A(p.counters, 8); A(p.scan, 1);
     ColDiv* coldiv_d = nullptr; A(coldiv_d, T);
     A(p.range_cnt, cap / 4096 + 2); A(p.range_pre, cap / 4096 + 2);

@@ -19,8 +19,36 @@ __device__ __forceinline__ uint32_t swz(uint32_t q) {
     return V == 1 ? q : (q ^ ((q >> 3) & (V - 1)));
 }
 
-__device__ __forceinline__ uint32_t shr_pair(uint32_t lo, uint32_t hi, uint32_t sh) {
-    return __funnelshift_r(lo, hi, sh);
+
+// 16-byte shared-memory load kept as ONE vector access (a compiler-split load
+// would turn the conflict-free swizzled pattern into 4-way bank conflicts).
+__device__ __forceinline__ uint4 lds128(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(smem_u32(p))
+                 : "memory");
+    return r;
+}
+
+// 16 bytes starting at byte (4*sw + sh/8) of the 32-byte pair (lo, hi).
+__device__ __forceinline__ uint4 funnel16(const uint4& lo, const uint4& hi, uint32_t sw, uint32_t sh) {
+    const uint32_t W[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    switch (sw) {
+        case 0: return make_uint4(__funnelshift_r(W[0], W[1], sh), __funnelshift_r(W[1], W[2], sh), __funnelshift_r(W[2], W[3], sh), __funnelshift_r(W[3], W[4], sh));
+        case 1: return make_uint4(__funnelshift_r(W[1], W[2], sh), __funnelshift_r(W[2], W[3], sh), __funnelshift_r(W[3], W[4], sh), __funnelshift_r(W[4], W[5], sh));
+        case 2: return make_uint4(__funnelshift_r(W[2], W[3], sh), __funnelshift_r(W[3], W[4], sh), __funnelshift_r(W[4], W[5], sh), __funnelshift_r(W[5], W[6], sh));
+        default: return make_uint4(__funnelshift_r(W[3], W[4], sh), __funnelshift_r(W[4], W[5], sh), __funnelshift_r(W[5], W[6], sh), __funnelshift_r(W[6], W[7], sh));
+    }
+}
+
+__device__ __forceinline__ uint4 shfl_up4(const uint4& v, int d) {
+    return make_uint4(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d),
+                      __shfl_up_sync(0xffffffffu, v.z, d), __shfl_up_sync(0xffffffffu, v.w, d));
+}
+__device__ __forceinline__ uint4 shfl4(const uint4& v, int src) {
+    return make_uint4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                      __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
 }
 
 // Copies bytes [g, g+len) (len <= 512 * R) into shared vectors dst[swz(q)],
@@ -62,14 +90,7 @@ __device__ __forceinline__ void stage_piece(uint4* dst, const uint8_t* g, uint32
         const uint32_t w0 = __shfl_sync(0xffffffffu, n0.x, 0), w1 = __shfl_sync(0xffffffffu, n0.y, 0);
         const uint32_t w2 = __shfl_sync(0xffffffffu, n0.z, 0), w3 = __shfl_sync(0xffffffffu, n0.w, 0);
         if (lane == 31) nx = make_uint4(w0, w1, w2, w3);
-        const uint32_t W[8] = {v[r].x, v[r].y, v[r].z, v[r].w, nx.x, nx.y, nx.z, nx.w};
-        uint4 o;
-        switch (sw) {
-            case 0: o = make_uint4(shr_pair(W[0], W[1], sh), shr_pair(W[1], W[2], sh), shr_pair(W[2], W[3], sh), shr_pair(W[3], W[4], sh)); break;
-            case 1: o = make_uint4(shr_pair(W[1], W[2], sh), shr_pair(W[2], W[3], sh), shr_pair(W[3], W[4], sh), shr_pair(W[4], W[5], sh)); break;
-            case 2: o = make_uint4(shr_pair(W[2], W[3], sh), shr_pair(W[3], W[4], sh), shr_pair(W[4], W[5], sh), shr_pair(W[5], W[6], sh)); break;
-            default: o = make_uint4(shr_pair(W[3], W[4], sh), shr_pair(W[4], W[5], sh), shr_pair(W[5], W[6], sh), shr_pair(W[6], W[7], sh)); break;
-        }
+        const uint4 o = funnel16(v[r], nx, sw, sh);
         const uint32_t q = lane + 32 * r;
         if (q < nv_out) dst[swz<V>(q_base + q)] = o;
     }
@@ -83,55 +104,70 @@ __device__ __forceinline__ void stage(uint4* dst, const uint8_t* g, uint32_t len
         stage_piece<4, V>(dst, g + off, min(2048u, len - off), off >> 4);
 }
 
-// Reads lane-consecutive vector i (of V) of a swizzled buffer.
+// ---- asynchronous global -> shared copies (cp.async, no register staging) ------------------
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Queues the 16-byte slots covering [g, g+len) (g 16-byte aligned) into the
+// swizzled buffer dst; reads up to 15 bytes past len (callers pad the source).
 template <int V>
-__device__ __forceinline__ uint4 lane_vec(const uint4* buf, int i) {
+__device__ __forceinline__ void stage_async(uint4* dst, const uint8_t* g, uint32_t len) {
     const int lane = threadIdx.x & 31;
-    return buf[swz<V>(uint32_t(lane * V + i))];
+    const uint32_t nslots = (len + 15) >> 4;
+    for (uint32_t q = lane; q < nslots; q += 32) cp_async16(dst + swz<V>(q), g + 16 * q);
 }
 
-// 32-bit word `w` of a swizzled buffer.
+// 32-bit word `w` of a swizzled buffer (single scalar accesses only).
 template <int V>
 __device__ __forceinline__ uint32_t smem_word(const uint4* buf, uint32_t w) {
     return reinterpret_cast<const uint32_t*>(buf)[swz<V>(w >> 2) * 4 + (w & 3)];
 }
 
+// Reads lane-consecutive vector i (of V) of a swizzled buffer.
+template <int V>
+__device__ __forceinline__ uint4 lane_vec(const uint4* buf, int i) {
+    const int lane = threadIdx.x & 31;
+    return lds128(buf + swz<V>(uint32_t(lane * V + i)));
+}
+
+
 // Copies `len` bytes, packed from byte 0 of swizzled shared buffer `src`, to
-// global `dst` (any alignment): whole 16-byte blocks with one vector store
-// (funnel-shifted out of shared memory), the partial head/tail blocks bytewise.
-// Bytes of `dst` outside [dst, dst+len) are never written.
+// global `dst` (any alignment).  Lane k of a round writes aligned 16-byte block
+// k of the destination: with a byte offset s = dst & 15 that block holds the
+// tail of source slot k-1 and the head of slot k, so every lane loads ONE slot
+// (conflict-free) and takes its neighbour's by shuffle.  Whole blocks are one
+// vector store; the partial head/tail blocks are written bytewise, so bytes of
+// `dst` outside [dst, dst+len) are never touched.
 template <int V>
 __device__ __forceinline__ void unstage(uint8_t* dst, const uint4* src, uint32_t len) {
     if (len == 0) return;
     const int lane = threadIdx.x & 31;
-    const uintptr_t da = reinterpret_cast<uintptr_t>(dst);
-    const uint32_t s = uint32_t(da & 15);
+    const uint32_t s = uint32_t(reinterpret_cast<uintptr_t>(dst) & 15);
     uint8_t* base = dst - s;
-    const uint32_t nblk = (s + len + 15) >> 4;
-    const uint32_t sh = ((16 - s) & 3) * 8;  // byte shift of every block's source start
-    for (uint32_t k = lane; k < nblk; k += 32) {
+    const uint32_t nblk = (s + len + 15) >> 4, nslots = (len + 15) >> 4;
+    const uint32_t sb = (16 - s) & 15, sw = sb >> 2, sh = (sb & 3) * 8;
+    uint4 carry = make_uint4(0, 0, 0, 0);  // slot (round start - 1)
+    for (uint32_t k0 = 0; k0 < nblk; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const uint4 cur = k < nslots ? lds128(src + swz<V>(k)) : make_uint4(0, 0, 0, 0);
+        uint4 prv = shfl_up4(cur, 1);
+        if (lane == 0) prv = carry;
+        carry = shfl4(cur, 31);
+        if (k >= nblk) continue;
+        const uint4 out = s == 0 ? cur : funnel16(prv, cur, sw, sh);
         const int32_t o = int32_t(16 * k) - int32_t(s);  // source offset of the block's first byte
         if (o >= 0 && uint32_t(o) + 16 <= len) {
-            const uint32_t w0 = uint32_t(o) >> 2;
-            const uint32_t x0 = smem_word<V>(src, w0), x1 = smem_word<V>(src, w0 + 1);
-            const uint32_t x2 = smem_word<V>(src, w0 + 2), x3 = smem_word<V>(src, w0 + 3);
-            uint4 out;
-            if (sh == 0) {
-                out = make_uint4(x0, x1, x2, x3);
-            } else {
-                const uint32_t x4 = smem_word<V>(src, w0 + 4);
-                out = make_uint4(__funnelshift_r(x0, x1, sh), __funnelshift_r(x1, x2, sh), __funnelshift_r(x2, x3, sh),
-                                 __funnelshift_r(x3, x4, sh));
-            }
             *reinterpret_cast<uint4*>(base + 16 * k) = out;
         } else {
-#pragma unroll 1
+            const uint32_t w[4] = {out.x, out.y, out.z, out.w};
+#pragma unroll
             for (int b = 0; b < 16; ++b) {
                 const int32_t so = o + b;
-                if (so >= 0 && uint32_t(so) < len) {
-                    const uint32_t w = smem_word<V>(src, uint32_t(so) >> 2);
-                    base[16 * k + b] = uint8_t(w >> (8 * (so & 3)));
-                }
+                if (so >= 0 && uint32_t(so) < len) base[16 * k + b] = uint8_t(w[b >> 2] >> (8 * (b & 3)));
             }
         }
     }

@@ -137,6 +137,7 @@ pulse_status pulse_synth_base(uint16_t* dev_out, uint64_t n, uint64_t seed, doub
     const unsigned grid = unsigned(std::min<uint64_t>((n + 2047) / 2048, uint64_t(sm_count()) * 16));
     k_synth_base<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(dev_out, n, seed, float(std::log(median)),
                                                                       float(sigma));
+    PULSE_LAUNCHED("k_synth_base", static_cast<cudaStream_t>(stream));
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? PULSE_OK : pulse::cuda_fail(e, "synth_base");
 }
@@ -162,6 +163,7 @@ pulse_status pulse_synth_mutate(pulse_context* ctx, const uint16_t* dev_base, ui
         const uint64_t B = std::max<uint64_t>(1, (target - count) / cluster_width);
         const unsigned grid = unsigned((B + 255) / 256);
         k_synth_mark<<<grid, 256, 0, s>>>(bitmap, n, mseed, cluster_width, k, B, all, counter);
+        PULSE_LAUNCHED("k_synth_mark", s);
         k += B;
         unsigned long long c = 0;
         cudaMemcpyAsync(&c, counter, sizeof(c), cudaMemcpyDeviceToHost, s);
@@ -169,8 +171,10 @@ pulse_status pulse_synth_mutate(pulse_context* ctx, const uint16_t* dev_base, ui
         count = c;
     }
     if (count < target) k_synth_mark_exact<<<1, 1, 0, s>>>(bitmap, n, mseed, cluster_width, k, all, counter, target);
+    PULSE_LAUNCHED("k_synth_mark_exact", s);
     const unsigned grid = unsigned(std::min<uint64_t>((n + 2047) / 2048, uint64_t(sm_count()) * 16));
     k_synth_flip<<<grid, 256, 0, s>>>(dev_base, dev_out, bitmap, n);
+    PULSE_LAUNCHED("k_synth_flip", s);
     unsigned long long c = 0;
     cudaMemcpyAsync(&c, counter, sizeof(c), cudaMemcpyDeviceToHost, s);
     cudaFreeAsync(bitmap, s);
