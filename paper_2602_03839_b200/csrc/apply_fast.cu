@@ -12,9 +12,14 @@
 //                    (rows: restart at each tensor; columns: restart at each new
 //                    row, index_coding.hpp:141-153); flags escape markers.
 //   F2 f_range_scan  one CTA: exclusive scan of the range aggregates.
-//   F3 f_agg<1>      recompute every (row, col) / index and apply the reference
-//                    checks (zero gap, column range, index range) -- no writes.
-//   F4 f_agg<2>      only if nothing failed: recompute and W[flat] = value.
+//   F3 f_pass<apply> recompute every (row, col) / index, apply the reference
+//                    checks (zero gap, column range, index range) and, for each
+//                    entry that passes, save W[flat] to a backup and write the
+//                    value -- an entry that fails is never written.
+//   F4 f_pass<restore> only if some check failed anywhere: recompute and put the
+//                    backed-up values back, so a bad patch never half-applies
+//                    (the reference validates on a copy, patch.hpp:311).
+//   (decode-only callers -- int64 indices out -- run validate, then scatter.)
 //
 // Data movement.  A warp works on 1024-entry chunks.  It stages a chunk's row
 // bytes / column units / u32 gaps (and, for F4, its values) from the body into
@@ -48,12 +53,15 @@ constexpr uint32_t kPer = kChunk / 32;  // consecutive entries per lane
 constexpr uint64_t H = SegSumOp::kHead;
 
 enum Repr : int { kCoo = 0, kI32 = 1, kFlat = 2 };
-enum Pass : int { kAgg = 0, kValidate = 1, kScatter = 2 };
+enum Pass : int { kAgg = 0, kValidate = 1, kScatter = 2, kApply = 3, kRestore = 4 };
+__host__ __device__ constexpr bool checks(int pass) { return pass == kValidate || pass == kApply || pass == kRestore; }
+__host__ __device__ constexpr bool reports(int pass) { return pass == kValidate || pass == kApply; }
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;  // decoded-index marker of an entry that failed a check
 
 // Per-warp staging area (bytes).  a: COO rows (1 KiB used) or u32 gaps (4 KiB);
 // b: COO column units; v: values; x: decoded tensor-local indices.
 constexpr uint32_t kABytes = kChunk * 4, kBBytes = kChunk * 2, kVBytes = kChunk * 2, kXBytes = kChunk * 4;
-__host__ __device__ constexpr uint32_t warp_smem(int pass) { return kABytes + kBBytes + (pass == kScatter ? kVBytes + kXBytes : 0); }
+__host__ __device__ constexpr uint32_t warp_smem(int pass) { return kABytes + kBBytes + (pass >= kScatter ? kVBytes + kXBytes : 0); }
 
 __device__ __forceinline__ uint32_t lanemask_le() {
     uint32_t m;
@@ -203,6 +211,7 @@ struct ApplyArgs {
     uint64_t* err;
     uint16_t* const* weights;
     int64_t* out_idx;
+    uint16_t* backup;  // [entries]: pre-apply value of every written element (kApply / kRestore)
 };
 
 // Walker path over entries [first, last) for one pass.  (ar, ac): aggregates
@@ -228,49 +237,62 @@ __device__ __noinline__ void slow_span(const ApplyArgs& A, uint64_t first, uint6
             }
             continue;
         }
-        constexpr bool kScat = kPass == kScatter;
+        // per entry: (valid, flat index); `valid` false once a check failed
+        bool ok = f.valid;
+        uint64_t flat = 0;
         if (coo) {
             const bool hr = f.valid && f.o == 0;
             const bool nr = f.valid && (f.o == 0 || f.a != 0);
             const uint64_t row = seg_round_scan(hr, f.a, ar);
             const uint64_t col = seg_round_scan(nr, f.b, ac);
-            if (!f.valid) continue;
-            if (!kScat) {
-                if (!nr && f.b == 0) { report(A.err, error_key(f.e, kStageCols, f.o, kZeroColGap)); continue; }
-                if (col >= f.cols) { report(A.err, error_key(f.e, kStageRange, f.o, kColRange)); continue; }
+            if (ok && checks(kPass)) {
+                uint64_t key = kNoError;
+                if (!nr && f.b == 0) key = error_key(f.e, kStageCols, f.o, kZeroColGap);
+                else if (col >= f.cols) key = error_key(f.e, kStageRange, f.o, kColRange);
+                else if (row * f.cols + col >= f.numel) key = error_key(f.e, kStageRange, f.o, kIdxRange);
+                if (key != kNoError) {
+                    ok = false;
+                    if (reports(kPass)) report(A.err, key);
+                }
             }
-            const uint64_t flat = row * f.cols + col;
-            if (!kScat) {
-                if (flat >= f.numel) report(A.err, error_key(f.e, kStageRange, f.o, kIdxRange));
-            } else if (A.out_idx) {
-                A.out_idx[i] = int64_t(flat);
-            } else {
-                A.weights[f.tensor][flat] = uint16_t(rd_u16(A.body + f.val_off + 2 * f.o));
-            }
+            flat = row * f.cols + col;
         } else if (kRepr == kI32) {
             const bool hr = f.valid && f.o == 0;
             const uint64_t idx = seg_round_scan(hr, f.a, ar);
-            if (!f.valid) continue;
-            if (!kScat) {
-                if (f.o > 0 && f.a == 0) { report(A.err, error_key(f.e, kStageRows, f.o, kZeroGap)); continue; }
-                if (idx >= f.numel) report(A.err, error_key(f.e, kStageRows, f.o, kIdxRange));
-            } else if (A.out_idx) {
-                A.out_idx[i] = int64_t(idx);
-            } else {
-                A.weights[f.tensor][idx] = uint16_t(rd_u16(A.body + f.val_off + 2 * f.o));
+            if (ok && checks(kPass)) {
+                uint64_t key = kNoError;
+                if (f.o > 0 && f.a == 0) key = error_key(f.e, kStageRows, f.o, kZeroGap);
+                else if (idx >= f.numel) key = error_key(f.e, kStageRows, f.o, kIdxRange);
+                if (key != kNoError) {
+                    ok = false;
+                    if (reports(kPass)) report(A.err, key);
+                }
             }
+            flat = idx;
         } else {  // FLAT_INT32: one running global sum (patch.hpp:219-237)
             const uint64_t S = seg_round_scan(false, f.a, ar);
-            if (!f.valid) continue;
             const int64_t local = int64_t(S) - int64_t(gap_base) - int64_t(f.flat_base);
-            if (!kScat) {
-                if (f.a == 0 && (i > 0 || has_prev)) { report(A.err, error_key(f.e, kStageRows, f.o, kZeroGap)); continue; }
-                if (local < 0 || uint64_t(local) >= f.numel) report(A.err, error_key(f.e, kStageRows, f.o, kIdxRange));
-            } else if (A.out_idx) {
-                A.out_idx[i] = local;
-            } else {
-                A.weights[f.tensor][local] = uint16_t(rd_u16(A.body + f.val_off + 2 * f.o));
+            if (ok && checks(kPass)) {
+                uint64_t key = kNoError;
+                if (f.a == 0 && (i > 0 || has_prev)) key = error_key(f.e, kStageRows, f.o, kZeroGap);
+                else if (local < 0 || uint64_t(local) >= f.numel) key = error_key(f.e, kStageRows, f.o, kIdxRange);
+                if (key != kNoError) {
+                    ok = false;
+                    if (reports(kPass)) report(A.err, key);
+                }
             }
+            flat = uint64_t(local);
+        }
+        if (!ok || kPass == kValidate) continue;
+        if (kPass == kScatter) {
+            if (A.out_idx) A.out_idx[i] = int64_t(flat);
+            else A.weights[f.tensor][flat] = uint16_t(rd_u16(A.body + f.val_off + 2 * f.o));
+        } else if (kPass == kApply) {
+            uint16_t* w = A.weights[f.tensor] + flat;
+            A.backup[i] = *w;
+            *w = uint16_t(rd_u16(A.body + f.val_off + 2 * f.o));
+        } else if (kPass == kRestore) {
+            A.weights[f.tensor][flat] = A.backup[i];
         }
     }
 }
@@ -286,8 +308,8 @@ f_pass(ApplyArgs A) {
     extern __shared__ __align__(16) uint8_t smem[];
     if (fast_blocked(A.flags)) return;
     if (kPass == kScatter && *(volatile const uint64_t*)A.err != kNoError) return;
+    if (kPass == kRestore && *(volatile const uint64_t*)A.err == kNoError) return;  // nothing failed: keep
     constexpr bool coo = kRepr == kCoo;
-    constexpr int VA = coo ? 2 : 8;  // vectors per lane of the a buffer
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint8_t* ws = smem + warp * warp_smem(kPass);
     uint4* sa = reinterpret_cast<uint4*>(ws);
@@ -328,7 +350,8 @@ f_pass(ApplyArgs A) {
             } else {
                 stage<8>(sa, A.body + L.idx_off + 4 * o0, 4 * len);
             }
-            if (kPass == kScatter && !A.out_idx) stage<1>(reinterpret_cast<uint4*>(sv), A.body + L.val_off + 2 * o0, 2 * len);
+            if ((kPass == kScatter && !A.out_idx) || kPass == kApply)
+                stage<1>(reinterpret_cast<uint4*>(sv), A.body + L.val_off + 2 * o0, 2 * len);
             __syncwarp();
             // ---- this lane's kPer consecutive entries, straight from shared memory ----
             const int nv = max(0, min(int(kPer), int(len) - lane * int(kPer)));
@@ -357,7 +380,7 @@ f_pass(ApplyArgs A) {
 #define PULSE_AV(j) (coo ? (aw[(j) >> 2] >> (8 * ((j) & 3))) & 0xFFu : aw[(j) % kAW])
 #define PULSE_BV(j) (coo ? (bw[((j) >> 1) % kBW] >> (16 * ((j) & 1))) & 0xFFFFu : 0u)
             const uint64_t ol = o0 + uint64_t(lane) * kPer;
-            const uint64_t nrows = coo && kPass == kValidate ? L.numel / L.cols : 0;  // ordinal of this lane's first entry
+            const uint64_t nrows = coo ? L.numel / L.cols : 0;
             // lane aggregates
             uint64_t lr = 0, lc = 0;
             bool lmark = false;
@@ -394,58 +417,87 @@ f_pass(ApplyArgs A) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const int j = 4 * i + c;
-                    xv[c] = 0;
+                    xv[c] = kInvalid;
                     if (j >= nv) continue;
                     const uint32_t a = PULSE_AV(j), b = PULSE_BV(j);
                     const uint64_t o = ol + j;
+                    uint64_t key = kNoError;
                     if (coo) {
                         const bool nr = o == 0 || a != 0;
                         row = o == 0 ? a : row + a;
                         col = nr ? b : col + b;
-                        if (kPass == kValidate) {
+                        if (checks(kPass)) {
                             // patch.hpp:247-254; with col < cols, flat >= numel <=> row >= numel / cols
-                            if (!nr && b == 0) { report_cold(A.err, error_key(e, kStageCols, o, kZeroColGap)); continue; }
-                            if (col >= L.cols) { report_cold(A.err, error_key(e, kStageRange, o, kColRange)); continue; }
-                            if (row >= nrows) report_cold(A.err, error_key(e, kStageRange, o, kIdxRange));
+                            if (!nr && b == 0) key = error_key(e, kStageCols, o, kZeroColGap);
+                            else if (col >= L.cols) key = error_key(e, kStageRange, o, kColRange);
+                            else if (row >= nrows) key = error_key(e, kStageRange, o, kIdxRange);
                         }
-                        if (kPass == kScatter) xv[c] = uint32_t(row) * uint32_t(L.cols) + uint32_t(col);
+                        if (key == kNoError) xv[c] = uint32_t(row) * uint32_t(L.cols) + uint32_t(col);
                     } else if (kRepr == kI32) {
                         row = o == 0 ? a : row + a;
-                        if (kPass == kValidate) {
-                            if (o > 0 && a == 0) { report_cold(A.err, error_key(e, kStageRows, o, kZeroGap)); continue; }
-                            if (row >= L.numel) report_cold(A.err, error_key(e, kStageRows, o, kIdxRange));
+                        if (checks(kPass)) {
+                            if (o > 0 && a == 0) key = error_key(e, kStageRows, o, kZeroGap);
+                            else if (row >= L.numel) key = error_key(e, kStageRows, o, kIdxRange);
                         }
-                        xv[c] = uint32_t(row);
+                        if (key == kNoError) xv[c] = uint32_t(row);
                     } else {
                         row += a;
                         const int64_t local = int64_t(row) - int64_t(gap_base) - int64_t(L.flat_base);
-                        if (kPass == kValidate) {
+                        if (checks(kPass)) {
                             const uint64_t gi = c0 + uint64_t(lane) * kPer + j;
-                            if (a == 0 && (gi > 0 || has_prev)) { report_cold(A.err, error_key(e, kStageRows, o, kZeroGap)); continue; }
-                            if (local < 0 || uint64_t(local) >= L.numel) report_cold(A.err, error_key(e, kStageRows, o, kIdxRange));
+                            if (a == 0 && (gi > 0 || has_prev)) key = error_key(e, kStageRows, o, kZeroGap);
+                            else if (local < 0 || uint64_t(local) >= L.numel) key = error_key(e, kStageRows, o, kIdxRange);
                         }
-                        xv[c] = uint32_t(local);
+                        if (key == kNoError) xv[c] = uint32_t(local);
                     }
+                    if (reports(kPass) && key != kNoError) report_cold(A.err, key);
                 }
-                if (kPass == kScatter) sx[swz<8>(uint32_t(lane * 8 + i))] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
+                if (kPass >= kScatter) sx[swz<8>(uint32_t(lane * 8 + i))] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
             }
 #undef PULSE_AV
 #undef PULSE_BV
-            if (kPass != kScatter) continue;
-            // ---- indices are in shared memory in entry order: coalesced scatter ----
+            if (kPass < kScatter) continue;
+            // ---- indices are in shared memory in entry order: coalesced writes ----
             __syncwarp();
             const uint32_t* xs = reinterpret_cast<const uint32_t*>(sx);
-            if (A.out_idx) {
+            if (kPass == kScatter && A.out_idx) {
                 for (uint32_t k = lane; k < len; k += 32) {
                     const uint32_t q = k >> 2;
                     A.out_idx[c0 + k] = int64_t(xs[swz<8>(q) * 4 + (k & 3)]);
                 }
-            } else {
+            } else if (kPass == kScatter) {
                 uint16_t* W = A.weights[L.tensor];
 #pragma unroll 4
                 for (uint32_t k = lane; k < len; k += 32) {
                     const uint32_t q = k >> 2;
                     W[xs[swz<8>(q) * 4 + (k & 3)]] = sv[k];
+                }
+            } else if (kPass == kApply) {
+                // all of this lane's backup reads in flight at once, then the writes
+                uint16_t* W = A.weights[L.tensor];
+                uint16_t* bk = A.backup + c0;
+                uint32_t xk[kPer];
+                uint16_t old[kPer];
+#pragma unroll
+                for (int t = 0; t < int(kPer); ++t) {
+                    const uint32_t k = uint32_t(lane) + 32u * t;
+                    xk[t] = k < len ? xs[swz<8>(k >> 2) * 4 + (k & 3)] : kInvalid;
+                    old[t] = xk[t] != kInvalid ? W[xk[t]] : uint16_t(0);
+                }
+#pragma unroll
+                for (int t = 0; t < int(kPer); ++t) {
+                    const uint32_t k = uint32_t(lane) + 32u * t;
+                    if (xk[t] != kInvalid) {
+                        bk[k] = old[t];
+                        W[xk[t]] = sv[k];
+                    }
+                }
+            } else {  // kRestore
+                uint16_t* W = A.weights[L.tensor];
+                const uint16_t* bk = A.backup + c0;
+                for (uint32_t k = lane; k < len; k += 32) {
+                    const uint32_t x = xs[swz<8>(k >> 2) * 4 + (k & 3)];
+                    if (x != kInvalid) W[x] = bk[k];
                 }
             }
             __syncwarp();
@@ -549,8 +601,13 @@ void launch_all(const ApplyArgs& a, bool scatter, cudaStream_t s) {
     launch_pass<kRepr, kAgg>(a, s);
     f_range_scan<<<1, kScanThreads, 0, s>>>(a.totals, a.agg, a.flags);
     PULSE_LAUNCHED("f_range_scan", s);
-    launch_pass<kRepr, kValidate>(a, s);
-    if (scatter) launch_pass<kRepr, kScatter>(a, s);
+    if (a.weights) {  // in place: checked writes with backup, restore if anything failed
+        launch_pass<kRepr, kApply>(a, s);
+        launch_pass<kRepr, kRestore>(a, s);
+    } else {          // indices only: validate, then write them
+        launch_pass<kRepr, kValidate>(a, s);
+        if (scatter) launch_pass<kRepr, kScatter>(a, s);
+    }
 }
 }  // namespace
 
@@ -569,6 +626,8 @@ void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uin
     a.err = p.err;
     a.weights = weights_slot >= 0 ? p.slot[weights_slot] : nullptr;
     a.out_idx = out_indices;
+    a.backup = reinterpret_cast<uint16_t*>(p.rowgap);  // general-decoder scratch, idle on this path
+    if (out_indices) a.weights = nullptr;
     const bool scatter = weights_slot >= 0 || out_indices;
     if (repr == PULSE_COO_DOWNSCALED) launch_all<kCoo>(a, scatter, s);
     else if (repr == PULSE_COO_INT32) launch_all<kI32>(a, scatter, s);

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kLT, 1)
 d_layout(const pulse_patch_entry* __restrict__ entries, uint32_t n_e, const uint64_t* __restrict__ numel,
          const uint64_t* __restrict__ cols, uint32_t repr, EntryLayout* __restrict__ el,
          uint64_t* __restrict__ es, uint64_t* __restrict__ ck, uint64_t* __restrict__ totals,
-         uint64_t* __restrict__ err, uint32_t* __restrict__ flags) {
+         uint64_t* __restrict__ err, uint32_t* __restrict__ flags, uint64_t cap) {
     __shared__ uint64_t s_tmp[32];
     uint64_t base_e = 0, base_c = 0, base_f = 0;
     for (uint32_t e0 = 0; e0 < n_e; e0 += kLT) {
@@ -152,6 +152,12 @@ d_layout(const pulse_patch_entry* __restrict__ entries, uint32_t n_e, const uint
         ck[n_e] = base_c;
         totals[kTotEntries] = base_e;
         totals[kTotRowChunks] = base_c;
+        if (base_e > cap) {  // more entries than the plan's scratch holds: decode nothing
+            report(err, error_key(0, kStageTensor, 0, kCapacity));
+            totals[kTotEntries] = 0;
+            totals[kTotRowChunks] = 0;
+            atomicExch(flags, 1u);
+        }
     }
 }
 
@@ -545,7 +551,7 @@ static void decode_prologue(const PlanDev& p, const pulse_patch_entry* entries, 
     cudaMemsetAsync(p.d_flags, 0, 4 * sizeof(uint32_t), s);
     cudaMemsetAsync(p.err, 0xFF, sizeof(uint64_t), s);
     d_layout<<<1, kLT, 0, s>>>(entries, n_entries, p.numel, p.cols, repr, p.elay, p.d_es, p.d_ck,
-                              p.d_totals, p.err, p.d_flags);
+                              p.d_totals, p.err, p.d_flags, p.cap);
     PULSE_LAUNCHED("d_layout", s);
 }
 

@@ -623,26 +623,44 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                 }
             }
         } else {
-            // dense ticket (staging overflowed): re-stream it from global memory
+            // dense ticket (more changes than the staging buffer holds): the look-back
+            // group re-streams it from global memory (L2-resident, TMA just read it):
+            // 16 elements per thread per round as two 16-byte loads of each snapshot,
+            // the next round prefetched in registers, one group scan per round.
             const SegDesc sd = k.segs[ti.si];
             const uint16_t* pp = k.prev_ptrs[sd.tensor] + sd.elem_off + ti.toff;
             const uint16_t* cp = k.curr_ptrs[sd.tensor] + sd.elem_off + ti.toff;
             const uint32_t nin = min(kTicketElems, sd.numel - ti.toff);
-            if (lt == 0) S.lb_run = 0;
-            named_sync(kBarLb, kLbThreads);
-            for (uint32_t e0 = 0; e0 < nin; e0 += kLbThreads * 8) {
-                const uint32_t e = e0 + lt * 8;
-                uint32_t mm = 0;
-                uint16_t vals[8];
-#pragma unroll
-                for (uint32_t q = 0; q < 8; ++q) {
-                    vals[q] = 0;
-                    if (e + q < nin) {
-                        vals[q] = cp[e + q];
-                        if (vals[q] != pp[e + q]) mm |= 1u << q;
+            constexpr uint32_t kPer = 16, kRound = kLbThreads * kPer;  // 2048 elements per round
+            auto load16 = [&](uint32_t e, uint4 (&a)[2], uint4 (&c)[2]) {
+                if (e + kPer <= nin) {  // ticket bases are 16-byte aligned (tensor base, 2^31 and 2^16 offsets)
+                    a[0] = ld_stream(pp + e);
+                    a[1] = ld_stream(pp + e + 8);
+                    c[0] = ld_stream(cp + e);
+                    c[1] = ld_stream(cp + e + 8);
+                } else {
+                    uint32_t ta[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    for (uint32_t q = 0; q < kPer && e + q < nin; ++q) {
+                        ta[q >> 1] |= uint32_t(pp[e + q]) << ((q & 1) * 16);
+                        tc[q >> 1] |= uint32_t(cp[e + q]) << ((q & 1) * 16);
                     }
+                    a[0] = make_uint4(ta[0], ta[1], ta[2], ta[3]);
+                    a[1] = make_uint4(ta[4], ta[5], ta[6], ta[7]);
+                    c[0] = make_uint4(tc[0], tc[1], tc[2], tc[3]);
+                    c[1] = make_uint4(tc[4], tc[5], tc[6], tc[7]);
                 }
-                uint32_t inc = __popc(mm);
+            };
+            uint4 na[2], nc[2];
+            if (uint32_t(lt) * kPer < nin) load16(uint32_t(lt) * kPer, na, nc);
+            uint64_t run = 0;
+            for (uint32_t e0 = 0; e0 < nin; e0 += kRound) {
+                const uint32_t e = e0 + uint32_t(lt) * kPer;
+                uint4 av[2] = {na[0], na[1]}, cv2[2] = {nc[0], nc[1]};
+                const bool mine = e < nin;
+                if (e0 + kRound < nin && e + kRound < nin) load16(e + kRound, na, nc);
+                const uint32_t mm = mine ? (change_mask(av[0], cv2[0]) | (change_mask(av[1], cv2[1]) << 8)) : 0u;
+                const uint32_t cnt = __popc(mm);
+                uint32_t inc = cnt;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
@@ -651,23 +669,25 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                 if (lane == 31) S.lb_warp_tot[warp - kLbFirst] = inc;
                 named_sync(kBarLb, kLbThreads);
                 uint32_t before = 0, all = 0;
+#pragma unroll
                 for (int w = 0; w < kLbWarps; ++w) {
-                    if (w < warp - kLbFirst) before += S.lb_warp_tot[w];
-                    all += S.lb_warp_tot[w];
+                    const uint32_t t = S.lb_warp_tot[w];
+                    if (w < warp - kLbFirst) before += t;
+                    all += t;
                 }
-                uint64_t pos = G + S.lb_run + before + inc - __popc(mm);
-                while (mm) {
-                    const int q = __ffs(mm) - 1;
-                    mm &= mm - 1;
+                uint64_t pos = G + run + before + inc - cnt;
+                uint32_t m2 = mm;
+                while (m2) {
+                    const int q = __ffs(m2) - 1;
+                    m2 &= m2 - 1;
                     if (pos < k.capacity) {
                         k.out_idx[pos] = ti.toff + e + q;
-                        k.out_val[pos] = vals[q];
+                        k.out_val[pos] = lane_value(q < 8 ? cv2[0] : cv2[1], q & 7);
                     }
                     ++pos;
                 }
-                named_sync(kBarLb, kLbThreads);
-                if (lt == 0) S.lb_run += all;
-                named_sync(kBarLb, kLbThreads);
+                run += all;
+                named_sync(kBarLb, kLbThreads);  // lb_warp_tot is rewritten next round
             }
         }
         named_sync(kBarLb, kLbThreads);  // flush done before the buffer is reused

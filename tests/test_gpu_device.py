@@ -167,3 +167,71 @@ def test_dense_ticket_slow_path():
         assert p.status == 0 and p.n_changes == n - 10000
         idx, _ = plan.decode_indices(p)
         assert np.array_equal(idx.cpu().numpy(), R.diff(a, b)[0])
+
+
+def _corrupt_last_entry(p, repr_, ts):
+    """Corrupt the final index entry of the last changed tensor in place while
+    keeping the fixed (escape-free) layout: a column past the row for
+    COO_DOWNSCALED, a gap far past the tensor for the int32 representations."""
+    e = p.host_entries[p.n_entries - 1]
+    body = p.body
+    off, cnt = int(e["idx_off"]), int(e["count"])
+    if repr_ == COO_DOWNSCALED:
+        pos = off + cnt + 2 * (cnt - 1)           # last column unit
+        body[pos] = 0xFE
+        body[pos + 1] = 0xFF                      # 0xFFFE: not a marker, > any column extent used here
+    else:
+        pos = off + 4 * (cnt - 1)                 # last u32 gap
+        body[pos:pos + 4] = torch.tensor([0xF0, 0xFF, 0xFF, 0x7F], dtype=torch.uint8, device=body.device)
+    return pos
+
+
+@pytest.mark.parametrize("repr_", [COO_DOWNSCALED, COO_INT32, FLAT_INT32])
+def test_corrupt_patch_never_half_applies(repr_):
+    """A late bad entry: apply reports the reference's error kind and the
+    weights are bit-identical to before (checked writes + restore)."""
+    D = _dev()
+    R = restatement()
+    rng = np.random.default_rng(11)
+    sizes = [(300 * 1000, 1000), (70000, 700), (4096 * 64, 4096)]
+    prevs = [rng.integers(0, 65536, n, dtype=np.uint16) for n, _ in sizes]
+    currs = []
+    for a in prevs:
+        b = a.copy()
+        b[rng.random(a.size) < 0.02] ^= 1
+        currs.append(b)
+    plan = D.DevicePlan(sizes, sum(n for n, _ in sizes))
+    plan.bind(0, [torch.from_numpy(a.view(np.int16)).cuda() for a in prevs])
+    plan.bind(1, [torch.from_numpy(b.view(np.int16)).cuda() for b in currs])
+    w = [torch.from_numpy(a.view(np.int16)).cuda() for a in prevs]
+    plan.bind(2, w)
+    p = plan.encode(1, 0, repr_)
+    assert p.status == 0
+    _corrupt_last_entry(p, repr_, sizes)
+    res = D.parse_result(plan.apply(2, p))
+    assert int(res["status"]) in (7, 11), res          # CorruptStreamError (reference kind for these)
+    assert int(res["status"]) == 7
+    for a, t in zip(prevs, w):
+        assert np.array_equal(t.cpu().numpy().view(np.uint16), a)   # nothing half-applied
+    # and a clean patch still applies after the failed one
+    p2 = plan.encode(1, 0, repr_)
+    assert int(D.parse_result(plan.apply(2, p2))["status"]) == 0
+    for b, t in zip(currs, w):
+        assert np.array_equal(t.cpu().numpy().view(np.uint16), b)
+
+
+def test_apply_rejects_more_entries_than_capacity():
+    D = _dev()
+    n = 50000
+    a = np.arange(n, dtype=np.uint16)
+    b = a ^ 1
+    big = D.DevicePlan([(n, 100)], n)
+    big.bind(0, [torch.from_numpy(a.view(np.int16)).cuda()])
+    big.bind(1, [torch.from_numpy(b.view(np.int16)).cuda()])
+    p = big.encode(1, 0, COO_DOWNSCALED)
+    small = D.DevicePlan([(n, 100)], 1000)
+    w = torch.from_numpy(a.view(np.int16)).cuda()
+    small.bind(2, [w])
+    res = D.parse_result(small.apply(2, p))
+    assert int(res["status"]) == 15
+    assert np.array_equal(w.cpu().numpy().view(np.uint16), a)
