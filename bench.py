@@ -261,6 +261,8 @@ def run_pulse(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"  # keep rank 0's stdout to the one JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
@@ -293,6 +295,8 @@ def run_pulse(args):
     state = {"body": 0, "changes": 0}
 
     def step(k, record=False):
+        """scan -> (all-gather summaries, K2, size exchange, FLAT carry) -> apply:
+        entirely stream-ordered on the device, no host round trip."""
         cs, ps = (1, 0) if k % 2 == 0 else (0, 1)
         if record:
             e0 = torch.cuda.Event(enable_timing=True)
@@ -301,20 +305,26 @@ def run_pulse(args):
         if record:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record(stream)
-        # K1 summaries all-gathered (NCCL), K2, entry table to host, size exchange (NCCL)
-        sec = sp.encode_after_scan(patch)
+        sp.emit_async(patch)
         if record:
             a0 = torch.cuda.Event(enable_timing=True)
             a0.record(stream)
-        sp.apply(2, sec)
+        sp.apply_async(2, patch)
         if record:
             a1 = torch.cuda.Event(enable_timing=True)
             a1.record(stream)
             ev["s0"].append(e0); ev["s1"].append(e1); ev["a0"].append(a0); ev["a1"].append(a1)
-        state["body"] = patch.body_bytes
-        state["changes"] = patch.n_changes
+
+    def check_step():
+        """Host check of the last step's encode and apply results (outside timing)."""
+        patch.fetch()
         if patch.status != 0:
             patch.raise_for_status([n for n, _ in mine])
+        res = D.parse_result(sp.apply_res)
+        if int(res["status"]) != 0:
+            raise RuntimeError(f"apply failed: {res}")
+        state["body"] = patch.body_bytes
+        state["changes"] = patch.n_changes
 
     def barrier():
         torch.cuda.synchronize()
@@ -324,9 +334,11 @@ def run_pulse(args):
 
     for k in range(args.warmup):
         step(k)
+        check_step()
     # W must equal prev again before the timed loop starts on an even step
     if args.warmup % 2 == 1:
         step(args.warmup)
+        check_step()
     barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
@@ -337,6 +349,7 @@ def run_pulse(args):
         t1.record(stream)
         torch.cuda.synchronize()
     barrier()
+    check_step()
     ms = t0.elapsed_time(t1) / args.steps
     scan_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["s0"], ev["s1"]))
     apply_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["a0"], ev["a1"]))
@@ -346,6 +359,7 @@ def run_pulse(args):
     ok = bool(torch.equal(w, prev if args.steps % 2 == 0 else curr))
     for k in (args.steps, args.steps + 1):
         step(k)
+        check_step()
         torch.cuda.synchronize()
         ok = ok and bool(torch.equal(w, curr if k % 2 == 0 else prev))
 
@@ -380,8 +394,13 @@ def run_pulse(args):
         # dominant kernel K1: reads both snapshots (4 B/elem) + writes 6 B per change (u32 idx + u16 value)
         k1_bytes = 4 * D_el + 6 * state["changes"]
         k1_gbs = k1_bytes / (scan_ms / 1e3) / 1e9
-        n_apply = 6  # d_layout, f_range_agg, f_range_scan, f_apply x2, d_finalize (general-path kernels exit early)
+        # our launches per step: K1 (k1_tma, k1_finalize); K2 (k2_scan_escapes [COO only], k2_layout,
+        # k2_emit); FLAT carry [sharded FLAT only]; apply (d_layout, f_pass agg, f_range_scan, f_pass apply,
+        # f_pass restore, d_clear_status, general-path kernels that exit at once on the fast path
+        # [COO: d_rows, d_col_layout, d_cols, d_assemble; int32: d_fixed], d_scatter, d_finalize)
         n_emit = 3 if args.repr == 0 else 2
+        n_carry = 1 if (world > 1 and args.repr == 2) else 0
+        n_apply = 12 if args.repr == 0 else 9
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True,
@@ -400,7 +419,7 @@ def run_pulse(args):
                          "traffic": profiled_traffic(args, world),
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": k1_bytes},
-            "gpu_launches": (2 + n_emit + n_apply) * args.steps,
+            "gpu_launches": (2 + n_emit + n_carry + n_apply) * args.steps,
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -191,6 +191,21 @@ pulse_status pulse_apply(pulse_plan* plan, uint32_t weights_slot, uint32_t repre
                          uint32_t n_entries, const pulse_flat_carry* dev_carry,
                          pulse_result* dev_result, void* stream);
 
+/* pulse_apply with the entry count taken from the encode's device result
+ * (`dev_patch_result`, as written by pulse_encode_emit) instead of the host:
+ * a sharded encode -> apply step then needs no host round trip.  If the
+ * encode failed (status != 0) nothing is applied and its error is reported
+ * in `dev_result`. */
+pulse_status pulse_apply_patch(pulse_plan* plan, uint32_t weights_slot, uint32_t representation,
+                               const uint8_t* dev_body, const pulse_patch_entry* dev_entries,
+                               const pulse_result* dev_patch_result, const pulse_flat_carry* dev_carry,
+                               pulse_result* dev_result, void* stream);
+
+/* Device-side FLAT_INT32 carry of shard `rank` from the all-gathered scan
+ * summaries of every rank (the nearest earlier rank that emitted an index). */
+pulse_status pulse_flat_carry_from_summaries(const pulse_scan_summary* dev_gathered, uint32_t rank,
+                                             pulse_flat_carry* dev_out, void* stream);
+
 /* Decode only: parse the payloads to flat int64 indices (dev_indices, in
  * entry order) without touching weights. */
 pulse_status pulse_decode_indices(pulse_plan* plan, uint32_t representation,

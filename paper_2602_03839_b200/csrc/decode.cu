@@ -94,12 +94,24 @@ __global__ void __launch_bounds__(kLT, 1)
 d_layout(const pulse_patch_entry* __restrict__ entries, uint32_t n_e, const uint64_t* __restrict__ numel,
          const uint64_t* __restrict__ cols, uint32_t repr, EntryLayout* __restrict__ el,
          uint64_t* __restrict__ es, uint64_t* __restrict__ ck, uint64_t* __restrict__ totals,
-         uint64_t* __restrict__ err, uint32_t* __restrict__ flags, uint64_t cap) {
+         uint64_t* __restrict__ err, uint32_t* __restrict__ flags, uint64_t cap,
+         const pulse_result* __restrict__ patch_result) {
     __shared__ uint64_t s_tmp[32];
+    // With `patch_result` (the encode's device result) the entry count comes from
+    // the device and a failed encode applies nothing: entries past the count are
+    // empty, and the encode's own first error becomes this call's error.
+    uint32_t n_live = n_e;
+    if (patch_result) {
+        const pulse_result pr = *patch_result;
+        n_live = pr.status != 0 ? 0u : min(pr.n_entries, n_e);
+        if (pr.status != 0 && threadIdx.x == 0)
+            report(err, error_key(uint32_t(pr.err_tensor), pr.err_stage, pr.err_elem,
+                                  pr.err_check ? pr.err_check : uint32_t(kCapacity)));
+    }
     uint64_t base_e = 0, base_c = 0, base_f = 0;
     for (uint32_t e0 = 0; e0 < n_e; e0 += kLT) {
         const uint32_t e = e0 + threadIdx.x;
-        const bool v = e < n_e;
+        const bool v = e < n_live;
         pulse_patch_entry pe{};
         if (v) pe = entries[e];
         const uint64_t ne = v ? numel[pe.tensor] : 0;
@@ -108,6 +120,14 @@ d_layout(const pulse_patch_entry* __restrict__ entries, uint32_t n_e, const uint
         const uint64_t xe = cta_excl_sum(v ? pe.count : 0, s_tmp, te);
         const uint64_t xc = cta_excl_sum(nchunks, s_tmp, tc);
         const uint64_t xf = cta_excl_sum(ne, s_tmp, tf);
+        if (!v && e < n_e) {  // empty entry (past the device-side count)
+            EntryLayout L{};
+            L.es = base_e + xe;
+            L.ck = base_c + xc;
+            el[e] = L;
+            es[e] = L.es;
+            ck[e] = L.ck;
+        }
         if (v) {
             EntryLayout L;
             L.tensor = pe.tensor;
@@ -546,12 +566,12 @@ __global__ void d_finalize(const uint64_t* __restrict__ totals, uint32_t n_e, co
 static unsigned persistent_grid() { return unsigned(sm_count() * 8); }
 
 static void decode_prologue(const PlanDev& p, const pulse_patch_entry* entries, uint32_t n_entries,
-                            uint32_t repr, cudaStream_t s) {
+                            uint32_t repr, cudaStream_t s, const pulse_result* patch_result = nullptr) {
     cudaMemsetAsync(p.d_totals, 0, 16 * sizeof(uint64_t), s);
     cudaMemsetAsync(p.d_flags, 0, 4 * sizeof(uint32_t), s);
     cudaMemsetAsync(p.err, 0xFF, sizeof(uint64_t), s);
     d_layout<<<1, kLT, 0, s>>>(entries, n_entries, p.numel, p.cols, repr, p.elay, p.d_es, p.d_ck,
-                              p.d_totals, p.err, p.d_flags, p.cap);
+                              p.d_totals, p.err, p.d_flags, p.cap, patch_result);
     PULSE_LAUNCHED("d_layout", s);
 }
 
@@ -565,8 +585,8 @@ __global__ void d_clear_status(uint64_t* __restrict__ st, uint64_t n, const uint
 void launch_decode(const PlanDev& p, uint32_t repr, const uint8_t* body,
                    const pulse_patch_entry* entries, uint32_t n_entries,
                    const pulse_flat_carry* carry, int weights_slot, int64_t* out_indices,
-                   pulse_result* result, cudaStream_t s) {
-    decode_prologue(p, entries, n_entries, repr, s);
+                   pulse_result* result, cudaStream_t s, const pulse_result* patch_result) {
+    decode_prologue(p, entries, n_entries, repr, s, patch_result);
     uint64_t* out = out_indices ? reinterpret_cast<uint64_t*>(out_indices) : p.flat;
     const unsigned g = persistent_grid();
     uint64_t* st0 = p.d_status;
@@ -623,6 +643,27 @@ void launch_apply_idx64(const PlanDev& p, const int64_t* idx64, const uint16_t* 
     }
     d_finalize<<<1, 32, 0, s>>>(p.d_totals, n_entries, p.err, result);
     PULSE_LAUNCHED("d_finalize", s);
+}
+
+// FLAT_INT32 carry of shard `rank` from all ranks' scan summaries (device side
+// of shard.flat_carry): the nearest earlier rank that emitted an index.
+__global__ void k_flat_carry(const pulse_scan_summary* __restrict__ gathered, uint32_t rank,
+                             pulse_flat_carry* __restrict__ out) {
+    if (threadIdx.x) return;
+    pulse_flat_carry c{0, 0};
+    for (int q = int(rank) - 1; q >= 0; --q) {
+        if (gathered[q].has_change) {
+            c.has_prev = 1;
+            c.gap_base = gathered[q].last_gap_base;
+            break;
+        }
+    }
+    *out = c;
+}
+
+void launch_flat_carry(const pulse_scan_summary* gathered, uint32_t rank, pulse_flat_carry* out, cudaStream_t s) {
+    k_flat_carry<<<1, 32, 0, s>>>(gathered, rank, out);
+    PULSE_LAUNCHED("k_flat_carry", s);
 }
 
 PULSE_DEFINE_WATCHDOG_SETTER(set_watchdog_decode)

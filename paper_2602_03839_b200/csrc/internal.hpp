@@ -139,7 +139,8 @@ void launch_encode_emit(const PlanDev& p, uint32_t repr, const pulse_scan_summar
 void launch_decode(const PlanDev& p, uint32_t repr, const uint8_t* body,
                    const pulse_patch_entry* entries, uint32_t n_entries,
                    const pulse_flat_carry* carry, int weights_slot, int64_t* out_indices,
-                   pulse_result* result, cudaStream_t s);
+                   pulse_result* result, cudaStream_t s, const pulse_result* patch_result = nullptr);
+void launch_flat_carry(const pulse_scan_summary* gathered, uint32_t rank, pulse_flat_carry* out, cudaStream_t s);
 // Validate caller-provided int64 indices (decode over an in-memory SparsePatch,
 // patch.hpp:325-336) and scatter values into `weights_slot`.
 void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uint32_t n_entries,

@@ -295,6 +295,27 @@ pulse_status pulse_apply(pulse_plan* plan, uint32_t weights_slot, uint32_t repr,
     return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "apply launch");
 }
 
+pulse_status pulse_apply_patch(pulse_plan* plan, uint32_t weights_slot, uint32_t repr, const uint8_t* dev_body,
+                               const pulse_patch_entry* dev_entries, const pulse_result* dev_patch_result,
+                               const pulse_flat_carry* dev_carry, pulse_result* dev_result, void* stream) {
+    if (!plan || repr > 2 || weights_slot >= PULSE_MAX_SLOTS || !plan->bound[weights_slot] || !dev_result ||
+        !dev_patch_result)
+        return fail(PULSE_E_ARGUMENT, "apply_patch: bad argument");
+    cudaSetDevice(plan->device);
+    launch_decode(plan->dev, repr, dev_body, dev_entries, plan->dev.n_tensors, dev_carry, int(weights_slot), nullptr,
+                  dev_result, static_cast<cudaStream_t>(stream), dev_patch_result);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "apply launch");
+}
+
+pulse_status pulse_flat_carry_from_summaries(const pulse_scan_summary* dev_gathered, uint32_t rank,
+                                             pulse_flat_carry* dev_out, void* stream) {
+    if (!dev_gathered || !dev_out) return fail(PULSE_E_ARGUMENT, "flat_carry: null argument");
+    launch_flat_carry(dev_gathered, rank, dev_out, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "flat_carry launch");
+}
+
 pulse_status pulse_decode_indices(pulse_plan* plan, uint32_t repr, const uint8_t* dev_body,
                                   const pulse_patch_entry* dev_entries, uint32_t n_entries,
                                   const pulse_flat_carry* dev_carry, int64_t* dev_indices,

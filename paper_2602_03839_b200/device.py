@@ -171,6 +171,16 @@ class DevicePlan:
                                   _ptr(patch.entries), n, _ptr(carry), _ptr(res), _stream_ptr(stream)))
         return res
 
+    def apply_patch(self, weights_slot: int, patch: DevicePatch, carry: torch.Tensor | None = None,
+                    result: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """apply() with the entry count read on the device from the patch's
+        encode result (no host round trip; a failed encode applies nothing)."""
+        res = result if result is not None else torch.zeros(72, dtype=torch.uint8, device=patch.body.device)
+        N.check(N.lib.pulse_apply_patch(self._plan, weights_slot, patch.representation, _ptr(patch.body),
+                                        _ptr(patch.entries), _ptr(patch.result), _ptr(carry), _ptr(res),
+                                        _stream_ptr(stream)))
+        return res
+
     def decode_indices(self, patch: DevicePatch, n_entries: int | None = None, carry: torch.Tensor | None = None,
                        stream=None):
         n = patch.n_entries if n_entries is None else n_entries
@@ -180,6 +190,12 @@ class DevicePlan:
         N.check(N.lib.pulse_decode_indices(self._plan, patch.representation, _ptr(patch.body), _ptr(patch.entries), n,
                                            _ptr(carry), _ptr(out), _ptr(res), _stream_ptr(stream)))
         return out[:total], res
+
+
+def flat_carry_from_summaries(gathered: torch.Tensor, rank: int, out: torch.Tensor, stream=None):
+    """Device-side FLAT carry (16-byte pulse_flat_carry in `out`) of shard `rank`."""
+    N.check(N.lib.pulse_flat_carry_from_summaries(_ptr(gathered), rank, _ptr(out), _stream_ptr(stream)))
+    return out
 
 
 def parse_result(res: torch.Tensor):

@@ -124,6 +124,11 @@ class ShardedPulse:
         self.gathered = torch.zeros(SUMMARY_BYTES * self.world, dtype=torch.uint8, device=self.device)
         self.carry_dev = torch.zeros(16, dtype=torch.uint8, device=self.device)
         self._carry_host = torch.zeros(16, dtype=torch.uint8).pin_memory()
+        # device-side size exchange: bytes 8..24 of every rank's pulse_result
+        # (body_bytes u64, n_entries u32, status i32)
+        self.size_send = torch.zeros(16, dtype=torch.uint8, device=self.device)
+        self.sizes_all = torch.zeros(16 * self.world, dtype=torch.uint8, device=self.device)
+        self.apply_res = torch.zeros(72, dtype=torch.uint8, device=self.device)
 
     def bind(self, slot: int, local_tensors):
         self.plan.bind(slot, local_tensors)
@@ -163,6 +168,34 @@ class ShardedPulse:
             self.carry_dev.copy_(self._carry_host, non_blocking=True)
             carry = self.carry_dev
         return self.plan.apply(weights_slot, sec.patch, carry=carry)
+
+    # ---- fully device-side step (no host round trip) ---------------------------------------------
+    def emit_async(self, patch):
+        """After scan(): all-gather of the summaries, K2 (FLAT continued across
+        ranks), the device-side size exchange and the FLAT carry for apply --
+        all stream-ordered, nothing read back to the host."""
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.gathered, self.send)
+            self.plan.emit(patch, gathered=self.gathered, n_ranks=self.world, rank=self.rank)
+            self.size_send.copy_(patch.result[8:24])
+            dist.all_gather_into_tensor(self.sizes_all, self.size_send)
+            if patch.representation == 2:
+                self.D.flat_carry_from_summaries(self.gathered, self.rank, self.carry_dev)
+        else:
+            self.plan.emit(patch)
+
+    def apply_async(self, weights_slot: int, patch):
+        """Apply this rank's section with the entry count read on the device."""
+        carry = self.carry_dev if (self.world > 1 and patch.representation == 2) else None
+        return self.plan.apply_patch(weights_slot, patch, carry=carry, result=self.apply_res)
+
+    def exchanged_sizes(self):
+        """Host view of the last device-side size exchange: (body_bytes, n_entries, status) per rank."""
+        raw = self.sizes_all.cpu().numpy().reshape(self.world, 16)
+        body = raw[:, 0:8].copy().view(np.uint64)[:, 0]
+        ent = raw[:, 8:12].copy().view(np.uint32)[:, 0]
+        st = raw[:, 12:16].copy().view(np.int32)[:, 0]
+        return body, ent, st
 
     def gather(self, sec: Section, root: int = 0):
         """Full PULP body and entry table (global tensor ids) on `root`."""

@@ -235,3 +235,36 @@ def test_apply_rejects_more_entries_than_capacity():
     res = D.parse_result(small.apply(2, p))
     assert int(res["status"]) == 15
     assert np.array_equal(w.cpu().numpy().view(np.uint16), a)
+
+
+@pytest.mark.parametrize("repr_", [COO_DOWNSCALED, COO_INT32, FLAT_INT32])
+def test_apply_patch_device_count_and_failed_encode(repr_):
+    """pulse_apply_patch takes the entry count from the encode's device result;
+    a failed encode (capacity) applies nothing and reports the encode's error."""
+    D = _dev()
+    rng = np.random.default_rng(5)
+    sizes = [(40000, 200), (12345, 5), (9000, 9000)]
+    prevs = [rng.integers(0, 65536, n, dtype=np.uint16) for n, _ in sizes]
+    currs = []
+    for a in prevs:
+        b = a.copy()
+        b[rng.random(a.size) < 0.05] ^= 1
+        currs.append(b)
+    for cap, ok in ((sum(n for n, _ in sizes), True), (100, False)):
+        plan = D.DevicePlan(sizes, cap)
+        plan.bind(0, [torch.from_numpy(a.view(np.int16)).cuda() for a in prevs])
+        plan.bind(1, [torch.from_numpy(b.view(np.int16)).cuda() for b in currs])
+        w = [torch.from_numpy(a.view(np.int16)).cuda() for a in prevs]
+        plan.bind(2, w)
+        p = plan.new_patch(repr_)
+        plan.scan(1, 0)
+        plan.emit(p)
+        res = D.parse_result(plan.apply_patch(2, p))   # no host fetch in between
+        if ok:
+            assert int(res["status"]) == 0
+            for b, t in zip(currs, w):
+                assert np.array_equal(t.cpu().numpy().view(np.uint16), b)
+        else:
+            assert int(res["status"]) == 15
+            for a, t in zip(prevs, w):
+                assert np.array_equal(t.cpu().numpy().view(np.uint16), a)
