@@ -85,7 +85,8 @@ __device__ __forceinline__ uint16_t lane_value(const uint4& v, int k) {
 
 struct K1Args {
     uint32_t* trace;  // optional per-ticket progress trace (debug)
-    int experiment;   // 1: consumers only release stages (TMA streaming rate)
+    int experiment;   // 1: consumers only release stages (TMA streaming rate); 2: no global
+                      // write-back of staged entries; 3: consumers count but do not stage
     const SegDesc* segs;
     const uint32_t* tile_seg;
     uint32_t n_segs;
@@ -229,7 +230,10 @@ constexpr int kLbWarps = 4;                          // warps 9..12
 constexpr int kLbFirst = kConsumerWarps + 1;
 constexpr int kLbThreads = kLbWarps * 32;
 constexpr int kThreadsTotal = (kConsumerWarps + 1 + kLbWarps) * 32;  // 416
-constexpr uint32_t kStageCap = 8192;                 // staged entries per ticket buffer
+constexpr uint32_t kRecCap = 1344;                   // record mode: staged changed 16-byte vectors per buffer
+constexpr uint32_t kStageCap = 8192;                 // element mode: staged changed elements per buffer
+constexpr uint32_t kDenseTicket = 3072;              // changes above which the next ticket uses element mode
+enum : uint32_t { kModeRecords = 0, kModeElements = 1 };
 constexpr int kBufs = 3;                             // ticket staging buffers (consumers may run ahead)
 constexpr uint32_t kChunks = kSubs * kConsumerWarps; // (sub-tile, warp) chunks per ticket
 constexpr uint32_t kBarLb = 2;                       // named barrier id of the look-back group
@@ -253,12 +257,27 @@ struct TicketInfo {
 struct Smem {
     uint4 prev[kStages][kSubElems / 8];
     uint4 curr[kStages][kSubElems / 8];
-    uint16_t st_idx[kBufs][kStageCap];   // element offset within the ticket
-    uint16_t st_val[kBufs][kStageCap];
-    uint32_t chunk_off[kBufs][kChunks];  // where each (sub, warp) chunk was staged
-    uint32_t chunk_cnt[kBufs][kChunks];
+    // Staging, one buffer per ticket in flight, in one of two layouts chosen per
+    // ticket (S.mode): records -- one per changed 16-byte vector, its 8 current
+    // values and meta.x = vector index in the ticket | change mask << 16,
+    // meta.y = (sub, warp) chunk | element offset of its first change in the
+    // chunk << 8 (cheap per change; sparse tickets) -- or elements -- (offset in
+    // ticket, value) per change (more changes per byte; dense tickets).
+    union StageBuf {
+        struct {
+            uint4 val[kRecCap];
+            uint2 meta[kRecCap];
+        } rec;
+        struct {
+            uint16_t idx[kStageCap];
+            uint16_t val[kStageCap];
+        } el;
+    } stg[kBufs];
+    uint32_t chunk_off[kBufs][kChunks];  // element mode: where each (sub, warp) chunk was staged
+    uint32_t chunk_cnt[kBufs][kChunks];  // changed elements per (sub, warp) chunk
+    uint32_t mode[kBufs];                // staging layout of the ticket in each buffer
     uint32_t chunk_pre[kChunks + 1]; // ordered prefix (look-back group)
-    uint32_t fill[kBufs];            // staging bump allocator
+    uint32_t fill[kBufs];            // staging bump allocator (records or elements)
     uint32_t overflow[kBufs];
     uint32_t tk_cnt[kBufs];          // ticket count, summed by the consumer warps
     uint32_t tk_arrived[kBufs];      // consumer warps done with the ticket
@@ -270,6 +289,7 @@ struct Smem {
     uint32_t lb_run, lb_count;
     uint64_t lb_G;
 };
+static_assert(sizeof(Smem) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
 }  // namespace tma
 
 // Look-back with 4 status words per lane per round (128 predecessors).
@@ -338,6 +358,7 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
             mbar_init(&S.tk_empty[i], 1);
             S.fill[i] = 0;
             S.overflow[i] = 0;
+            S.mode[i] = kModeRecords;
             S.tk_cnt[i] = 0;
             S.tk_arrived[i] = 0;
         }
@@ -403,6 +424,7 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
         int stage = 0, buf = 0;
         uint32_t phase = 0, bphase = 0;
         uint32_t wcount = 0;  // this warp's changes in the current ticket
+        uint32_t tmode = kModeRecords;  // staging layout of the current ticket
         // Last warp of a ticket publishes its aggregate right away, so other CTAs'
         // look-backs never wait on this CTA's look-back group.
         auto finish_ticket = [&](const StageDesc& d) {
@@ -461,7 +483,10 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                 if (++stage == kStages) { stage = 0; phase ^= 1; }
                 continue;
             }
-            if (d.sub == 0) mbar_wait(&S.tk_empty[buf], bphase ^ 1);  // staging buffer flushed
+            if (d.sub == 0) {
+                mbar_wait(&S.tk_empty[buf], bphase ^ 1);  // staging buffer flushed
+                tmode = S.mode[buf];
+            }
             uint4 av[kVecPerWarp / 32], cv[kVecPerWarp / 32];
             const uint32_t v0 = warp * kVecPerWarp + lane;
             if (d.vec_bytes == kSubElems * 2) {  // full sub-tile (block-uniform)
@@ -514,7 +539,7 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                 continue;
             }
 
-            // order inside the warp slice: (j, lane, q); packed 16-bit scans for j pairs
+            // element order inside the warp slice: (j, lane, q); packed 16-bit scans for j pairs
             const uint32_t lo = __popc(m[0]) | (__popc(m[1]) << 16);
             const uint32_t hi = __popc(m[2]) | (__popc(m[3]) << 16);
             uint32_t ilo = lo, ihi = hi;
@@ -530,31 +555,66 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
             const uint32_t tlo = __shfl_sync(0xffffffffu, ilo, 31), thi = __shfl_sync(0xffffffffu, ihi, 31);
             const uint32_t t0 = tlo & 0xFFFF, t1 = tlo >> 16, t2 = thi & 0xFFFF, t3 = thi >> 16;
             const uint32_t total = t0 + t1 + t2 + t3;
-            uint32_t off = 0;
-            if (lane == 0 && total) off = atomicAdd(&S.fill[buf], total);
-            off = __shfl_sync(0xffffffffu, off, 0);
-            if (lane == 0) {
-                S.chunk_off[buf][d.sub * kConsumerWarps + warp] = off;
-                S.chunk_cnt[buf][d.sub * kConsumerWarps + warp] = total;
-                if (off + total > kStageCap) S.overflow[buf] = 1;
-            }
-            if (total) {
-                const uint32_t exlo = ilo - lo, exhi = ihi - hi;
-                const uint32_t pj[4] = {exlo & 0xFFFF, t0 + (exlo >> 16), t0 + t1 + (exhi & 0xFFFF),
-                                        t0 + t1 + t2 + (exhi >> 16)};
+            const uint32_t chunk = d.sub * kConsumerWarps + warp;
+            const uint32_t exlo = ilo - lo, exhi = ihi - hi;
+            const uint32_t pj[4] = {exlo & 0xFFFF, t0 + (exlo >> 16), t0 + t1 + (exhi & 0xFFFF),
+                                    t0 + t1 + t2 + (exhi >> 16)};
+            if (tmode == kModeRecords) {
+                // one record per changed vector, records in (j, lane) order
+                uint32_t rb[4], nrec = 0;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    uint32_t mm = m[j];
-                    uint32_t pos = off + pj[j];
-                    const uint32_t e = d.sub * kSubElems + (v0 + 32 * j) * 8;
-                    while (mm) {
-                        const int q = __ffs(mm) - 1;
-                        mm &= mm - 1;
-                        if (pos < kStageCap) {
-                            S.st_idx[buf][pos] = uint16_t(e + q);
-                            S.st_val[buf][pos] = lane_value(cv[j], q);
+                    rb[j] = __ballot_sync(0xffffffffu, m[j] != 0);
+                    nrec += __popc(rb[j]);
+                }
+                uint32_t off = 0;
+                if (lane == 0 && nrec) off = atomicAdd(&S.fill[buf], nrec);
+                off = __shfl_sync(0xffffffffu, off, 0);
+                if (lane == 0) {
+                    S.chunk_cnt[buf][chunk] = total;
+                    if (off + nrec > kRecCap) S.overflow[buf] = 1;
+                }
+                if (k.experiment != 3) {
+                    const uint32_t lt_mask = (1u << lane) - 1u;
+                    uint32_t rbase = off;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (m[j]) {
+                            const uint32_t r = rbase + __popc(rb[j] & lt_mask);
+                            if (r < kRecCap) {
+                                const uint32_t vec = d.sub * (kSubElems / 8) + v0 + 32 * j;
+                                S.stg[buf].rec.val[r] = cv[j];
+                                S.stg[buf].rec.meta[r] = make_uint2(vec | (m[j] << 16), chunk | (pj[j] << 8));
+                            }
                         }
-                        ++pos;
+                        rbase += __popc(rb[j]);
+                    }
+                }
+            } else {
+                // element entries (offset in ticket, value), chunk-contiguous
+                uint32_t off = 0;
+                if (lane == 0 && total) off = atomicAdd(&S.fill[buf], total);
+                off = __shfl_sync(0xffffffffu, off, 0);
+                if (lane == 0) {
+                    S.chunk_off[buf][chunk] = off;
+                    S.chunk_cnt[buf][chunk] = total;
+                    if (off + total > kStageCap) S.overflow[buf] = 1;
+                }
+                if (total && k.experiment != 3) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t mm = m[j];
+                        uint32_t pos = off + pj[j];
+                        const uint32_t e = d.sub * kSubElems + (v0 + 32 * j) * 8;
+                        while (mm) {
+                            const int q = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            if (pos < kStageCap) {
+                                S.stg[buf].el.idx[pos] = uint16_t(e + q);
+                                S.stg[buf].el.val[pos] = lane_value(cv[j], q);
+                            }
+                            ++pos;
+                        }
                     }
                 }
             }
@@ -608,7 +668,30 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
         named_sync(kBarLb, kLbThreads);
         const uint64_t G = S.lb_G;
         const uint32_t count = S.lb_count;
-        if (!S.overflow[buf]) {
+        if (k.experiment == 2 || k.experiment == 3) {
+            // attribution experiments: no write-back
+        } else if (!S.overflow[buf] && S.mode[buf] == kModeRecords) {
+            // expand the staged records: record -> its changed elements, at the
+            // ticket prefix G + its chunk's element prefix + its offset in the chunk
+            const uint32_t nrec = S.fill[buf];
+            for (uint32_t r = lt; r < nrec; r += kLbThreads) {
+                const uint2 meta = S.stg[buf].rec.meta[r];
+                const uint4 v = S.stg[buf].rec.val[r];
+                const uint32_t vec = meta.x & 0xFFFF, mask = meta.x >> 16;
+                uint64_t pos = G + S.chunk_pre[meta.y & 0xFF] + (meta.y >> 8);
+                const uint32_t ebase = ti.toff + vec * 8;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (mask & (1u << q)) {
+                        if (pos < k.capacity) {
+                            k.out_idx[pos] = ebase + q;
+                            k.out_val[pos] = lane_value(v, q);
+                        }
+                        ++pos;
+                    }
+                }
+            }
+        } else if (!S.overflow[buf]) {
             for (uint32_t q = lt; q < count; q += kLbThreads) {
                 // chunk holding output ordinal q: last c with chunk_pre[c] <= q
                 uint32_t lo = 0, hi = nch;
@@ -618,8 +701,8 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                 }
                 const uint32_t src = S.chunk_off[buf][lo] + (q - S.chunk_pre[lo]);
                 if (G + q < k.capacity) {
-                    k.out_idx[G + q] = ti.toff + S.st_idx[buf][src];
-                    k.out_val[G + q] = S.st_val[buf][src];
+                    k.out_idx[G + q] = ti.toff + S.stg[buf].el.idx[src];
+                    k.out_val[G + q] = S.stg[buf].el.val[src];
                 }
             }
         } else {
@@ -695,6 +778,9 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
             if (k.trace) atomicOr(k.trace + ti.tile, 16u);
             S.fill[buf] = 0;
             S.overflow[buf] = 0;
+            // layout for the next ticket staged in this buffer: neighbouring tickets
+            // have similar density (same tensor), so follow this one's
+            S.mode[buf] = count > kDenseTicket ? kModeElements : kModeRecords;
             S.tk_cnt[buf] = 0;
             S.tk_arrived[buf] = 0;
             mbar_arrive(&S.tk_empty[buf]);
