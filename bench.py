@@ -310,6 +310,7 @@ def run_pulse(args):
             a0 = torch.cuda.Event(enable_timing=True)
             a0.record(stream)
         sp.apply_async(2, patch)
+        sp.join()  # the size exchange (side stream) belongs to the step
         if record:
             a1 = torch.cuda.Event(enable_timing=True)
             a1.record(stream)
@@ -325,6 +326,10 @@ def run_pulse(args):
             raise RuntimeError(f"apply failed: {res}")
         state["body"] = patch.body_bytes
         state["changes"] = patch.n_changes
+        if world > 1:  # the device-side size exchange saw this rank's section and no failures
+            bb, _, st = sp.exchanged_sizes()
+            if int(bb[rank]) != patch.body_bytes or any(int(x) != 0 for x in st):
+                raise RuntimeError(f"size exchange mismatch: {bb} {st}")
 
     def barrier():
         torch.cuda.synchronize()

@@ -129,6 +129,7 @@ class ShardedPulse:
         self.size_send = torch.zeros(16, dtype=torch.uint8, device=self.device)
         self.sizes_all = torch.zeros(16 * self.world, dtype=torch.uint8, device=self.device)
         self.apply_res = torch.zeros(72, dtype=torch.uint8, device=self.device)
+        self._side = None
 
     def bind(self, slot: int, local_tensors):
         self.plan.bind(slot, local_tensors)
@@ -171,18 +172,33 @@ class ShardedPulse:
 
     # ---- fully device-side step (no host round trip) ---------------------------------------------
     def emit_async(self, patch):
-        """After scan(): all-gather of the summaries, K2 (FLAT continued across
-        ranks), the device-side size exchange and the FLAT carry for apply --
-        all stream-ordered, nothing read back to the host."""
-        if self.world > 1:
+        """After scan(): K2 and the size exchange, stream-ordered, nothing read
+        back to the host.  Only FLAT_INT32 needs other ranks before K2 (its gap
+        stream continues across shards): it all-gathers the scan summaries and
+        derives the carry on the device.  The other representations emit
+        independently, and the (body bytes, entries) exchange runs on a side
+        stream, overlapped with apply (join with `join()`)."""
+        if self.world == 1:
+            self.plan.emit(patch)
+            return
+        main = torch.cuda.current_stream(self.device)
+        if patch.representation == 2:
             dist.all_gather_into_tensor(self.gathered, self.send)
             self.plan.emit(patch, gathered=self.gathered, n_ranks=self.world, rank=self.rank)
-            self.size_send.copy_(patch.result[8:24])
-            dist.all_gather_into_tensor(self.sizes_all, self.size_send)
-            if patch.representation == 2:
-                self.D.flat_carry_from_summaries(self.gathered, self.rank, self.carry_dev)
+            self.D.flat_carry_from_summaries(self.gathered, self.rank, self.carry_dev)
         else:
             self.plan.emit(patch)
+        self.size_send.copy_(patch.result[8:24])
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device)
+        self._side.wait_stream(main)
+        with torch.cuda.stream(self._side):
+            dist.all_gather_into_tensor(self.sizes_all, self.size_send)
+
+    def join(self):
+        """Make the current stream wait for the side-stream size exchange."""
+        if self._side is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self._side)
 
     def apply_async(self, weights_slot: int, patch):
         """Apply this rank's section with the entry count read on the device."""
