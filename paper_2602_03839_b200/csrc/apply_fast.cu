@@ -303,7 +303,7 @@ __device__ __noinline__ void slow_span(const ApplyArgs& A, uint64_t first, uint6
 // F1 / F3 / F4: one kernel body, three passes
 // =============================================================================================
 template <int kRepr, int kPass>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kPass >= kScatter ? 2 : 4)
 f_pass(ApplyArgs A) {
     extern __shared__ __align__(16) uint8_t smem[];
     if (fast_blocked(A.flags)) return;
@@ -381,6 +381,8 @@ f_pass(ApplyArgs A) {
 #define PULSE_BV(j) (coo ? (bw[((j) >> 1) % kBW] >> (16 * ((j) & 1))) & 0xFFFFu : 0u)
             const uint64_t ol = o0 + uint64_t(lane) * kPer;
             const uint64_t nrows = coo ? L.numel / L.cols : 0;
+            const bool lane_first = ol == 0;  // this lane holds the entry's first index (ordinal 0)
+            const bool lane_gfirst = c0 + uint64_t(lane) * kPer == 0;  // ... the patch's first entry
             // lane aggregates
             uint64_t lr = 0, lc = 0;
             bool lmark = false;
@@ -388,9 +390,10 @@ f_pass(ApplyArgs A) {
             for (int j = 0; j < int(kPer); ++j) {
                 if (j < nv) {
                     const uint32_t a = PULSE_AV(j), b = PULSE_BV(j);
-                    const bool hr = kRepr != kFlat && ol + j == 0;
+                    const bool first = j == 0 && lane_first;
+                    const bool hr = kRepr != kFlat && first;
                     if (coo) {
-                        const bool hc = ol + j == 0 || a != 0;
+                        const bool hc = first || a != 0;
                         lmark |= a == 0xFF || b == 0xFFFF;
                         lc = hc ? (H | b) : lc + b;
                     }
@@ -420,36 +423,39 @@ f_pass(ApplyArgs A) {
                     xv[c] = kInvalid;
                     if (j >= nv) continue;
                     const uint32_t a = PULSE_AV(j), b = PULSE_BV(j);
-                    const uint64_t o = ol + j;
+                    const bool first = j == 0 && lane_first;
+#define PULSE_ORD (ol + uint64_t(j))  /* entry ordinal, only for error keys */
                     uint64_t key = kNoError;
                     if (coo) {
-                        const bool nr = o == 0 || a != 0;
-                        row = o == 0 ? a : row + a;
+                        const bool nr = first || a != 0;
+                        row = first ? a : row + a;
                         col = nr ? b : col + b;
                         if (checks(kPass)) {
                             // patch.hpp:247-254; with col < cols, flat >= numel <=> row >= numel / cols
-                            if (!nr && b == 0) key = error_key(e, kStageCols, o, kZeroColGap);
-                            else if (col >= L.cols) key = error_key(e, kStageRange, o, kColRange);
-                            else if (row >= nrows) key = error_key(e, kStageRange, o, kIdxRange);
+                            if (!nr && b == 0) key = error_key(e, kStageCols, PULSE_ORD, kZeroColGap);
+                            else if (col >= L.cols) key = error_key(e, kStageRange, PULSE_ORD, kColRange);
+                            else if (row >= nrows) key = error_key(e, kStageRange, PULSE_ORD, kIdxRange);
                         }
                         if (key == kNoError) xv[c] = uint32_t(row) * uint32_t(L.cols) + uint32_t(col);
                     } else if (kRepr == kI32) {
-                        row = o == 0 ? a : row + a;
+                        row = first ? a : row + a;
                         if (checks(kPass)) {
-                            if (o > 0 && a == 0) key = error_key(e, kStageRows, o, kZeroGap);
-                            else if (row >= L.numel) key = error_key(e, kStageRows, o, kIdxRange);
+                            if (!first && a == 0) key = error_key(e, kStageRows, PULSE_ORD, kZeroGap);
+                            else if (row >= L.numel) key = error_key(e, kStageRows, PULSE_ORD, kIdxRange);
                         }
                         if (key == kNoError) xv[c] = uint32_t(row);
                     } else {
                         row += a;
                         const int64_t local = int64_t(row) - int64_t(gap_base) - int64_t(L.flat_base);
                         if (checks(kPass)) {
-                            const uint64_t gi = c0 + uint64_t(lane) * kPer + j;
-                            if (a == 0 && (gi > 0 || has_prev)) key = error_key(e, kStageRows, o, kZeroGap);
-                            else if (local < 0 || uint64_t(local) >= L.numel) key = error_key(e, kStageRows, o, kIdxRange);
+                            // the patch's very first gap may be 0 only without a previous shard
+                            const bool gfirst = j == 0 && lane_gfirst;
+                            if (a == 0 && (!gfirst || has_prev)) key = error_key(e, kStageRows, PULSE_ORD, kZeroGap);
+                            else if (local < 0 || uint64_t(local) >= L.numel) key = error_key(e, kStageRows, PULSE_ORD, kIdxRange);
                         }
                         if (key == kNoError) xv[c] = uint32_t(local);
                     }
+#undef PULSE_ORD
                     if (reports(kPass) && key != kNoError) report_cold(A.err, key);
                 }
                 if (kPass >= kScatter) sx[swz<8>(uint32_t(lane * 8 + i))] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
