@@ -206,6 +206,17 @@ pulse_status pulse_apply_patch(pulse_plan* plan, uint32_t weights_slot, uint32_t
 pulse_status pulse_flat_carry_from_summaries(const pulse_scan_summary* dev_gathered, uint32_t rank,
                                              pulse_flat_carry* dev_out, void* stream);
 
+/* Analyses (absorption.hpp:38-78) on bound snapshots, one HBM pass each:
+ * elements whose bit patterns differ between two slots (the count behind
+ * sparsity(), :55-78), and elements whose bf16 magnitude pattern (bits &
+ * 0x7FFF) is above `magnitude_bits` and not NaN (frozen_fraction(), :38-46;
+ * the host maps the threshold to the largest magnitude pattern <= it).
+ * `dev_count` is one device uint64. */
+pulse_status pulse_count_changed(pulse_plan* plan, uint32_t slot_a, uint32_t slot_b, uint64_t* dev_count,
+                                 void* stream);
+pulse_status pulse_count_above(pulse_plan* plan, uint32_t slot, uint32_t magnitude_bits, uint64_t* dev_count,
+                               void* stream);
+
 /* Decode only: parse the payloads to flat int64 indices (dev_indices, in
  * entry order) without touching weights. */
 pulse_status pulse_decode_indices(pulse_plan* plan, uint32_t representation,
@@ -305,6 +316,18 @@ pulse_status pulse_read_patch_bytes(const uint8_t* data, uint64_t n, pulse_patch
  * process (all threads); a benchmark/diagnostic aid with no reference
  * counterpart.  reset != 0 zeroes the counters after reading them. */
 void pulse_transfer_stats(uint64_t* h2d_bytes, uint64_t* d2h_bytes, int reset);
+
+/* sparsity -- absorption.hpp:55-78 (k is metadata, as in the reference). */
+typedef struct pulse_sparsity_report {
+    uint64_t k;
+    uint64_t changed;
+    uint64_t total;
+    double sparsity; /* 1 - changed / total; 1.0 when total == 0 */
+} pulse_sparsity_report;
+pulse_status pulse_sparsity(const pulse_checkpoint* a, const pulse_checkpoint* b, uint64_t k,
+                            pulse_sparsity_report* out);
+/* frozen_fraction -- absorption.hpp:38-46: fraction of weights with |w| > threshold. */
+pulse_status pulse_frozen_fraction(const pulse_checkpoint* checkpoint, double threshold, double* out);
 
 /* hash_weights -- sha256.hpp:93-116; Sha256 -- sha256.hpp:51-87. */
 pulse_status pulse_hash_weights(const pulse_checkpoint* checkpoint, uint8_t* out32);

@@ -139,6 +139,7 @@ class Reference:
             "ref_decompress": (C.c_int, [C.c_char_p, u64, u32, pp(vp)]),
             "ref_write_checkpoint_bytes": (C.c_int, [vp, pp(vp)]),
             "ref_sparsity": (C.c_int, [vp, vp, pp(u64), pp(u64)]),
+            "ref_frozen_fraction": (C.c_int, [vp, C.c_double, pp(C.c_double)]),
             "ref_time_step": (C.c_int, [vp, vp, u32, u32, C.c_int] + [pp(C.c_double)] * 5 + [pp(u64), pp(u64)]),
         }
         for name, (res, args) in sig.items():
@@ -351,6 +352,27 @@ class Reference:
         finally:
             self.L.ref_ckpt_free(h)
         return self._take_buf(out.value)
+
+    def sparsity(self, a: Checkpoint, b: Checkpoint):
+        """absorption.hpp:55-78 -> (changed, total)"""
+        ha, hb = self.ckpt_handle(a), self.ckpt_handle(b)
+        ch, tot = C.c_uint64(), C.c_uint64()
+        try:
+            self._check(self.L.ref_sparsity(ha, hb, C.byref(ch), C.byref(tot)))
+        finally:
+            self.L.ref_ckpt_free(ha)
+            self.L.ref_ckpt_free(hb)
+        return ch.value, tot.value
+
+    def frozen_fraction(self, c: Checkpoint, threshold: float) -> float:
+        """absorption.hpp:38-46"""
+        h = self.ckpt_handle(c)
+        out = C.c_double()
+        try:
+            self._check(self.L.ref_frozen_fraction(h, threshold, C.byref(out)))
+        finally:
+            self.L.ref_ckpt_free(h)
+        return out.value
 
     def time_step(self, prev_h, curr_h, repr_=COO_DOWNSCALED, codec=IDENTITY, verify=False):
         """Times one reference step on prebuilt handles (see ref_shim.cpp ref_time_step)."""

@@ -361,6 +361,14 @@ int ref_sparsity(void* cur, void* prev, uint64_t* changed, uint64_t* total) {
     SHIM_CATCH
 }
 
+// absorption.hpp:38-46
+int ref_frozen_fraction(void* ck, double threshold, double* out) {
+    SHIM_TRY
+    *out = pulse::frozen_fraction(*static_cast<pulse::Checkpoint*>(ck), threshold);
+    return 0;
+    SHIM_CATCH
+}
+
 // ---- CPU baseline timing (reference path, single thread as the reference runs) ----
 // One "step" of the reference hot path on (prev, curr):
 //   encode (patch.hpp:264, includes hash_weights) -> write_patch_bytes

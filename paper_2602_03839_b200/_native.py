@@ -112,6 +112,10 @@ class TensorPatchC(C.Structure):
                 ("values", C.POINTER(C.c_uint16)), ("n_values", C.c_uint64)]
 
 
+class SparsityReportC(C.Structure):
+    _fields_ = [("k", C.c_uint64), ("changed", C.c_uint64), ("total", C.c_uint64), ("sparsity", C.c_double)]
+
+
 vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32
 _SIGS = {
     "pulse_last_error": (C.c_char_p, []),
@@ -149,6 +153,10 @@ _SIGS = {
     "pulse_decode_index_payloads": (i32, [vp, C.POINTER(vp), C.POINTER(u64), u32]),
     "pulse_write_patch_bytes": (i32, [vp, C.POINTER(vp)]),
     "pulse_read_patch_bytes": (i32, [C.c_char_p, u64, C.POINTER(vp)]),
+    "pulse_count_changed": (i32, [vp, u32, u32, vp, vp]),
+    "pulse_count_above": (i32, [vp, u32, u32, vp, vp]),
+    "pulse_sparsity": (i32, [C.POINTER(CheckpointC), C.POINTER(CheckpointC), u64, C.POINTER(SparsityReportC)]),
+    "pulse_frozen_fraction": (i32, [C.POINTER(CheckpointC), C.c_double, C.POINTER(C.c_double)]),
     "pulse_transfer_stats": (None, [C.POINTER(u64), C.POINTER(u64), C.c_int]),
     "pulse_hash_weights": (i32, [C.POINTER(CheckpointC), C.c_char_p]),
     "pulse_sha256_new": (i32, [C.POINTER(vp)]),

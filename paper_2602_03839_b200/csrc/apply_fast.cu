@@ -380,7 +380,7 @@ f_pass(ApplyArgs A) {
 #define PULSE_AV(j) (coo ? (aw[(j) >> 2] >> (8 * ((j) & 3))) & 0xFFu : aw[(j) % kAW])
 #define PULSE_BV(j) (coo ? (bw[((j) >> 1) % kBW] >> (16 * ((j) & 1))) & 0xFFFFu : 0u)
             const uint64_t ol = o0 + uint64_t(lane) * kPer;
-            const uint64_t nrows = coo ? L.numel / L.cols : 0;
+            const uint64_t nrows = L.numel / (coo && L.cols ? L.cols : 1);  // COO row extent
             const bool lane_first = ol == 0;  // this lane holds the entry's first index (ordinal 0)
             const bool lane_gfirst = c0 + uint64_t(lane) * kPer == 0;  // ... the patch's first entry
             // lane aggregates

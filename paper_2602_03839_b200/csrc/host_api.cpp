@@ -14,6 +14,7 @@
 #include <zlib.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <condition_variable>
 #include <cstring>
@@ -1144,6 +1145,125 @@ void pulse_transfer_stats(uint64_t* h2d, uint64_t* d2h, int reset) {
         g_h2d_bytes = 0;
         g_d2h_bytes = 0;
     }
+}
+
+// ---- absorption.hpp analyses -----------------------------------------------------------------
+namespace {
+// Uploads the given tensors (one or two snapshots, same geometry) into the
+// engine arenas and binds them to slots 0 / 1 of a plan over that geometry.
+pulse_plan* bind_for_count(Engine& E, const std::vector<const pulse_tensor*>& a,
+                           const std::vector<const pulse_tensor*>* b) {
+    std::vector<pulse_tensor_geom> geom(a.size());
+    std::vector<uint64_t> numel(a.size());
+    for (size_t k = 0; k < a.size(); ++k) {
+        geom[k].numel = a[k]->numel;
+        geom[k].cols = uint64_t(a[k]->shape[a[k]->rank - 1]);
+        numel[k] = a[k]->numel;
+    }
+    uint64_t total = 0;
+    const auto off = arena_offsets(numel, total);
+    uint16_t* A = E.arena_a.as<uint16_t>(total);
+    uint16_t* B = b ? E.arena_b.as<uint16_t>(total) : nullptr;
+    for (size_t k = 0; k < a.size(); ++k) {
+        E.stager.h2d(A + off[k], a[k]->data, numel[k] * 2, E.stream);
+        if (b) E.stager.h2d(B + off[k], (*b)[k]->data, numel[k] * 2, E.stream);
+    }
+    pulse_plan* plan = E.get_plan(geom, 1);
+    std::vector<const void*> pa(a.size()), pb(a.size());
+    for (size_t k = 0; k < a.size(); ++k) {
+        pa[k] = A + off[k];
+        if (b) pb[k] = B + off[k];
+    }
+    if (pulse_plan_bind(plan, 0, pa.data()) || (b && pulse_plan_bind(plan, 1, pb.data())))
+        raise(PULSE_E_CUDA, pulse_last_error());
+    return plan;
+}
+
+uint64_t read_count(Engine& E) {
+    uint64_t* d = E.misc.as<uint64_t>(2);
+    uint64_t h = 0;
+    cuda_check(counted_copy(&h, d, 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
+    E.sync();
+    return h;
+}
+
+// Largest bf16 magnitude pattern m in [0, 0x7F80] whose value is <= t, or -1
+// (every non-NaN |w| exceeds t); |w| > t  <=>  (bits & 0x7FFF) > m for non-NaN w.
+int32_t magnitude_cutoff(double t) {
+    auto value = [](uint32_t m) {
+        const uint32_t f = m << 16;
+        float x;
+        std::memcpy(&x, &f, 4);
+        return double(x);
+    };
+    if (!(value(0) <= t)) return -1;
+    uint32_t lo = 0, hi = 0x7F80;  // value(lo) <= t
+    if (value(hi) <= t) return int32_t(hi);
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (value(mid) <= t) lo = mid; else hi = mid;
+    }
+    return int32_t(lo);
+}
+}  // namespace
+
+pulse_status pulse_sparsity(const pulse_checkpoint* a, const pulse_checkpoint* b, uint64_t k,
+                            pulse_sparsity_report* out) {
+    return guarded([&] {
+        if (!a || !b || !out) raise(PULSE_E_ARGUMENT, "null argument");
+        const auto oa = sorted_order(a), ob = sorted_order(b);
+        if (oa.size() != ob.size()) raise(PULSE_E_TENSOR_SET, "checkpoints have different tensor counts");
+        std::vector<const pulse_tensor*> ta, tb;
+        uint64_t total = 0;
+        for (size_t i = 0; i < oa.size(); ++i) {
+            const pulse_tensor& x = a->tensors[oa[i]];
+            const pulse_tensor& y = b->tensors[ob[i]];
+            if (std::strcmp(x.name, y.name) != 0)
+                raise(PULSE_E_TENSOR_SET, std::string("tensor sets differ: '") + x.name + "' vs '" + y.name + "'");
+            if (x.rank != y.rank || !std::equal(x.shape, x.shape + x.rank, y.shape) || x.numel != y.numel)
+                raise(PULSE_E_SHAPE_MISMATCH, std::string("tensor '") + x.name + "' shapes differ");
+            total += x.numel;
+            if (x.numel) {
+                ta.push_back(&x);
+                tb.push_back(&y);
+            }
+        }
+        uint64_t changed = 0;
+        if (!ta.empty()) {
+            Engine& E = engine();
+            std::lock_guard<std::mutex> lk(E.mu);
+            pulse_plan* plan = bind_for_count(E, ta, &tb);
+            if (pulse_count_changed(plan, 0, 1, E.misc.as<uint64_t>(2), E.stream)) raise(PULSE_E_CUDA, pulse_last_error());
+            changed = read_count(E);
+        }
+        out->k = k;
+        out->changed = changed;
+        out->total = total;
+        out->sparsity = total ? 1.0 - double(changed) / double(total) : 1.0;
+    });
+}
+
+pulse_status pulse_frozen_fraction(const pulse_checkpoint* c, double threshold, double* out) {
+    return guarded([&] {
+        if (!c || !out) raise(PULSE_E_ARGUMENT, "null argument");
+        std::vector<const pulse_tensor*> ts;
+        uint64_t total = 0;
+        for (uint32_t i = 0; i < c->n_tensors; ++i) {
+            total += c->tensors[i].numel;
+            if (c->tensors[i].numel) ts.push_back(&c->tensors[i]);
+        }
+        if (total == 0) raise(PULSE_E_ARGUMENT, "frozen fraction of an empty checkpoint is undefined");
+        uint64_t above = 0;
+        if (!std::isnan(threshold)) {  // |w| > NaN is false for every weight
+            Engine& E = engine();
+            std::lock_guard<std::mutex> lk(E.mu);
+            pulse_plan* plan = bind_for_count(E, ts, nullptr);
+            const uint32_t cut = uint32_t(magnitude_cutoff(threshold));
+            if (pulse_count_above(plan, 0, cut, E.misc.as<uint64_t>(2), E.stream)) raise(PULSE_E_CUDA, pulse_last_error());
+            above = read_count(E);
+        }
+        *out = double(above) / double(total);
+    });
 }
 
 // ---- sha256.hpp -----------------------------------------------------------------------------

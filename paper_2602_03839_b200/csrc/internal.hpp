@@ -175,6 +175,10 @@ void set_watchdog_decode(unsigned long long* slot);
 void set_watchdog_synth(unsigned long long* slot);
 void set_watchdog_index(unsigned long long* slot);
 void set_watchdog_apply(unsigned long long* slot);
+void set_watchdog_reduce(unsigned long long* slot);
+// reduce.cu (absorption.hpp analyses)
+void launch_count_changed(const PlanDev& p, uint32_t slot_a, uint32_t slot_b, uint64_t* out, cudaStream_t s);
+void launch_count_above(const PlanDev& p, uint32_t slot, uint32_t magnitude_bits, uint64_t* out, cudaStream_t s);
 
 }  // namespace dev
 }  // namespace pulse

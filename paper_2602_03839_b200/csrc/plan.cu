@@ -82,6 +82,7 @@ void pulse_install_watchdog(int device) {
         set_watchdog_index(g_wd_dev);
         set_watchdog_apply(g_wd_dev);
         set_watchdog_helpers(g_wd_dev);
+        set_watchdog_reduce(g_wd_dev);
         done[device] = true;
     }
 }
@@ -306,6 +307,27 @@ pulse_status pulse_apply_patch(pulse_plan* plan, uint32_t weights_slot, uint32_t
                   dev_result, static_cast<cudaStream_t>(stream), dev_patch_result);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "apply launch");
+}
+
+pulse_status pulse_count_changed(pulse_plan* plan, uint32_t slot_a, uint32_t slot_b, uint64_t* dev_count,
+                                 void* stream) {
+    if (!plan || !dev_count || slot_a >= PULSE_MAX_SLOTS || slot_b >= PULSE_MAX_SLOTS || !plan->bound[slot_a] ||
+        !plan->bound[slot_b])
+        return fail(PULSE_E_ARGUMENT, "count_changed: bad argument");
+    cudaSetDevice(plan->device);
+    launch_count_changed(plan->dev, slot_a, slot_b, dev_count, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "count_changed launch");
+}
+
+pulse_status pulse_count_above(pulse_plan* plan, uint32_t slot, uint32_t magnitude_bits, uint64_t* dev_count,
+                               void* stream) {
+    if (!plan || !dev_count || slot >= PULSE_MAX_SLOTS || !plan->bound[slot])
+        return fail(PULSE_E_ARGUMENT, "count_above: bad argument");
+    cudaSetDevice(plan->device);
+    launch_count_above(plan->dev, slot, magnitude_bits, dev_count, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "count_above launch");
 }
 
 pulse_status pulse_flat_carry_from_summaries(const pulse_scan_summary* dev_gathered, uint32_t rank,

@@ -244,6 +244,30 @@ def decompress(data: bytes, codec: int) -> bytes:
     return _take(b)
 
 
+@dataclass
+class SparsityReport:
+    k: int = 1
+    changed: int = 0
+    total: int = 0
+    sparsity: float = 1.0
+
+
+def sparsity(a: Checkpoint, b: Checkpoint, k: int = 1) -> SparsityReport:
+    """absorption.hpp:55-78 (one device pass over both snapshots)."""
+    va, vb = CheckpointView(a), CheckpointView(b)
+    r = N.SparsityReportC()
+    N.check(N.lib.pulse_sparsity(C.byref(va.c), C.byref(vb.c), k, C.byref(r)))
+    return SparsityReport(r.k, r.changed, r.total, r.sparsity)
+
+
+def frozen_fraction(c: Checkpoint, threshold: float) -> float:
+    """absorption.hpp:38-46 (one device pass)."""
+    v = CheckpointView(c)
+    out = C.c_double()
+    N.check(N.lib.pulse_frozen_fraction(C.byref(v.c), threshold, C.byref(out)))
+    return out.value
+
+
 def transfer_stats(reset=False):
     """(h2d_bytes, d2h_bytes) the host API has copied so far in this process."""
     a, b = C.c_uint64(), C.c_uint64()

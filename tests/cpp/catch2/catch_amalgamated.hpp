@@ -157,6 +157,7 @@ private:
         catch_shim::report(caught_, #expr " throws " #type, __FILE__, __LINE__, fatal);                      \
     } while (0)
 #define CHECK_THROWS_AS(expr, type) CATCH_SHIM_THROWS(expr, type, false)
+#define CAPTURE(...) ((void)0)  // Catch logs the values on failure; the shim reports the expression
 #define REQUIRE_THROWS_AS(expr, type) CATCH_SHIM_THROWS(expr, type, true)
 #define CHECK_NOTHROW(expr)                                                                    \
     do {                                                                                       \

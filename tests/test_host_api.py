@@ -145,3 +145,51 @@ def test_errors_map_to_reference_kinds(golden):
         with pytest.raises(OracleError) as r:
             R.decode(rb, R.read_patch_bytes(wire))
         assert e.value.kind == r.value.kind
+
+
+# ---- absorption.hpp analyses (row a21 + frozen_fraction) ------------------------------------------
+@pytest.mark.gpu
+def test_sparsity_matches_reference(golden):
+    if not have_reference():
+        pytest.skip("oracle/_ref not built")
+    R = reference()
+    for name in golden.names:
+        prev, curr, m = golden.case(name)
+        r = H.sparsity(mirror(curr), mirror(prev), k=3)
+        ch, tot = R.sparsity(curr, prev)
+        assert (r.changed, r.total, r.k) == (ch, tot, 3), name
+        assert r.sparsity == (1.0 - ch / tot if tot else 1.0)
+        assert H.sparsity(mirror(prev), mirror(prev)).changed == 0
+
+
+@pytest.mark.gpu
+def test_frozen_fraction_matches_reference_and_numpy(golden):
+    rng = np.random.default_rng(9)
+    bits = rng.integers(0, 65536, 300001, dtype=np.uint16)
+    bits[:8] = [0x0000, 0x8000, 0x7F80, 0xFF80, 0x7FC0, 0xFFC1, 0x0001, 0x3F80]  # zeros, infs, NaNs, subnormal, 1.0
+    c = H.Checkpoint(0, [H.Tensor("w", (300001,), bits)])
+    with np.errstate(invalid="ignore"):  # NaN patterns
+        f32 = (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    for t in [0.0, 1.0, 0.25, 7.68e-4, 1e-40, -1.0, float("inf"), float("nan"), 3.0e38, 2.0 ** -133]:
+        want = float(np.count_nonzero(np.abs(f32) > t)) / bits.size
+        got = H.frozen_fraction(c, t)
+        assert got == want, (t, got, want)
+        if have_reference():
+            from oracle.oracle import Checkpoint, Tensor
+            assert got == reference().frozen_fraction(Checkpoint(0, [Tensor("w", (300001,), bits)]), t), t
+    with pytest.raises(H.PulseError):
+        H.frozen_fraction(H.Checkpoint(0, []), 0.1)
+
+
+@pytest.mark.gpu
+def test_sparsity_errors_match_reference():
+    a = H.Checkpoint(0, [H.Tensor("w", (2,), np.zeros(2, np.uint16))])
+    with pytest.raises(H.PulseError) as e:
+        H.sparsity(a, H.Checkpoint(0, [H.Tensor("x", (2,), np.zeros(2, np.uint16))]))
+    assert e.value.kind == "TensorSetError"
+    with pytest.raises(H.PulseError) as e:
+        H.sparsity(a, H.Checkpoint(0, []))
+    assert e.value.kind == "TensorSetError"
+    with pytest.raises(H.PulseError) as e:
+        H.sparsity(a, H.Checkpoint(0, [H.Tensor("w", (2, 1), np.zeros(2, np.uint16))]))
+    assert e.value.kind == "ShapeMismatchError"
