@@ -47,6 +47,7 @@ def parse_args():
     ap.add_argument("--repr", type=int, default=0, choices=[0, 1, 2])
     ap.add_argument("--seed", type=int, default=1002)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-elems", type=int, default=96_000_000)
     return ap.parse_args()
@@ -345,17 +346,50 @@ def run_pulse(args):
         step(args.warmup)
         check_step()
     barrier()
+    # per-phase times (encode = scan, apply) from one eager pass over `steps` steps
+    for k in range(args.steps):
+        step(k, record=True)
+    barrier()
+    check_step()
+    # the timed loop replays the step as a CUDA graph (one per direction: the two
+    # snapshot slots swap), launch overhead off the host; eager launches if capture fails
+    graphs = None
+    # single GPU only: with NCCL collectives captured, process-group teardown hung
+    # on the pool (round 1); the sharded step times eager launches
+    if not args.no_graph and world == 1:
+        try:
+            graphs = []
+            for k in (0, 1):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    step(k)
+                graphs.append(g)
+            for k in (0, 1):  # the capture recorded, not ran: run both once, W is back at prev
+                graphs[k].replay()
+            torch.cuda.synchronize()
+            check_step()
+        except Exception as exc:  # noqa: BLE001
+            print(f"[bench] graph capture unavailable ({type(exc).__name__}: {exc}); timing eager launches",
+                  file=sys.stderr)
+            graphs = None
+            torch.cuda.synchronize()
+    barrier()
+    stream = torch.cuda.current_stream()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         t0.record(stream)
         for k in range(args.steps):
-            step(k, record=True)
+            if graphs:
+                graphs[k % 2].replay()
+            else:
+                step(k)
         t1.record(stream)
         torch.cuda.synchronize()
     barrier()
     check_step()
     ms = t0.elapsed_time(t1) / args.steps
+    graphs = None  # release the graphs (and anything they reference) before teardown
     scan_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["s0"], ev["s1"]))
     apply_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["a0"], ev["a1"]))
 
@@ -415,6 +449,7 @@ def run_pulse(args):
                        "sparsity": args.sparsity, "cluster_width": args.cluster_width,
                        "representation": REPR_NAMES[args.repr], "codec": "identity (device body)",
                        "parallelism": f"tensor-shard x{world}" if world > 1 else "single GPU",
+                       "launch": "cuda-graph replay" if graphs else "eager",
                        "l2": f"inputs {4 * d_total / 1e9:.1f} GB per step >> 126 MB L2 (no flush needed)"},
             "frac_of_hbm": round(value / peak, 4),
             "encode_ms": round(scan_max, 4), "apply_ms": round(apply_max, 4),
