@@ -389,6 +389,7 @@ def run_pulse(args):
     barrier()
     check_step()
     ms = t0.elapsed_time(t1) / args.steps
+    used_graph = bool(graphs)
     graphs = None  # release the graphs (and anything they reference) before teardown
     scan_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["s0"], ev["s1"]))
     apply_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["a0"], ev["a1"]))
@@ -449,7 +450,7 @@ def run_pulse(args):
                        "sparsity": args.sparsity, "cluster_width": args.cluster_width,
                        "representation": REPR_NAMES[args.repr], "codec": "identity (device body)",
                        "parallelism": f"tensor-shard x{world}" if world > 1 else "single GPU",
-                       "launch": "cuda-graph replay" if graphs else "eager",
+                       "launch": "cuda-graph replay" if used_graph else "eager",
                        "l2": f"inputs {4 * d_total / 1e9:.1f} GB per step >> 126 MB L2 (no flush needed)"},
             "frac_of_hbm": round(value / peak, 4),
             "encode_ms": round(scan_max, 4), "apply_ms": round(apply_max, 4),
