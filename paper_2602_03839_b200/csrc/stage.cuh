@@ -150,7 +150,11 @@ __device__ __forceinline__ void unstage(uint8_t* dst, const uint4* src, uint32_t
     uint8_t* base = dst - s;
     const uint32_t nblk = (s + len + 15) >> 4, nslots = (len + 15) >> 4;
     const uint32_t sb = (16 - s) & 15, sw = sb >> 2, sh = (sb & 3) * 8;
+    const uint32_t tail_k = nblk - 1;
+    const bool head_partial = s != 0 || len < 16;
+    const bool tail_partial = ((s + len) & 15) != 0;
     uint4 carry = make_uint4(0, 0, 0, 0);  // slot (round start - 1)
+    uint4 head = make_uint4(0, 0, 0, 0), tail = head;  // partial blocks, held by their lanes
     for (uint32_t k0 = 0; k0 < nblk; k0 += 32) {
         const uint32_t k = k0 + lane;
         const uint4 cur = k < nslots ? lds128(src + swz<V>(k)) : make_uint4(0, 0, 0, 0);
@@ -159,16 +163,24 @@ __device__ __forceinline__ void unstage(uint8_t* dst, const uint4* src, uint32_t
         carry = shfl4(cur, 31);
         if (k >= nblk) continue;
         const uint4 out = s == 0 ? cur : funnel16(prv, cur, sw, sh);
-        const int32_t o = int32_t(16 * k) - int32_t(s);  // source offset of the block's first byte
-        if (o >= 0 && uint32_t(o) + 16 <= len) {
-            *reinterpret_cast<uint4*>(base + 16 * k) = out;
-        } else {
-            const uint32_t w[4] = {out.x, out.y, out.z, out.w};
-#pragma unroll
-            for (int b = 0; b < 16; ++b) {
-                const int32_t so = o + b;
-                if (so >= 0 && uint32_t(so) < len) base[16 * k + b] = uint8_t(w[b >> 2] >> (8 * (b & 3)));
-            }
+        const bool partial = (k == 0 && head_partial) || (k == tail_k && tail_partial);
+        if (!partial) *reinterpret_cast<uint4*>(base + 16 * k) = out;
+        if (k == 0) head = out;
+        if (k == tail_k) tail = out;
+    }
+    // the (at most two) partial blocks: lanes 0-15 write the head block's bytes,
+    // lanes 16-31 the tail block's, each lane one byte
+    const int hl = 0, tl = int(tail_k & 31);
+    const uint4 h = shfl4(head, hl), t = shfl4(tail, tl);
+    const bool is_tail = lane >= 16;
+    const uint32_t bi = uint32_t(lane & 15);
+    const uint32_t k = is_tail ? tail_k : 0u;
+    if ((is_tail ? tail_partial : head_partial) && !(is_tail && tail_k == 0 && head_partial)) {
+        const uint4 v = is_tail ? t : h;
+        const int32_t so = int32_t(16 * k + bi) - int32_t(s);  // source offset of this byte
+        if (so >= 0 && uint32_t(so) < len) {
+            const uint32_t w = bi < 4 ? v.x : bi < 8 ? v.y : bi < 12 ? v.z : v.w;
+            base[16 * k + bi] = uint8_t(w >> (8 * (bi & 3)));
         }
     }
 }
