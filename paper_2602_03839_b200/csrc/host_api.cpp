@@ -14,6 +14,9 @@
 #include <zlib.h>
 
 #include <algorithm>
+#include <array>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <atomic>
 #include <condition_variable>
@@ -49,8 +52,28 @@ using namespace pulse::dev;
 // ---------------------------------------------------------------------------------------------
 // library-owned objects
 // ---------------------------------------------------------------------------------------------
+// Allocator that leaves elements uninitialised: the big host buffers below are
+// fully overwritten (by copies or DMA), so zero-filling them is wasted time.
+template <class T>
+struct NoInit : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = NoInit<U>;
+    };
+    NoInit() = default;
+    template <class U>
+    NoInit(const NoInit<U>&) noexcept {}
+    template <class U, class... A>
+    void construct(U* p, A&&... a) {
+        if constexpr (sizeof...(A) == 0) ::new (static_cast<void*>(p)) U;
+        else ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+template <class T>
+using RawVec = std::vector<T, NoInit<T>>;
+
 struct pulse_bytes {
-    std::vector<uint8_t> v;
+    RawVec<uint8_t> v;
 };
 
 struct PatchTensor {
@@ -72,6 +95,26 @@ struct pulse_sha256_ctx {
 };
 
 namespace {
+
+// PULSE_TIMING=1: per-stage wall times of the host API calls on stderr.
+struct StageTimer {
+    const char* what;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    static bool on() {
+        static const bool v = [] {
+            const char* e = getenv("PULSE_TIMING");
+            return e && *e && *e != '0';
+        }();
+        return v;
+    }
+    void lap(const char* stage) {
+        if (!on()) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[pulse timing] %s %s %.1f ms\n", what, stage,
+                     std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    }
+};
 
 // A failure with the reference's exception class and message.
 struct Failure {
@@ -290,6 +333,23 @@ struct Engine {
     uint64_t plan_cap = 0;
     DevBuf arena_a, arena_b, idx64, vals, body, entries, result, misc, out64;
     std::mutex mu;
+    // decode pipeline: upload and download streams + per-group events (lazy)
+    cudaStream_t s_up = nullptr, s_dn = nullptr;
+    std::vector<cudaEvent_t> ev_up, ev_cmp;
+
+    void pipeline_streams(size_t groups) {
+        if (!s_up) {
+            cuda_check(cudaStreamCreateWithFlags(&s_up, cudaStreamNonBlocking), "stream");
+            cuda_check(cudaStreamCreateWithFlags(&s_dn, cudaStreamNonBlocking), "stream");
+        }
+        while (ev_up.size() < groups) {
+            cudaEvent_t a, b;
+            cuda_check(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "event");
+            cuda_check(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "event");
+            ev_up.push_back(a);
+            ev_cmp.push_back(b);
+        }
+    }
 
     explicit Engine(int dev) : device(dev) {
         cuda_check(cudaSetDevice(dev), "cudaSetDevice");
@@ -528,12 +588,13 @@ const char* repr_name(uint32_t r) {
 // Returns the body (per tensor [index payload][value payload] for tensors with
 // indices) and, per patch tensor, (index payload offset, length).
 struct Coded {
-    std::vector<uint8_t> body;
+    RawVec<uint8_t> body;
     std::vector<std::pair<uint64_t, uint64_t>> payload;  // per tensor; len 0 if no indices
     std::vector<uint64_t> val_off;                        // per tensor (valid when indices exist)
 };
 
 Coded device_index_code(Engine& E, const pulse_patch* p, bool with_values) {
+    StageTimer tm{"index_code"};
     const uint32_t T = uint32_t(p->tensors.size());
     Coded out;
     out.payload.assign(T, {0, 0});
@@ -564,23 +625,30 @@ Coded device_index_code(Engine& E, const pulse_patch* p, bool with_values) {
     const PlanDev& d = plan->dev;
     int64_t* didx = E.idx64.as<int64_t>(n);
     uint16_t* dval = E.vals.as<uint16_t>(n);
-    std::vector<int64_t> flat_idx(n);
-    std::vector<uint16_t> flat_val(n, 0);
-    for (uint32_t t = 0; t < T; ++t) {
+    RawVec<int64_t> flat_idx(n);
+    RawVec<uint16_t> flat_val(n);
+    pool().parallel_for(T, [&](size_t t) {  // per-tensor gather into the flat upload buffers
         const auto& tp = p->tensors[t];
-        std::copy(tp.indices.begin(), tp.indices.end(), flat_idx.begin() + start[t]);
-        if (with_values && tp.values.size() == tp.indices.size())
-            std::copy(tp.values.begin(), tp.values.end(), flat_val.begin() + start[t]);
-    }
+        const size_t m = tp.indices.size();
+        if (m) std::memcpy(flat_idx.data() + start[t], tp.indices.data(), m * 8);
+        if (with_values && tp.values.size() == m) {
+            if (m) std::memcpy(flat_val.data() + start[t], tp.values.data(), m * 2);
+        } else if (m) {
+            std::memset(flat_val.data() + start[t], 0, m * 2);
+        }
+    });
+    tm.lap("gather");
     E.stager.h2d(didx, flat_idx.data(), n * 8, E.stream);
     E.stager.h2d(dval, flat_val.data(), n * 2, E.stream);
     cuda_check(counted_copy(d.id_start, start.data(), (T + 1) * 8, cudaMemcpyHostToDevice, E.stream), "H2D");
+    tm.lap("h2d");
     const uint64_t cap = 10 * n + 64;
     uint8_t* dbody = E.body.as<uint8_t>(cap);
     auto* dent = E.entries.as<pulse_patch_entry>(T);
     auto* dres = E.result.as<pulse_result>(1);
     launch_encode_emit_idx64(d, p->representation, didx, dval, dbody, cap, dent, dres, E.stream);
     const pulse_result r = fetch_result(E, dres);
+    tm.lap("device K2");
     if (host_dim >= 0 && (r.status == PULSE_OK || r.err_tensor >= uint64_t(host_dim)))
         raise(PULSE_E_DIMENSION, "tensor '" + p->tensors[host_dim].name + "' is too large for 32-bit indices");
     if (r.status != PULSE_OK) {
@@ -594,6 +662,7 @@ Coded device_index_code(Engine& E, const pulse_patch* p, bool with_values) {
     out.body.resize(r.body_bytes);
     E.stager.d2h(out.body.data(), dbody, r.body_bytes, E.stream);
     E.sync();
+    tm.lap("d2h");
     for (const auto& e : ents) {
         out.payload[e.tensor] = {e.idx_off, e.idx_nbytes};
         out.val_off[e.tensor] = e.val_off;
@@ -623,9 +692,10 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
         n += tp.values.size();
     }
     pulse_plan* plan = E.get_plan(geom, std::max<uint64_t>({n, body_len / 3 + 1, 1}));
-    std::vector<uint8_t> body(body_len);
-    for (uint32_t t = 0; t < T; ++t)
+    RawVec<uint8_t> body(body_len);
+    pool().parallel_for(T, [&](size_t t) {
         if (lens[t]) std::memcpy(body.data() + ents[t].idx_off, pl[t], lens[t]);
+    });
     uint8_t* dbody = E.body.as<uint8_t>(body_len + 64);
     E.stager.h2d(dbody, body.data(), body_len, E.stream);
     auto* dent = E.entries.as<pulse_patch_entry>(T);
@@ -638,13 +708,15 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
         const std::string nm = r.err_tensor < T ? p->tensors[r.err_tensor].name : "?";
         raise(pulse_status(r.status), device_message(r, nm, nullptr));
     }
-    std::vector<int64_t> flat(n);
+    RawVec<int64_t> flat(n);
     E.stager.d2h(flat.data(), dout, n * 8, E.stream);
-    uint64_t o = 0;
-    for (auto& tp : p->tensors) {
-        tp.indices.assign(flat.begin() + o, flat.begin() + o + tp.values.size());
-        o += tp.values.size();
-    }
+    std::vector<uint64_t> at(T + 1, 0);
+    for (uint32_t t = 0; t < T; ++t) at[t + 1] = at[t] + p->tensors[t].values.size();
+    pool().parallel_for(T, [&](size_t t) {
+        auto& tp = p->tensors[t];
+        tp.indices.resize(tp.values.size());
+        if (!tp.indices.empty()) std::memcpy(tp.indices.data(), flat.data() + at[t], tp.indices.size() * 8);
+    });
 }
 
 void validate_for_write(const pulse_patch* p) {  // patch_file.hpp:31-42
@@ -869,9 +941,11 @@ pulse_status pulse_decode(const pulse_checkpoint* previous, const pulse_patch* p
             }
             target[k] = uint32_t(f);
         }
+        StageTimer tm{"decode"};
         if (T > 0) {
             Engine& E = engine();
             std::lock_guard<std::mutex> lk(E.mu);
+            tm.lap("host checks");
             std::vector<pulse_tensor_geom> geom(T);
             std::vector<uint64_t> numel(T);
             for (uint32_t i = 0; i < T; ++i) {
@@ -885,41 +959,105 @@ pulse_status pulse_decode(const pulse_checkpoint* previous, const pulse_patch* p
             const auto off = arena_offsets(numel, total);
             for (uint32_t k = 0; k < stop; ++k) n += patch->tensors[k].indices.size();
             uint16_t* A = E.arena_a.as<uint16_t>(total);
-            for (uint32_t i = 0; i < T; ++i) E.stager.h2d(A + off[i], previous->tensors[i].data, numel[i] * 2, E.stream);
+            // Page-locked base and output buffers and no host-side error: validate the
+            // whole patch first, then run upload | scatter | download as a pipeline
+            // over groups of tensors, so both copy engines work at once.
+            bool pipelined = stop == P && host_err.st == PULSE_OK;
+            for (uint32_t i = 0; i < T && pipelined; ++i)
+                if (numel[i] && !(is_pinned(previous->tensors[i].data) && is_pinned(out_data[i]))) pipelined = false;
+            if (!pipelined)
+                for (uint32_t i = 0; i < T; ++i) E.stager.h2d(A + off[i], previous->tensors[i].data, numel[i] * 2, E.stream);
             pulse_plan* plan = E.get_plan(geom, std::max<uint64_t>(n, 1));
             std::vector<const void*> pa(T);
             for (uint32_t i = 0; i < T; ++i) pa[i] = A + off[i];
             if (pulse_plan_bind(plan, 2, pa.data())) raise(PULSE_E_CUDA, pulse_last_error());
+            int64_t* didx = nullptr;
+            uint16_t* dval = nullptr;
+            pulse_patch_entry* dent = nullptr;
+            std::vector<uint64_t> at(stop + 1, 0);
             if (stop > 0 && n > 0) {
-                std::vector<int64_t> idx(n);
-                std::vector<uint16_t> val(n);
+                // gathered on host threads while the base snapshot's DMA (queued above) runs
+                RawVec<int64_t> idx(n);
+                RawVec<uint16_t> val(n);
                 std::vector<pulse_patch_entry> ents(stop);
-                uint64_t o = 0;
                 for (uint32_t k = 0; k < stop; ++k) {
                     const auto& tp = patch->tensors[k];
-                    std::copy(tp.indices.begin(), tp.indices.end(), idx.begin() + o);
-                    std::copy(tp.values.begin(), tp.values.end(), val.begin() + o);
                     ents[k] = pulse_patch_entry{target[k], 0, tp.indices.size(), 0, 0, 0};
-                    o += tp.indices.size();
+                    at[k + 1] = at[k] + tp.indices.size();
                 }
-                int64_t* didx = E.idx64.as<int64_t>(n);
-                uint16_t* dval = E.vals.as<uint16_t>(n);
+                pool().parallel_for(stop, [&](size_t k) {
+                    const auto& tp = patch->tensors[k];
+                    const size_t m = tp.indices.size();
+                    if (m) std::memcpy(idx.data() + at[k], tp.indices.data(), m * 8);
+                    if (m) std::memcpy(val.data() + at[k], tp.values.data(), m * 2);
+                });
+                didx = E.idx64.as<int64_t>(n);
+                dval = E.vals.as<uint16_t>(n);
                 E.stager.h2d(didx, idx.data(), n * 8, E.stream);
                 E.stager.h2d(dval, val.data(), n * 2, E.stream);
-                auto* dent = E.entries.as<pulse_patch_entry>(stop);
+                dent = E.entries.as<pulse_patch_entry>(stop);
                 cuda_check(counted_copy(dent, ents.data(), stop * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice,
                                            E.stream), "H2D");
                 auto* dres = E.result.as<pulse_result>(1);
-                launch_apply_idx64(plan->dev, didx, dval, dent, stop, 2, dres, E.stream);
+                // sequential: validate + scatter in one go; pipelined: validate only here
+                launch_apply_idx64(plan->dev, didx, dval, dent, stop, pipelined ? -1 : 2, dres, E.stream);
                 const pulse_result r = fetch_result(E, dres);
                 if (r.status != PULSE_OK) {
                     const auto& tp = patch->tensors[r.err_tensor];
                     raise(pulse_status(r.status), device_message(r, tp.name, &tp.indices));
                 }
             }
+            tm.lap(pipelined ? "gather+upload+validate" : "upload+gather+apply");
             if (host_err.st != PULSE_OK) raise(host_err.st, host_err.msg);
-            for (uint32_t i = 0; i < T; ++i) E.stager.d2h(out_data[i], A + off[i], numel[i] * 2, E.stream);
-            E.sync();
+            if (!pipelined) {
+                for (uint32_t i = 0; i < T; ++i) E.stager.d2h(out_data[i], A + off[i], numel[i] * 2, E.stream);
+                E.sync();
+            } else {
+                // groups of ~1 GiB in name order; patch entries (name order) are contiguous per group
+                const auto ord = sorted_order(previous);
+                std::vector<uint32_t> rank_of(T);
+                for (uint32_t r = 0; r < T; ++r) rank_of[ord[r]] = r;
+                std::vector<std::array<uint32_t, 4>> groups;  // [r0, r1) tensors, [k0, k1) entries
+                uint32_t k = 0;
+                for (uint32_t r0 = 0; r0 < T;) {
+                    uint32_t r1 = r0;
+                    uint64_t bytes = 0;
+                    while (r1 < T && (r1 == r0 || bytes + numel[ord[r1]] * 2 <= (1ull << 30))) bytes += numel[ord[r1++]] * 2;
+                    const uint32_t k0 = k;
+                    while (k < stop && rank_of[target[k]] < r1) ++k;
+                    groups.push_back({r0, r1, k0, k});
+                    r0 = r1;
+                }
+                if (k != stop) {  // entries not in name order: one group covers everything
+                    groups.assign(1, {0u, T, 0u, stop});
+                }
+                E.pipeline_streams(groups.size());
+                auto* gres = E.result.as<pulse_result>(1);
+                for (size_t g = 0; g < groups.size(); ++g) {
+                    const auto [r0, r1, k0, k1] = groups[g];
+                    for (uint32_t r = r0; r < r1; ++r) {
+                        const uint32_t i = ord[r];
+                        if (numel[i])
+                            cuda_check(counted_copy(A + off[i], previous->tensors[i].data, numel[i] * 2,
+                                                    cudaMemcpyHostToDevice, E.s_up), "H2D");
+                    }
+                    cuda_check(cudaEventRecord(E.ev_up[g], E.s_up), "event");
+                    cuda_check(cudaStreamWaitEvent(E.stream, E.ev_up[g], 0), "wait");
+                    if (k1 > k0)
+                        launch_apply_idx64(plan->dev, didx + at[k0], dval + at[k0], dent + k0, k1 - k0, 2, gres, E.stream);
+                    cuda_check(cudaEventRecord(E.ev_cmp[g], E.stream), "event");
+                    cuda_check(cudaStreamWaitEvent(E.s_dn, E.ev_cmp[g], 0), "wait");
+                    for (uint32_t r = r0; r < r1; ++r) {
+                        const uint32_t i = ord[r];
+                        if (numel[i])
+                            cuda_check(counted_copy(out_data[i], A + off[i], numel[i] * 2, cudaMemcpyDeviceToHost, E.s_dn),
+                                       "D2H");
+                    }
+                }
+                cuda_check(cudaStreamSynchronize(E.s_dn), "D2H sync");
+                cuda_check(cudaStreamSynchronize(E.stream), "stream sync");
+            }
+            tm.lap(pipelined ? "pipeline" : "download");
         } else if (host_err.st != PULSE_OK) {
             raise(host_err.st, host_err.msg);
         }
@@ -978,25 +1116,44 @@ pulse_status pulse_write_patch_bytes(const pulse_patch* p, pulse_bytes** out) {
         validate_for_write(p);
         const char* rname = repr_name(p->representation);
         if (p->codec > PULSE_GZIP6) raise(PULSE_E_ARGUMENT, "unknown codec");
+        StageTimer tm{"write_patch_bytes"};
         Coded c;
         {
             Engine& E = engine();
             std::lock_guard<std::mutex> lk(E.mu);
             c = device_index_code(E, p, true);
         }
+        tm.lap("index coding");
         const size_t T = p->tensors.size();
+        // per tensor: its index blob and value blob (identity codec: straight out
+        // of the device body, no intermediate copy)
         std::vector<std::vector<uint8_t>> ib(T), vb(T);
+        std::vector<const uint8_t*> ip(T), vp(T);
+        std::vector<uint64_t> in(T), vn(T);
         pool().parallel_for(T, [&](size_t t) {  // blobs are independent: same bytes in any order
             const auto [o, len] = c.payload[t];
+            const bool body_vals = len || p->tensors[t].values.empty();
+            if (p->codec == PULSE_IDENTITY && body_vals) {
+                ip[t] = c.body.data() + o;
+                in[t] = len;
+                vp[t] = c.body.data() + c.val_off[t];
+                vn[t] = p->tensors[t].values.size() * 2;
+                return;
+            }
             ib[t] = codec_compress(c.body.data() + o, len, p->codec);
-            if (len || p->tensors[t].values.empty()) {
+            if (body_vals) {
                 const uint8_t* v = c.body.data() + c.val_off[t];
                 vb[t] = codec_compress(v, p->tensors[t].values.size() * 2, p->codec);
             } else {
                 const auto raw = value_payload(p->tensors[t].values);
                 vb[t] = codec_compress(raw.data(), raw.size(), p->codec);
             }
+            ip[t] = ib[t].data();
+            in[t] = ib[t].size();
+            vp[t] = vb[t].data();
+            vn[t] = vb[t].size();
         });
+        tm.lap("codec");
         nlohmann::json header;
         header["anchor_step"] = p->anchor_step;
         header["base_step"] = p->base_step;
@@ -1010,8 +1167,8 @@ pulse_status pulse_write_patch_bytes(const pulse_patch* p, pulse_bytes** out) {
             nlohmann::json e = {{"name", tp.name},
                                 {"shape", tp.shape},
                                 {"count", tp.indices.size()},
-                                {"index_nbytes", ib[t].size()},
-                                {"value_nbytes", vb[t].size()}};
+                                {"index_nbytes", in[t]},
+                                {"value_nbytes", vn[t]}};
             if (p->representation == PULSE_COO_DOWNSCALED) {
                 e["row_bits"] = 8;
                 e["col_bits"] = 16;
@@ -1020,9 +1177,11 @@ pulse_status pulse_write_patch_bytes(const pulse_patch* p, pulse_bytes** out) {
         }
         const std::string js = header.dump();
         auto res = std::make_unique<pulse_bytes>();
-        size_t total = 16 + js.size();
-        for (size_t t = 0; t < T; ++t) total += ib[t].size() + vb[t].size();
-        res->v.resize(total);
+        tm.lap("header");
+        std::vector<uint64_t> at(T + 1);
+        at[0] = 16 + js.size();
+        for (size_t t = 0; t < T; ++t) at[t + 1] = at[t] + in[t] + vn[t];
+        res->v.resize(at[T]);
         uint8_t* w = res->v.data();
         std::memcpy(w, "PULP", 4);
         const uint32_t ver = 1;
@@ -1030,13 +1189,11 @@ pulse_status pulse_write_patch_bytes(const pulse_patch* p, pulse_bytes** out) {
         for (int i = 0; i < 4; ++i) w[4 + i] = uint8_t(ver >> (8 * i));
         for (int i = 0; i < 8; ++i) w[8 + i] = uint8_t(hl >> (8 * i));
         std::memcpy(w + 16, js.data(), js.size());
-        size_t pos = 16 + js.size();
-        for (size_t t = 0; t < T; ++t) {
-            std::memcpy(w + pos, ib[t].data(), ib[t].size());
-            pos += ib[t].size();
-            std::memcpy(w + pos, vb[t].data(), vb[t].size());
-            pos += vb[t].size();
-        }
+        pool().parallel_for(T, [&](size_t t) {
+            if (in[t]) std::memcpy(w + at[t], ip[t], in[t]);
+            if (vn[t]) std::memcpy(w + at[t] + in[t], vp[t], vn[t]);
+        });
+        tm.lap("assemble");
         *out = res.release();
     });
 }
@@ -1069,7 +1226,15 @@ pulse_status pulse_read_patch_bytes(const uint8_t* bytes, uint64_t n, pulse_patc
         }
         pos += hl;
         auto p = std::make_unique<pulse_patch>();
-        std::vector<std::vector<uint8_t>> payloads;
+        // Pass 1 (sequential, cheap): header fields and blob bounds of every tensor.
+        // The first failure is recorded, not raised: an earlier tensor's codec
+        // error must still win, as in the reference's one-tensor-at-a-time read.
+        struct Blob {
+            uint64_t count, ipos, inb, vpos, vnb;
+        };
+        std::vector<Blob> blobs;
+        pulse_status stop_st = PULSE_OK;
+        std::string stop_msg;
         try {
             p->anchor_step = header.at("anchor_step").get<int64_t>();
             p->base_step = header.at("base_step").get<int64_t>();
@@ -1093,45 +1258,81 @@ pulse_status pulse_read_patch_bytes(const uint8_t* bytes, uint64_t n, pulse_patc
             else if (rn == "COO_INT32") p->representation = PULSE_COO_INT32;
             else if (rn == "FLAT_INT32") p->representation = PULSE_FLAT_INT32;
             else raise(PULSE_E_FORMAT, "unknown representation name: " + rn);
+        } catch (const nlohmann::json::exception& e) {
+            raise(PULSE_E_FORMAT, std::string("patch header schema error: ") + e.what());
+        }
+        try {
             for (const auto& entry : header.at("tensors")) {
                 PatchTensor tp;
                 tp.name = entry.at("name").get<std::string>();
                 tp.shape = entry.at("shape").get<std::vector<int64_t>>();
                 for (auto e : tp.shape)
                     if (e <= 0) raise(PULSE_E_FORMAT, "non-positive extent in tensor " + tp.name);
-                const auto count = entry.at("count").get<uint64_t>();
-                const auto inb = entry.at("index_nbytes").get<uint64_t>();
-                const auto vnb = entry.at("value_nbytes").get<uint64_t>();
+                Blob b{};
+                b.count = entry.at("count").get<uint64_t>();
+                b.inb = entry.at("index_nbytes").get<uint64_t>();
+                b.vnb = entry.at("value_nbytes").get<uint64_t>();
                 if (p->representation == PULSE_COO_DOWNSCALED) {
                     if (entry.at("row_bits").get<int>() != 8 || entry.at("col_bits").get<int>() != 16)
                         raise(PULSE_E_FORMAT, "unsupported delta widths for tensor " + tp.name);
                 }
-                if (inb > n - pos) raise(PULSE_E_TRUNCATION, "index blob truncated");
-                auto ip = codec_decompress(bytes + pos, inb, p->codec);
-                pos += inb;
-                if (vnb > n - pos) raise(PULSE_E_TRUNCATION, "value blob truncated");
-                auto vp = codec_decompress(bytes + pos, vnb, p->codec);
-                pos += vnb;
-                if (vp.size() != count * 2)
-                    raise(PULSE_E_FORMAT, "value payload length does not match change count for tensor " + tp.name);
-                tp.values.resize(count);
-                for (uint64_t i = 0; i < count; ++i) tp.values[i] = uint16_t(vp[2 * i] | (vp[2 * i + 1] << 8));
-                payloads.push_back(std::move(ip));
+                if (b.inb > n - pos) raise(PULSE_E_TRUNCATION, "index blob truncated");
+                b.ipos = pos;
+                pos += b.inb;
+                if (b.vnb > n - pos) raise(PULSE_E_TRUNCATION, "value blob truncated");
+                b.vpos = pos;
+                pos += b.vnb;
+                blobs.push_back(b);
                 p->tensors.push_back(std::move(tp));
             }
         } catch (const nlohmann::json::exception& e) {
-            raise(PULSE_E_FORMAT, std::string("patch header schema error: ") + e.what());
+            stop_st = PULSE_E_FORMAT;
+            stop_msg = std::string("patch header schema error: ") + e.what();
+        } catch (const Failure& f) {
+            stop_st = f.st;
+            stop_msg = f.msg;
         }
+        // Pass 2 (parallel over tensors): decompress, values (LE u16, memcpy on
+        // this little-endian host).  The identity codec's index blobs are used in place.
+        const size_t T = blobs.size();
+        std::vector<std::vector<uint8_t>> payloads(T);
+        std::vector<const uint8_t*> pl(T);
+        std::vector<uint64_t> lens(T);
+        std::vector<pulse_status> tst(T, PULSE_OK);
+        std::vector<std::string> tmsg(T);
+        pool().parallel_for(T, [&](size_t t) {
+            const Blob& b = blobs[t];
+            auto& tp = p->tensors[t];
+            try {
+                if (p->codec == PULSE_IDENTITY) {
+                    pl[t] = bytes + b.ipos;
+                    lens[t] = b.inb;
+                    if (b.vnb != b.count * 2)
+                        raise(PULSE_E_FORMAT, "value payload length does not match change count for tensor " + tp.name);
+                    tp.values.resize(b.count);
+                    if (b.count) std::memcpy(tp.values.data(), bytes + b.vpos, b.count * 2);
+                } else {
+                    payloads[t] = codec_decompress(bytes + b.ipos, b.inb, p->codec);
+                    pl[t] = payloads[t].data();
+                    lens[t] = payloads[t].size();
+                    const auto vp = codec_decompress(bytes + b.vpos, b.vnb, p->codec);
+                    if (vp.size() != b.count * 2)
+                        raise(PULSE_E_FORMAT, "value payload length does not match change count for tensor " + tp.name);
+                    tp.values.resize(b.count);
+                    if (b.count) std::memcpy(tp.values.data(), vp.data(), b.count * 2);
+                }
+            } catch (const Failure& f) {
+                tst[t] = f.st;
+                tmsg[t] = f.msg;
+            }
+        });
+        for (size_t t = 0; t < T; ++t)
+            if (tst[t] != PULSE_OK) raise(tst[t], tmsg[t]);
+        if (stop_st != PULSE_OK) raise(stop_st, stop_msg);
         if (pos != n) raise(PULSE_E_FORMAT, "patch has trailing bytes");
         if (!p->tensors.empty()) {
             Engine& E = engine();
             std::lock_guard<std::mutex> lk(E.mu);
-            std::vector<const uint8_t*> pl;
-            std::vector<uint64_t> lens;
-            for (auto& v : payloads) {
-                pl.push_back(v.data());
-                lens.push_back(v.size());
-            }
             device_decode_payloads(E, p.get(), pl, lens);
         }
         *out = p.release();
@@ -1406,7 +1607,8 @@ pulse_status pulse_compress(const uint8_t* data, uint64_t n, uint32_t codec, pul
     return guarded([&] {
         if (!out) raise(PULSE_E_ARGUMENT, "null argument");
         auto b = std::make_unique<pulse_bytes>();
-        b->v = codec_compress(data, n, codec);
+        const auto z = codec_compress(data, n, codec);
+        b->v.assign(z.begin(), z.end());
         *out = b.release();
     });
 }
@@ -1414,7 +1616,8 @@ pulse_status pulse_decompress(const uint8_t* data, uint64_t n, uint32_t codec, p
     return guarded([&] {
         if (!out) raise(PULSE_E_ARGUMENT, "null argument");
         auto b = std::make_unique<pulse_bytes>();
-        b->v = codec_decompress(data, n, codec);
+        const auto z = codec_decompress(data, n, codec);
+        b->v.assign(z.begin(), z.end());
         *out = b.release();
     });
 }

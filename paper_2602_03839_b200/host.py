@@ -180,9 +180,30 @@ def write_patch_bytes(patch) -> bytes:
     return _take(b)
 
 
-def read_patch_handle(data: bytes) -> PatchHandle:
+
+def write_patch_array(patch) -> np.ndarray:
+    """write_patch_bytes into a uint8 ndarray (the reference's Bytes is a byte
+    vector): one memcpy into a fresh array, which NumPy backs with huge pages --
+    cheaper than building a 100s-of-MB bytes object."""
+    h = patch if isinstance(patch, PatchHandle) else PatchHandle.from_patch(patch)
+    b = C.c_void_p()
+    N.check(N.lib.pulse_write_patch_bytes(h.ptr, C.byref(b)))
+    n = N.lib.pulse_bytes_size(b)
+    out = np.empty(n, np.uint8)
+    if n:
+        C.memmove(out.ctypes.data, N.lib.pulse_bytes_data(b), n)
+    N.lib.pulse_bytes_free(b)
+    return out
+
+
+def read_patch_handle(data) -> PatchHandle:
+    """read_patch_bytes into a library patch handle; `data` is bytes or a uint8 ndarray."""
     out = C.c_void_p()
-    N.check(N.lib.pulse_read_patch_bytes(data, len(data), C.byref(out)))
+    if isinstance(data, np.ndarray):
+        a = np.ascontiguousarray(data, dtype=np.uint8)
+        N.check(N.lib.pulse_read_patch_bytes(C.cast(a.ctypes.data, C.c_char_p), a.size, C.byref(out)))
+    else:
+        N.check(N.lib.pulse_read_patch_bytes(data, len(data), C.byref(out)))
     return PatchHandle(out)
 
 
@@ -286,6 +307,8 @@ def bench_e2e(args, mine, prev_dev, curr_dev, world, rank, steps=None, warmup=3)
     does).  The snapshots are the same bytes as the device-resident run
     (copied out once, untimed).  Wall-clock per step, max over ranks; the
     bytes moved are the library's own counters (pulse_transfer_stats)."""
+    import os
+    import sys
     import time
 
     import torch
@@ -310,13 +333,25 @@ def bench_e2e(args, mine, prev_dev, curr_dev, world, rank, steps=None, warmup=3)
     outs = [a_out[int(offs[i]):int(offs[i + 1])] for i in range(len(sizes))]
     steps = steps or max(1, min(args.steps, 3))
 
-    def step(k):
+    parts = {"encode": 0.0, "write": 0.0, "read": 0.0, "decode": 0.0}
+
+    def step(k, timed=False):
         # alternate direction like the device run: prev->curr, then curr->prev
         c, p = (1, 0) if k % 2 == 0 else (0, 1)
+        t0 = time.perf_counter()
         h = encode_handle(ck[c], ck[p], args.repr, IDENTITY, views=(views[c], views[p]))
-        wire = write_patch_bytes(h)
+        t1 = time.perf_counter()
+        wire = write_patch_array(h)
+        t2 = time.perf_counter()
+        if os.environ.get("PULSE_TIMING"):
+            print(f"[pulse timing] e2e write (incl. copy to bytes) {1e3 * (t2 - t1):.1f} ms", file=sys.stderr)
         back = read_patch_handle(wire)
+        t3 = time.perf_counter()
         decode_into(ck[p], back, outs, verify_hash=False, view=views[p])
+        t4 = time.perf_counter()
+        if timed:
+            for key, dt_ in zip(parts, (t1 - t0, t2 - t1, t3 - t2, t4 - t3)):
+                parts[key] += dt_
         return c
 
     for k in range(warmup):
@@ -326,7 +361,7 @@ def bench_e2e(args, mine, prev_dev, curr_dev, world, rank, steps=None, warmup=3)
     transfer_stats(reset=True)
     t0 = time.perf_counter()
     for k in range(steps):
-        last = step(k)
+        last = step(k, timed=True)
     dt = time.perf_counter() - t0
     h2d, d2h = transfer_stats()
     ok = bool(np.array_equal(a_out, (a_curr if last == 1 else a_prev)))
@@ -344,5 +379,6 @@ def bench_e2e(args, mine, prev_dev, curr_dev, world, rank, steps=None, warmup=3)
     return {"value": round(2 * d_total / s_step / 1e9, 4), "unit": "GB/s",
             "h2d_bytes_per_step": int(h2d // steps), "d2h_bytes_per_step": int(d2h // steps),
             "steps": steps, "warmup": warmup, "s_per_step": round(s_step, 4), "verified": ok,
-            "path": "pulse_encode -> pulse_write_patch_bytes -> pulse_read_patch_bytes -> "
+            "parts_s": {k_: round(v / steps, 4) for k_, v in parts.items()},
+            "path": "pulse_encode -> pulse_write_patch_bytes (into a uint8 array) -> pulse_read_patch_bytes -> "
                     "pulse_decode(verify_hash=false); identity codec; pinned host snapshots; wall clock"}

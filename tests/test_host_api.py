@@ -56,6 +56,9 @@ def test_encode_write_matches_reference_pulp(golden, repr_):
                 continue
             h = H.encode_handle(mirror(curr), mirror(prev), repr_, codec)
             assert H.write_patch_bytes(h) == want, (name, repr_, codec)
+            arr = H.write_patch_array(h)
+            assert arr.tobytes() == want
+            assert H.read_patch_handle(arr).to_patch().total_changes() == H.read_patch_bytes(want).total_changes()
 
 
 @pytest.mark.gpu
