@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpulse_cuda.so")
+# PULSE_LIB: an alternative build of the same library (experiment variants)
+LIB_PATH = os.environ.get("PULSE_LIB") or os.path.join(HERE, "libpulse_cuda.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2602_03839_b200.build` "

@@ -220,7 +220,16 @@ __global__ void __launch_bounds__(kThreads, 4) k1_ticket(K1Args k) {
 // a ticket held by a stalled CTA.
 // ---------------------------------------------------------------------------------------------
 namespace tma {
-constexpr int kStages = 4;
+#ifndef PULSE_K1_STAGES
+#define PULSE_K1_STAGES 4
+#endif
+#ifndef PULSE_K1_BUFS
+#define PULSE_K1_BUFS 3
+#endif
+#ifndef PULSE_K1_RECCAP
+#define PULSE_K1_RECCAP 1344
+#endif
+constexpr int kStages = PULSE_K1_STAGES;
 constexpr uint32_t kSubElems = 8192;                 // elements per stage (16 KiB + 16 KiB)
 constexpr uint32_t kSubs = kTicketElems / kSubElems; // 8 sub-tiles per ticket
 constexpr int kConsumerWarps = 8;
@@ -230,11 +239,14 @@ constexpr int kLbWarps = 4;                          // warps 9..12
 constexpr int kLbFirst = kConsumerWarps + 1;
 constexpr int kLbThreads = kLbWarps * 32;
 constexpr int kThreadsTotal = (kConsumerWarps + 1 + kLbWarps) * 32;  // 416
-constexpr uint32_t kRecCap = 1344;                   // record mode: staged changed 16-byte vectors per buffer
-constexpr uint32_t kStageCap = 8192;                 // element mode: staged changed elements per buffer
+constexpr uint32_t kRecCap = PULSE_K1_RECCAP;        // record mode: staged changed 16-byte vectors per buffer
+#ifndef PULSE_K1_STAGECAP
+#define PULSE_K1_STAGECAP 8192
+#endif
+constexpr uint32_t kStageCap = PULSE_K1_STAGECAP;    // element mode: staged changed elements per buffer
 constexpr uint32_t kDenseTicket = 3072;              // changes above which the next ticket uses element mode
 enum : uint32_t { kModeRecords = 0, kModeElements = 1 };
-constexpr int kBufs = 3;                             // ticket staging buffers (consumers may run ahead)
+constexpr int kBufs = PULSE_K1_BUFS;                 // ticket staging buffers (consumers may run ahead)
 constexpr uint32_t kChunks = kSubs * kConsumerWarps; // (sub-tile, warp) chunks per ticket
 constexpr uint32_t kBarLb = 2;                       // named barrier id of the look-back group
 static_assert(kVecPerWarp % 32 == 0, "whole vectors per lane");

@@ -4,6 +4,8 @@ import os
 import re
 import subprocess
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "pulse_cuda.h")
 LIB = os.path.join(ROOT, "paper_2602_03839_b200", "libpulse_cuda.so")
@@ -33,3 +35,24 @@ def test_library_loads_and_binding_resolves():
     assert N.lib.pulse_version().startswith(b"pulse-b200")
     for name in declared():
         assert hasattr(N.lib, name)
+
+
+def test_plain_c_consumer_compiles(tmp_path):
+    """include/pulse_cuda.h is a C header: a C11 program using it builds warning-free."""
+    import subprocess
+    src = os.path.join(ROOT, "examples", "c_abi_roundtrip.c")
+    out = tmp_path / "c_abi_roundtrip.o"
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-Werror", "-c", "-I", os.path.join(ROOT, "include"),
+                        src, "-o", str(out)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+def test_plain_c_consumer_round_trip():
+    import subprocess
+    exe = os.path.join(ROOT, "tests", "_bin", "c_abi_roundtrip")
+    if not os.path.exists(exe):
+        pytest.skip("examples/c_abi_roundtrip not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "C ABI round trip OK" in r.stdout

@@ -196,3 +196,36 @@ def test_sparsity_errors_match_reference():
     with pytest.raises(H.PulseError) as e:
         H.sparsity(a, H.Checkpoint(0, [H.Tensor("w", (2, 1), np.zeros(2, np.uint16))]))
     assert e.value.kind == "ShapeMismatchError"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("repr_", [0, 2])
+def test_decode_pipeline_with_pinned_buffers(golden, repr_):
+    """Page-locked base and output buffers take the validate-then-pipelined
+    (upload | scatter | download) decode; results equal the reference target,
+    and a failing decode leaves the outputs untouched."""
+    torch = pytest.importorskip("torch")
+    for name in ("roundtrip_s1", "esc_rows", "handcrafted"):
+        prev, curr, _ = golden.case(name)
+        pins = [torch.from_numpy(t.data.view(np.int16).copy()).pin_memory() for t in prev.tensors]
+        outs = [torch.empty_like(p).pin_memory() for p in pins]
+        pc = H.Checkpoint(prev.step, [H.Tensor(t.name, t.shape, p.numpy().view(np.uint16))
+                                      for t, p in zip(prev.tensors, pins)])
+        h = H.encode_handle(mirror(curr), mirror(prev), repr_, 0)
+        back = H.read_patch_handle(H.write_patch_array(h))
+        H.decode_into(pc, back, [o.numpy().view(np.uint16) for o in outs], verify_hash=True)
+        want = {t.name: t.data for t in curr.tensors}
+        for t, o in zip(prev.tensors, outs):
+            assert np.array_equal(o.numpy().view(np.uint16), want[t.name]), (name, t.name)
+        # corrupt: a patch whose shape no longer fits -> error, outputs unchanged
+        sentinel = [o.clone() for o in outs]
+        bad = H.read_patch_handle(H.write_patch_array(h)).to_patch()
+        if bad.tensors:
+            t0 = bad.tensors[0]
+            bad.tensors[0] = H.TensorPatch(t0.name, t0.shape, t0.indices.copy(), t0.values)
+            bad.tensors[0].indices[-1] = np.prod(t0.shape) + 5   # past the tensor
+            with pytest.raises(H.PulseError):
+                H.decode_into(pc, H.PatchHandle.from_patch(bad), [o.numpy().view(np.uint16) for o in outs],
+                              verify_hash=False)
+            for o, s_ in zip(outs, sentinel):
+                assert torch.equal(o, s_)
