@@ -434,11 +434,12 @@ def run_pulse(args):
         # dominant kernel K1: reads both snapshots (4 B/elem) + writes 6 B per change (u32 idx + u16 value)
         k1_bytes = 4 * D_el + 6 * state["changes"]
         k1_gbs = k1_bytes / (scan_ms / 1e3) / 1e9
-        # our launches per step: K1 (k1_tma, k1_finalize); K2 (k2_scan_escapes [COO only], k2_layout,
-        # k2_emit); FLAT carry [sharded FLAT only]; apply (d_layout, f_pass agg, f_range_scan, f_pass apply,
+        # our launches per step: K1 (k1_tma, k1_finalize); K2 (COO: optimistic k2_layout + k2_emit, then
+        # k2_scan_escapes / k2_layout / k2_emit that return at once unless an escape was seen; int32:
+        # k2_layout, k2_emit); FLAT carry [sharded FLAT only]; apply (d_layout, f_pass agg, f_range_scan, f_pass apply,
         # f_pass restore, d_clear_status, general-path kernels that exit at once on the fast path
         # [COO: d_rows, d_col_layout, d_cols, d_assemble; int32: d_fixed], d_scatter, d_finalize)
-        n_emit = 3 if args.repr == 0 else 2
+        n_emit = 5 if args.repr == 0 else 2
         n_carry = 1 if (world > 1 and args.repr == 2) else 0
         n_apply = 12 if args.repr == 0 else 9
         line = {

@@ -427,8 +427,9 @@ __device__ __noinline__ void k2a_span(const EntryMap& em, uint32_t repr, uint64_
 // =============================================================================================
 __global__ void __launch_bounds__(kThreads, 3)
 k2_scan_escapes(EntryMap em, uint32_t repr, uint64_t* __restrict__ range_cnt, uint32_t* __restrict__ t_resc,
-                uint32_t* __restrict__ t_cesc, uint64_t* __restrict__ err) {
+                uint32_t* __restrict__ t_cesc, uint64_t* __restrict__ err, const uint32_t* __restrict__ run_if) {
     extern __shared__ __align__(16) uint8_t smem[];
+    if (run_if && *(volatile const uint32_t*)run_if == 0) return;
     const uint64_t n = k2_entries(em);
     const uint64_t n_ranges = (n + kRangeEntries - 1) / kRangeEntries;
     const bool coo = repr == PULSE_COO_DOWNSCALED;
@@ -569,6 +570,8 @@ struct LayoutArgs {
     pulse_result* result;
     uint64_t* err;
     uint64_t cap;  // K1 capacity (mode A); ~0 for mode B
+    const uint32_t* run_if;  // run only if *run_if != 0 (exact re-run after an optimistic pass)
+    bool optimistic;         // COO: lay out assuming no escapes (range_pre pre-zeroed)
 };
 
 __device__ __forceinline__ int64_t entry_local(const EntryMap& em, uint64_t i) {
@@ -577,6 +580,7 @@ __device__ __forceinline__ int64_t entry_local(const EntryMap& em, uint64_t i) {
 }
 
 __global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
+    if (a.run_if && *(volatile const uint32_t*)a.run_if == 0) return;
     __shared__ uint64_t s_tmp[32];
     __shared__ int64_t s_max[32];
     const int tid = threadIdx.x;
@@ -587,7 +591,7 @@ __global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
 
     // (1) COO_DOWNSCALED: exclusive scan of the per-range escape counts (each
     // thread sums a contiguous block, one CTA scan, then writes its block)
-    if (coo && !overflow) {
+    if (coo && !overflow && !a.optimistic) {
         const uint64_t n_ranges = (n + kRangeEntries - 1) / kRangeEntries;
         const uint64_t per = (n_ranges + kLayoutThreads - 1) / kLayoutThreads;
         const uint64_t q0 = min(n_ranges, per * tid), q1 = min(n_ranges, q0 + per);
@@ -844,8 +848,10 @@ __device__ __noinline__ void k2b_span(const EntryMap& em, uint32_t repr, uint64_
 __global__ void __launch_bounds__(kThreads)
 k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
         const ulonglong2* __restrict__ range_pre, const uint16_t* __restrict__ vals,
-        const pulse_result* __restrict__ result, uint8_t* __restrict__ body) {
+        const pulse_result* __restrict__ result, uint8_t* __restrict__ body,
+        const uint32_t* __restrict__ run_if, uint32_t* __restrict__ esc_flag) {
     extern __shared__ __align__(16) uint8_t smem[];
+    if (run_if && *(volatile const uint32_t*)run_if == 0) return;
     if (result->status != 0) return;
     const uint64_t n = k2_entries(em);
     const uint64_t n_ranges = (n + kRangeEntries - 1) / kRangeEntries;
@@ -886,6 +892,7 @@ k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
         const uint4* sval = reinterpret_cast<const uint4*>(ws + 2 * kSIdx + b * kSVal);
         if (!staged || !c.fast) {
             k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
+            if (esc_flag && (R | Cc) && lane == 0) atomicExch(esc_flag, 1u);  // optimistic pass: escapes seen
             cur = nx;
             b ^= 1;
             continue;
@@ -969,6 +976,7 @@ k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
             unstage<1>(body + tl.val_off + 2 * j0, sval, 2 * len);
         }
         __syncwarp();
+        if (esc_flag && (R | Cc) && lane == 0) atomicExch(esc_flag, 1u);  // optimistic pass: escapes seen
         cur = nx;
         b ^= 1;
     }
@@ -998,11 +1006,6 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
         occ_scan = std::max(occ_scan, 1);
         occ_emit = std::max(occ_emit, 1);
     }
-    if (repr == PULSE_COO_DOWNSCALED || validate_args)
-        {
-        k2_scan_escapes<<<unsigned(sm_count() * occ_scan), kThreads, kWarps * kScanWarpSmem, s>>>(em, repr, p.range_cnt, p.t_resc, p.t_cesc, p.err);
-        PULSE_LAUNCHED("k2_scan_escapes", s);
-        }
     LayoutArgs a;
     a.range_cnt = p.range_cnt;
     a.range_pre = p.range_pre;
@@ -1021,11 +1024,41 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
     a.result = result;
     a.err = p.err;
     a.cap = cap;
-    k2_layout<<<1, kLayoutThreads, 0, s>>>(a);
-    PULSE_LAUNCHED("k2_layout", s);
-    k2_emit<<<unsigned(sm_count() * occ_emit), kThreads, kWarps * kEmitWarpSmem, s>>>(em, repr, p.tlay, p.range_pre, vals,
-                                                                             result, body);
-    PULSE_LAUNCHED("k2_emit", s);
+    a.run_if = nullptr;
+    a.optimistic = false;
+    const unsigned g_scan = unsigned(sm_count() * occ_scan), g_emit = unsigned(sm_count() * occ_emit);
+    auto exact = [&](const uint32_t* run_if) {  // K2a escape counts -> layout -> emit
+        if (repr == PULSE_COO_DOWNSCALED || validate_args) {
+            k2_scan_escapes<<<g_scan, kThreads, kWarps * kScanWarpSmem, s>>>(em, repr, p.range_cnt, p.t_resc, p.t_cesc,
+                                                                            p.err, run_if);
+            PULSE_LAUNCHED("k2_scan_escapes", s);
+        }
+        a.run_if = run_if;
+        a.optimistic = false;
+        k2_layout<<<1, kLayoutThreads, 0, s>>>(a);
+        PULSE_LAUNCHED("k2_layout", s);
+        k2_emit<<<g_emit, kThreads, kWarps * kEmitWarpSmem, s>>>(em, repr, p.tlay, p.range_pre, vals, result, body,
+                                                                 run_if, nullptr);
+        PULSE_LAUNCHED("k2_emit", s);
+    };
+    if (repr == PULSE_COO_DOWNSCALED && !validate_args && !em.idx64) {
+        // Optimistic COO_DOWNSCALED: lay out and emit assuming no entry needs an
+        // escape (none does on these shapes at <= 99.9% sparsity); the emit flags
+        // any escape it meets, and only then the exact pipeline re-runs (its three
+        // kernels return at once otherwise).
+        uint32_t* esc = p.d_flags + 2;
+        cudaMemsetAsync(esc, 0, sizeof(uint32_t), s);
+        cudaMemsetAsync(p.range_pre, 0, (p.cap / kRangeEntries + 2) * sizeof(ulonglong2), s);
+        a.optimistic = true;
+        k2_layout<<<1, kLayoutThreads, 0, s>>>(a);
+        PULSE_LAUNCHED("k2_layout (optimistic)", s);
+        k2_emit<<<g_emit, kThreads, kWarps * kEmitWarpSmem, s>>>(em, repr, p.tlay, p.range_pre, vals, result, body,
+                                                                 nullptr, esc);
+        PULSE_LAUNCHED("k2_emit (optimistic)", s);
+        exact(esc);
+    } else {
+        exact(nullptr);
+    }
 }
 
 void launch_encode_emit(const PlanDev& p, uint32_t repr, const pulse_scan_summary* gathered, uint32_t n_ranks,
