@@ -285,8 +285,9 @@ struct Smem {
             uint16_t val[kStageCap];
         } el;
     } stg[kBufs];
-    uint32_t chunk_off[kBufs][kChunks];  // element mode: where each (sub, warp) chunk was staged
+    uint32_t chunk_off[kBufs][kChunks];  // where each (sub, warp) chunk was staged (first record / element)
     uint32_t chunk_cnt[kBufs][kChunks];  // changed elements per (sub, warp) chunk
+    uint32_t chunk_ebase[kChunks];       // record mode (flush group): element scan at each chunk's first record
     uint32_t mode[kBufs];                // staging layout of the ticket in each buffer
     uint32_t chunk_pre[kChunks + 1]; // ordered prefix (look-back group)
     uint32_t fill[kBufs];            // staging bump allocator (records or elements)
@@ -551,28 +552,13 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                 continue;
             }
 
-            // element order inside the warp slice: (j, lane, q); packed 16-bit scans for j pairs
-            const uint32_t lo = __popc(m[0]) | (__popc(m[1]) << 16);
-            const uint32_t hi = __popc(m[2]) | (__popc(m[3]) << 16);
-            uint32_t ilo = lo, ihi = hi;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t a1 = __shfl_up_sync(0xffffffffu, ilo, off);
-                const uint32_t a2 = __shfl_up_sync(0xffffffffu, ihi, off);
-                if (lane >= off) {
-                    ilo += a1;
-                    ihi += a2;
-                }
-            }
-            const uint32_t tlo = __shfl_sync(0xffffffffu, ilo, 31), thi = __shfl_sync(0xffffffffu, ihi, 31);
-            const uint32_t t0 = tlo & 0xFFFF, t1 = tlo >> 16, t2 = thi & 0xFFFF, t3 = thi >> 16;
-            const uint32_t total = t0 + t1 + t2 + t3;
             const uint32_t chunk = d.sub * kConsumerWarps + warp;
-            const uint32_t exlo = ilo - lo, exhi = ihi - hi;
-            const uint32_t pj[4] = {exlo & 0xFFFF, t0 + (exlo >> 16), t0 + t1 + (exhi & 0xFFFF),
-                                    t0 + t1 + t2 + (exhi >> 16)};
             if (tmode == kModeRecords) {
-                // one record per changed vector, records in (j, lane) order
+                // one record per changed vector, records in (j, lane) order = element
+                // order; the flush group derives each record's element offset, so the
+                // consumers only need the chunk total (one warp reduction)
+                const uint32_t total = __reduce_add_sync(0xffffffffu, __popc(m[0]) + __popc(m[1]) + __popc(m[2]) +
+                                                                          __popc(m[3]));
                 uint32_t rb[4], nrec = 0;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -584,6 +570,7 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                 off = __shfl_sync(0xffffffffu, off, 0);
                 if (lane == 0) {
                     S.chunk_cnt[buf][chunk] = total;
+                    S.chunk_off[buf][chunk] = off;  // first record of the chunk
                     if (off + nrec > kRecCap) S.overflow[buf] = 1;
                 }
                 if (k.experiment != 3) {
@@ -596,14 +583,34 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                             if (r < kRecCap) {
                                 const uint32_t vec = d.sub * (kSubElems / 8) + v0 + 32 * j;
                                 S.stg[buf].rec.val[r] = cv[j];
-                                S.stg[buf].rec.meta[r] = make_uint2(vec | (m[j] << 16), chunk | (pj[j] << 8));
+                                S.stg[buf].rec.meta[r] = make_uint2(vec | (m[j] << 16), chunk);
                             }
                         }
                         rbase += __popc(rb[j]);
                     }
                 }
+                wcount += total;
             } else {
-                // element entries (offset in ticket, value), chunk-contiguous
+                // element entries (offset in ticket, value), chunk-contiguous; element
+                // order inside the warp slice: (j, lane, q), packed 16-bit scans for j pairs
+                const uint32_t lo = __popc(m[0]) | (__popc(m[1]) << 16);
+                const uint32_t hi = __popc(m[2]) | (__popc(m[3]) << 16);
+                uint32_t ilo = lo, ihi = hi;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t a1 = __shfl_up_sync(0xffffffffu, ilo, off);
+                    const uint32_t a2 = __shfl_up_sync(0xffffffffu, ihi, off);
+                    if (lane >= off) {
+                        ilo += a1;
+                        ihi += a2;
+                    }
+                }
+                const uint32_t tlo = __shfl_sync(0xffffffffu, ilo, 31), thi = __shfl_sync(0xffffffffu, ihi, 31);
+                const uint32_t t0 = tlo & 0xFFFF, t1 = tlo >> 16, t2 = thi & 0xFFFF, t3 = thi >> 16;
+                const uint32_t total = t0 + t1 + t2 + t3;
+                const uint32_t exlo = ilo - lo, exhi = ihi - hi;
+                const uint32_t pj[4] = {exlo & 0xFFFF, t0 + (exlo >> 16), t0 + t1 + (exhi & 0xFFFF),
+                                        t0 + t1 + t2 + (exhi >> 16)};
                 uint32_t off = 0;
                 if (lane == 0 && total) off = atomicAdd(&S.fill[buf], total);
                 off = __shfl_sync(0xffffffffu, off, 0);
@@ -629,8 +636,8 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                         }
                     }
                 }
+                wcount += total;
             }
-            wcount += total;
             if (d.sub + 1 == d.n_sub) finish_ticket(d);
             if (++stage == kStages) {
                 stage = 0;
@@ -683,14 +690,51 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
         if (k.experiment == 2 || k.experiment == 3) {
             // attribution experiments: no write-back
         } else if (!S.overflow[buf] && S.mode[buf] == kModeRecords) {
-            // expand the staged records: record -> its changed elements, at the
-            // ticket prefix G + its chunk's element prefix + its offset in the chunk
+            // expand the staged records: record -> its changed elements at G + its
+            // chunk's element prefix + its offset in the chunk.  Records sit in the
+            // buffer chunk by chunk (each chunk contiguous, in element order), so a
+            // running scan of popc(mask) in buffer order, minus its value at the
+            // chunk's first record, is that offset.
             const uint32_t nrec = S.fill[buf];
+            uint32_t run = 0;  // elements of the records before this round
+            for (uint32_t r0 = 0; r0 < nrec; r0 += kLbThreads) {
+                const uint32_t r = r0 + uint32_t(lt);
+                uint2 meta = make_uint2(0, 0);
+                uint4 v = make_uint4(0, 0, 0, 0);
+                uint32_t cnt = 0;
+                if (r < nrec) {
+                    meta = S.stg[buf].rec.meta[r];
+                    v = S.stg[buf].rec.val[r];
+                    cnt = __popc(meta.x >> 16);
+                }
+                uint32_t inc = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += x;
+                }
+                if (lane == 31) S.lb_warp_tot[warp - kLbFirst] = inc;
+                named_sync(kBarLb, kLbThreads);
+                uint32_t before = 0, all = 0;
+#pragma unroll
+                for (int w = 0; w < kLbWarps; ++w) {
+                    const uint32_t t = S.lb_warp_tot[w];
+                    if (w < warp - kLbFirst) before += t;
+                    all += t;
+                }
+                const uint32_t ex = run + before + inc - cnt;  // elements before record r (buffer order)
+                const uint32_t ch = meta.y & 0xFF;
+                if (r < nrec && S.chunk_off[buf][ch] == r) S.chunk_ebase[ch] = ex;
+                named_sync(kBarLb, kLbThreads);  // chunk_ebase complete for this round's chunk starts
+                if (r < nrec) S.stg[buf].rec.meta[r].y = ch | (ex << 8);
+                run += all;
+            }
+            named_sync(kBarLb, kLbThreads);
             for (uint32_t r = lt; r < nrec; r += kLbThreads) {
                 const uint2 meta = S.stg[buf].rec.meta[r];
                 const uint4 v = S.stg[buf].rec.val[r];
-                const uint32_t vec = meta.x & 0xFFFF, mask = meta.x >> 16;
-                uint64_t pos = G + S.chunk_pre[meta.y & 0xFF] + (meta.y >> 8);
+                const uint32_t vec = meta.x & 0xFFFF, mask = meta.x >> 16, ch = meta.y & 0xFF;
+                uint64_t pos = G + S.chunk_pre[ch] + ((meta.y >> 8) - S.chunk_ebase[ch]);
                 const uint32_t ebase = ti.toff + vec * 8;
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
