@@ -529,18 +529,25 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                     cv[j] = b;
                 }
             }
-            // any difference in this lane's 32 elements? (XOR-OR, LOP3-fusable)
-            uint32_t diff = 0;
+            // any difference per vector? (XOR-OR, LOP3-fusable)
+            uint32_t xd[kVecPerWarp / 32], diff = 0;
 #pragma unroll
-            for (int j = 0; j < int(kVecPerWarp / 32); ++j)
-                diff |= (av[j].x ^ cv[j].x) | (av[j].y ^ cv[j].y) | (av[j].z ^ cv[j].z) | (av[j].w ^ cv[j].w);
+            for (int j = 0; j < int(kVecPerWarp / 32); ++j) {
+                xd[j] = (av[j].x ^ cv[j].x) | (av[j].y ^ cv[j].y) | (av[j].z ^ cv[j].z) | (av[j].w ^ cv[j].w);
+                diff |= xd[j];
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[stage]);  // operands are in registers: stage may be refilled
             const bool warp_changed = __any_sync(0xffffffffu, diff != 0);
-            uint32_t m[kVecPerWarp / 32] = {0, 0, 0, 0};
-            if (warp_changed && diff) {
+            // per-element masks only for the vector groups some lane changed in (clustered
+            // updates usually touch one of the four); rbj[j] = lanes with a changed vector j
+            uint32_t m[kVecPerWarp / 32] = {0, 0, 0, 0}, rbj[kVecPerWarp / 32] = {0, 0, 0, 0};
+            if (warp_changed) {
 #pragma unroll
-                for (int j = 0; j < int(kVecPerWarp / 32); ++j) m[j] = change_mask(av[j], cv[j]);
+                for (int j = 0; j < int(kVecPerWarp / 32); ++j) {
+                    rbj[j] = __ballot_sync(0xffffffffu, xd[j] != 0);
+                    if (rbj[j] && xd[j]) m[j] = change_mask(av[j], cv[j]);
+                }
             }
             if (!warp_changed) {  // common case at high sparsity: nothing to stage
                 if (lane == 0) S.chunk_cnt[buf][d.sub * kConsumerWarps + warp] = 0;
@@ -562,7 +569,7 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                 uint32_t rb[4], nrec = 0;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    rb[j] = __ballot_sync(0xffffffffu, m[j] != 0);
+                    rb[j] = rbj[j];  // m[j] != 0 exactly when vector j differs
                     nrec += __popc(rb[j]);
                 }
                 uint32_t off = 0;
