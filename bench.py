@@ -354,9 +354,7 @@ def run_pulse(args):
     # the timed loop replays the step as a CUDA graph (one per direction: the two
     # snapshot slots swap), launch overhead off the host; eager launches if capture fails
     graphs = None
-    # single GPU only: with NCCL collectives captured, process-group teardown hung
-    # on the pool (round 1); the sharded step times eager launches
-    if not args.no_graph and world == 1:
+    if not args.no_graph:
         try:
             graphs = []
             for k in (0, 1):
@@ -470,6 +468,13 @@ def run_pulse(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        torch.cuda.synchronize()
+        if used_graph:
+            # NCCL communicators captured in CUDA graphs: process-group teardown can
+            # block on them, so leave without it once every rank is done
+            sys.stdout.flush()
+            sys.stderr.flush()
+            os._exit(0)
         dist.destroy_process_group()
     return 0
 
