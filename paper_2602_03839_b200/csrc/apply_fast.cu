@@ -212,6 +212,9 @@ struct ApplyArgs {
     uint16_t* const* weights;
     int64_t* out_idx;
     uint16_t* backup;  // [entries]: pre-apply value of every written element (kApply / kRestore)
+    uint64_t* scan_status;               // F2 look-back words (2 per block, zeroed per call)
+    unsigned long long* scan_ticket;     // F2 block ticket (zeroed per call)
+    uint32_t scan_blocks;                // F2 grid: blocks for the plan's capacity
 };
 
 // Walker path over entries [first, last) for one pass.  (ar, ac): aggregates
@@ -519,7 +522,7 @@ f_pass(ApplyArgs A) {
 // F2: exclusive SegSum scan of the range aggregates (one CTA of 1024)
 // =============================================================================================
 constexpr int kScanThreads = 1024;
-constexpr int kScanPer = 8;  // items held in registers per thread per block
+constexpr int kScanPer = 4;  // items per thread
 
 __device__ __forceinline__ void cta_seg_exclusive(uint64_t& vr, uint64_t& vc, uint64_t* s_r, uint64_t* s_c) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -545,43 +548,57 @@ __device__ __forceinline__ void cta_seg_exclusive(uint64_t& vr, uint64_t& vc, ui
     __syncthreads();
 }
 
+// One 1024-thread CTA per block of 4096 range aggregates, blocks taken in ticket
+// order and chained by a decoupled look-back (one status word per block and
+// stream) -- the scan is spread over several SMs instead of serialising ~18K
+// 64-bit segmented adds on one.
+constexpr uint64_t kScanBlock = uint64_t(kScanThreads) * kScanPer;
+
 __global__ void __launch_bounds__(kScanThreads, 1)
-f_range_scan(const uint64_t* __restrict__ totals, ulonglong2* __restrict__ agg, const uint32_t* __restrict__ flags) {
+f_range_scan(const uint64_t* __restrict__ totals, ulonglong2* __restrict__ agg, const uint32_t* __restrict__ flags,
+             uint64_t* __restrict__ status, unsigned long long* __restrict__ ticket) {
     __shared__ uint64_t s_r[32], s_c[32];
-    __shared__ uint64_t s_carry[2];
+    __shared__ uint64_t s_blk, s_tot[2], s_pre[2];
     if (fast_blocked(flags)) return;
     const uint64_t n = totals[0];
     const uint64_t n_ranges = (n + kRange - 1) / kRange;
-    if (threadIdx.x == 0) s_carry[0] = s_carry[1] = 0;
+    const uint64_t n_blocks = (n_ranges + kScanBlock - 1) / kScanBlock;
+    if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1ull);
     __syncthreads();
-    constexpr uint64_t kBlock = uint64_t(kScanThreads) * kScanPer;
-    for (uint64_t b0 = 0; b0 < n_ranges; b0 += kBlock) {
-        const uint64_t q0 = b0 + uint64_t(threadIdx.x) * kScanPer;
-        ulonglong2 v[kScanPer];
+    const uint64_t blk = s_blk;
+    if (blk >= n_blocks) return;
+    const uint64_t q0 = blk * kScanBlock + uint64_t(threadIdx.x) * kScanPer;
+    ulonglong2 v[kScanPer];
 #pragma unroll
-        for (int j = 0; j < kScanPer; ++j) v[j] = q0 + j < n_ranges ? agg[q0 + j] : make_ulonglong2(0, 0);
-        uint64_t sr = 0, sc = 0;
+    for (int j = 0; j < kScanPer; ++j) v[j] = q0 + j < n_ranges ? agg[q0 + j] : make_ulonglong2(0, 0);
+    uint64_t ar = 0, ac = 0;  // this thread's aggregate
 #pragma unroll
-        for (int j = 0; j < kScanPer; ++j) {
-            sr = SegSumOp::op(sr, v[j].x);
-            sc = SegSumOp::op(sc, v[j].y);
+    for (int j = 0; j < kScanPer; ++j) {
+        ar = SegSumOp::op(ar, v[j].x);
+        ac = SegSumOp::op(ac, v[j].y);
+    }
+    uint64_t er = ar, ec = ac;
+    cta_seg_exclusive(er, ec, s_r, s_c);  // -> exclusive within the block
+    if (threadIdx.x == kScanThreads - 1) {
+        s_tot[0] = SegSumOp::op(er, ar);
+        s_tot[1] = SegSumOp::op(ec, ac);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // warp 0: the block's exclusive prefix for both streams
+        const uint64_t pr = lookback<SegSumOp>(status, blk, s_tot[0]);
+        const uint64_t pc = lookback<SegSumOp>(status + n_blocks, blk, s_tot[1]);
+        if (threadIdx.x == 0) {
+            s_pre[0] = pr;
+            s_pre[1] = pc;
         }
-        cta_seg_exclusive(sr, sc, s_r, s_c);
-        const uint64_t cr = s_carry[0], cc = s_carry[1];
-        sr = SegSumOp::op(cr, sr);
-        sc = SegSumOp::op(cc, sc);
+    }
+    __syncthreads();
+    uint64_t sr = SegSumOp::op(s_pre[0], er), sc = SegSumOp::op(s_pre[1], ec);
 #pragma unroll
-        for (int j = 0; j < kScanPer; ++j) {  // in place: aggregate -> exclusive prefix
-            if (q0 + j < n_ranges) agg[q0 + j] = make_ulonglong2(sr & (H - 1), sc & (H - 1));
-            sr = SegSumOp::op(sr, v[j].x);
-            sc = SegSumOp::op(sc, v[j].y);
-        }
-        __syncthreads();
-        if (threadIdx.x == kScanThreads - 1) {
-            s_carry[0] = sr & (H - 1);
-            s_carry[1] = sc & (H - 1);
-        }
-        __syncthreads();
+    for (int j = 0; j < kScanPer; ++j) {  // in place: aggregate -> exclusive prefix
+        if (q0 + j < n_ranges) agg[q0 + j] = make_ulonglong2(sr & (H - 1), sc & (H - 1));
+        sr = SegSumOp::op(sr, v[j].x);
+        sc = SegSumOp::op(sc, v[j].y);
     }
 }
 
@@ -605,7 +622,8 @@ void launch_pass(const ApplyArgs& a, cudaStream_t s) {
 template <int kRepr>
 void launch_all(const ApplyArgs& a, bool scatter, cudaStream_t s) {
     launch_pass<kRepr, kAgg>(a, s);
-    f_range_scan<<<1, kScanThreads, 0, s>>>(a.totals, a.agg, a.flags);
+    cudaMemsetAsync(a.scan_status, 0, 2 * sizeof(uint64_t) * a.scan_blocks, s);
+    f_range_scan<<<a.scan_blocks, kScanThreads, 0, s>>>(a.totals, a.agg, a.flags, a.scan_status, a.scan_ticket);
     PULSE_LAUNCHED("f_range_scan", s);
     if (a.weights) {  // in place: checked writes with backup, restore if anything failed
         launch_pass<kRepr, kApply>(a, s);
@@ -633,6 +651,9 @@ void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uin
     a.weights = weights_slot >= 0 ? p.slot[weights_slot] : nullptr;
     a.out_idx = out_indices;
     a.backup = reinterpret_cast<uint16_t*>(p.rowgap);  // general-decoder scratch, idle on this path
+    a.scan_status = p.d_status;  // general-decoder look-back words, idle on this path
+    a.scan_ticket = reinterpret_cast<unsigned long long*>(p.d_totals + 15);  // zeroed by decode_prologue
+    a.scan_blocks = uint32_t((p.cap / kRange + 2 + kScanBlock - 1) / kScanBlock);
     if (out_indices) a.weights = nullptr;
     const bool scatter = weights_slot >= 0 || out_indices;
     if (repr == PULSE_COO_DOWNSCALED) launch_all<kCoo>(a, scatter, s);
