@@ -38,6 +38,8 @@
 // If d_layout or F1 finds anything the fixed layout cannot express (escapes,
 // short/long payloads, marker bytes), `flags[0]` routes the patch to the
 // general parser in decode.cu instead; every kernel checks it on entry.
+#include <cstdlib>
+
 #include "device.cuh"
 #include "internal.hpp"
 #include "stage.cuh"
@@ -625,10 +627,11 @@ void launch_all(const ApplyArgs& a, bool scatter, cudaStream_t s) {
     cudaMemsetAsync(a.scan_status, 0, 2 * sizeof(uint64_t) * a.scan_blocks, s);
     f_range_scan<<<a.scan_blocks, kScanThreads, 0, s>>>(a.totals, a.agg, a.flags, a.scan_status, a.scan_ticket);
     PULSE_LAUNCHED("f_range_scan", s);
-    if (a.weights) {  // in place: checked writes with backup, restore if anything failed
+    static const int mode = getenv("PULSE_APPLY_MODE") ? atoi(getenv("PULSE_APPLY_MODE")) : 0;
+    if (a.weights && mode == 0) {  // in place: checked writes with backup, restore if anything failed
         launch_pass<kRepr, kApply>(a, s);
         launch_pass<kRepr, kRestore>(a, s);
-    } else {          // indices only: validate, then write them
+    } else {          // indices only (or PULSE_APPLY_MODE=1 in place): validate, then write them
         launch_pass<kRepr, kValidate>(a, s);
         if (scatter) launch_pass<kRepr, kScatter>(a, s);
     }
