@@ -611,11 +611,13 @@ namespace {
 template <int kRepr, int kPass>
 void launch_pass(const ApplyArgs& a, cudaStream_t s) {
     const uint32_t smem = kWarps * warp_smem(kPass);
-    static int per_sm = 0;  // per instantiation: resident CTAs per SM (persistent grid)
+    static PerDeviceInt occ;  // per instantiation and device: resident CTAs per SM (persistent grid)
+    int& per_sm = occ.here();
     if (!per_sm) {
         cudaFuncSetAttribute(f_pass<kRepr, kPass>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f_pass<kRepr, kPass>, kThreads, smem);
-        per_sm = per_sm > 0 ? per_sm : 1;
+        int v = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, f_pass<kRepr, kPass>, kThreads, smem);
+        per_sm = v > 0 ? v : 1;
     }
     f_pass<kRepr, kPass><<<unsigned(sm_count() * per_sm), kThreads, smem, s>>>(a);
     PULSE_LAUNCHED("f_pass", s);

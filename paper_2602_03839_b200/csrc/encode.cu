@@ -881,7 +881,7 @@ __global__ void k1_finalize(const SegDesc* __restrict__ segs, uint32_t n_segs,
 // =============================================================================================
 // launchers
 // =============================================================================================
-static int g_sms = 0;
+static PerDeviceInt g_sms;
 void debug_sync(const char* kernel, cudaStream_t s) {
     static const bool on = [] {
         const char* e = getenv("PULSE_DEBUG_SYNC");
@@ -894,13 +894,13 @@ void debug_sync(const char* kernel, cudaStream_t s) {
 }
 
 int sm_count() {
-    if (!g_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_sms <= 0) g_sms = 148;
+    int& n = g_sms.here();
+    if (!n) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, current_device());
+        n = v > 0 ? v : 148;
     }
-    return g_sms;
+    return n;
 }
 
 // PULSE_K1 = tma (default) | static | ticket
@@ -923,17 +923,22 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
     K1Args k{p.trace, experiment, p.segs, p.tile_seg, p.n_segs, p.n_tiles, p.slot[prev_slot], p.slot[curr_slot], p.idx32, p.val16,
              p.cap, p.seg_start, p.k1_status, reinterpret_cast<unsigned long long*>(p.counters)};
     if (p.n_tiles > 0) {
-        static int per_sm_static = 0, per_sm_ticket = 0;
+        static PerDeviceInt occ_static, occ_ticket, tma_attr;
+        int& per_sm_static = occ_static.here();
+        int& per_sm_ticket = occ_ticket.here();
         if (!per_sm_static) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_static, k1_static, kThreads, 0);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ticket, k1_ticket, kThreads, 0);
+            int a = 0, b = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k1_static, kThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_ticket, kThreads, 0);
+            per_sm_ticket = b;
+            per_sm_static = a > 0 ? a : -1;  // nonzero: configured
         }
         bool launched = false;
         if (k1_variant() == 0 && p.tma_tiles > 0) {
-            static bool attr = false;
+            int& attr = tma_attr.here();
             if (!attr) {
                 cudaFuncSetAttribute(k1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(tma::Smem)));
-                attr = true;
+                attr = 1;
             }
             K1Args kt = k;
             kt.n_tiles = p.tma_tiles;

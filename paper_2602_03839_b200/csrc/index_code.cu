@@ -993,18 +993,17 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
     cudaMemsetAsync(p.t_resc, 0, p.n_tensors * sizeof(uint32_t), s);
     cudaMemsetAsync(p.t_cesc, 0, p.n_tensors * sizeof(uint32_t), s);
     cudaMemsetAsync(p.err, 0xFF, sizeof(uint64_t), s);
-    static bool configured = false;
-    if (!configured) {
+    static PerDeviceInt occ_scan_d, occ_emit_d;
+    int& occ_scan = occ_scan_d.here();
+    int& occ_emit = occ_emit_d.here();
+    if (!occ_scan) {  // per device: the shared-memory opt-in, then occupancy
         cudaFuncSetAttribute(k2_scan_escapes, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWarps * kScanWarpSmem));
         cudaFuncSetAttribute(k2_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWarps * kEmitWarpSmem));
-        configured = true;
-    }
-    static int occ_scan = 0, occ_emit = 0;
-    if (!occ_scan) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_scan, k2_scan_escapes, kThreads, kWarps * kScanWarpSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_emit, k2_emit, kThreads, kWarps * kEmitWarpSmem);
-        occ_scan = std::max(occ_scan, 1);
-        occ_emit = std::max(occ_emit, 1);
+        int a = 0, b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k2_scan_escapes, kThreads, kWarps * kScanWarpSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k2_emit, kThreads, kWarps * kEmitWarpSmem);
+        occ_emit = std::max(b, 1);
+        occ_scan = std::max(a, 1);
     }
     LayoutArgs a;
     a.range_cnt = p.range_cnt;

@@ -157,6 +157,19 @@ void launch_encode_emit_idx64(const PlanDev& p, uint32_t repr, const int64_t* id
                               pulse_result* result, cudaStream_t s);
 
 int sm_count();
+// Per-device one-time launch configuration: function attributes (the dynamic
+// shared-memory opt-in) and occupancy are per device, so caches index by the
+// current device.  A race only repeats an idempotent setup.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & (kMaxDevices - 1);
+}
+struct PerDeviceInt {
+    int v[kMaxDevices] = {};
+    int& here() { return v[current_device()]; }
+};
 // PULSE_DEBUG_SYNC=1: synchronise after every launch and report the first
 // failing kernel by name on stderr (debugging aid; off by default).
 void debug_sync(const char* kernel, cudaStream_t s);

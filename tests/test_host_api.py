@@ -229,3 +229,21 @@ def test_decode_pipeline_with_pinned_buffers(golden, repr_):
                               verify_hash=False)
             for o, s_ in zip(outs, sentinel):
                 assert torch.equal(o, s_)
+
+
+@pytest.mark.gpu
+def test_host_api_on_two_devices_in_one_process(golden):
+    """Launch configuration (shared-memory opt-in, occupancy) is per device: one
+    process driving two GPUs round-trips on both."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    prev, curr, _ = golden.case("esc_rows")
+    for dev in (0, 1, 0):
+        torch.cuda.set_device(dev)
+        for repr_ in (0, 1, 2):
+            h = H.encode_handle(mirror(curr), mirror(prev), repr_, 2)
+            out = H.decode(mirror(prev), H.read_patch_handle(H.write_patch_array(h)), verify_hash=True)
+            for a, b in zip(sorted(out.tensors, key=lambda t: t.name), curr.sorted()):
+                assert np.array_equal(a.data, b.data), (dev, repr_)
+    torch.cuda.set_device(0)
