@@ -268,3 +268,48 @@ def test_apply_patch_device_count_and_failed_encode(repr_):
             assert int(res["status"]) == 15
             for a, t in zip(prevs, w):
                 assert np.array_equal(t.cpu().numpy().view(np.uint16), a)
+
+
+@pytest.mark.parametrize("numel,cols", [((1 << 31) + (1 << 20) + 24, 4096 + 8), ((1 << 32) + 4096, 1 << 20)])
+def test_segmented_and_wide_tensors_round_trip(numel, cols):
+    """Tensors past 2^31 elements are split into 32-bit segments by K1/K2; past
+    2^32 the index coding and apply take their 64-bit paths.  Size-independent
+    checks: exact change count, exact round trip for every representation, and
+    the decoded indices around the segment boundary against a host diff."""
+    D = _dev()
+    if torch.cuda.get_device_properties(0).total_memory < 60 * (1 << 30):
+        pytest.skip("needs a large-memory GPU")
+    rows = numel // cols
+    n = rows * cols
+    prev = torch.empty(n, dtype=torch.int16, device="cuda")
+    curr = torch.empty_like(prev)
+    D.synth_base(prev, seed=5)
+    changed = D.synth_mutate(prev, curr, 0.9999, 64, seed=6)
+    # force changes right around the 2^31 split and the last element
+    for p in [(1 << 31) - 2, (1 << 31) - 1, 1 << 31, (1 << 31) + 1, n - 1]:
+        if p < n:
+            curr[p] = prev[p] ^ 1
+    torch.cuda.synchronize()
+    want = int((curr != prev).sum().item())
+    plan = D.DevicePlan([(n, cols)], want + 1024)
+    w = prev.clone()
+    plan.bind(0, [prev])
+    plan.bind(1, [curr])
+    plan.bind(2, [w])
+    for repr_ in (COO_DOWNSCALED, COO_INT32, FLAT_INT32):
+        p = plan.encode(1, 0, repr_)
+        if repr_ != COO_DOWNSCALED and n >= (1 << 31):
+            assert p.status == 12  # DimensionError: int32 representations reject 2^31+ tensors (patch.hpp:99-103)
+            continue
+        assert p.status == 0 and p.n_changes == want, (repr_, p.status)
+        idx, _ = plan.decode_indices(p)
+        lo, hi = (1 << 31) - 4096, (1 << 31) + 4096
+        seg = idx[(idx >= lo) & (idx < hi)].cpu().numpy()
+        ref = (torch.nonzero(curr[lo:hi] != prev[lo:hi]).flatten() + lo).cpu().numpy()
+        assert np.array_equal(seg, ref)
+        w.copy_(prev)
+        res = D.parse_result(plan.apply(2, p))
+        assert int(res["status"]) == 0
+        assert torch.equal(w, curr)
+    del prev, curr, w
+    torch.cuda.empty_cache()
