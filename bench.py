@@ -451,7 +451,12 @@ def run_pulse(args):
                        "parallelism": f"tensor-shard x{world}" if world > 1 else "single GPU",
                        "launch": "cuda-graph replay" if used_graph else "eager",
                        "l2": f"inputs {4 * d_total / 1e9:.1f} GB per step >> 126 MB L2 (no flush needed)"},
-            "frac_of_hbm": round(value / peak, 4),
+            # the step against the HBM roofline (north_star: bytes read + written / peak), algorithmic
+            # bytes per SURVEY §8(d): encode 4d + P_idx + 2n (snapshots in, patch body out), apply
+            # P_idx + 2n (patch in) + 2n (scattered writes); the K1->K2 intermediate is not counted
+            "frac_of_hbm": round((4 * d_total + 2 * body_total + 2 * changes_total) / (ms_max / 1e3) / 1e9 / peak, 4),
+            "step_bytes": int(4 * d_total + 2 * body_total + 2 * changes_total),
+            "weight_gbs_frac_of_peak": round(value / peak, 4),
             "encode_ms": round(scan_max, 4), "apply_ms": round(apply_max, 4),
             "patch_mb": round(body_total / 1e6, 3), "changes": int(changes_total),
             "roofline": {"kernel": "k1_diff_compact", "bound": "hbm", "achieved": round(k1_gbs, 2),

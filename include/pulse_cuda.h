@@ -349,6 +349,43 @@ pulse_status pulse_upscale_coo(const uint8_t* payload, uint64_t n, uint64_t coun
 pulse_status pulse_compress(const uint8_t* raw, uint64_t n, uint32_t codec, pulse_bytes** out);
 pulse_status pulse_decompress(const uint8_t* enveloped, uint64_t n, uint32_t codec, pulse_bytes** out);
 
+/* ======================================================================= */
+/* PULC checkpoint container -- container.hpp:18-150                        */
+/* ======================================================================= */
+
+/* write_checkpoint_bytes -- container.hpp:58-90: "PULC", u32 1, u64 header
+ * length, JSON tensor table (sorted keys), then every tensor's LE bf16 payload
+ * at a 64-byte aligned offset from the 64-byte aligned payload base, tensors in
+ * insertion order.  device_data != 0: the tensors' `data` pointers are DEVICE
+ * pointers of the current device, and each payload is copied straight out of
+ * HBM into its place in the file (no host Checkpoint in between). */
+pulse_status pulse_write_checkpoint_bytes(const pulse_checkpoint* checkpoint, int device_data, pulse_bytes** out);
+
+/* read_checkpoint_bytes -- container.hpp:92-142, in two steps: parse (the
+ * header, every payload bound and Checkpoint::validate, with the reference's
+ * checks, order and exception classes), then copy the payloads out to host or
+ * device memory.  The parsed table refers to the caller's bytes by offset. */
+typedef struct pulse_container pulse_container;
+typedef struct pulse_container_tensor {
+    const char* name;
+    const int64_t* shape;
+    uint32_t rank;
+    uint64_t numel;
+    uint64_t payload_offset; /* absolute byte offset of the LE bf16 payload in the container */
+} pulse_container_tensor;
+pulse_status pulse_container_parse(const uint8_t* data, uint64_t n, pulse_container** out);
+void pulse_container_free(pulse_container* container);
+uint64_t pulse_container_step(const pulse_container* container);
+uint32_t pulse_container_num_tensors(const pulse_container* container);
+pulse_status pulse_container_get_tensor(const pulse_container* container, uint32_t i, pulse_container_tensor* out);
+/* Copies tensor i's payload (numel * 2 bytes) from `data` -- the bytes that
+ * were parsed, `n` long -- to dst[i]: host memory (device == 0) or device
+ * memory of the current device (device != 0; DMA straight from `data` when it
+ * is page-locked, else through pinned staging).  Returns when the copies are
+ * complete. */
+pulse_status pulse_container_copy_out(const pulse_container* container, const uint8_t* data, uint64_t n,
+                                      int device, void* const* dst);
+
 #ifdef __cplusplus
 }
 #endif

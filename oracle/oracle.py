@@ -138,6 +138,7 @@ class Reference:
             "ref_compress": (C.c_int, [C.c_char_p, u64, u32, pp(vp)]),
             "ref_decompress": (C.c_int, [C.c_char_p, u64, u32, pp(vp)]),
             "ref_write_checkpoint_bytes": (C.c_int, [vp, pp(vp)]),
+            "ref_read_checkpoint_bytes": (C.c_int, [C.c_char_p, u64, pp(vp)]),
             "ref_sparsity": (C.c_int, [vp, vp, pp(u64), pp(u64)]),
             "ref_frozen_fraction": (C.c_int, [vp, C.c_double, pp(C.c_double)]),
             "ref_time_step": (C.c_int, [vp, vp, u32, u32, C.c_int] + [pp(C.c_double)] * 5 + [pp(u64), pp(u64)]),
@@ -352,6 +353,11 @@ class Reference:
         finally:
             self.L.ref_ckpt_free(h)
         return self._take_buf(out.value)
+
+    def read_checkpoint_bytes(self, data: bytes) -> Checkpoint:
+        out = C.c_void_p()
+        self._check(self.L.ref_read_checkpoint_bytes(data, len(data), C.byref(out)))
+        return self.ckpt_from_handle(out.value)
 
     def sparsity(self, a: Checkpoint, b: Checkpoint):
         """absorption.hpp:55-78 -> (changed, total)"""

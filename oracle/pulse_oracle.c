@@ -6,7 +6,7 @@
  * lines it restates.  It is the CPU checker for the CUDA kernels: tests/,
  * __graft_entry__.smoke() and bench.py's cpu_baseline leg are the only
  * callers.  Pinned by tests/test_oracle.py against the reference's own
- * known-answer vectors (tests/*.cpp in the reference) and against golden
+ * known-answer vectors (the reference test sources proj/tests/test_<name>.cpp) and against golden
  * fixtures produced by the reference itself (tests/golden/make_golden.py).
  *
  * Status codes follow include/pulse_cuda.h (0 ok, 2 argument, 6 truncation,

@@ -350,6 +350,14 @@ int ref_write_checkpoint_bytes(void* h, void** out) {
     SHIM_CATCH
 }
 
+// container.hpp:92-142
+int ref_read_checkpoint_bytes(const uint8_t* data, uint64_t n, void** out) {
+    SHIM_TRY
+    *out = new pulse::Checkpoint(pulse::read_checkpoint_bytes(std::span<const uint8_t>(data, n)));
+    return 0;
+    SHIM_CATCH
+}
+
 // absorption.hpp:55-78
 int ref_sparsity(void* cur, void* prev, uint64_t* changed, uint64_t* total) {
     SHIM_TRY

@@ -113,6 +113,11 @@ class TensorPatchC(C.Structure):
                 ("values", C.POINTER(C.c_uint16)), ("n_values", C.c_uint64)]
 
 
+class ContainerTensorC(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("shape", C.POINTER(C.c_int64)), ("rank", C.c_uint32),
+                ("numel", C.c_uint64), ("payload_offset", C.c_uint64)]
+
+
 class SparsityReportC(C.Structure):
     _fields_ = [("k", C.c_uint64), ("changed", C.c_uint64), ("total", C.c_uint64), ("sparsity", C.c_double)]
 
@@ -170,6 +175,14 @@ _SIGS = {
     "pulse_upscale_coo": (i32, [C.c_char_p, u64, u64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "pulse_compress": (i32, [C.c_char_p, u64, u32, C.POINTER(vp)]),
     "pulse_decompress": (i32, [C.c_char_p, u64, u32, C.POINTER(vp)]),
+    # PULC container
+    "pulse_write_checkpoint_bytes": (i32, [C.POINTER(CheckpointC), C.c_int, C.POINTER(vp)]),
+    "pulse_container_parse": (i32, [vp, u64, C.POINTER(vp)]),
+    "pulse_container_free": (None, [vp]),
+    "pulse_container_step": (u64, [vp]),
+    "pulse_container_num_tensors": (u32, [vp]),
+    "pulse_container_get_tensor": (i32, [vp, u32, C.POINTER(ContainerTensorC)]),
+    "pulse_container_copy_out": (i32, [vp, vp, u64, C.c_int, C.POINTER(vp)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)

@@ -1622,4 +1622,181 @@ pulse_status pulse_decompress(const uint8_t* data, uint64_t n, uint32_t codec, p
     });
 }
 
+
+// ---- container.hpp: the PULC checkpoint container ------------------------------------------
+// Layout (container.hpp:52-57): "PULC", u32 1, u64 header length, JSON
+// {"step", "tensors": [{"dtype", "name", "nbytes", "offset", "shape"}]} (nlohmann
+// dump, keys sorted), then the LE bf16 payloads at 64-byte aligned offsets from
+// the 64-byte aligned payload base.  On this little-endian host a payload IS the
+// tensor's u16 array, so every payload moves as one copy -- a memcpy or a DMA
+// straight to/from HBM -- instead of the reference's per-element u16le loop
+// (container.hpp:88, :140).
+pulse_status pulse_write_checkpoint_bytes(const pulse_checkpoint* c, int device_data, pulse_bytes** out) {
+    return guarded([&] {
+        if (!c || !out || (c->n_tensors && !c->tensors)) raise(PULSE_E_ARGUMENT, "null argument");
+        validate_checkpoint(c);  // Checkpoint::validate, container.hpp:59
+        const uint32_t T = c->n_tensors;
+        nlohmann::json header;
+        header["step"] = c->step;
+        auto& table = header["tensors"] = nlohmann::json::array();
+        std::vector<uint64_t> rel(T);
+        uint64_t off = 0;
+        for (uint32_t i = 0; i < T; ++i) {  // insertion order, not name order
+            const pulse_tensor& t = c->tensors[i];
+            const uint64_t nb = t.numel * 2;
+            rel[i] = off;
+            table.push_back({{"name", t.name},
+                             {"dtype", "bf16"},
+                             {"shape", std::vector<int64_t>(t.shape, t.shape + t.rank)},
+                             {"offset", off},
+                             {"nbytes", nb}});
+            off = (off + nb + 63) & ~uint64_t(63);
+        }
+        const std::string js = header.dump();
+        const uint64_t base = (16 + js.size() + 63) & ~uint64_t(63);
+        uint64_t total = 16 + js.size();
+        if (T) total = base + rel[T - 1] + c->tensors[T - 1].numel * 2;
+        auto res = std::make_unique<pulse_bytes>();
+        res->v.resize(total);
+        uint8_t* w = res->v.data();
+        std::memcpy(w, "PULC", 4);
+        for (int i = 0; i < 4; ++i) w[4 + i] = uint8_t(1u >> (8 * i));
+        for (int i = 0; i < 8; ++i) w[8 + i] = uint8_t(uint64_t(js.size()) >> (8 * i));
+        std::memcpy(w + 16, js.data(), js.size());
+        if (T) {
+            // zero padding between the header / payloads (the reference's push_back(0) fill)
+            std::memset(w + 16 + js.size(), 0, base - 16 - js.size());
+            for (uint32_t i = 0; i + 1 < T; ++i) {
+                const uint64_t e = base + rel[i] + c->tensors[i].numel * 2;
+                std::memset(w + e, 0, base + rel[i + 1] - e);
+            }
+        }
+        if (device_data && T) {
+            for (uint32_t i = 0; i < T; ++i) {
+                cudaPointerAttributes a{};
+                if (cudaPointerGetAttributes(&a, c->tensors[i].data) != cudaSuccess || a.type != cudaMemoryTypeDevice) {
+                    cudaGetLastError();
+                    raise(PULSE_E_ARGUMENT, std::string("tensor ") + c->tensors[i].name + ": data is not a device pointer");
+                }
+            }
+            Engine& E = engine();
+            std::lock_guard<std::mutex> lk(E.mu);
+            for (uint32_t i = 0; i < T; ++i)
+                E.stager.d2h(w + base + rel[i], c->tensors[i].data, c->tensors[i].numel * 2, E.stream);
+        } else {
+            pool().parallel_for(T, [&](size_t i) {
+                if (c->tensors[i].numel) std::memcpy(w + base + rel[i], c->tensors[i].data, c->tensors[i].numel * 2);
+            });
+        }
+        *out = res.release();
+    });
+}
+
+}  // extern "C"
+
+struct pulse_container {
+    uint64_t step = 0;
+    struct Entry {
+        std::string name;
+        std::vector<int64_t> shape;
+        uint64_t numel = 0, begin = 0;
+    };
+    std::vector<Entry> tensors;
+    uint64_t end = 0;  // the container's exact length
+};
+
+extern "C" {
+
+pulse_status pulse_container_parse(const uint8_t* bytes, uint64_t n, pulse_container** out) {
+    return guarded([&] {
+        if (!out || (n && !bytes)) raise(PULSE_E_ARGUMENT, "null argument");
+        // container.hpp:92-142, check for check
+        if (n < 4) raise(PULSE_E_TRUNCATION, "container shorter than magic");
+        if (std::memcmp(bytes, "PULC", 4) != 0) raise(PULSE_E_BAD_MAGIC, "not a checkpoint container (bad magic)");
+        if (n < 8) raise(PULSE_E_TRUNCATION, "unexpected end of data");
+        uint32_t version = 0;
+        for (int i = 0; i < 4; ++i) version |= uint32_t(bytes[4 + i]) << (8 * i);
+        if (version != 1) raise(PULSE_E_VERSION, "unsupported container version " + std::to_string(version));
+        if (n < 16) raise(PULSE_E_TRUNCATION, "unexpected end of data");
+        uint64_t hl = 0;
+        for (int i = 0; i < 8; ++i) hl |= uint64_t(bytes[8 + i]) << (8 * i);
+        if (hl > n - 16) raise(PULSE_E_TRUNCATION, "container header truncated");
+        nlohmann::json header;
+        try {
+            header = nlohmann::json::parse(bytes + 16, bytes + 16 + hl);
+        } catch (const nlohmann::json::exception& e) {
+            raise(PULSE_E_FORMAT, std::string("container header is not valid JSON: ") + e.what());
+        }
+        auto c = std::make_unique<pulse_container>();
+        c->end = 16 + hl;  // no payload: the file ends after the header
+        try {
+            c->step = header.at("step").get<uint64_t>();
+            const uint64_t base = (16 + hl + 63) & ~uint64_t(63);
+            for (const auto& e : header.at("tensors")) {
+                pulse_container::Entry t;
+                t.name = e.at("name").get<std::string>();
+                if (e.at("dtype").get<std::string>() != "bf16") raise(PULSE_E_FORMAT, "unsupported dtype for tensor " + t.name);
+                t.shape = e.at("shape").get<std::vector<int64_t>>();
+                const uint64_t off = e.at("offset").get<uint64_t>();
+                const uint64_t nb = e.at("nbytes").get<uint64_t>();
+                if (off % 64) raise(PULSE_E_FORMAT, "misaligned tensor payload for " + t.name);
+                t.numel = 1;
+                for (int64_t x : t.shape) {
+                    if (x <= 0) raise(PULSE_E_FORMAT, "non-positive extent in tensor " + t.name);
+                    t.numel *= uint64_t(x);
+                }
+                if (nb != t.numel * 2) raise(PULSE_E_FORMAT, "payload length does not match shape for tensor " + t.name);
+                t.begin = base + off;
+                if (t.begin + nb > n) raise(PULSE_E_TRUNCATION, "tensor payload truncated for " + t.name);
+                c->end = std::max(c->end, t.begin + nb);
+                c->tensors.push_back(std::move(t));
+            }
+        } catch (const nlohmann::json::exception& e) {
+            raise(PULSE_E_FORMAT, std::string("container header schema error: ") + e.what());
+        }
+        if (n != c->end) raise(PULSE_E_FORMAT, "container has trailing bytes");
+        // Checkpoint::validate (checkpoint.hpp:54-70), as read_checkpoint_bytes ends with it
+        std::unordered_map<std::string_view, int> seen;
+        for (const auto& t : c->tensors) {
+            if (t.name.empty()) raise(PULSE_E_ARGUMENT, "tensor with empty name");
+            if (!seen.emplace(t.name, 0).second) raise(PULSE_E_ARGUMENT, "duplicate tensor name: " + t.name);
+            if (t.shape.empty()) raise(PULSE_E_ARGUMENT, "tensor " + t.name + " has empty shape");
+        }
+        *out = c.release();
+    });
+}
+
+void pulse_container_free(pulse_container* c) { delete c; }
+uint64_t pulse_container_step(const pulse_container* c) { return c ? c->step : 0; }
+uint32_t pulse_container_num_tensors(const pulse_container* c) { return c ? uint32_t(c->tensors.size()) : 0; }
+
+pulse_status pulse_container_get_tensor(const pulse_container* c, uint32_t i, pulse_container_tensor* out) {
+    if (!c || !out) return fail(PULSE_E_ARGUMENT, "null argument");
+    if (i >= c->tensors.size()) return fail(PULSE_E_ARGUMENT, "tensor index out of range");
+    const auto& t = c->tensors[i];
+    *out = pulse_container_tensor{t.name.c_str(), t.shape.data(), uint32_t(t.shape.size()), t.numel, t.begin};
+    return PULSE_OK;
+}
+
+pulse_status pulse_container_copy_out(const pulse_container* c, const uint8_t* data, uint64_t n, int device,
+                                      void* const* dst) {
+    return guarded([&] {
+        if (!c || (!dst && !c->tensors.empty()) || (!data && c->end)) raise(PULSE_E_ARGUMENT, "null argument");
+        if (n != c->end) raise(PULSE_E_ARGUMENT, "bytes are not the parsed container (length differs)");
+        const size_t T = c->tensors.size();
+        if (!device) {
+            pool().parallel_for(T, [&](size_t i) {
+                if (c->tensors[i].numel) std::memcpy(dst[i], data + c->tensors[i].begin, c->tensors[i].numel * 2);
+            });
+            return;
+        }
+        if (!T) return;
+        Engine& E = engine();
+        std::lock_guard<std::mutex> lk(E.mu);
+        for (size_t i = 0; i < T; ++i)
+            E.stager.h2d(dst[i], data + c->tensors[i].begin, c->tensors[i].numel * 2, E.stream);
+        E.sync();
+    });
+}
+
 }  // extern "C"

@@ -296,6 +296,86 @@ def transfer_stats(reset=False):
     return a.value, b.value
 
 
+# ---- container.hpp: the PULC checkpoint container --------------------------------------------
+def _buf(data):
+    """(pointer, length, keep-alive) of bytes / a uint8 ndarray."""
+    if isinstance(data, np.ndarray):
+        a = np.ascontiguousarray(data, dtype=np.uint8)
+        return a.ctypes.data, a.size, a
+    b = bytes(data)
+    return C.cast(C.c_char_p(b), C.c_void_p).value, len(b), b
+
+
+def write_checkpoint_bytes(ck: Checkpoint) -> bytes:
+    """container.hpp:58-90 (canonical: equal checkpoints give equal bytes)."""
+    v = CheckpointView(ck)
+    out = C.c_void_p()
+    N.check(N.lib.pulse_write_checkpoint_bytes(C.byref(v.c), 0, C.byref(out)))
+    return _take(out)
+
+
+class Container:
+    """A parsed PULC container (container.hpp:92-142 checks); tensors refer to
+    the caller's bytes by payload offset."""
+
+    def __init__(self, data):
+        self._ptr, self._n, self._keep = _buf(data)
+        h = C.c_void_p()
+        N.check(N.lib.pulse_container_parse(self._ptr, self._n, C.byref(h)))
+        self.h = h
+        self.step = int(N.lib.pulse_container_step(h))
+        self.tensors = []
+        for i in range(N.lib.pulse_container_num_tensors(h)):
+            t = N.ContainerTensorC()
+            N.check(N.lib.pulse_container_get_tensor(h, i, C.byref(t)))
+            self.tensors.append((t.name.decode(), tuple(t.shape[k] for k in range(t.rank)), int(t.numel),
+                                 int(t.payload_offset)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            N.lib.pulse_container_free(self.h)
+            self.h = None
+
+    def copy_out(self, dst_ptrs, device: bool):
+        arr = (C.c_void_p * max(1, len(dst_ptrs)))(*dst_ptrs)
+        N.check(N.lib.pulse_container_copy_out(self.h, self._ptr, self._n, int(device), arr))
+
+
+def read_checkpoint_bytes(data) -> Checkpoint:
+    """container.hpp:92-142"""
+    c = Container(data)
+    out = Checkpoint(c.step, [Tensor(n, s, np.empty(k, np.uint16)) for n, s, k, _ in c.tensors])
+    c.copy_out([t.data.ctypes.data for t in out.tensors], device=False)
+    return out
+
+
+def read_checkpoint_to_device(data, device_tensors) -> Container:
+    """Parse + check like read_checkpoint_bytes, then copy tensor i's payload
+    straight into device_tensors[i] (a CUDA tensor of numel 2-byte elements)."""
+    c = Container(data)
+    if len(device_tensors) != len(c.tensors):
+        raise PulseError(2, "one device tensor per container tensor required")
+    for t, (name, _, k, _) in zip(device_tensors, c.tensors):
+        if not t.is_cuda or t.element_size() != 2 or t.numel() != k or not t.is_contiguous():
+            raise PulseError(2, f"device tensor for {name} must be a contiguous CUDA tensor of {k} 2-byte elements")
+    c.copy_out([t.data_ptr() for t in device_tensors], device=True)
+    return c
+
+
+def write_checkpoint_bytes_from_device(step: int, names, shapes, device_tensors) -> bytes:
+    """PULC bytes of a checkpoint resident in HBM (payloads copied straight out of the device)."""
+    keep, arr = [], (N.Tensor * max(1, len(names)))()
+    for i, (name, shape, t) in enumerate(zip(names, shapes, device_tensors)):
+        shp = np.ascontiguousarray(shape, dtype=np.int64)
+        nm = name.encode()
+        keep += [shp, nm]
+        arr[i] = N.Tensor(nm, shp.ctypes.data_as(C.POINTER(C.c_int64)), len(shape), t.data_ptr(), t.numel())
+    ck = N.CheckpointC(step, arr, len(names))
+    out = C.c_void_p()
+    N.check(N.lib.pulse_write_checkpoint_bytes(C.byref(ck), 1, C.byref(out)))
+    return _take(out)
+
+
 # ---- end-to-end benchmark leg ---------------------------------------------------------------------
 def bench_e2e(args, mine, prev_dev, curr_dev, world, rank, steps=None, warmup=3):
     """The benchmark metric measured end to end through the public host API.

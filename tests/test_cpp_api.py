@@ -11,7 +11,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "tests", "_bin")
 
-HOST_SUITES = ["test_bf16", "test_compression", "test_hashing", "test_synthetic"]
+HOST_SUITES = ["test_bf16", "test_compression", "test_hashing", "test_synthetic", "test_container"]
 GPU_SUITES = ["test_patch", "test_index_coding", "test_patch_file", "test_metrics", "test_absorption"]
 
 
