@@ -217,6 +217,11 @@ struct ApplyArgs {
     uint64_t* scan_status;               // F2 look-back words (2 per block, zeroed per call)
     unsigned long long* scan_ticket;     // F2 block ticket (zeroed per call)
     uint32_t scan_blocks;                // F2 grid: blocks for the plan's capacity
+    uint32_t* range_e;                   // [ranges] F0 out: patch entry holding each range's first entry
+    uint32_t* range_flag;                // [ranges] F1s out: list of the non-plain ranges (exact checks in F3)
+    unsigned long long* n_flagged;       // its length (zeroed by decode_prologue)
+    uint64_t* slack;                     // [ranges] F1s out: cols - 1 - first row segment's local end column
+    int vmode;                           // F3 validate: 0 = non-plain ranges (all if suspect), 1 = all if any failure
 };
 
 // Walker path over entries [first, last) for one pass.  (ar, ac): aggregates
@@ -328,7 +333,21 @@ f_pass(ApplyArgs A) {
     const uint64_t gap_base = has_prev ? A.carry->gap_base : 0;
     const uint64_t stride = uint64_t(gridDim.x) * kWarps;
 
-    for (uint64_t rg = uint64_t(blockIdx.x) * kWarps + warp; rg < n_ranges; rg += stride) {
+    // F3 validate after F1s: exact checks where F1s could not decide (see f_stream)
+    // (non-plain ranges only: the list F1s built, one range per warp)
+    bool filter = false;
+    uint64_t n_items = n_ranges;
+    if (kPass == kValidate && A.range_flag) {
+        const bool suspect = *(volatile const uint32_t*)(A.flags + 1) != 0;
+        if (A.vmode == 0) {
+            filter = !suspect;
+            if (filter) n_items = *(volatile const unsigned long long*)A.n_flagged;
+        } else {  // second launch: re-check everything only if the filtered pass found a failure
+            if (suspect || *(volatile const uint64_t*)A.err == kNoError) return;
+        }
+    }
+    for (uint64_t it = uint64_t(blockIdx.x) * kWarps + warp; it < n_items; it += stride) {
+        const uint64_t rg = filter ? A.range_flag[it] : it;
         const uint64_t r0 = rg * kRange, r1 = min(r0 + kRange, n);
         uint64_t ar = 0, ac = 0;  // kAgg: aggregates; else running (row, col) / sums
         if (kPass != kAgg) {
@@ -338,6 +357,7 @@ f_pass(ApplyArgs A) {
         }
         bool marker = false;
         uint32_t e = upper_index<uint64_t>(A.es, 0, A.n_e, r0);
+        if (kPass == kAgg && lane == 0) A.range_e[rg] = e;
         for (uint64_t c0 = r0; c0 < r1; c0 += kChunk) {
             const uint32_t len = uint32_t(r1 - c0 < kChunk ? r1 - c0 : kChunk);
             while (A.es[e + 1] <= c0) ++e;
@@ -521,6 +541,421 @@ f_pass(ApplyArgs A) {
 }
 
 // =============================================================================================
+// Streaming passes over fixed-layout payloads: F1s f_stream<agg> and F5 f_stream<scatter>
+// =============================================================================================
+// F1s (aggregates + checks) and F5 (the in-place scatter of a patch that has
+// passed every check) share one skeleton, leaner and latency-hidden next to F1/F3:
+//  * 512-entry chunks, 16 consecutive entries per lane; three CTAs per SM;
+//  * the next chunk's rows / columns / u32 gaps (/ values) are in flight
+//    (cp.async of the 16-byte blocks covering them, double-buffered) while the
+//    current one decodes; the payload's byte alignment is removed on the
+//    shared-memory read (funnel shifts), not through registers;
+//  * per-lane running values in 32 bits where they fit (COO rows / columns);
+//  * each range's patch entry comes from F0 f_range_entries (two dependent
+//    loads per range instead of a binary search).
+//
+// Checks without the carry.  Inside a range that holds no patch-entry start or
+// end ("plain" range) every reference check but one is local or monotone:
+//   zero gaps (patch.hpp:201-203, 225-227; index_coding.hpp:147-149) -- local;
+//   rows / int32 indices / FLAT positions (patch.hpp:206-208, 231-233, 252-254)
+//     -- non-decreasing within an entry, so bounded by the entry's first and
+//     last entries, which lie in non-plain ranges;
+//   COO columns (patch.hpp:247-250) -- increasing within a row: a column is
+//     known exactly once a row starts inside the range (checked here); the
+//     range's first row segment ends at carry + P, checked by F2 once the
+//     carry is known (`slack` = cols - 1 - P).
+// Non-plain ranges (and every range, once anything looked wrong) go through the
+// exact F3 checks (f_pass<validate>), which also pin the reference's first
+// failing entry; F5 runs only if nothing failed.
+constexpr uint64_t kNoSlack = ~0ull;
+
+// Per-warp staging of F1s (1024-entry chunks: more bytes in flight per warp for
+// a pass that only reads) and F5 (512-entry chunks, values and decoded indices
+// too).  Lane l reads its fields as slots [P*l, P*l + P] of a buffer swizzled
+// with V = P (P = 16-byte slots per lane).
+template <int kRepr, bool kAgg_>
+struct SLay {
+    static constexpr bool coo = kRepr == kCoo;
+    static constexpr uint32_t ch = kAgg_ ? 1024 : 512;                        // entries per chunk
+    static constexpr uint32_t per = ch / 32;                                  // entries per lane
+    static constexpr uint32_t va = coo ? per / 16 : per / 4;                  // rows | u32 gaps
+    static constexpr uint32_t vb = per / 8;                                   // columns
+    static constexpr uint32_t a_slots = 32 * va + 1;
+    static constexpr uint32_t b_slots = coo ? 32 * vb + 1 : 0;
+    static constexpr uint32_t v_slots = kAgg_ ? 0 : 2 * ch / 16 + 1;          // values (V=1)
+    static constexpr uint32_t buf = 16 * (a_slots + b_slots + v_slots);
+    static constexpr uint32_t warp = 2 * buf + (kAgg_ ? 0 : 4 * ch);          // 2 buffers (+ decoded indices)
+};
+
+// Queues the 16-byte blocks covering [g, g+len) into dst (swizzle V); returns g & 15.
+template <int V>
+__device__ __forceinline__ uint32_t stage_cover(uint4* dst, const uint8_t* g, uint32_t len) {
+    const int lane = threadIdx.x & 31;
+    const uintptr_t ga = reinterpret_cast<uintptr_t>(g);
+    const uint32_t s = uint32_t(ga & 15);
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(ga - s);
+    const uint32_t nslots = len ? (s + len + 15) >> 4 : 0;
+    for (uint32_t q = lane; q < nslots; q += 32) cp_async16(dst + swz<V>(q), base + 16 * q);
+    return s;
+}
+
+// 16 payload bytes starting at byte s + 16*k of a staged buffer (slots k, k+1).
+template <int V>
+__device__ __forceinline__ uint4 staged16(const uint4* buf, uint32_t k, uint32_t s) {
+    const uint4 lo = lds128(buf + swz<V>(k));
+    if (s == 0) return lo;
+    const uint4 hi = lds128(buf + swz<V>(k + 1));
+    return funnel16(lo, hi, s >> 2, (s & 3) * 8);
+}
+
+struct SCtx {
+    uint32_t e;
+    uint32_t tensor;
+    uint64_t lo, hi;  // entries [lo, hi) belong to patch entry e
+    uint64_t idx_off, count, val_off, numel, cols, flat_base;
+};
+
+__device__ __forceinline__ void load_sctx(SCtx& c, const ApplyArgs& A, uint32_t e) {
+    c.e = e;
+    c.lo = A.es[e];
+    c.hi = A.es[e + 1];
+    const EntryLayout& L = A.el[e];
+    c.tensor = uint32_t(L.tensor);
+    c.idx_off = L.idx_off;
+    c.count = L.count;
+    c.val_off = L.val_off;
+    c.numel = L.numel;
+    c.cols = L.cols;
+    c.flat_base = L.flat_base;
+}
+
+// F0: the patch entry holding each range's first entry.
+__global__ void f_range_entries(ApplyArgs A) {
+    if (fast_blocked(A.flags)) return;
+    const uint64_t n = A.totals[0];
+    const uint64_t n_ranges = (n + kRange - 1) / kRange;
+    for (uint64_t rg = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; rg < n_ranges;
+         rg += uint64_t(gridDim.x) * blockDim.x)
+        A.range_e[rg] = upper_index<uint64_t>(A.es, 0, A.n_e, rg * kRange);
+}
+
+// One staged fast chunk of f_stream: lane aggregates + warp scan, then either
+// the carry-free checks (F1s) or the decode + scatter (F5).  Branch-free per
+// entry; kFull (every chunk but a range's last) drops the tail guards.
+template <int kRepr, bool kAgg_, bool kFull>
+__device__ __forceinline__ void chunk_body(const ApplyArgs& A, const SCtx& cur, uint64_t c0, uint32_t len, uint64_t r0,
+                                           const uint8_t* bb, uint32_t* sx, const uint32_t* sh, bool has_prev,
+                                           uint64_t gap_base, uint64_t& ar, uint64_t& ac, bool& suspect,
+                                           bool& marker, uint64_t& slack) {
+    using Y = SLay<kRepr, kAgg_>;
+    constexpr bool coo = kRepr == kCoo;
+    constexpr int kPer = int(Y::per);
+    const int lane = threadIdx.x & 31;
+    const uint4* sa = reinterpret_cast<const uint4*>(bb);
+    const uint4* sb = reinterpret_cast<const uint4*>(bb + 16 * Y::a_slots);
+    const uint64_t o0 = c0 - cur.lo;
+    const int nv = kFull ? kPer : max(0, min(kPer, int(len) - lane * kPer));
+    const uint64_t i0 = c0 + uint64_t(lane) * kPer;  // global ordinal of the lane's first entry
+    const bool lane_first = o0 + uint64_t(lane) * kPer == 0;
+    // this lane's fields: COO rows (4 per word) + columns (2 per word); int32: u32 gaps
+    constexpr int kAW = coo ? kPer / 4 : kPer, kBW = coo ? kPer / 2 : 1;
+    uint32_t aw[kAW], bw[kBW];
+#pragma unroll
+    for (int i = 0; i < int(Y::va); ++i) {
+        const uint4 q = staged16<Y::va>(sa, uint32_t(Y::va * lane + i), sh[0]);
+        aw[4 * i] = q.x; aw[4 * i + 1] = q.y; aw[4 * i + 2] = q.z; aw[4 * i + 3] = q.w;
+    }
+    if (coo) {
+#pragma unroll
+        for (int i = 0; i < int(Y::vb); ++i) {
+            const uint4 q = staged16<Y::vb>(sb, uint32_t(Y::vb * lane + i), sh[1]);
+            bw[(4 * i) % kBW] = q.x; bw[(4 * i + 1) % kBW] = q.y; bw[(4 * i + 2) % kBW] = q.z; bw[(4 * i + 3) % kBW] = q.w;
+        }
+    } else {
+        bw[0] = 0;
+    }
+    if (!kFull) {  // entries past the chunk read as (0, 0) and are never heads
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            if (j >= nv) {
+                if (coo) {
+                    aw[(j >> 2) % kAW] &= ~(0xFFu << (8 * (j & 3)));
+                    bw[(j >> 1) % kBW] &= ~(0xFFFFu << (16 * (j & 1)));
+                } else {
+                    aw[j % kAW] = 0;
+                }
+            }
+        }
+    }
+#define PULSE_SA(j) (coo ? (aw[((j) >> 2) % kAW] >> (8 * ((j) & 3))) & 0xFFu : aw[(j) % kAW])
+#define PULSE_SB(j) (coo ? (bw[((j) >> 1) % kBW] >> (16 * ((j) & 1))) & 0xFFFFu : 0u)
+    // ---- lane aggregates (+ the carry-free checks of F1s) ----
+    uint64_t lr, lc = 0;
+    bool bad = false, mk = false, head0 = lane_first;
+    uint32_t P = 0;  // COO: column sum of the lane's entries before its first row start
+    bool hc = false;
+    if (coo) {
+        uint32_t rs = 0;
+#pragma unroll
+        for (int w = 0; w < kAW; ++w) {
+            rs = __dp4a(aw[w], 0x01010101u, rs);
+            if (kAgg_) mk |= ((~aw[w] - 0x01010101u) & aw[w] & 0x80808080u) != 0;  // a 0xFF row byte
+        }
+        if (kAgg_) {
+#pragma unroll
+            for (int w = 0; w < kBW; ++w) mk |= ((~bw[w] - 0x00010001u) & bw[w] & 0x80008000u) != 0;  // 0xFFFF
+        }
+        uint32_t c = 0;
+        const uint32_t cols = uint32_t(cur.cols);
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const uint32_t a = PULSE_SA(j), bv = PULSE_SB(j);
+            const bool nr = a != 0 || (j == 0 && lane_first);
+            if (j == 0) head0 = nr;
+            if (kAgg_) {
+                bad |= !nr && bv == 0 && (kFull || j < nv);  // zero column gap within a row
+                P += (hc || nr) ? 0u : bv;
+            }
+            c = nr ? bv : c + bv;
+            hc |= nr;
+            if (kAgg_) bad |= hc && c >= cols;  // rows that start in this lane: columns known
+        }
+        lr = uint64_t(rs) | (lane_first ? H : 0);
+        lc = uint64_t(c) | (hc ? H : 0);
+    } else {
+        uint64_t r = 0;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const uint32_t a = PULSE_SA(j);
+            r += a;
+            if (kAgg_) {
+                if (kRepr == kI32) bad |= a == 0 && !(j == 0 && lane_first) && (kFull || j < nv);
+                else bad |= a == 0 && (i0 + j > 0 || has_prev) && (kFull || j < nv);
+            }
+        }
+        lr = r | (kRepr == kI32 && lane_first ? H : 0);
+    }
+    uint64_t ir = lr, ic = lc;
+    warp_segscan2(ir, ic);
+    const uint64_t tr = __shfl_sync(0xffffffffu, ir, 31), tc = __shfl_sync(0xffffffffu, ic, 31);
+    uint64_t er = __shfl_up_sync(0xffffffffu, ir, 1), ec = __shfl_up_sync(0xffffffffu, ic, 1);
+    if (lane == 0) er = ec = 0;
+    if (kAgg_) {
+        uint64_t pend = kNoSlack;
+        if (coo && hc) {
+            // the lane's first row segment ends in this lane, at column (state at lane start) + P
+            const uint64_t cs = SegSumOp::op(ac, ec);
+            const uint64_t end = (cs & (H - 1)) + P;
+            if (cs & H) bad |= end >= cur.cols;              // a row started earlier in the range: exact
+            else if (i0 > r0 || !head0) pend = end;           // the range's first row segment: carry needed
+        }
+        suspect |= __any_sync(0xffffffffu, bad);
+        marker |= __any_sync(0xffffffffu, mk);
+        if (coo) {
+            const uint32_t who = __ballot_sync(0xffffffffu, pend != kNoSlack);
+            if (who) {  // at most one lane per range: the first row start after its first entry
+                const uint64_t p = __shfl_sync(0xffffffffu, pend, __ffs(who) - 1);
+                if (p >= cur.cols) suspect = true;
+                else slack = cur.cols - 1 - p;
+            }
+        }
+        ar = SegSumOp::op(ar, tr);
+        ac = SegSumOp::op(ac, tc);
+        return;
+    }
+    // ---- F5: decode into shared memory (lane-consecutive, swizzled), then scatter ----
+    uint64_t row = SegSumOp::op(ar, er) & (H - 1);
+    const uint64_t col = SegSumOp::op(ac, ec) & (H - 1);
+    ar = SegSumOp::op(ar, tr) & (H - 1);
+    ac = SegSumOp::op(ac, tc) & (H - 1);
+    const uint32_t cols32 = uint32_t(cur.cols);
+    uint32_t r32 = uint32_t(row), c32 = uint32_t(col);
+    const uint64_t flat_off = gap_base + cur.flat_base;
+#pragma unroll
+    for (int i = 0; i < kPer / 4; ++i) {
+        uint32_t xv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int j = 4 * i + k;
+            const uint32_t a = PULSE_SA(j), bv = PULSE_SB(j);
+            const bool first = j == 0 && lane_first;
+            if (coo) {
+                r32 = first ? a : r32 + a;
+                c32 = (first || a != 0) ? bv : c32 + bv;
+                xv[k] = r32 * cols32 + c32;
+            } else if (kRepr == kI32) {
+                r32 = first ? a : r32 + a;
+                xv[k] = r32;
+            } else {
+                row += a;
+                xv[k] = uint32_t(row - flat_off);
+            }
+        }
+        reinterpret_cast<uint4*>(sx)[swz<4>(uint32_t(lane * 4 + i))] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
+    }
+#undef PULSE_SA
+#undef PULSE_SB
+    __syncwarp();
+    // 32 consecutive changes per store instruction
+    uint16_t* W = A.weights[cur.tensor];
+    const uint8_t* sv = bb + 16 * (Y::a_slots + Y::b_slots);
+    const uint32_t sv_s = sh[2];
+    if ((sv_s & 1) == 0) {
+        const uint16_t* sv16 = reinterpret_cast<const uint16_t*>(sv + sv_s);
+#pragma unroll 4
+        for (uint32_t k = lane; k < len; k += 32) W[smem_word<4>(reinterpret_cast<const uint4*>(sx), k)] = sv16[k];
+    } else {
+#pragma unroll 4
+        for (uint32_t k = lane; k < len; k += 32) {
+            const uint32_t vb = sv_s + 2 * k;
+            W[smem_word<4>(reinterpret_cast<const uint4*>(sx), k)] = uint16_t(sv[vb] | uint32_t(sv[vb + 1]) << 8);
+        }
+    }
+}
+
+template <int kRepr, bool kAgg_>
+__global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    using Y = SLay<kRepr, kAgg_>;
+    constexpr bool coo = kRepr == kCoo;
+    constexpr bool agg = kAgg_;
+    constexpr uint32_t kSChunk = Y::ch, kSPer = Y::per;
+    if (fast_blocked(A.flags)) return;
+    if (!agg && *(volatile const uint64_t*)A.err != kNoError) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* ws = smem + warp * Y::warp;
+    uint32_t* sx = reinterpret_cast<uint32_t*>(ws + 2 * Y::buf);
+
+    const uint64_t n = A.totals[0];
+    const uint64_t n_ranges = (n + kRange - 1) / kRange;
+    const bool has_prev = A.carry && A.carry->has_prev;
+    const uint64_t gap_base = has_prev ? A.carry->gap_base : 0;
+    const uint64_t stride = uint64_t(gridDim.x) * kWarps;
+
+    uint64_t rg = uint64_t(blockIdx.x) * kWarps + warp;
+    if (rg >= n_ranges) return;
+    uint64_t c0 = rg * kRange;
+    SCtx cur;
+    load_sctx(cur, A, A.range_e[rg]);
+    auto range_end = [&](uint64_t r) { return min(r * kRange + kRange, n); };
+    auto chunk_len = [&](uint64_t r, uint64_t c) {
+        const uint64_t r1 = range_end(r);
+        return uint32_t(r1 - c < kSChunk ? r1 - c : kSChunk);
+    };
+    auto is_fast = [&](const SCtx& c, uint64_t cc, uint32_t len) {
+        return c.hi >= cc + len && c.numel < (1ull << 32);
+    };
+    // always commits one cp.async group (possibly empty): the wait<1> below then
+    // always means "everything but the chunk after this one"
+    auto prefetch = [&](bool any, const SCtx& c, uint64_t cc, uint32_t len, uint32_t b, uint32_t* sh) {
+        if (any && is_fast(c, cc, len)) {
+            uint8_t* bb = ws + b * Y::buf;
+            const uint64_t o0 = cc - c.lo;
+            if (coo) {
+                sh[0] = stage_cover<Y::va>(reinterpret_cast<uint4*>(bb), A.body + c.idx_off + o0, len);
+                sh[1] = stage_cover<Y::vb>(reinterpret_cast<uint4*>(bb + 16 * Y::a_slots),
+                                           A.body + c.idx_off + c.count + 2 * o0, 2 * len);
+            } else {
+                sh[0] = stage_cover<Y::va>(reinterpret_cast<uint4*>(bb), A.body + c.idx_off + 4 * o0, 4 * len);
+            }
+            if (!agg)
+                sh[2] = stage_cover<1>(reinterpret_cast<uint4*>(bb + 16 * (Y::a_slots + Y::b_slots)),
+                                       A.body + c.val_off + 2 * o0, 2 * len);
+        }
+        cp_async_commit();
+    };
+    // range state (F1s): plain range?, first-row-segment slack, anything wrong, escape markers
+    bool plain = false, suspect = false, marker = false;
+    uint64_t slack = kNoSlack;
+    auto range_begin = [&](uint64_t r, const SCtx& c) {
+        plain = c.lo < r * kRange && c.hi > range_end(r) && c.numel < (1ull << 32);
+        slack = kNoSlack;
+    };
+    uint32_t len = chunk_len(rg, c0);
+    uint32_t sh_cur[3] = {0, 0, 0}, sh_nx[3] = {0, 0, 0};
+    uint32_t b = 0;
+    prefetch(true, cur, c0, len, 0, sh_cur);
+    uint64_t ar = 0, ac = 0;
+    if (agg) {
+        range_begin(rg, cur);
+    } else {
+        const ulonglong2 p = A.agg[rg];
+        ar = p.x;
+        ac = p.y;
+    }
+    while (true) {
+        // ---- the next chunk: position and entry context (loads overlap the wait below) ----
+        uint64_t rg_nx = rg, c_nx = c0 + len;
+        if (c_nx >= range_end(rg)) {
+            rg_nx = rg + stride;
+            c_nx = rg_nx * kRange;
+        }
+        const bool has_nx = rg_nx < n_ranges;
+        SCtx nx = cur;
+        uint32_t len_nx = 0;
+        ulonglong2 carry_nx = make_ulonglong2(0, 0);
+        if (has_nx) {
+            len_nx = chunk_len(rg_nx, c_nx);
+            if (rg_nx != rg) {
+                if (!agg) carry_nx = A.agg[rg_nx];
+                load_sctx(nx, A, A.range_e[rg_nx]);
+            } else if (c_nx >= cur.hi) {
+                uint32_t e = cur.e + 1;
+                while (A.es[e + 1] <= c_nx) ++e;
+                load_sctx(nx, A, e);
+            }
+        }
+        if (!is_fast(cur, c0, len)) {
+            // straddles patch entries or a tensor >= 2^32 elements: per-round walker (never plain)
+            slow_span<kRepr, agg ? kAgg : kScatter>(A, c0, c0 + len, ar, ac, marker, has_prev, gap_base);
+            prefetch(has_nx, nx, c_nx, len_nx, b ^ 1, sh_nx);
+        } else {
+            prefetch(has_nx, nx, c_nx, len_nx, b ^ 1, sh_nx);
+            cp_async_wait<1>();
+            __syncwarp();
+            const uint8_t* bb = ws + b * Y::buf;
+            if (len == kSChunk)
+                chunk_body<kRepr, agg, true>(A, cur, c0, len, rg * kRange, bb, sx, sh_cur, has_prev, gap_base, ar, ac,
+                                             suspect, marker, slack);
+            else
+                chunk_body<kRepr, agg, false>(A, cur, c0, len, rg * kRange, bb, sx, sh_cur, has_prev, gap_base, ar,
+                                              ac, suspect, marker, slack);
+            __syncwarp();
+        }
+        const bool range_done = !has_nx || rg_nx != rg;
+        if (agg && range_done) {
+            if (lane == 0) {
+                A.agg[rg] = make_ulonglong2(ar, ac);
+                if (!plain) A.range_flag[atomicAdd(A.n_flagged, 1ull)] = uint32_t(rg);
+                A.slack[rg] = plain ? slack : kNoSlack;
+            }
+            if (marker && lane == 0) atomicExch(A.flags, 1u);
+            if (suspect && lane == 0) atomicExch(A.flags + 1, 1u);
+            marker = suspect = false;
+        }
+        if (!has_nx) break;
+        if (rg_nx != rg) {
+            if (agg) {
+                ar = ac = 0;
+                range_begin(rg_nx, nx);
+            } else {
+                ar = carry_nx.x;
+                ac = carry_nx.y;
+            }
+        }
+        rg = rg_nx;
+        c0 = c_nx;
+        len = len_nx;
+        cur = nx;
+        sh_cur[0] = sh_nx[0];
+        sh_cur[1] = sh_nx[1];
+        sh_cur[2] = sh_nx[2];
+        b ^= 1;
+    }
+    cp_async_wait<0>();
+}
+
+// =============================================================================================
 // F2: exclusive SegSum scan of the range aggregates (one CTA of 1024)
 // =============================================================================================
 constexpr int kScanThreads = 1024;
@@ -557,8 +992,9 @@ __device__ __forceinline__ void cta_seg_exclusive(uint64_t& vr, uint64_t& vc, ui
 constexpr uint64_t kScanBlock = uint64_t(kScanThreads) * kScanPer;
 
 __global__ void __launch_bounds__(kScanThreads, 1)
-f_range_scan(const uint64_t* __restrict__ totals, ulonglong2* __restrict__ agg, const uint32_t* __restrict__ flags,
-             uint64_t* __restrict__ status, unsigned long long* __restrict__ ticket) {
+f_range_scan(const uint64_t* __restrict__ totals, ulonglong2* __restrict__ agg, uint32_t* __restrict__ flags,
+             uint64_t* __restrict__ status, unsigned long long* __restrict__ ticket,
+             const uint64_t* __restrict__ slack) {
     __shared__ uint64_t s_r[32], s_c[32];
     __shared__ uint64_t s_blk, s_tot[2], s_pre[2];
     if (fast_blocked(flags)) return;
@@ -598,7 +1034,11 @@ f_range_scan(const uint64_t* __restrict__ totals, ulonglong2* __restrict__ agg, 
     uint64_t sr = SegSumOp::op(s_pre[0], er), sc = SegSumOp::op(s_pre[1], ec);
 #pragma unroll
     for (int j = 0; j < kScanPer; ++j) {  // in place: aggregate -> exclusive prefix
-        if (q0 + j < n_ranges) agg[q0 + j] = make_ulonglong2(sr & (H - 1), sc & (H - 1));
+        if (q0 + j < n_ranges) {
+            agg[q0 + j] = make_ulonglong2(sr & (H - 1), sc & (H - 1));
+            // F1s deferred check: the range's first row segment ends at carry + P < cols
+            if (slack && (sc & (H - 1)) > slack[q0 + j]) atomicExch(flags + 1, 1u);
+        }
         sr = SegSumOp::op(sr, v[j].x);
         sc = SegSumOp::op(sc, v[j].y);
     }
@@ -623,20 +1063,61 @@ void launch_pass(const ApplyArgs& a, cudaStream_t s) {
     PULSE_LAUNCHED("f_pass", s);
 }
 
+template <int kRepr, bool kAgg_>
+void launch_stream(const ApplyArgs& a, cudaStream_t s) {
+    const uint32_t smem = kWarps * SLay<kRepr, kAgg_>::warp;
+    static PerDeviceInt occ;
+    int& per_sm = occ.here();
+    if (!per_sm) {
+        cudaFuncSetAttribute(f_stream<kRepr, kAgg_>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        int v = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, f_stream<kRepr, kAgg_>, kThreads, smem);
+        per_sm = v > 0 ? v : 1;
+    }
+    f_stream<kRepr, kAgg_><<<unsigned(sm_count() * per_sm), kThreads, smem, s>>>(a);
+    PULSE_LAUNCHED(kAgg_ ? "f_stream<agg>" : "f_stream<scatter>", s);
+}
+
+void launch_range_scan(const ApplyArgs& a, const uint64_t* slack, cudaStream_t s) {
+    cudaMemsetAsync(a.scan_status, 0, 2 * sizeof(uint64_t) * a.scan_blocks, s);
+    f_range_scan<<<a.scan_blocks, kScanThreads, 0, s>>>(a.totals, a.agg, a.flags, a.scan_status, a.scan_ticket,
+                                                        slack);
+    PULSE_LAUNCHED("f_range_scan", s);
+}
+
 template <int kRepr>
 void launch_all(const ApplyArgs& a, bool scatter, cudaStream_t s) {
-    launch_pass<kRepr, kAgg>(a, s);
-    cudaMemsetAsync(a.scan_status, 0, 2 * sizeof(uint64_t) * a.scan_blocks, s);
-    f_range_scan<<<a.scan_blocks, kScanThreads, 0, s>>>(a.totals, a.agg, a.flags, a.scan_status, a.scan_ticket);
-    PULSE_LAUNCHED("f_range_scan", s);
+    // PULSE_APPLY_MODE (A/B experiments): 1 = F1 + checked scatter with backup and restore;
+    // 2 = F1 + exact validation of every range + F3 scatter; default: the pipeline below
     static const int mode = getenv("PULSE_APPLY_MODE") ? atoi(getenv("PULSE_APPLY_MODE")) : 0;
-    if (a.weights && mode == 0) {  // in place: checked writes with backup, restore if anything failed
-        launch_pass<kRepr, kApply>(a, s);
-        launch_pass<kRepr, kRestore>(a, s);
-    } else {          // indices only (or PULSE_APPLY_MODE=1 in place): validate, then write them
-        launch_pass<kRepr, kValidate>(a, s);
-        if (scatter) launch_pass<kRepr, kScatter>(a, s);
+    if (mode == 1 || mode == 2) {
+        ApplyArgs b = a;
+        b.range_flag = nullptr;
+        launch_pass<kRepr, kAgg>(b, s);
+        launch_range_scan(b, nullptr, s);
+        if (b.weights && mode == 1) {
+            launch_pass<kRepr, kApply>(b, s);
+            launch_pass<kRepr, kRestore>(b, s);
+        } else {
+            launch_pass<kRepr, kValidate>(b, s);
+            if (scatter) launch_pass<kRepr, kScatter>(b, s);
+        }
+        return;
     }
+    // F0 range entries -> F1s aggregates + carry-free checks -> F2 scan (+ deferred column
+    // check) -> F3 exact checks where F1s could not decide (twice: the second only re-checks
+    // everything if the first found a failure, to report the reference's first one) -> F5 scatter
+    f_range_entries<<<unsigned(sm_count() * 2), kThreads, 0, s>>>(a);
+    PULSE_LAUNCHED("f_range_entries", s);
+    launch_stream<kRepr, true>(a, s);
+    launch_range_scan(a, a.slack, s);
+    ApplyArgs v = a;
+    v.vmode = 0;
+    launch_pass<kRepr, kValidate>(v, s);
+    v.vmode = 1;
+    launch_pass<kRepr, kValidate>(v, s);
+    if (scatter && a.weights) launch_stream<kRepr, false>(a, s);
+    else if (scatter) launch_pass<kRepr, kScatter>(a, s);
 }
 }  // namespace
 
@@ -659,6 +1140,14 @@ void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uin
     a.scan_status = p.d_status;  // general-decoder look-back words, idle on this path
     a.scan_ticket = reinterpret_cast<unsigned long long*>(p.d_totals + 15);  // zeroed by decode_prologue
     a.scan_blocks = uint32_t((p.cap / kRange + 2 + kScanBlock - 1) / kScanBlock);
+    // general-decoder scratch, idle on this path: colent [cap] u32 >= 2 x ranges, rowgap
+    // [cap] u32 >= 2 x ranges u64 (the legacy backup of PULSE_APPLY_MODE=1 uses rowgap instead)
+    const uint64_t n_rg = p.cap / kRange + 2;
+    a.range_e = p.colent;
+    a.range_flag = p.colent + n_rg;
+    a.n_flagged = reinterpret_cast<unsigned long long*>(p.d_totals + 14);  // zeroed by decode_prologue
+    a.slack = reinterpret_cast<uint64_t*>(p.rowgap);
+    a.vmode = 0;
     if (out_indices) a.weights = nullptr;
     const bool scatter = weights_slot >= 0 || out_indices;
     if (repr == PULSE_COO_DOWNSCALED) launch_all<kCoo>(a, scatter, s);

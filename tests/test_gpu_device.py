@@ -313,3 +313,152 @@ def test_segmented_and_wide_tensors_round_trip(numel, cols):
         assert torch.equal(w, curr)
     del prev, curr, w
     torch.cuda.empty_cache()
+
+
+def _first_failure(repr_, entries, body, sizes, has_prev=False):
+    """The reference's first failing (entry, check, ordinal) for a fixed-layout body
+    (patch.hpp:178-262, index_coding.hpp:130-158), or None; numpy restatement used
+    as the checker for the corruption tests below."""
+    glob = 0
+    any_decoded = has_prev
+    flat_base = 0
+    for k, e in enumerate(entries):
+        t = int(e["tensor"])
+        numel, cols = sizes[t]
+        cnt, off = int(e["count"]), int(e["idx_off"])
+        if repr_ == COO_DOWNSCALED:
+            rg = np.frombuffer(body, np.uint8, cnt, off).astype(np.int64)
+            cv = np.frombuffer(body, "<u2", cnt, off + cnt).astype(np.int64)
+            head = rg != 0
+            head[0] = True
+            zero = np.flatnonzero(~head & (cv == 0))
+            if zero.size:
+                return k, 3, int(zero[0])
+            rows = np.cumsum(rg)
+            seg = np.cumsum(head) - 1
+            starts = np.flatnonzero(head)
+            csum = np.cumsum(cv)
+            base = (csum - cv)[starts]
+            colv = csum - base[seg]
+            bad_c = colv >= cols
+            bad_i = rows * cols + colv >= numel
+            i = np.flatnonzero(bad_c | bad_i)
+            if i.size:
+                return k, (4 if bad_c[i[0]] else 5), int(i[0])
+        else:
+            g = np.frombuffer(body, "<u4", cnt, off).astype(np.int64)
+            if repr_ == COO_INT32:
+                idx = np.cumsum(g)
+                zero = g == 0
+                zero[0] = False
+                rng_ = idx >= numel
+            else:
+                gl = glob + np.cumsum(g) if any_decoded else g[0] + np.concatenate([[0], np.cumsum(g[1:])])
+                zero = g == 0
+                if not any_decoded:
+                    zero[0] = False
+                local = gl - flat_base
+                rng_ = (local < 0) | (local >= numel)
+                glob = int(gl[-1])
+                any_decoded = True
+            i = np.flatnonzero(zero | rng_)
+            if i.size:
+                return k, (2 if zero[i[0]] else 5), int(i[0])
+        flat_base += numel
+    return None
+
+
+@pytest.mark.parametrize("repr_", [COO_DOWNSCALED, COO_INT32, FLAT_INT32])
+@pytest.mark.parametrize("where", ["range_start", "slack", "mid_range", "row_jump", "zero_gap"])
+def test_mid_tensor_corruption_reports_first_failure(repr_, where):
+    """Bad entries deep inside a large tensor (ranges holding no tensor start or
+    end, where apply checks without the carry): the first failing entry and
+    check are the reference's, and nothing is written."""
+    D = _dev()
+    rng = np.random.default_rng(5)
+    sizes = [(2000 * 4096, 4096), (300 * 700, 700)]
+    prevs = [rng.integers(0, 65536, n, dtype=np.uint16) for n, _ in sizes]
+    currs = []
+    for a in prevs:
+        b = a.copy()
+        b[rng.random(a.size) < 0.02] ^= 1
+        currs.append(b)
+    plan = D.DevicePlan(sizes, sum(n for n, _ in sizes))
+    plan.bind(0, [torch.from_numpy(a.view(np.int16)).cuda() for a in prevs])
+    plan.bind(1, [torch.from_numpy(b.view(np.int16)).cuda() for b in currs])
+    w = [torch.from_numpy(a.view(np.int16)).cuda() for a in prevs]
+    plan.bind(2, w)
+    p = plan.encode(1, 0, repr_)
+    assert p.status == 0
+    e0 = p.host_entries[0]
+    off, cnt = int(e0["idx_off"]), int(e0["count"])
+    assert cnt > 5 * 4096
+    body = p.body[: p.body_bytes].cpu().numpy().copy()
+    k = 2 * 4096 + (0 if where == "range_start" else 1500)  # entry ordinal in tensor 0 (entries start at 0)
+    if repr_ == COO_DOWNSCALED:
+        rows = body[off:off + cnt]
+        cpos = off + cnt + 2 * k
+        if where == "row_jump":
+            rows[k:k + 20] = 200                       # rows past the tensor from here on
+        elif where == "zero_gap":
+            j = k + int(np.flatnonzero(rows[k:] == 0)[0])  # a non-head entry
+            cpos = off + cnt + 2 * j
+            body[cpos:cpos + 2] = 0
+        elif where == "slack":
+            # the range's first row segment [r, h) ends exactly at column `cols` while its
+            # range-local sum stays below it: only the carry from earlier ranges shows it
+            cv = body[off + cnt:off + 3 * cnt].view("<u2").astype(np.int64)
+            r = next(x for x in range(k, cnt, 4096) if rows[x] == 0 and rows[x - 1] == 0 and cv[x - 1] > 0)
+            h = r + int(np.flatnonzero(rows[r:] != 0)[0])
+            hh = r - 1 - int(np.flatnonzero(rows[:r][::-1] != 0)[0])  # head of the row holding r - 1
+            carry = int(cv[hh:r].sum())
+            local = int(cv[r:h].sum())
+            delta = 4096 - carry - local
+            assert 0 < carry and 0 < delta and cv[h - 1] + delta < 0xFFFF and local + delta < 4096
+            cv[h - 1] += delta
+            body[off + cnt:off + 3 * cnt] = cv.astype("<u2").view(np.uint8)
+        else:
+            j = k + int(np.flatnonzero(rows[k:] == 0)[0])  # a column inside a row
+            cpos = off + cnt + 2 * j
+            body[cpos:cpos + 2] = [0xFE, 0xFF]
+    else:
+        pos = off + 4 * k
+        if where == "zero_gap":
+            body[pos:pos + 4] = 0
+        elif where == "row_jump":
+            body[pos:pos + 4] = [0, 0, 0, 0x10]       # a 2^28 gap: every later index out of range
+        else:
+            body[pos:pos + 4] = [0xF0, 0xFF, 0xFF, 0x7F]
+    want = _first_failure(repr_, p.host_entries[: p.n_entries], body.tobytes(), sizes)
+    assert want is not None
+    p.body[: p.body_bytes] = torch.from_numpy(body).cuda()
+    res = D.parse_result(plan.apply(2, p))
+    assert int(res["status"]) == 7, res
+    assert (int(res["err_tensor"]), int(res["err_check"]), int(res["err_elem"])) == want, (res, want)
+    for a, t in zip(prevs, w):
+        assert np.array_equal(t.cpu().numpy().view(np.uint16), a)
+
+
+def test_clean_patch_checks_pass_on_plain_ranges():
+    """No false alarm: a large clean patch in every representation applies exactly
+    (the carry-free checks of plain ranges and the deferred column check)."""
+    D = _dev()
+    rng = np.random.default_rng(9)
+    sizes = [(3000 * 4096, 4096), (1 << 20, 1 << 20), (1000 * 9, 9)]
+    prevs = [rng.integers(0, 65536, n, dtype=np.uint16) for n, _ in sizes]
+    currs = []
+    for i, a in enumerate(prevs):
+        b = a.copy()
+        b[rng.random(a.size) < (0.3 if i == 2 else 0.01)] ^= 1
+        currs.append(b)
+    plan = D.DevicePlan(sizes, sum(n for n, _ in sizes))
+    plan.bind(0, [torch.from_numpy(a.view(np.int16)).cuda() for a in prevs])
+    plan.bind(1, [torch.from_numpy(b.view(np.int16)).cuda() for b in currs])
+    for repr_ in (COO_DOWNSCALED, COO_INT32, FLAT_INT32):
+        w = [torch.from_numpy(a.view(np.int16)).cuda() for a in prevs]
+        plan.bind(2, w)
+        p = plan.encode(1, 0, repr_)
+        res = D.parse_result(plan.apply(2, p))
+        assert int(res["status"]) == 0, (repr_, res)
+        for b, t in zip(currs, w):
+            assert np.array_equal(t.cpu().numpy().view(np.uint16), b)
