@@ -845,7 +845,103 @@ __device__ __noinline__ void k2b_span(const EntryMap& em, uint32_t repr, uint64_
     }
 }
 
-__global__ void __launch_bounds__(kThreads)
+// Largest i in [0, n) with a[i] <= x (a[0] <= x), by the whole warp: 32 probes
+// per round, so a few hundred segments take two dependent loads, not nine.
+__device__ __forceinline__ uint32_t warp_upper_index(const uint64_t* a, uint32_t n, uint64_t x) {
+    const int lane = threadIdx.x & 31;
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t p = lo + uint32_t(lane) * step;
+        const uint32_t m = __ballot_sync(0xffffffffu, p < hi && a[p] <= x);
+        lo += uint32_t(31 - __clz(m)) * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
+
+// One staged fast chunk of K2b: COO_DOWNSCALED row/column entries or int32 gaps,
+// then the value blob.  Returns false (nothing written) if a COO entry needs an
+// escape -- the caller then re-emits the chunk with the walker.  kFull (every
+// chunk but a range's last) drops the per-entry tail guards.
+template <bool kFull>
+__device__ __forceinline__ bool k2b_chunk(const EntryMap& em, uint32_t repr, const FastCtx& c, const TensorLayout& tl,
+                                          uint64_t c0, uint32_t len, uint32_t sg, uint64_t R, uint64_t Cc,
+                                          uint4* sidx, const uint4* sval, uint8_t* __restrict__ body) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t Lp = lane_pred(em, sidx, c0, c, sg);
+    const int nv = kFull ? int(kLaneE) : max(0, min(int(kLaneE), int(len) - lane * int(kLaneE)));
+    const uint64_t j0 = c0 - c.ts;                                     // ordinal of the chunk's first entry
+    const bool lane_first = j0 + uint64_t(lane) * kLaneE == 0;         // lane holds the tensor's first entry
+    if (repr == PULSE_COO_DOWNSCALED) {
+        uint32_t prow = div_magic(Lp, c.magic, c.shift), pcol = Lp - prow * c.cols32;
+        uint32_t rw[kLaneE / 4], cw2[kLaneE / 2];
+        bool esc = false;
+#pragma unroll
+        for (int i = 0; i < int(kLaneE / 4); ++i) {
+            const uint4 q = lane_vec<8>(sidx, i);
+            uint32_t rr = 0, c0w = 0, c1w = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int j = 4 * i + k;
+                const bool v = kFull || j < nv;
+                const uint32_t Lj = PULSE_LANE_L(q, k);
+                const uint32_t row = div_magic(Lj, c.magic, c.shift), col = Lj - row * c.cols32;
+                const bool first = j == 0 && lane_first;
+                const bool nr = first || row != prow;
+                const uint32_t rgap = first ? row : row - prow;
+                const uint32_t cval = nr ? col : col - pcol;
+                esc |= v && (rgap >= 0xFF || cval >= 0xFFFF);
+                rr |= (v ? rgap & 0xFF : 0u) << (8 * k);
+                const uint32_t cpart = (v ? cval & 0xFFFF : 0u) << (16 * (k & 1));
+                if (k < 2) c0w |= cpart;
+                else c1w |= cpart;
+                prow = row;
+                pcol = col;
+            }
+            rw[i] = rr;
+            cw2[2 * i] = c0w;
+            cw2[2 * i + 1] = c1w;
+        }
+        if (__any_sync(0xffffffffu, esc)) return false;  // escapes: variable-size entries
+        // packed rows (1 KiB, V=2) and columns (2 KiB, V=4) replace the chunk's indices
+        uint4* srow = sidx;
+        uint4* scol = sidx + kChunkE / 16;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            srow[swz<2>(uint32_t(lane * 2 + i))] = make_uint4(rw[4 * i], rw[4 * i + 1], rw[4 * i + 2], rw[4 * i + 3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            scol[swz<4>(uint32_t(lane * 4 + i))] = make_uint4(cw2[4 * i], cw2[4 * i + 1], cw2[4 * i + 2], cw2[4 * i + 3]);
+        __syncwarp();
+        unstage<2>(body + tl.idx_off + j0 + 4 * (R - tl.rts), srow, len);
+        unstage<4>(body + tl.idx_off + tl.row_bytes + 2 * j0 + 4 * (Cc - tl.cts), scol, 2 * len);
+    } else {
+        const uint64_t first_add = repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0;
+        uint32_t prev = Lp;
+        __syncwarp();  // every lane has read its predecessor before gaps overwrite indices
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {  // in place: each lane rewrites only its own slots
+            const uint32_t slot = swz<8>(uint32_t(lane * 8 + i));
+            const uint4 q = lds128(sidx + slot);
+            uint32_t g[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t Lj = PULSE_LANE_L(q, k);
+                g[k] = (i == 0 && k == 0 && lane_first) ? uint32_t(uint64_t(Lj) + first_add) : Lj - prev;
+                prev = Lj;
+            }
+            sidx[slot] = make_uint4(g[0], g[1], g[2], g[3]);
+        }
+        __syncwarp();
+        unstage<8>(body + tl.idx_off + 4 * j0, sidx, 4 * len);
+    }
+    unstage<1>(body + tl.val_off + 2 * j0, sval, 2 * len);
+    return true;
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
 k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
         const ulonglong2* __restrict__ range_pre, const uint16_t* __restrict__ vals,
         const pulse_result* __restrict__ result, uint8_t* __restrict__ body,
@@ -873,6 +969,12 @@ k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
     prefetch(cur, 0);
     uint64_t R = 0, Cc = 0;
     uint32_t sg = 0, b = 0;
+    // segment context, cached while consecutive chunks stay in one segment
+    FastCtx c{};
+    TensorLayout tl{};
+    uint32_t ctx_sg = ~0u;
+    uint64_t ctx_hi = 0;
+    bool ctx_ok = false;  // 32-bit fast path allowed for the cached segment's tensor
     while (cur.ok) {
         const ChunkIt nx = chunk_next(cur, stride, n_ranges, n);
         prefetch(nx, b ^ 1);
@@ -883,99 +985,33 @@ k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
                 R = p.x;
                 Cc = p.y;
             }
-            sg = em.n_segs ? upper_index<uint64_t>(em.seg_start, 0, em.n_segs, cur.c0) : 0;
+            sg = em.n_segs ? warp_upper_index(em.seg_start, em.n_segs, cur.c0) : 0;
         }
         const uint64_t c0 = cur.c0;
         const uint32_t len = cur.len;
-        const FastCtx c = fast_ctx(em, c0, len, sg);
+        if (sg != ctx_sg || c0 >= ctx_hi) {
+            c = fast_ctx(em, c0, len, sg);
+            tl = tlay[c.t];
+            ctx_sg = sg;
+            ctx_hi = em.seg_start[sg + 1];
+            ctx_ok = !em.idx64 && !em.coldiv[c.t].wide && em.numel[c.t] < (1ull << 32);
+        }
+        c.fast = ctx_ok && ctx_hi >= c0 + len;
         uint4* sidx = reinterpret_cast<uint4*>(ws + b * kSIdx);
         const uint4* sval = reinterpret_cast<const uint4*>(ws + 2 * kSIdx + b * kSVal);
-        if (!staged || !c.fast) {
-            k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
-            if (esc_flag && (R | Cc) && lane == 0) atomicExch(esc_flag, 1u);  // optimistic pass: escapes seen
-            cur = nx;
-            b ^= 1;
-            continue;
-        }
-        cp_async_wait<1>();
-        __syncwarp();
-        const uint32_t Lp = lane_pred(em, sidx, c0, c, sg);
-        const int nv = max(0, min(int(kLaneE), int(len) - lane * int(kLaneE)));
-        const uint64_t j0 = c0 - c.ts;                                     // ordinal of the chunk's first entry
-        const bool lane_first = j0 + uint64_t(lane) * kLaneE == 0;         // lane holds the tensor's first entry
-        const TensorLayout tl = tlay[c.t];
-        bool via_walker = false;
-        if (coo) {
-            uint32_t prow = div_magic(Lp, c.magic, c.shift), pcol = Lp - prow * c.cols32;
-            uint32_t rw[kLaneE / 4], cw2[kLaneE / 2];
-            bool esc = false;
-#pragma unroll
-            for (int q = 0; q < int(kLaneE / 4); ++q) rw[q] = 0;
-#pragma unroll
-            for (int q = 0; q < int(kLaneE / 2); ++q) cw2[q] = 0;
-#pragma unroll
-            for (int i = 0; i < int(kLaneE / 4); ++i) {
-                const uint4 q = lane_vec<8>(sidx, i);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int j = 4 * i + k;
-                    if (j < nv) {
-                        const uint32_t Lj = PULSE_LANE_L(q, k);
-                        const uint32_t row = div_magic(Lj, c.magic, c.shift), col = Lj - row * c.cols32;
-                        const bool first = j == 0 && lane_first;
-                        const bool nr = first || row != prow;
-                        const uint32_t rgap = first ? row : row - prow;
-                        const uint32_t cval = nr ? col : col - pcol;
-                        esc |= rgap >= 0xFF || cval >= 0xFFFF;
-                        rw[j >> 2] |= (rgap & 0xFF) << (8 * (j & 3));
-                        cw2[j >> 1] |= (cval & 0xFFFF) << (16 * (j & 1));
-                        prow = row;
-                        pcol = col;
-                    }
-                }
-            }
-            if (__any_sync(0xffffffffu, esc)) {
-                via_walker = true;  // escapes: variable-size entries
-            } else {
-                // packed rows (1 KiB, V=2) and columns (2 KiB, V=4) replace the chunk's indices
-                uint4* srow = sidx;
-                uint4* scol = sidx + kChunkE / 16;
-                __syncwarp();
-#pragma unroll
-                for (int i = 0; i < 2; ++i) srow[swz<2>(uint32_t(lane * 2 + i))] = make_uint4(rw[4 * i], rw[4 * i + 1], rw[4 * i + 2], rw[4 * i + 3]);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) scol[swz<4>(uint32_t(lane * 4 + i))] = make_uint4(cw2[4 * i], cw2[4 * i + 1], cw2[4 * i + 2], cw2[4 * i + 3]);
-                __syncwarp();
-                unstage<2>(body + tl.idx_off + j0 + 4 * (R - tl.rts), srow, len);
-                unstage<4>(body + tl.idx_off + tl.row_bytes + 2 * j0 + 4 * (Cc - tl.cts), scol, 2 * len);
-            }
-        } else {
-            const uint64_t first_add = repr == PULSE_FLAT_INT32 && tl.has_prev ? tl.gap_base : 0;
-            uint32_t prev = Lp;
-            __syncwarp();  // every lane has read its predecessor before gaps overwrite indices
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {  // in place: each lane rewrites only its own slots
-                const uint32_t slot = swz<8>(uint32_t(lane * 8 + i));
-                const uint4 q = lds128(sidx + slot);
-                uint32_t g[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t Lj = PULSE_LANE_L(q, k);
-                    g[k] = (i == 0 && k == 0 && lane_first) ? uint32_t(uint64_t(Lj) + first_add) : Lj - prev;
-                    prev = Lj;
-                }
-                sidx[slot] = make_uint4(g[0], g[1], g[2], g[3]);
-            }
+        bool done = false;
+        if (staged && c.fast) {
+            cp_async_wait<1>();
             __syncwarp();
-            unstage<8>(body + tl.idx_off + 4 * j0, sidx, 4 * len);
-        }
-        if (via_walker) {
+            done = len == kChunkE ? k2b_chunk<true>(em, repr, c, tl, c0, len, sg, R, Cc, sidx, sval, body)
+                                  : k2b_chunk<false>(em, repr, c, tl, c0, len, sg, R, Cc, sidx, sval, body);
             __syncwarp();
-            k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
-        } else {
-            unstage<1>(body + tl.val_off + 2 * j0, sval, 2 * len);
         }
-        __syncwarp();
+        if (!done) {  // segment boundary, caller int64 indices, or escapes: per-round walker
+            cp_async_wait<1>();  // this chunk's staging lands before its buffer is reused
+            k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
+            __syncwarp();
+        }
         if (esc_flag && (R | Cc) && lane == 0) atomicExch(esc_flag, 1u);  // optimistic pass: escapes seen
         cur = nx;
         b ^= 1;
