@@ -70,6 +70,7 @@ namespace detail {
         case PULSE_E_TENSOR_SET: throw TensorSetError(msg);
         case PULSE_E_INDEX_RANGE: throw IndexRangeError(msg);
         case PULSE_E_DIMENSION: throw DimensionError(msg);
+        case PULSE_E_PROTOCOL: throw ProtocolViolationError(msg);
         case PULSE_E_HASH_MISMATCH: {
             // "hash mismatch: expected <hex>, actual <hex>"
             const auto e = msg.find("expected "), a = msg.find(", actual ");

@@ -50,7 +50,8 @@ typedef enum pulse_status {
     PULSE_E_DIMENSION = 12,      /* pulse::DimensionError        error.hpp:71  */
     PULSE_E_HASH_MISMATCH = 13,  /* pulse::HashMismatchError     error.hpp:77  */
     PULSE_E_CUDA = 14,           /* device/runtime failure (no reference analogue) */
-    PULSE_E_CAPACITY = 15        /* caller arena too small; see `required` */
+    PULSE_E_CAPACITY = 15,       /* caller arena too small; see `required` */
+    PULSE_E_PROTOCOL = 16        /* pulse::ProtocolViolationError error.hpp:112 */
 } pulse_status;
 
 /* SparseRepresentation (patch.hpp:20-24) and CodecId (compression.hpp:31-37). */
@@ -385,6 +386,59 @@ pulse_status pulse_container_get_tensor(const pulse_container* container, uint32
  * complete. */
 pulse_status pulse_container_copy_out(const pulse_container* container, const uint8_t* data, uint64_t n,
                                       int device, void* const* dst);
+
+/* ======================================================================= */
+/* Resident checkpoints: the sync path on device (sync.hpp:78-92, 166-211, */
+/* 308-352)                                                                */
+/* ======================================================================= */
+
+/* A checkpoint held in HBM of the current device, with its step and weights
+ * hash -- the consumer's SyncState (sync.hpp:78-92) and the publisher's last
+ * published snapshot.  PULP patches are applied to it in place straight from
+ * their blobs (no int64 index round trip), and new patches are encoded from
+ * it against device-resident weights and written straight from the device
+ * body, hashing the target once (sync.hpp:176 and patch.hpp:282 hash it
+ * twice). */
+typedef struct pulse_resident pulse_resident;
+
+/* checkpoint_to_state: uploads `checkpoint` (validated; host data) and hashes
+ * it.  `max_changes` sizes the device scratch (grown on demand). */
+pulse_status pulse_resident_create(const pulse_checkpoint* checkpoint, uint64_t max_changes, pulse_resident** out);
+void pulse_resident_destroy(pulse_resident* r);
+uint64_t pulse_resident_step(const pulse_resident* r);
+uint64_t pulse_resident_last_anchor_step(const pulse_resident* r);
+pulse_status pulse_resident_hash(const pulse_resident* r, uint8_t* out32);
+uint32_t pulse_resident_num_tensors(const pulse_resident* r);
+/* Device pointer of tensor i (the checkpoint's insertion order). */
+pulse_status pulse_resident_tensor(const pulse_resident* r, uint32_t i, void** dev_ptr);
+/* Copies every tensor to host memory out[i] (numel values each). */
+pulse_status pulse_resident_download(const pulse_resident* r, uint16_t* const* out);
+
+/* apply_delta (sync.hpp:308-329) for the PULP bytes of the delta to `step`:
+ * patch.base_step must equal the held step and patch.target_step `step`, and
+ * patch.target_hash `expected_hash32` when non-NULL (the manifest's weights
+ * hash) -- else PULSE_E_PROTOCOL; tensor names / shapes as decode checks them
+ * (patch.hpp:314-324); then validate-then-scatter in place.  verify_hash != 0
+ * re-hashes the result (decode's check, patch.hpp:341-346) and on a mismatch
+ * puts the overwritten values back before failing with HashMismatchError, so
+ * a failed apply never changes the held state. */
+pulse_status pulse_resident_apply(pulse_resident* r, const uint8_t* pulp, uint64_t n, uint64_t step,
+                                  const uint8_t* expected_hash32, int verify_hash);
+/* walk_deltas (sync.hpp:331-352): the deltas to steps held+1 .. held+k, in
+ * order; the next patch is parsed and uploaded while the current one applies.
+ * Returns the number applied in *applied (stops at the first failure). */
+pulse_status pulse_resident_walk(pulse_resident* r, const uint8_t* const* pulps, const uint64_t* sizes, uint32_t k,
+                                 int verify_hash, uint32_t* applied);
+/* publish_checkpoint's patch (sync.hpp:166-181): `dev_current` (device
+ * pointers, insertion order, same tensors as the held checkpoint) at step
+ * held+1 is encoded against the held weights on the device; the PULP bytes
+ * come straight from the device body (codec on host threads) with
+ * anchor_step as given; the target hash (sha256 of dev_current, computed
+ * once) goes to out_hash32.  advance != 0 then applies the patch to the held
+ * weights, so the resident becomes the new last-published snapshot. */
+pulse_status pulse_resident_publish(pulse_resident* r, const void* const* dev_current, uint64_t step,
+                                    uint32_t representation, uint32_t codec, uint64_t anchor_step, int advance,
+                                    pulse_bytes** out_pulp, uint8_t* out_hash32);
 
 #ifdef __cplusplus
 }

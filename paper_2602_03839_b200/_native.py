@@ -26,7 +26,7 @@ STATUS = {
     0: "OK", 1: "Error", 2: "ArgumentError", 3: "FormatError", 4: "BadMagicError", 5: "VersionError",
     6: "TruncationError", 7: "CorruptStreamError", 8: "ModelMismatchError", 9: "ShapeMismatchError",
     10: "TensorSetError", 11: "IndexRangeError", 12: "DimensionError", 13: "HashMismatchError",
-    14: "CudaError", 15: "CapacityError",
+    14: "CudaError", 15: "CapacityError", 16: "ProtocolViolationError",
 }
 COO_DOWNSCALED, COO_INT32, FLAT_INT32 = 0, 1, 2
 IDENTITY, LZ4, ZSTD1, ZSTD3, GZIP6 = 0, 1, 2, 3, 4
@@ -183,6 +183,18 @@ _SIGS = {
     "pulse_container_num_tensors": (u32, [vp]),
     "pulse_container_get_tensor": (i32, [vp, u32, C.POINTER(ContainerTensorC)]),
     "pulse_container_copy_out": (i32, [vp, vp, u64, C.c_int, C.POINTER(vp)]),
+    # resident checkpoints (sync path)
+    "pulse_resident_create": (i32, [C.POINTER(CheckpointC), u64, C.POINTER(vp)]),
+    "pulse_resident_destroy": (None, [vp]),
+    "pulse_resident_step": (u64, [vp]),
+    "pulse_resident_last_anchor_step": (u64, [vp]),
+    "pulse_resident_hash": (i32, [vp, C.c_char_p]),
+    "pulse_resident_num_tensors": (u32, [vp]),
+    "pulse_resident_tensor": (i32, [vp, u32, C.POINTER(vp)]),
+    "pulse_resident_download": (i32, [vp, C.POINTER(vp)]),
+    "pulse_resident_apply": (i32, [vp, vp, u64, u64, C.c_char_p, C.c_int]),
+    "pulse_resident_walk": (i32, [vp, C.POINTER(vp), C.POINTER(u64), u32, C.c_int, C.POINTER(u32)]),
+    "pulse_resident_publish": (i32, [vp, C.POINTER(vp), u64, u32, u32, u64, C.c_int, C.POINTER(vp), C.c_char_p]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)

@@ -191,6 +191,24 @@ __global__ void k_coo_unpack(const uint8_t* __restrict__ p, uint64_t len, uint64
     if (pos != len) report(err, error_key(0, kStageTrailing, 0, kTrailing));
 }
 
+// Values at decoded indices: out[i] = W_t[idx[i]] for entry e's tensor t,
+// entries [start[e], start[e+1]) (the resident apply's undo copy).
+__global__ void k_gather_values(uint16_t* const* __restrict__ w, const pulse_patch_entry* __restrict__ ents,
+                                const uint64_t* __restrict__ start, uint32_t n_e, const int64_t* __restrict__ idx,
+                                uint16_t* __restrict__ out) {
+    const uint64_t n = start[n_e];
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t e = upper_index<uint64_t>(start, 0, n_e, i);
+        out[i] = w[ents[e].tensor][idx[i]];
+    }
+}
+
+void launch_gather_values(const PlanDev& p, int slot, const pulse_patch_entry* ents, const uint64_t* start,
+                          uint32_t n_e, const int64_t* idx, uint16_t* out, cudaStream_t s) {
+    k_gather_values<<<sm_count() * 4, 256, 0, s>>>(p.slot[slot], ents, start, n_e, idx, out);
+    PULSE_LAUNCHED("k_gather_values", s);
+}
+
 void launch_export_indices(const PlanDev& p, int64_t* out, cudaStream_t s) {
     k_export_indices<<<sm_count() * 4, 256, 0, s>>>(p.segs, p.seg_start, p.n_segs, p.idx32, out);
     PULSE_LAUNCHED("k_export_indices", s);

@@ -742,6 +742,212 @@ std::vector<uint8_t> value_payload(const std::vector<uint16_t>& v) {  // patch.h
     return out;
 }
 
+// One tensor's record and its two (codec-applied) blobs for assemble_pulp.
+struct PulpTensorRef {
+    const std::string* name;
+    const std::vector<int64_t>* shape;
+    uint64_t count;
+    const uint8_t* ip;
+    uint64_t in;
+    const uint8_t* vp;
+    uint64_t vn;
+};
+
+// patch_file.hpp:44-83: the sorted-key JSON header (nlohmann, as the reference)
+// and the container; blobs are copied in on the thread pool.
+std::unique_ptr<pulse_bytes> assemble_pulp(int64_t anchor_step, int64_t base_step, int64_t target_step,
+                                           const uint8_t* target_hash, uint32_t codec, uint32_t representation,
+                                           const std::vector<PulpTensorRef>& refs) {
+    const size_t T = refs.size();
+    nlohmann::json header;
+    header["anchor_step"] = anchor_step;
+    header["base_step"] = base_step;
+    header["target_step"] = target_step;
+    header["target_hash"] = hex(target_hash);
+    header["codec"] = codec;
+    header["representation"] = repr_name(representation);
+    auto& table = header["tensors"] = nlohmann::json::array();
+    for (size_t t = 0; t < T; ++t) {
+        const auto& r = refs[t];
+        nlohmann::json e = {{"name", *r.name},
+                            {"shape", *r.shape},
+                            {"count", r.count},
+                            {"index_nbytes", r.in},
+                            {"value_nbytes", r.vn}};
+        if (representation == PULSE_COO_DOWNSCALED) {
+            e["row_bits"] = 8;
+            e["col_bits"] = 16;
+        }
+        table.push_back(std::move(e));
+    }
+    const std::string js = header.dump();
+    auto res = std::make_unique<pulse_bytes>();
+    std::vector<uint64_t> at(T + 1);
+    at[0] = 16 + js.size();
+    for (size_t t = 0; t < T; ++t) at[t + 1] = at[t] + refs[t].in + refs[t].vn;
+    res->v.resize(at[T]);
+    uint8_t* w = res->v.data();
+    std::memcpy(w, "PULP", 4);
+    const uint32_t ver = 1;
+    const uint64_t hl = js.size();
+    for (int i = 0; i < 4; ++i) w[4 + i] = uint8_t(ver >> (8 * i));
+    for (int i = 0; i < 8; ++i) w[8 + i] = uint8_t(hl >> (8 * i));
+    std::memcpy(w + 16, js.data(), js.size());
+    pool().parallel_for(T, [&](size_t t) {
+        if (refs[t].in) std::memcpy(w + at[t], refs[t].ip, refs[t].in);
+        if (refs[t].vn) std::memcpy(w + at[t] + refs[t].in, refs[t].vp, refs[t].vn);
+    });
+    return res;
+}
+
+// PULP container -> header, tensors (values filled, indices not yet decoded) and
+// each tensor's raw (decompressed) index payload: patch_file.hpp:85-147 up to
+// the index decoding, with the reference's checks and error order.
+struct ParsedPulp {
+    std::unique_ptr<pulse_patch> p;
+    std::vector<std::vector<uint8_t>> store;  // decompressed index payloads (non-identity codecs)
+    std::vector<const uint8_t*> pl;           // index payload of each tensor
+    std::vector<uint64_t> lens;
+};
+
+ParsedPulp parse_pulp(const uint8_t* bytes, uint64_t n) {
+    uint64_t pos = 0;
+    auto need = [&](uint64_t k) {
+        if (n - pos < k) raise(PULSE_E_TRUNCATION, "unexpected end of data");
+    };
+    if (n < 4) raise(PULSE_E_TRUNCATION, "patch shorter than magic");
+    if (std::memcmp(bytes, "PULP", 4) != 0) raise(PULSE_E_BAD_MAGIC, "not a patch file (bad magic)");
+    pos = 4;
+    need(4);
+    uint32_t version = 0;
+    for (int i = 0; i < 4; ++i) version |= uint32_t(bytes[pos + i]) << (8 * i);
+    pos += 4;
+    if (version != 1) raise(PULSE_E_VERSION, "unsupported patch version " + std::to_string(version));
+    need(8);
+    uint64_t hl = 0;
+    for (int i = 0; i < 8; ++i) hl |= uint64_t(bytes[pos + i]) << (8 * i);
+    pos += 8;
+    if (hl > n - pos) raise(PULSE_E_TRUNCATION, "patch header truncated");
+    nlohmann::json header;
+    try {
+        header = nlohmann::json::parse(bytes + pos, bytes + pos + hl);
+    } catch (const nlohmann::json::exception& e) {
+        raise(PULSE_E_FORMAT, std::string("patch header is not valid JSON: ") + e.what());
+    }
+    pos += hl;
+    auto p = std::make_unique<pulse_patch>();
+    // Pass 1 (sequential, cheap): header fields and blob bounds of every tensor.
+    // The first failure is recorded, not raised: an earlier tensor's codec
+    // error must still win, as in the reference's one-tensor-at-a-time read.
+    struct Blob {
+        uint64_t count, ipos, inb, vpos, vnb;
+    };
+    std::vector<Blob> blobs;
+    pulse_status stop_st = PULSE_OK;
+    std::string stop_msg;
+    try {
+        p->anchor_step = header.at("anchor_step").get<int64_t>();
+        p->base_step = header.at("base_step").get<int64_t>();
+        p->target_step = header.at("target_step").get<int64_t>();
+        const std::string hx = header.at("target_hash").get<std::string>();
+        if (hx.size() != 64) raise(PULSE_E_FORMAT, "sha256 hex digest must be 64 characters");
+        for (int i = 0; i < 32; ++i) {
+            auto nib = [](char ch) -> int {
+                if (ch >= '0' && ch <= '9') return ch - '0';
+                if (ch >= 'a' && ch <= 'f') return ch - 'a' + 10;
+                if (ch >= 'A' && ch <= 'F') return ch - 'A' + 10;
+                raise(PULSE_E_FORMAT, "invalid hex character in digest");
+            };
+            p->target_hash[i] = uint8_t(nib(hx[2 * i]) << 4 | nib(hx[2 * i + 1]));
+        }
+        const uint32_t codec = header.at("codec").get<uint32_t>();
+        if (codec > PULSE_GZIP6) raise(PULSE_E_FORMAT, "unknown codec id " + std::to_string(codec));
+        p->codec = codec;
+        const std::string rn = header.at("representation").get<std::string>();
+        if (rn == "COO_DOWNSCALED") p->representation = PULSE_COO_DOWNSCALED;
+        else if (rn == "COO_INT32") p->representation = PULSE_COO_INT32;
+        else if (rn == "FLAT_INT32") p->representation = PULSE_FLAT_INT32;
+        else raise(PULSE_E_FORMAT, "unknown representation name: " + rn);
+    } catch (const nlohmann::json::exception& e) {
+        raise(PULSE_E_FORMAT, std::string("patch header schema error: ") + e.what());
+    }
+    try {
+        for (const auto& entry : header.at("tensors")) {
+            PatchTensor tp;
+            tp.name = entry.at("name").get<std::string>();
+            tp.shape = entry.at("shape").get<std::vector<int64_t>>();
+            for (auto e : tp.shape)
+                if (e <= 0) raise(PULSE_E_FORMAT, "non-positive extent in tensor " + tp.name);
+            Blob b{};
+            b.count = entry.at("count").get<uint64_t>();
+            b.inb = entry.at("index_nbytes").get<uint64_t>();
+            b.vnb = entry.at("value_nbytes").get<uint64_t>();
+            if (p->representation == PULSE_COO_DOWNSCALED) {
+                if (entry.at("row_bits").get<int>() != 8 || entry.at("col_bits").get<int>() != 16)
+                    raise(PULSE_E_FORMAT, "unsupported delta widths for tensor " + tp.name);
+            }
+            if (b.inb > n - pos) raise(PULSE_E_TRUNCATION, "index blob truncated");
+            b.ipos = pos;
+            pos += b.inb;
+            if (b.vnb > n - pos) raise(PULSE_E_TRUNCATION, "value blob truncated");
+            b.vpos = pos;
+            pos += b.vnb;
+            blobs.push_back(b);
+            p->tensors.push_back(std::move(tp));
+        }
+    } catch (const nlohmann::json::exception& e) {
+        stop_st = PULSE_E_FORMAT;
+        stop_msg = std::string("patch header schema error: ") + e.what();
+    } catch (const Failure& f) {
+        stop_st = f.st;
+        stop_msg = f.msg;
+    }
+    // Pass 2 (parallel over tensors): decompress, values (LE u16, memcpy on
+    // this little-endian host).  The identity codec's index blobs are used in place.
+    const size_t T = blobs.size();
+    ParsedPulp out;
+    std::vector<std::vector<uint8_t>>& payloads = out.store;
+    std::vector<const uint8_t*>& pl = out.pl;
+    std::vector<uint64_t>& lens = out.lens;
+    payloads.resize(T);
+    pl.resize(T);
+    lens.resize(T);
+    std::vector<pulse_status> tst(T, PULSE_OK);
+    std::vector<std::string> tmsg(T);
+    pool().parallel_for(T, [&](size_t t) {
+        const Blob& b = blobs[t];
+        auto& tp = p->tensors[t];
+        try {
+            if (p->codec == PULSE_IDENTITY) {
+                pl[t] = bytes + b.ipos;
+                lens[t] = b.inb;
+                if (b.vnb != b.count * 2)
+                    raise(PULSE_E_FORMAT, "value payload length does not match change count for tensor " + tp.name);
+                tp.values.resize(b.count);
+                if (b.count) std::memcpy(tp.values.data(), bytes + b.vpos, b.count * 2);
+            } else {
+                payloads[t] = codec_decompress(bytes + b.ipos, b.inb, p->codec);
+                pl[t] = payloads[t].data();
+                lens[t] = payloads[t].size();
+                const auto vp = codec_decompress(bytes + b.vpos, b.vnb, p->codec);
+                if (vp.size() != b.count * 2)
+                    raise(PULSE_E_FORMAT, "value payload length does not match change count for tensor " + tp.name);
+                tp.values.resize(b.count);
+                if (b.count) std::memcpy(tp.values.data(), vp.data(), b.count * 2);
+            }
+        } catch (const Failure& f) {
+            tst[t] = f.st;
+            tmsg[t] = f.msg;
+        }
+    });
+    for (size_t t = 0; t < T; ++t)
+        if (tst[t] != PULSE_OK) raise(tst[t], tmsg[t]);
+    if (stop_st != PULSE_OK) raise(stop_st, stop_msg);
+    if (pos != n) raise(PULSE_E_FORMAT, "patch has trailing bytes");
+    out.p = std::move(p);
+    return out;
+}
+
 }  // namespace
 
 // =============================================================================================
@@ -1154,45 +1360,13 @@ pulse_status pulse_write_patch_bytes(const pulse_patch* p, pulse_bytes** out) {
             vn[t] = vb[t].size();
         });
         tm.lap("codec");
-        nlohmann::json header;
-        header["anchor_step"] = p->anchor_step;
-        header["base_step"] = p->base_step;
-        header["target_step"] = p->target_step;
-        header["target_hash"] = hex(p->target_hash);
-        header["codec"] = p->codec;
-        header["representation"] = rname;
-        auto& table = header["tensors"] = nlohmann::json::array();
+        std::vector<PulpTensorRef> refs(T);
         for (size_t t = 0; t < T; ++t) {
             const auto& tp = p->tensors[t];
-            nlohmann::json e = {{"name", tp.name},
-                                {"shape", tp.shape},
-                                {"count", tp.indices.size()},
-                                {"index_nbytes", in[t]},
-                                {"value_nbytes", vn[t]}};
-            if (p->representation == PULSE_COO_DOWNSCALED) {
-                e["row_bits"] = 8;
-                e["col_bits"] = 16;
-            }
-            table.push_back(std::move(e));
+            refs[t] = {&tp.name, &tp.shape, tp.indices.size(), ip[t], in[t], vp[t], vn[t]};
         }
-        const std::string js = header.dump();
-        auto res = std::make_unique<pulse_bytes>();
-        tm.lap("header");
-        std::vector<uint64_t> at(T + 1);
-        at[0] = 16 + js.size();
-        for (size_t t = 0; t < T; ++t) at[t + 1] = at[t] + in[t] + vn[t];
-        res->v.resize(at[T]);
-        uint8_t* w = res->v.data();
-        std::memcpy(w, "PULP", 4);
-        const uint32_t ver = 1;
-        const uint64_t hl = js.size();
-        for (int i = 0; i < 4; ++i) w[4 + i] = uint8_t(ver >> (8 * i));
-        for (int i = 0; i < 8; ++i) w[8 + i] = uint8_t(hl >> (8 * i));
-        std::memcpy(w + 16, js.data(), js.size());
-        pool().parallel_for(T, [&](size_t t) {
-            if (in[t]) std::memcpy(w + at[t], ip[t], in[t]);
-            if (vn[t]) std::memcpy(w + at[t] + in[t], vp[t], vn[t]);
-        });
+        auto res = assemble_pulp(p->anchor_step, p->base_step, p->target_step, p->target_hash, p->codec,
+                                 p->representation, refs);
         tm.lap("assemble");
         *out = res.release();
     });
@@ -1201,141 +1375,13 @@ pulse_status pulse_write_patch_bytes(const pulse_patch* p, pulse_bytes** out) {
 pulse_status pulse_read_patch_bytes(const uint8_t* bytes, uint64_t n, pulse_patch** out) {
     return guarded([&] {
         if (!out || (n && !bytes)) raise(PULSE_E_ARGUMENT, "null argument");
-        uint64_t pos = 0;
-        auto need = [&](uint64_t k) {
-            if (n - pos < k) raise(PULSE_E_TRUNCATION, "unexpected end of data");
-        };
-        if (n < 4) raise(PULSE_E_TRUNCATION, "patch shorter than magic");
-        if (std::memcmp(bytes, "PULP", 4) != 0) raise(PULSE_E_BAD_MAGIC, "not a patch file (bad magic)");
-        pos = 4;
-        need(4);
-        uint32_t version = 0;
-        for (int i = 0; i < 4; ++i) version |= uint32_t(bytes[pos + i]) << (8 * i);
-        pos += 4;
-        if (version != 1) raise(PULSE_E_VERSION, "unsupported patch version " + std::to_string(version));
-        need(8);
-        uint64_t hl = 0;
-        for (int i = 0; i < 8; ++i) hl |= uint64_t(bytes[pos + i]) << (8 * i);
-        pos += 8;
-        if (hl > n - pos) raise(PULSE_E_TRUNCATION, "patch header truncated");
-        nlohmann::json header;
-        try {
-            header = nlohmann::json::parse(bytes + pos, bytes + pos + hl);
-        } catch (const nlohmann::json::exception& e) {
-            raise(PULSE_E_FORMAT, std::string("patch header is not valid JSON: ") + e.what());
-        }
-        pos += hl;
-        auto p = std::make_unique<pulse_patch>();
-        // Pass 1 (sequential, cheap): header fields and blob bounds of every tensor.
-        // The first failure is recorded, not raised: an earlier tensor's codec
-        // error must still win, as in the reference's one-tensor-at-a-time read.
-        struct Blob {
-            uint64_t count, ipos, inb, vpos, vnb;
-        };
-        std::vector<Blob> blobs;
-        pulse_status stop_st = PULSE_OK;
-        std::string stop_msg;
-        try {
-            p->anchor_step = header.at("anchor_step").get<int64_t>();
-            p->base_step = header.at("base_step").get<int64_t>();
-            p->target_step = header.at("target_step").get<int64_t>();
-            const std::string hx = header.at("target_hash").get<std::string>();
-            if (hx.size() != 64) raise(PULSE_E_FORMAT, "sha256 hex digest must be 64 characters");
-            for (int i = 0; i < 32; ++i) {
-                auto nib = [](char ch) -> int {
-                    if (ch >= '0' && ch <= '9') return ch - '0';
-                    if (ch >= 'a' && ch <= 'f') return ch - 'a' + 10;
-                    if (ch >= 'A' && ch <= 'F') return ch - 'A' + 10;
-                    raise(PULSE_E_FORMAT, "invalid hex character in digest");
-                };
-                p->target_hash[i] = uint8_t(nib(hx[2 * i]) << 4 | nib(hx[2 * i + 1]));
-            }
-            const uint32_t codec = header.at("codec").get<uint32_t>();
-            if (codec > PULSE_GZIP6) raise(PULSE_E_FORMAT, "unknown codec id " + std::to_string(codec));
-            p->codec = codec;
-            const std::string rn = header.at("representation").get<std::string>();
-            if (rn == "COO_DOWNSCALED") p->representation = PULSE_COO_DOWNSCALED;
-            else if (rn == "COO_INT32") p->representation = PULSE_COO_INT32;
-            else if (rn == "FLAT_INT32") p->representation = PULSE_FLAT_INT32;
-            else raise(PULSE_E_FORMAT, "unknown representation name: " + rn);
-        } catch (const nlohmann::json::exception& e) {
-            raise(PULSE_E_FORMAT, std::string("patch header schema error: ") + e.what());
-        }
-        try {
-            for (const auto& entry : header.at("tensors")) {
-                PatchTensor tp;
-                tp.name = entry.at("name").get<std::string>();
-                tp.shape = entry.at("shape").get<std::vector<int64_t>>();
-                for (auto e : tp.shape)
-                    if (e <= 0) raise(PULSE_E_FORMAT, "non-positive extent in tensor " + tp.name);
-                Blob b{};
-                b.count = entry.at("count").get<uint64_t>();
-                b.inb = entry.at("index_nbytes").get<uint64_t>();
-                b.vnb = entry.at("value_nbytes").get<uint64_t>();
-                if (p->representation == PULSE_COO_DOWNSCALED) {
-                    if (entry.at("row_bits").get<int>() != 8 || entry.at("col_bits").get<int>() != 16)
-                        raise(PULSE_E_FORMAT, "unsupported delta widths for tensor " + tp.name);
-                }
-                if (b.inb > n - pos) raise(PULSE_E_TRUNCATION, "index blob truncated");
-                b.ipos = pos;
-                pos += b.inb;
-                if (b.vnb > n - pos) raise(PULSE_E_TRUNCATION, "value blob truncated");
-                b.vpos = pos;
-                pos += b.vnb;
-                blobs.push_back(b);
-                p->tensors.push_back(std::move(tp));
-            }
-        } catch (const nlohmann::json::exception& e) {
-            stop_st = PULSE_E_FORMAT;
-            stop_msg = std::string("patch header schema error: ") + e.what();
-        } catch (const Failure& f) {
-            stop_st = f.st;
-            stop_msg = f.msg;
-        }
-        // Pass 2 (parallel over tensors): decompress, values (LE u16, memcpy on
-        // this little-endian host).  The identity codec's index blobs are used in place.
-        const size_t T = blobs.size();
-        std::vector<std::vector<uint8_t>> payloads(T);
-        std::vector<const uint8_t*> pl(T);
-        std::vector<uint64_t> lens(T);
-        std::vector<pulse_status> tst(T, PULSE_OK);
-        std::vector<std::string> tmsg(T);
-        pool().parallel_for(T, [&](size_t t) {
-            const Blob& b = blobs[t];
-            auto& tp = p->tensors[t];
-            try {
-                if (p->codec == PULSE_IDENTITY) {
-                    pl[t] = bytes + b.ipos;
-                    lens[t] = b.inb;
-                    if (b.vnb != b.count * 2)
-                        raise(PULSE_E_FORMAT, "value payload length does not match change count for tensor " + tp.name);
-                    tp.values.resize(b.count);
-                    if (b.count) std::memcpy(tp.values.data(), bytes + b.vpos, b.count * 2);
-                } else {
-                    payloads[t] = codec_decompress(bytes + b.ipos, b.inb, p->codec);
-                    pl[t] = payloads[t].data();
-                    lens[t] = payloads[t].size();
-                    const auto vp = codec_decompress(bytes + b.vpos, b.vnb, p->codec);
-                    if (vp.size() != b.count * 2)
-                        raise(PULSE_E_FORMAT, "value payload length does not match change count for tensor " + tp.name);
-                    tp.values.resize(b.count);
-                    if (b.count) std::memcpy(tp.values.data(), vp.data(), b.count * 2);
-                }
-            } catch (const Failure& f) {
-                tst[t] = f.st;
-                tmsg[t] = f.msg;
-            }
-        });
-        for (size_t t = 0; t < T; ++t)
-            if (tst[t] != PULSE_OK) raise(tst[t], tmsg[t]);
-        if (stop_st != PULSE_OK) raise(stop_st, stop_msg);
-        if (pos != n) raise(PULSE_E_FORMAT, "patch has trailing bytes");
-        if (!p->tensors.empty()) {
+        ParsedPulp pp = parse_pulp(bytes, n);
+        if (!pp.p->tensors.empty()) {
             Engine& E = engine();
             std::lock_guard<std::mutex> lk(E.mu);
-            device_decode_payloads(E, p.get(), pl, lens);
+            device_decode_payloads(E, pp.p.get(), pp.pl, pp.lens);
         }
-        *out = p.release();
+        *out = pp.p.release();
     });
 }
 
@@ -1796,6 +1842,412 @@ pulse_status pulse_container_copy_out(const pulse_container* c, const uint8_t* d
         for (size_t i = 0; i < T; ++i)
             E.stager.h2d(dst[i], data + c->tensors[i].begin, c->tensors[i].numel * 2, E.stream);
         E.sync();
+    });
+}
+
+}  // extern "C"
+
+// =============================================================================================
+// Resident checkpoints: the sync path on the device (sync.hpp:78-92, 166-211, 308-352)
+// =============================================================================================
+struct pulse_resident {
+    int device = 0;
+    pulse_plan* plan = nullptr;
+    uint64_t cap = 0;
+    uint64_t step = 0, last_anchor = 0;
+    uint8_t hash[32] = {};
+    std::vector<std::string> names;           // insertion order
+    std::vector<std::vector<int64_t>> shapes;
+    std::vector<uint64_t> numel;
+    std::vector<uint32_t> order;              // plan (name-order) index -> insertion index
+    std::vector<uint32_t> plan_of;            // insertion index -> plan index
+    std::unordered_map<std::string, uint32_t> by_name;
+    void* arena = nullptr;                    // resident weights; tensor i at element off[i]
+    std::vector<uint64_t> off;
+    DevBuf body, entries, result, idx64, backup, start;
+    void* pinned[2] = {nullptr, nullptr};     // hash pipeline (D2H | SHA-256)
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaStream_t hstream = nullptr;
+    ~pulse_resident() {
+        if (plan) pulse_plan_destroy(plan);
+        if (arena) cudaFree(arena);
+        for (int i = 0; i < 2; ++i) {
+            if (pinned[i]) cudaFreeHost(pinned[i]);
+            if (ev[i]) cudaEventDestroy(ev[i]);
+        }
+        if (hstream) cudaStreamDestroy(hstream);
+        for (DevBuf* b : {&body, &entries, &result, &idx64, &backup, &start})
+            if (b->p) cudaFree(b->p);
+    }
+    uint16_t* tensor(uint32_t i) const { return static_cast<uint16_t*>(arena) + off[i]; }
+};
+
+namespace {
+
+constexpr size_t kHashChunk = 64u << 20;
+
+// SHA-256 of device tensors in the given order (sha256.hpp:93-116 over HBM):
+// chunk k+1 is copied to pinned memory while chunk k is hashed.
+void hash_device(pulse_resident* r, const std::vector<std::pair<const uint8_t*, uint64_t>>& parts, uint8_t out[32]) {
+    if (!r->hstream) {
+        cuda_check(cudaStreamCreateWithFlags(&r->hstream, cudaStreamNonBlocking), "stream");
+        for (int i = 0; i < 2; ++i) {
+            cuda_check(cudaHostAlloc(&r->pinned[i], kHashChunk, cudaHostAllocDefault), "pinned");
+            cuda_check(cudaEventCreateWithFlags(&r->ev[i], cudaEventDisableTiming), "event");
+        }
+    }
+    std::vector<std::pair<const uint8_t*, uint64_t>> pieces;
+    for (auto [p, n] : parts)
+        for (uint64_t o = 0; o < n; o += kHashChunk) pieces.emplace_back(p + o, std::min<uint64_t>(kHashChunk, n - o));
+    EVP_MD_CTX* ctx = EVP_MD_CTX_new();
+    if (!ctx || EVP_DigestInit_ex(ctx, EVP_sha256(), nullptr) != 1) raise(PULSE_E_ERROR, "failed to initialize SHA-256 context");
+    auto issue = [&](size_t k) {
+        const int b = int(k & 1);
+        cuda_check(counted_copy(r->pinned[b], pieces[k].first, pieces[k].second, cudaMemcpyDeviceToHost, r->hstream), "D2H");
+        cuda_check(cudaEventRecord(r->ev[b], r->hstream), "event");
+    };
+    if (!pieces.empty()) issue(0);
+    for (size_t k = 0; k < pieces.size(); ++k) {
+        if (k + 1 < pieces.size()) {
+            // buffer (k+1)&1 was hashed in iteration k-1 (synchronously), so it is free
+            issue(k + 1);
+        }
+        cuda_check(cudaEventSynchronize(r->ev[k & 1]), "D2H wait");
+        if (EVP_DigestUpdate(ctx, r->pinned[k & 1], pieces[k].second) != 1) raise(PULSE_E_ERROR, "SHA-256 update failed");
+    }
+    unsigned int len = 0;
+    if (EVP_DigestFinal_ex(ctx, out, &len) != 1 || len != 32) raise(PULSE_E_ERROR, "SHA-256 finalize failed");
+    EVP_MD_CTX_free(ctx);
+}
+
+std::vector<std::pair<const uint8_t*, uint64_t>> name_order_parts(const pulse_resident* r,
+                                                                  const std::vector<const void*>& ptrs) {
+    std::vector<std::pair<const uint8_t*, uint64_t>> parts;
+    for (uint32_t k = 0; k < r->order.size(); ++k) {
+        const uint32_t i = r->order[k];
+        parts.emplace_back(static_cast<const uint8_t*>(ptrs[i]), r->numel[i] * 2);
+    }
+    return parts;
+}
+
+// (Re)creates the plan with room for `cap` changes and binds the resident weights to slot 0.
+void resident_plan(pulse_resident* r, Engine& E, uint64_t cap) {
+    if (r->plan && cap <= r->cap) return;
+    if (r->plan) {
+        E.sync();
+        pulse_plan_destroy(r->plan);
+        r->plan = nullptr;
+    }
+    const uint32_t T = uint32_t(r->names.size());
+    std::vector<pulse_tensor_geom> geom(T);
+    std::vector<const void*> ptrs(T);
+    for (uint32_t k = 0; k < T; ++k) {
+        const uint32_t i = r->order[k];
+        geom[k] = {r->numel[i], uint64_t(r->shapes[i].back())};
+        ptrs[k] = r->tensor(i);
+    }
+    r->cap = std::max<uint64_t>(cap, 1024);
+    if (pulse_plan_create(E.ctx, geom.data(), T, r->cap, &r->plan) != PULSE_OK)
+        raise(PULSE_E_CUDA, std::string("plan: ") + pulse_last_error());
+    if (pulse_plan_bind(r->plan, 0, ptrs.data()) != PULSE_OK) raise(PULSE_E_CUDA, pulse_last_error());
+}
+
+// apply_delta (sync.hpp:308-329) for an already parsed PULP.
+void resident_apply_parsed(pulse_resident* r, Engine& E, ParsedPulp& pp, uint64_t step, const uint8_t* expected,
+                           bool verify) {
+    const pulse_patch* p = pp.p.get();
+    if (p->base_step != int64_t(r->step))
+        raise(PULSE_E_PROTOCOL, "delta at step " + std::to_string(step) + " does not base on the held step");
+    if (p->target_step != int64_t(step)) raise(PULSE_E_PROTOCOL, "patch steps disagree with the manifest");
+    if (expected && std::memcmp(p->target_hash, expected, 32) != 0)
+        raise(PULSE_E_PROTOCOL, "patch target hash disagrees with the manifest");
+    const uint32_t P = uint32_t(p->tensors.size());
+    // decode's tensor checks (patch.hpp:314-324), in patch order
+    std::vector<pulse_patch_entry> ents(P);
+    uint64_t body_len = 0, n = 0;
+    for (uint32_t k = 0; k < P; ++k) {
+        const auto& tp = p->tensors[k];
+        const auto it = r->by_name.find(tp.name);
+        if (it == r->by_name.end()) raise(PULSE_E_TENSOR_SET, "patch references unknown tensor '" + tp.name + "'");
+        if (tp.shape != r->shapes[it->second])
+            raise(PULSE_E_SHAPE_MISMATCH, "tensor '" + tp.name + "' shape differs between patch and checkpoint");
+        const uint64_t cnt = tp.values.size();
+        ents[k] = pulse_patch_entry{r->plan_of[it->second], 0, cnt, body_len, pp.lens[k], body_len + pp.lens[k]};
+        body_len += pp.lens[k] + 2 * cnt;
+        n += cnt;
+    }
+    if (P == 0) {
+        r->step = step;
+        std::memcpy(r->hash, p->target_hash, 32);
+        r->last_anchor = std::max<uint64_t>(r->last_anchor, uint64_t(p->anchor_step));
+        return;
+    }
+    resident_plan(r, E, n);
+    // the device body: [index payload][value payload] per tensor, as the kernels read it
+    uint8_t* dbody = r->body.as<uint8_t>(body_len + 64);
+    RawVec<uint8_t> host(body_len);
+    pool().parallel_for(P, [&](size_t k) {
+        if (pp.lens[k]) std::memcpy(host.data() + ents[k].idx_off, pp.pl[k], pp.lens[k]);
+        const auto& v = p->tensors[k].values;
+        if (!v.empty()) std::memcpy(host.data() + ents[k].val_off, v.data(), v.size() * 2);
+    });
+    E.stager.h2d(dbody, host.data(), body_len, E.stream);
+    auto* dent = r->entries.as<pulse_patch_entry>(P);
+    cuda_check(counted_copy(dent, ents.data(), P * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice, E.stream), "H2D");
+    auto* dres = r->result.as<pulse_result>(1);
+    auto fail_on = [&](const pulse_result& res) {
+        if (res.status == PULSE_OK) return;
+        const std::string nm = res.err_tensor < P ? p->tensors[res.err_tensor].name : "?";
+        raise(pulse_status(res.status), device_message(res, nm, nullptr));
+    };
+    int64_t* didx = nullptr;
+    uint16_t* dbak = nullptr;
+    uint64_t* dstart = nullptr;
+    if (verify) {  // keep what the scatter overwrites: indices, then the old values
+        didx = r->idx64.as<int64_t>(n);
+        if (pulse_decode_indices(r->plan, p->representation, dbody, dent, P, nullptr, didx, dres, E.stream) != PULSE_OK)
+            raise(PULSE_E_CUDA, pulse_last_error());
+        fail_on(fetch_result(E, dres));
+        std::vector<uint64_t> st(P + 1, 0);
+        for (uint32_t k = 0; k < P; ++k) st[k + 1] = st[k] + ents[k].count;
+        dstart = r->start.as<uint64_t>(P + 1);
+        cuda_check(counted_copy(dstart, st.data(), (P + 1) * 8, cudaMemcpyHostToDevice, E.stream), "H2D");
+        dbak = r->backup.as<uint16_t>(n);
+        launch_gather_values(r->plan->dev, 0, dent, dstart, P, didx, dbak, E.stream);
+    }
+    if (pulse_apply(r->plan, 0, p->representation, dbody, dent, P, nullptr, dres, E.stream) != PULSE_OK)
+        raise(PULSE_E_CUDA, pulse_last_error());
+    fail_on(fetch_result(E, dres));  // validate-then-scatter: a failure wrote nothing
+    if (verify) {  // patch.hpp:341-346 on the resident weights
+        std::vector<const void*> ptrs(r->names.size());
+        for (uint32_t i = 0; i < ptrs.size(); ++i) ptrs[i] = r->tensor(i);
+        uint8_t h[32];
+        hash_device(r, name_order_parts(r, ptrs), h);
+        if (std::memcmp(h, p->target_hash, 32) != 0) {
+            launch_apply_idx64(r->plan->dev, didx, dbak, dent, P, 0, dres, E.stream);  // put the old values back
+            fail_on(fetch_result(E, dres));
+            raise(PULSE_E_HASH_MISMATCH, "hash mismatch: expected " + hex(p->target_hash) + ", actual " + hex(h));
+        }
+    }
+    r->step = step;
+    std::memcpy(r->hash, p->target_hash, 32);
+    r->last_anchor = std::max<uint64_t>(r->last_anchor, uint64_t(p->anchor_step));
+}
+
+}  // namespace
+
+extern "C" {
+
+pulse_status pulse_resident_create(const pulse_checkpoint* c, uint64_t max_changes, pulse_resident** out) {
+    return guarded([&] {
+        if (!c || !out) raise(PULSE_E_ARGUMENT, "null argument");
+        validate_checkpoint(c);
+        auto r = std::make_unique<pulse_resident>();
+        const uint32_t T = c->n_tensors;
+        r->step = c->step;
+        r->order = sorted_order(c);
+        r->plan_of.assign(T, 0);
+        for (uint32_t k = 0; k < T; ++k) r->plan_of[r->order[k]] = k;
+        for (uint32_t i = 0; i < T; ++i) {
+            const pulse_tensor& t = c->tensors[i];
+            r->names.emplace_back(t.name);
+            r->shapes.emplace_back(t.shape, t.shape + t.rank);
+            r->numel.push_back(t.numel);
+            r->by_name[t.name] = i;
+        }
+        uint64_t total = 0;
+        r->off = arena_offsets(r->numel, total);
+        // the hash of the held checkpoint (checkpoint_to_state), overlapping the upload
+        auto hash = std::async(std::launch::async, [&] { hash_checkpoint(c, r->hash); });
+        Engine& E = engine();
+        std::lock_guard<std::mutex> lk(E.mu);
+        cudaGetDevice(&r->device);
+        cuda_check(cudaMalloc(&r->arena, std::max<uint64_t>(total, 8) * 2), "resident weights");
+        for (uint32_t i = 0; i < T; ++i) E.stager.h2d(r->tensor(i), c->tensors[i].data, r->numel[i] * 2, E.stream);
+        if (T) resident_plan(r.get(), E, max_changes);
+        E.sync();
+        hash.get();
+        *out = r.release();
+    });
+}
+
+void pulse_resident_destroy(pulse_resident* r) {
+    if (!r) return;
+    cudaDeviceSynchronize();
+    delete r;
+}
+uint64_t pulse_resident_step(const pulse_resident* r) { return r ? r->step : 0; }
+uint64_t pulse_resident_last_anchor_step(const pulse_resident* r) { return r ? r->last_anchor : 0; }
+pulse_status pulse_resident_hash(const pulse_resident* r, uint8_t* out32) {
+    if (!r || !out32) return fail(PULSE_E_ARGUMENT, "null argument");
+    std::memcpy(out32, r->hash, 32);
+    return PULSE_OK;
+}
+uint32_t pulse_resident_num_tensors(const pulse_resident* r) { return r ? uint32_t(r->names.size()) : 0; }
+pulse_status pulse_resident_tensor(const pulse_resident* r, uint32_t i, void** dev_ptr) {
+    if (!r || !dev_ptr) return fail(PULSE_E_ARGUMENT, "null argument");
+    if (i >= r->names.size()) return fail(PULSE_E_ARGUMENT, "tensor index out of range");
+    *dev_ptr = r->tensor(i);
+    return PULSE_OK;
+}
+
+pulse_status pulse_resident_download(const pulse_resident* r, uint16_t* const* out) {
+    return guarded([&] {
+        if (!r || (!out && !r->names.empty())) raise(PULSE_E_ARGUMENT, "null argument");
+        Engine& E = engine();
+        std::lock_guard<std::mutex> lk(E.mu);
+        for (uint32_t i = 0; i < r->names.size(); ++i) E.stager.d2h(out[i], r->tensor(i), r->numel[i] * 2, E.stream);
+        E.sync();
+    });
+}
+
+pulse_status pulse_resident_apply(pulse_resident* r, const uint8_t* pulp, uint64_t n, uint64_t step,
+                                  const uint8_t* expected_hash32, int verify_hash) {
+    return guarded([&] {
+        if (!r || (n && !pulp)) raise(PULSE_E_ARGUMENT, "null argument");
+        ParsedPulp pp = parse_pulp(pulp, n);
+        Engine& E = engine();
+        std::lock_guard<std::mutex> lk(E.mu);
+        resident_apply_parsed(r, E, pp, step, expected_hash32, verify_hash != 0);
+    });
+}
+
+pulse_status pulse_resident_walk(pulse_resident* r, const uint8_t* const* pulps, const uint64_t* sizes, uint32_t k,
+                                 int verify_hash, uint32_t* applied) {
+    if (applied) *applied = 0;
+    return guarded([&] {
+        if (!r || (k && (!pulps || !sizes))) raise(PULSE_E_ARGUMENT, "null argument");
+        if (k == 0) return;
+        // the next patch is parsed (JSON header, codec) on a host thread while this one applies
+        std::future<ParsedPulp> next = std::async(std::launch::async, [&] { return parse_pulp(pulps[0], sizes[0]); });
+        for (uint32_t j = 0; j < k; ++j) {
+            ParsedPulp pp = next.get();
+            if (j + 1 < k) next = std::async(std::launch::async, [&, j] { return parse_pulp(pulps[j + 1], sizes[j + 1]); });
+            struct Drain {  // never leave a parse running on a failure
+                std::future<ParsedPulp>& f;
+                ~Drain() {
+                    if (f.valid()) f.wait();
+                }
+            } drain{next};
+            Engine& E = engine();
+            std::lock_guard<std::mutex> lk(E.mu);
+            resident_apply_parsed(r, E, pp, r->step + 1, nullptr, verify_hash != 0);
+            if (applied) *applied = j + 1;
+        }
+    });
+}
+
+pulse_status pulse_resident_publish(pulse_resident* r, const void* const* dev_current, uint64_t step,
+                                    uint32_t repr, uint32_t codec, uint64_t anchor_step, int advance,
+                                    pulse_bytes** out_pulp, uint8_t* out_hash32) {
+    return guarded([&] {
+        if (!r || !out_pulp || (!dev_current && !r->names.empty())) raise(PULSE_E_ARGUMENT, "null argument");
+        if (step != r->step + 1) raise(PULSE_E_ARGUMENT, "publish requires consecutive steps");
+        repr_name(repr);
+        if (codec > PULSE_GZIP6) raise(PULSE_E_ARGUMENT, "unknown codec");
+        const uint32_t T = uint32_t(r->names.size());
+        std::vector<const void*> cur(dev_current, dev_current + T);
+        for (uint32_t i = 0; i < T; ++i) {
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, cur[i]) != cudaSuccess || a.type != cudaMemoryTypeDevice) {
+                cudaGetLastError();
+                raise(PULSE_E_ARGUMENT, "tensor " + r->names[i] + ": current data is not a device pointer");
+            }
+        }
+        Engine& E = engine();
+        std::lock_guard<std::mutex> lk(E.mu);
+        uint8_t target_hash[32] = {};
+        // the target hash once, from HBM, on a host thread while the device encodes
+        std::future<void> hash;
+        if (T)
+            hash = std::async(std::launch::async, [&] {
+                cudaSetDevice(r->device);
+                hash_device(r, name_order_parts(r, cur), target_hash);
+            });
+        struct Join {
+            std::future<void>& f;
+            ~Join() {
+                if (f.valid()) f.wait();
+            }
+        } join{hash};
+        RawVec<uint8_t> body;
+        std::vector<pulse_patch_entry> ents;
+        std::vector<PulpTensorRef> refs;
+        uint8_t* dbody = nullptr;
+        pulse_patch_entry* dent = nullptr;
+        if (T) {
+            std::vector<const void*> planp(T);
+            for (uint32_t k = 0; k < T; ++k) planp[k] = cur[r->order[k]];
+            resident_plan(r, E, r->cap);
+            pulse_scan_summary sm{};
+            for (int attempt = 0; attempt < 2; ++attempt) {
+                if (pulse_plan_bind(r->plan, 1, planp.data()) != PULSE_OK) raise(PULSE_E_CUDA, pulse_last_error());
+                if (pulse_encode_scan(r->plan, 1, 0, nullptr, E.stream) != PULSE_OK) raise(PULSE_E_CUDA, pulse_last_error());
+                cuda_check(counted_copy(&sm, r->plan->dev.scan, sizeof(sm), cudaMemcpyDeviceToHost, E.stream), "D2H");
+                E.sync();
+                if (sm.status != PULSE_E_CAPACITY) break;
+                resident_plan(r, E, sm.n_changes + sm.n_changes / 16 + 1024);
+            }
+            auto* dres = r->result.as<pulse_result>(1);
+            dent = r->entries.as<pulse_patch_entry>(T);
+            uint64_t cap = 14 * sm.n_changes + 1024;  // >= any escape-coded body (<= 11 + 2 bytes per change)
+            pulse_result res{};
+            for (int attempt = 0; attempt < 2; ++attempt) {
+                dbody = r->body.as<uint8_t>(cap + 64);
+                if (pulse_encode_emit(r->plan, repr, nullptr, 1, 0, dbody, cap, dent, dres, E.stream) != PULSE_OK)
+                    raise(PULSE_E_CUDA, pulse_last_error());
+                res = fetch_result(E, dres);
+                if (res.status != PULSE_E_CAPACITY) break;
+                cap = res.required + 1024;
+            }
+            if (res.status != PULSE_OK) {
+                const std::string nm = res.err_tensor < T ? r->names[r->order[res.err_tensor]] : "?";
+                raise(pulse_status(res.status), device_message(res, nm, nullptr));
+            }
+            ents.resize(res.n_entries);
+            if (res.n_entries)
+                cuda_check(counted_copy(ents.data(), dent, res.n_entries * sizeof(pulse_patch_entry),
+                                        cudaMemcpyDeviceToHost, E.stream), "D2H");
+            body.resize(res.body_bytes);
+            E.stager.d2h(body.data(), dbody, res.body_bytes, E.stream);
+            E.sync();
+        }
+        // codec per tensor blob on the thread pool (identity: straight out of the body)
+        const size_t P = ents.size();
+        std::vector<std::vector<uint8_t>> ib(P), vb(P);
+        refs.resize(P);
+        pool().parallel_for(P, [&](size_t k) {
+            const auto& e = ents[k];
+            const uint32_t i = r->order[e.tensor];
+            const uint8_t* ip = body.data() + e.idx_off;
+            const uint8_t* vp = body.data() + e.val_off;
+            uint64_t in = e.idx_nbytes, vn = e.count * 2;
+            if (codec != PULSE_IDENTITY) {
+                ib[k] = codec_compress(ip, in, codec);
+                vb[k] = codec_compress(vp, vn, codec);
+                ip = ib[k].data();
+                in = ib[k].size();
+                vp = vb[k].data();
+                vn = vb[k].size();
+            }
+            refs[k] = {&r->names[i], &r->shapes[i], e.count, ip, in, vp, vn};
+        });
+        if (hash.valid()) hash.get();
+        if (!T) hash_tensors({}, target_hash);  // SHA-256 of nothing
+        auto res = assemble_pulp(int64_t(anchor_step), int64_t(r->step), int64_t(step), target_hash, codec, repr, refs);
+        if (advance) {  // the held weights become the published snapshot: the patch, applied in place
+            if (P) {
+                auto* dres = r->result.as<pulse_result>(1);
+                if (pulse_apply(r->plan, 0, repr, dbody, dent, uint32_t(P), nullptr, dres, E.stream) != PULSE_OK)
+                    raise(PULSE_E_CUDA, pulse_last_error());
+                const pulse_result ar = fetch_result(E, dres);
+                if (ar.status != PULSE_OK) raise(pulse_status(ar.status), "self-apply of the published patch failed");
+            }
+            r->step = step;
+            std::memcpy(r->hash, target_hash, 32);
+        }
+        if (out_hash32) std::memcpy(out_hash32, target_hash, 32);
+        *out_pulp = res.release();
     });
 }
 

@@ -176,6 +176,8 @@ void debug_sync(const char* kernel, cudaStream_t s);
 #define PULSE_LAUNCHED(name, stream) ::pulse::dev::debug_sync(name, stream)
 // helpers.cu (host-buffer API support)
 void launch_export_indices(const PlanDev& p, int64_t* out, cudaStream_t s);
+void launch_gather_values(const PlanDev& p, int slot, const pulse_patch_entry* ents, const uint64_t* start,
+                          uint32_t n_e, const int64_t* idx, uint16_t* out, cudaStream_t s);
 void launch_delta_encode(const int64_t* in, uint64_t n, int64_t* out, uint64_t* err, cudaStream_t s);
 void launch_delta_decode(const int64_t* in, uint64_t n, int64_t* out, uint64_t* err, cudaStream_t s);
 void launch_coo_pack(const int64_t* rows, const int64_t* cols, uint64_t n, uint8_t* out, uint64_t* nbytes,

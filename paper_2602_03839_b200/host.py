@@ -376,6 +376,81 @@ def write_checkpoint_bytes_from_device(step: int, names, shapes, device_tensors)
     return _take(out)
 
 
+# ---- resident checkpoints: the sync path on the device (sync.hpp) -----------------------------
+class Resident:
+    """A checkpoint held in HBM with its step and weights hash (the consumer's
+    SyncState, sync.hpp:78-92, and the publisher's last published snapshot).
+    apply / walk = apply_delta / walk_deltas (sync.hpp:308-352) straight from
+    PULP bytes; publish = publish_checkpoint's patch (sync.hpp:166-181) encoded
+    on the device against the held weights."""
+
+    def __init__(self, ck: Checkpoint, max_changes: int = 1 << 20):
+        v = CheckpointView(ck)
+        h = C.c_void_p()
+        N.check(N.lib.pulse_resident_create(C.byref(v.c), max_changes, C.byref(h)))
+        self.h = h
+        self.names = [t.name for t in ck.tensors]
+        self.shapes = [tuple(t.shape) for t in ck.tensors]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            N.lib.pulse_resident_destroy(self.h)
+            self.h = None
+
+    @property
+    def step(self) -> int:
+        return int(N.lib.pulse_resident_step(self.h))
+
+    @property
+    def last_anchor_step(self) -> int:
+        return int(N.lib.pulse_resident_last_anchor_step(self.h))
+
+    @property
+    def weights_hash(self) -> bytes:
+        out = C.create_string_buffer(32)
+        N.check(N.lib.pulse_resident_hash(self.h, out))
+        return out.raw
+
+    def tensor_ptr(self, i: int) -> int:
+        p = C.c_void_p()
+        N.check(N.lib.pulse_resident_tensor(self.h, i, C.byref(p)))
+        return int(p.value)
+
+    def download(self) -> Checkpoint:
+        outs = [np.empty(int(np.prod(s)), np.uint16) for s in self.shapes]
+        arr = (C.c_void_p * max(1, len(outs)))(*[o.ctypes.data for o in outs])
+        N.check(N.lib.pulse_resident_download(self.h, arr))
+        return Checkpoint(self.step, [Tensor(n, s, o) for n, s, o in zip(self.names, self.shapes, outs)])
+
+    def apply(self, pulp, step: int, expected_hash: bytes | None = None, verify: bool = True):
+        ptr, n, keep = _buf(pulp)
+        N.check(N.lib.pulse_resident_apply(self.h, ptr, n, step, expected_hash, int(verify)))
+        del keep
+
+    def walk(self, pulps, verify: bool = True) -> int:
+        bufs = [_buf(p) for p in pulps]
+        ptrs = (C.c_void_p * max(1, len(bufs)))(*[b[0] for b in bufs])
+        sizes = (C.c_uint64 * max(1, len(bufs)))(*[b[1] for b in bufs])
+        applied = C.c_uint32()
+        try:
+            N.check(N.lib.pulse_resident_walk(self.h, ptrs, sizes, len(bufs), int(verify), C.byref(applied)))
+        finally:
+            self.last_walk_applied = applied.value
+        return applied.value
+
+    def publish(self, device_tensors, step: int, representation=COO_DOWNSCALED, codec=ZSTD1,
+                anchor_step: int | None = None, advance: bool = True):
+        """(PULP bytes, target hash) of the snapshot in `device_tensors` (CUDA
+        tensors, this checkpoint's tensor order) at `step` = held step + 1."""
+        arr = (C.c_void_p * max(1, len(device_tensors)))(*[t.data_ptr() for t in device_tensors])
+        out = C.c_void_p()
+        hsh = C.create_string_buffer(32)
+        anchor = self.step if anchor_step is None else anchor_step
+        N.check(N.lib.pulse_resident_publish(self.h, arr, step, representation, codec, anchor, int(advance),
+                                             C.byref(out), hsh))
+        return _take(out), hsh.raw
+
+
 # ---- end-to-end benchmark leg ---------------------------------------------------------------------
 def bench_e2e(args, mine, prev_dev, curr_dev, world, rank, steps=None, warmup=3):
     """The benchmark metric measured end to end through the public host API.
