@@ -404,6 +404,11 @@ typedef struct pulse_resident pulse_resident;
 /* checkpoint_to_state: uploads `checkpoint` (validated; host data) and hashes
  * it.  `max_changes` sizes the device scratch (grown on demand). */
 pulse_status pulse_resident_create(const pulse_checkpoint* checkpoint, uint64_t max_changes, pulse_resident** out);
+/* The same from a checkpoint already in HBM: `checkpoint` gives names, shapes
+ * and step, its `data` pointers are device pointers of the current device
+ * (copied device to device; the hash is taken from HBM). */
+pulse_status pulse_resident_create_device(const pulse_checkpoint* checkpoint, uint64_t max_changes,
+                                          pulse_resident** out);
 void pulse_resident_destroy(pulse_resident* r);
 uint64_t pulse_resident_step(const pulse_resident* r);
 uint64_t pulse_resident_last_anchor_step(const pulse_resident* r);

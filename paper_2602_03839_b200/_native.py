@@ -185,6 +185,7 @@ _SIGS = {
     "pulse_container_copy_out": (i32, [vp, vp, u64, C.c_int, C.POINTER(vp)]),
     # resident checkpoints (sync path)
     "pulse_resident_create": (i32, [C.POINTER(CheckpointC), u64, C.POINTER(vp)]),
+    "pulse_resident_create_device": (i32, [C.POINTER(CheckpointC), u64, C.POINTER(vp)]),
     "pulse_resident_destroy": (None, [vp]),
     "pulse_resident_step": (u64, [vp]),
     "pulse_resident_last_anchor_step": (u64, [vp]),

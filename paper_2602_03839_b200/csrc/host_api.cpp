@@ -2071,6 +2071,48 @@ pulse_status pulse_resident_create(const pulse_checkpoint* c, uint64_t max_chang
     });
 }
 
+pulse_status pulse_resident_create_device(const pulse_checkpoint* c, uint64_t max_changes, pulse_resident** out) {
+    return guarded([&] {
+        if (!c || !out) raise(PULSE_E_ARGUMENT, "null argument");
+        validate_checkpoint(c);
+        const uint32_t T = c->n_tensors;
+        for (uint32_t i = 0; i < T; ++i) {
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, c->tensors[i].data) != cudaSuccess || a.type != cudaMemoryTypeDevice) {
+                cudaGetLastError();
+                raise(PULSE_E_ARGUMENT, std::string("tensor ") + c->tensors[i].name + ": data is not a device pointer");
+            }
+        }
+        auto r = std::make_unique<pulse_resident>();
+        r->step = c->step;
+        r->order = sorted_order(c);
+        r->plan_of.assign(T, 0);
+        for (uint32_t k = 0; k < T; ++k) r->plan_of[r->order[k]] = k;
+        for (uint32_t i = 0; i < T; ++i) {
+            const pulse_tensor& t = c->tensors[i];
+            r->names.emplace_back(t.name);
+            r->shapes.emplace_back(t.shape, t.shape + t.rank);
+            r->numel.push_back(t.numel);
+            r->by_name[t.name] = i;
+        }
+        uint64_t total = 0;
+        r->off = arena_offsets(r->numel, total);
+        Engine& E = engine();
+        std::lock_guard<std::mutex> lk(E.mu);
+        cudaGetDevice(&r->device);
+        cuda_check(cudaMalloc(&r->arena, std::max<uint64_t>(total, 8) * 2), "resident weights");
+        for (uint32_t i = 0; i < T; ++i)
+            cuda_check(cudaMemcpyAsync(r->tensor(i), c->tensors[i].data, r->numel[i] * 2, cudaMemcpyDeviceToDevice,
+                                       E.stream), "D2D");
+        if (T) resident_plan(r.get(), E, max_changes);
+        E.sync();
+        std::vector<const void*> ptrs(T);
+        for (uint32_t i = 0; i < T; ++i) ptrs[i] = r->tensor(i);
+        hash_device(r.get(), name_order_parts(r.get(), ptrs), r->hash);
+        *out = r.release();
+    });
+}
+
 void pulse_resident_destroy(pulse_resident* r) {
     if (!r) return;
     cudaDeviceSynchronize();

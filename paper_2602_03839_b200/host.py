@@ -392,6 +392,24 @@ class Resident:
         self.names = [t.name for t in ck.tensors]
         self.shapes = [tuple(t.shape) for t in ck.tensors]
 
+    @classmethod
+    def from_device(cls, step: int, names, shapes, device_tensors, max_changes: int = 1 << 20):
+        """A resident copy of a checkpoint already in HBM (CUDA tensors of 2-byte elements)."""
+        keep, arr = [], (N.Tensor * max(1, len(names)))()
+        for i, (name, shape, t) in enumerate(zip(names, shapes, device_tensors)):
+            shp = np.ascontiguousarray(shape, dtype=np.int64)
+            nm = name.encode()
+            keep += [shp, nm]
+            arr[i] = N.Tensor(nm, shp.ctypes.data_as(C.POINTER(C.c_int64)), len(shape), t.data_ptr(), t.numel())
+        ck = N.CheckpointC(step, arr, len(names))
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        N.check(N.lib.pulse_resident_create_device(C.byref(ck), max_changes, C.byref(h)))
+        self.h = h
+        self.names = list(names)
+        self.shapes = [tuple(s) for s in shapes]
+        return self
+
     def __del__(self):
         if getattr(self, "h", None):
             N.lib.pulse_resident_destroy(self.h)
