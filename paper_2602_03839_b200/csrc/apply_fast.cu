@@ -52,6 +52,7 @@ namespace {
 constexpr uint32_t kRange = 4096;  // entries per warp range (aggregate granularity)
 constexpr uint32_t kChunk = 1024;  // entries staged per warp step
 constexpr uint32_t kPer = kChunk / 32;  // consecutive entries per lane
+constexpr uint32_t kChunksPerRange = kRange / kChunk;
 constexpr uint64_t H = SegSumOp::kHead;
 
 enum Repr : int { kCoo = 0, kI32 = 1, kFlat = 2 };
@@ -220,6 +221,7 @@ struct ApplyArgs {
     uint32_t* range_e;                   // [ranges] F0 out: patch entry holding each range's first entry
     uint32_t* range_flag;                // [ranges] F1s out: list of the non-plain ranges (exact checks in F3)
     unsigned long long* n_flagged;       // its length (zeroed by decode_prologue)
+    ulonglong2* chunk_pre;               // [ranges x 4] F1s out (non-plain ranges): in-range prefix at each 1024-chunk
     uint64_t* slack;                     // [ranges] F1s out: cols - 1 - first row segment's local end column
     int vmode;                           // F3 validate: 0 = non-plain ranges (all if suspect), 1 = all if any failure
 };
@@ -333,37 +335,49 @@ f_pass(ApplyArgs A) {
     const uint64_t gap_base = has_prev ? A.carry->gap_base : 0;
     const uint64_t stride = uint64_t(gridDim.x) * kWarps;
 
-    // F3 validate after F1s: exact checks where F1s could not decide (see f_stream)
-    // (non-plain ranges only: the list F1s built, one range per warp)
+    // F3 validate after F1s: exact checks where F1s could not decide (see f_stream).
+    // Filtered: the non-plain ranges F1s listed, one 1024-entry chunk per warp, each
+    // starting from its range's carry combined with F1s's in-range chunk prefix.
     bool filter = false;
     uint64_t n_items = n_ranges;
     if (kPass == kValidate && A.range_flag) {
         const bool suspect = *(volatile const uint32_t*)(A.flags + 1) != 0;
         if (A.vmode == 0) {
             filter = !suspect;
-            if (filter) n_items = *(volatile const unsigned long long*)A.n_flagged;
+            if (filter) n_items = *(volatile const unsigned long long*)A.n_flagged * kChunksPerRange;
         } else {  // second launch: re-check everything only if the filtered pass found a failure
             if (suspect || *(volatile const uint64_t*)A.err == kNoError) return;
         }
     }
     for (uint64_t it = uint64_t(blockIdx.x) * kWarps + warp; it < n_items; it += stride) {
-        const uint64_t rg = filter ? A.range_flag[it] : it;
-        const uint64_t r0 = rg * kRange, r1 = min(r0 + kRange, n);
+        const uint64_t rg = filter ? A.range_flag[it / kChunksPerRange] : it;
+        const uint64_t r0 = rg * kRange, r_end = min(r0 + kRange, n);
+        const uint64_t c_first = filter ? r0 + (it % kChunksPerRange) * kChunk : r0;
+        const uint64_t r1 = filter ? min(c_first + kChunk, r_end) : r_end;
+        if (c_first >= r1) continue;
         uint64_t ar = 0, ac = 0;  // kAgg: aggregates; else running (row, col) / sums
         if (kPass != kAgg) {
             const ulonglong2 p = A.agg[rg];
             ar = p.x;
             ac = p.y;
+            if (filter) {
+                const ulonglong2 q = A.chunk_pre[rg * kChunksPerRange + it % kChunksPerRange];
+                ar = SegSumOp::op(ar, q.x) & (H - 1);
+                ac = SegSumOp::op(ac, q.y) & (H - 1);
+            }
         }
         bool marker = false;
-        uint32_t e = upper_index<uint64_t>(A.es, 0, A.n_e, r0);
+        uint32_t e = upper_index<uint64_t>(A.es, 0, A.n_e, c_first);
         if (kPass == kAgg && lane == 0) A.range_e[rg] = e;
-        for (uint64_t c0 = r0; c0 < r1; c0 += kChunk) {
-            const uint32_t len = uint32_t(r1 - c0 < kChunk ? r1 - c0 : kChunk);
+        // chunks end at the next 1024-aligned entry, the range end or the patch entry's end:
+        // a chunk never straddles two entries, so only tensors >= 2^32 take the walker
+        for (uint64_t c0 = c_first, c_end = 0; c0 < r1; c0 = c_end) {
             while (A.es[e + 1] <= c0) ++e;
             const uint64_t lo = A.es[e], hi = A.es[e + 1];
+            c_end = min(min(r1, (c0 / kChunk + 1) * kChunk), hi);
+            const uint32_t len = uint32_t(c_end - c0);
             const EntryLayout L = A.el[e];
-            if (hi < c0 + len || L.numel >= (1ull << 32)) {
+            if (L.numel >= (1ull << 32)) {
                 slow_span<kRepr, kPass>(A, c0, c0 + len, ar, ac, marker, has_prev, gap_base);
                 continue;
             }
@@ -587,6 +601,9 @@ struct SLay {
     static constexpr uint32_t warp = 2 * buf + (kAgg_ ? 0 : 4 * ch);          // 2 buffers (+ decoded indices)
 };
 
+static_assert(SLay<kCoo, true>::ch == kChunk && SLay<kI32, true>::ch == kChunk,
+              "F1s chunks are F3's validate chunks (chunk_pre)");
+
 // Queues the 16-byte blocks covering [g, g+len) into dst (swizzle V); returns g & 15.
 template <int V>
 __device__ __forceinline__ uint32_t stage_cover(uint4* dst, const uint8_t* g, uint32_t len) {
@@ -742,8 +759,10 @@ __device__ __forceinline__ void chunk_body(const ApplyArgs& A, const SCtx& cur, 
     if (lane == 0) er = ec = 0;
     if (kAgg_) {
         uint64_t pend = kNoSlack;
-        if (coo && hc) {
+        if (coo && hc && !lane_first) {
             // the lane's first row segment ends in this lane, at column (state at lane start) + P
+            // (not when the lane starts a patch entry: the segment before is the previous
+            // entry's, whose end lies in this non-plain range and gets the exact checks)
             const uint64_t cs = SegSumOp::op(ac, ec);
             const uint64_t end = (cs & (H - 1)) + P;
             if (cs & H) bad |= end >= cur.cols;              // a row started earlier in the range: exact
@@ -838,9 +857,10 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
     SCtx cur;
     load_sctx(cur, A, A.range_e[rg]);
     auto range_end = [&](uint64_t r) { return min(r * kRange + kRange, n); };
-    auto chunk_len = [&](uint64_t r, uint64_t c) {
-        const uint64_t r1 = range_end(r);
-        return uint32_t(r1 - c < kSChunk ? r1 - c : kSChunk);
+    // chunks end at the next kSChunk-aligned entry, the range end or the patch entry's
+    // end: a chunk never straddles two entries, so only tensors >= 2^32 take the walker
+    auto chunk_len = [&](uint64_t r, uint64_t c, const SCtx& cx) {
+        return uint32_t(min(min(range_end(r), (c / kSChunk + 1) * kSChunk), cx.hi) - c);
     };
     auto is_fast = [&](const SCtx& c, uint64_t cc, uint32_t len) {
         return c.hi >= cc + len && c.numel < (1ull << 32);
@@ -871,7 +891,7 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
         plain = c.lo < r * kRange && c.hi > range_end(r) && c.numel < (1ull << 32);
         slack = kNoSlack;
     };
-    uint32_t len = chunk_len(rg, c0);
+    uint32_t len = chunk_len(rg, c0, cur);
     uint32_t sh_cur[3] = {0, 0, 0}, sh_nx[3] = {0, 0, 0};
     uint32_t b = 0;
     prefetch(true, cur, c0, len, 0, sh_cur);
@@ -895,7 +915,6 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
         uint32_t len_nx = 0;
         ulonglong2 carry_nx = make_ulonglong2(0, 0);
         if (has_nx) {
-            len_nx = chunk_len(rg_nx, c_nx);
             if (rg_nx != rg) {
                 if (!agg) carry_nx = A.agg[rg_nx];
                 load_sctx(nx, A, A.range_e[rg_nx]);
@@ -904,7 +923,10 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
                 while (A.es[e + 1] <= c_nx) ++e;
                 load_sctx(nx, A, e);
             }
+            len_nx = chunk_len(rg_nx, c_nx, nx);
         }
+        if (agg && !plain && lane == 0 && c0 % kChunk == 0)
+            A.chunk_pre[rg * kChunksPerRange + (c0 - rg * kRange) / kChunk] = make_ulonglong2(ar, ac);
         if (!is_fast(cur, c0, len)) {
             // straddles patch entries or a tensor >= 2^32 elements: per-round walker (never plain)
             slow_span<kRepr, agg ? kAgg : kScatter>(A, c0, c0 + len, ar, ac, marker, has_prev, gap_base);
@@ -1146,6 +1168,7 @@ void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uin
     a.range_e = p.colent;
     a.range_flag = p.colent + n_rg;
     a.n_flagged = reinterpret_cast<unsigned long long*>(p.d_totals + 14);  // zeroed by decode_prologue
+    a.chunk_pre = a.agg + n_rg;  // flat scratch [cap] u64 >= 10 x ranges u64
     a.slack = reinterpret_cast<uint64_t*>(p.rowgap);
     a.vmode = 0;
     if (out_indices) a.weights = nullptr;
