@@ -83,11 +83,24 @@ struct PatchTensor {
     std::vector<uint16_t> values;
 };
 
+// The identity-coded payloads of a patch, as K2 lays them out: one body with
+// each tensor's [index payload][value payload] (write_patch_bytes' blobs).
+struct Coded {
+    RawVec<uint8_t> body;
+    std::vector<std::pair<uint64_t, uint64_t>> payload;  // per tensor; len 0 if no indices
+    std::vector<uint64_t> val_off;                        // per tensor (valid when indices exist)
+};
+
 struct pulse_patch {
     int64_t base_step = 0, target_step = 0, anchor_step = 0;
     uint32_t representation = PULSE_COO_DOWNSCALED, codec = PULSE_ZSTD1;
     uint8_t target_hash[32] = {};
     std::vector<PatchTensor> tensors;
+    // encode() also runs K2 while the snapshots are resident; write_patch_bytes reuses
+    // that body for the same representation.  Any change to the tensors drops it.
+    Coded coded;
+    bool coded_valid = false;
+    uint32_t coded_repr = 0;
 };
 
 struct pulse_sha256_ctx {
@@ -587,12 +600,6 @@ const char* repr_name(uint32_t r) {
 // ---- device index coding over a host patch (patch.hpp:116-174) ----------------------------
 // Returns the body (per tensor [index payload][value payload] for tensors with
 // indices) and, per patch tensor, (index payload offset, length).
-struct Coded {
-    RawVec<uint8_t> body;
-    std::vector<std::pair<uint64_t, uint64_t>> payload;  // per tensor; len 0 if no indices
-    std::vector<uint64_t> val_off;                        // per tensor (valid when indices exist)
-};
-
 Coded device_index_code(Engine& E, const pulse_patch* p, bool with_values) {
     StageTimer tm{"index_code"};
     const uint32_t T = uint32_t(p->tensors.size());
@@ -1004,6 +1011,7 @@ pulse_status pulse_patch_add_tensor(pulse_patch* p, const pulse_tensor_patch* v)
     t.indices.assign(v->indices, v->indices + v->n_indices);
     t.values.assign(v->values, v->values + v->n_values);
     p->tensors.push_back(std::move(t));
+    p->coded_valid = false;
     return PULSE_OK;
 }
 
@@ -1089,6 +1097,31 @@ pulse_status pulse_encode(const pulse_checkpoint* current, const pulse_checkpoin
             E.stager.d2h(idx.data(), didx, n * 8, E.stream);
             E.stager.d2h(val.data(), d.val16, n * 2, E.stream);
             E.sync();
+            // K2 too, while the snapshots are resident and the target hash is still running:
+            // write_patch_bytes then reuses these payloads instead of uploading the indices again
+            if (n > 0) {
+                const uint64_t bcap = 14 * n + 1024;  // >= any escape-coded body
+                uint8_t* dbody = E.body.as<uint8_t>(bcap + 64);
+                auto* dent = E.entries.as<pulse_patch_entry>(T);
+                auto* dres = E.result.as<pulse_result>(1);
+                if (pulse_encode_emit(plan, repr, nullptr, 1, 0, dbody, bcap, dent, dres, E.stream) == PULSE_OK) {
+                    const pulse_result er = fetch_result(E, dres);
+                    if (er.status == PULSE_OK) {  // e.g. DimensionError: write_patch_bytes reports it
+                        std::vector<pulse_patch_entry> ents(er.n_entries);
+                        cuda_check(counted_copy(ents.data(), dent, er.n_entries * sizeof(pulse_patch_entry),
+                                                cudaMemcpyDeviceToHost, E.stream), "D2H");
+                        patch->coded.body.resize(er.body_bytes);
+                        E.stager.d2h(patch->coded.body.data(), dbody, er.body_bytes, E.stream);
+                        E.sync();
+                        for (const auto& e : ents) {
+                            patch->coded.payload.emplace_back(e.idx_off, e.idx_nbytes);
+                            patch->coded.val_off.push_back(e.val_off);
+                        }
+                        patch->coded_valid = true;
+                        patch->coded_repr = repr;
+                    }
+                }
+            }
             // per-tensor ranges: segments of a tensor are consecutive (2^31-element splits)
             uint32_t sg = 0;
             for (uint32_t k = 0; k < T; ++k) {
@@ -1311,6 +1344,7 @@ pulse_status pulse_decode_index_payloads(pulse_patch* patch, const uint8_t* cons
         std::lock_guard<std::mutex> lk(E.mu);
         std::vector<const uint8_t*> pl(payloads, payloads + n);
         std::vector<uint64_t> lens(sizes, sizes + n);
+        patch->coded_valid = false;
         device_decode_payloads(E, patch, pl, lens);
     });
 }
@@ -1323,13 +1357,16 @@ pulse_status pulse_write_patch_bytes(const pulse_patch* p, pulse_bytes** out) {
         const char* rname = repr_name(p->representation);
         if (p->codec > PULSE_GZIP6) raise(PULSE_E_ARGUMENT, "unknown codec");
         StageTimer tm{"write_patch_bytes"};
-        Coded c;
-        {
+        Coded computed;
+        const bool reuse = p->coded_valid && p->coded_repr == p->representation &&
+                           p->coded.payload.size() == p->tensors.size();
+        if (!reuse) {
             Engine& E = engine();
             std::lock_guard<std::mutex> lk(E.mu);
-            c = device_index_code(E, p, true);
+            computed = device_index_code(E, p, true);
         }
-        tm.lap("index coding");
+        const Coded& c = reuse ? p->coded : computed;
+        tm.lap(reuse ? "index coding (from encode)" : "index coding");
         const size_t T = p->tensors.size();
         // per tensor: its index blob and value blob (identity codec: straight out
         // of the device body, no intermediate copy)
