@@ -391,6 +391,7 @@ def run_pulse(args):
     graphs = None  # release the graphs (and anything they reference) before teardown
     scan_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["s0"], ev["s1"]))
     apply_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["a0"], ev["a1"]))
+    emit_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev["s1"], ev["a0"]))
 
     # correctness: after the timed loop W must equal the last step's target, and
     # two more (untimed) steps must each land exactly on theirs
@@ -401,7 +402,7 @@ def run_pulse(args):
         torch.cuda.synchronize()
         ok = ok and bool(torch.equal(w, curr if k % 2 == 0 else prev))
 
-    t_ms = torch.tensor([ms, scan_ms, apply_ms, float(not ok)], dtype=torch.float64, device=dev)
+    t_ms = torch.tensor([ms, scan_ms, apply_ms, float(not ok), emit_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
         tot = torch.tensor([float(state["body"]), float(state["changes"])], dtype=torch.float64, device=dev)
@@ -409,7 +410,7 @@ def run_pulse(args):
         body_total, changes_total = tot.tolist()
     else:
         body_total, changes_total = float(state["body"]), float(state["changes"])
-    ms_max, scan_max, apply_max, bad = t_ms.tolist()
+    ms_max, scan_max, apply_max, bad, emit_max = t_ms.tolist()
 
     e2e = None
     if not args.no_e2e:
@@ -434,12 +435,13 @@ def run_pulse(args):
         k1_gbs = k1_bytes / (scan_ms / 1e3) / 1e9
         # our launches per step: K1 (k1_tma, k1_finalize); K2 (COO: optimistic k2_layout + k2_emit, then
         # k2_scan_escapes / k2_layout / k2_emit that return at once unless an escape was seen; int32:
-        # k2_layout, k2_emit); FLAT carry [sharded FLAT only]; apply (d_layout, f_pass agg, f_range_scan, f_pass apply,
-        # f_pass restore, d_clear_status, general-path kernels that exit at once on the fast path
-        # [COO: d_rows, d_col_layout, d_cols, d_assemble; int32: d_fixed], d_scatter, d_finalize)
+        # k2_layout, k2_emit); FLAT carry [sharded FLAT only]; apply (d_layout, f_range_entries, f_stream agg,
+        # f_range_scan, f_pass validate x2, f_stream scatter, d_clear_status, general-path kernels that exit
+        # at once on the fast path [COO: d_rows, d_col_layout, d_cols, d_assemble; int32: d_fixed],
+        # d_scatter, d_finalize)
         n_emit = 5 if args.repr == 0 else 2
         n_carry = 1 if (world > 1 and args.repr == 2) else 0
-        n_apply = 12 if args.repr == 0 else 9
+        n_apply = 14 if args.repr == 0 else 11
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True,
@@ -464,6 +466,17 @@ def run_pulse(args):
                          "traffic": profiled_traffic(args, world),
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": k1_bytes},
+            # every phase against the same peak (eager pass, CUDA events on the launching stream,
+            # max over ranks); bytes per SURVEY 8(d): K2 reads the K1 intermediate (6 B/change) and
+            # writes the body; apply reads the body and writes 2 B per change (scattered sectors)
+            "phases": {
+                "k1_scan": {"ms": round(scan_max, 4), "bytes": int(4 * d_total + 6 * changes_total),
+                            "frac": round((4 * d_total + 6 * changes_total) / (scan_max / 1e3) / 1e9 / peak, 4)},
+                "k2_emit": {"ms": round(emit_max, 4), "bytes": int(6 * changes_total + body_total),
+                            "frac": round((6 * changes_total + body_total) / (emit_max / 1e3) / 1e9 / peak, 4)},
+                "apply": {"ms": round(apply_max, 4), "bytes": int(body_total + 2 * changes_total),
+                          "frac": round((body_total + 2 * changes_total) / (apply_max / 1e3) / 1e9 / peak, 4)},
+            },
             "gpu_launches": (2 + n_emit + n_carry + n_apply) * args.steps,
             "clocks": clocks.summary(),
             "e2e": e2e,
