@@ -456,9 +456,10 @@ def run_pulse(args):
             # the step against the HBM roofline (north_star: bytes read + written / peak), algorithmic
             # bytes per SURVEY §8(d): encode 4d + P_idx + 2n (snapshots in, patch body out), apply
             # P_idx + 2n (patch in) + 2n (scattered writes); the K1->K2 intermediate is not counted
-            "frac_of_hbm": round((4 * d_total + 2 * body_total + 2 * changes_total) / (ms_max / 1e3) / 1e9 / peak, 4),
+            "frac_of_hbm": round((4 * d_total + 2 * body_total + 2 * changes_total) / (ms_max / 1e3) / 1e9
+                                 / (peak * world), 4),
             "step_bytes": int(4 * d_total + 2 * body_total + 2 * changes_total),
-            "weight_gbs_frac_of_peak": round(value / peak, 4),
+            "weight_gbs_frac_of_peak": round(value / (peak * world), 4),
             "encode_ms": round(scan_max, 4), "apply_ms": round(apply_max, 4),
             "patch_mb": round(body_total / 1e6, 3), "changes": int(changes_total),
             "roofline": {"kernel": "k1_diff_compact", "bound": "hbm", "achieved": round(k1_gbs, 2),
@@ -466,17 +467,13 @@ def run_pulse(args):
                          "traffic": profiled_traffic(args, world),
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": k1_bytes},
-            # every phase against the same peak (eager pass, CUDA events on the launching stream,
-            # max over ranks); bytes per SURVEY 8(d): K2 reads the K1 intermediate (6 B/change) and
-            # writes the body; apply reads the body and writes 2 B per change (scattered sectors)
-            "phases": {
-                "k1_scan": {"ms": round(scan_max, 4), "bytes": int(4 * d_total + 6 * changes_total),
-                            "frac": round((4 * d_total + 6 * changes_total) / (scan_max / 1e3) / 1e9 / peak, 4)},
-                "k2_emit": {"ms": round(emit_max, 4), "bytes": int(6 * changes_total + body_total),
-                            "frac": round((6 * changes_total + body_total) / (emit_max / 1e3) / 1e9 / peak, 4)},
-                "apply": {"ms": round(apply_max, 4), "bytes": int(body_total + 2 * changes_total),
-                          "frac": round((body_total + 2 * changes_total) / (apply_max / 1e3) / 1e9 / peak, 4)},
-            },
+            # every phase against the peak of the GPUs doing it (eager pass, CUDA events on the launching
+            # stream, max over ranks); whole-job bytes per SURVEY 8(d): K2 reads the K1 intermediate
+            # (6 B/change) and writes the body; apply reads the body and writes 2 B per change (scattered)
+            "phases": {k: {"ms": round(t, 4), "bytes": int(b), "frac": round(b / (t / 1e3) / 1e9 / (peak * world), 4)}
+                       for k, t, b in (("k1_scan", scan_max, 4 * d_total + 6 * changes_total),
+                                       ("k2_emit", emit_max, 6 * changes_total + body_total),
+                                       ("apply", apply_max, body_total + 2 * changes_total))},
             "gpu_launches": (2 + n_emit + n_carry + n_apply) * args.steps,
             "clocks": clocks.summary(),
             "e2e": e2e,
