@@ -755,17 +755,18 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                 }
             }
         } else if (!S.overflow[buf]) {
-            for (uint32_t q = lt; q < count; q += kLbThreads) {
-                // chunk holding output ordinal q: last c with chunk_pre[c] <= q
-                uint32_t lo = 0, hi = nch;
-                while (hi - lo > 1) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (S.chunk_pre[mid] <= q) lo = mid; else hi = mid;
-                }
-                const uint32_t src = S.chunk_off[buf][lo] + (q - S.chunk_pre[lo]);
-                if (G + q < k.capacity) {
-                    k.out_idx[G + q] = ti.toff + S.stg[buf].el.idx[src];
-                    k.out_val[G + q] = S.stg[buf].el.val[src];
+            // element mode: each chunk's staged entries are contiguous and go to
+            // G + chunk_pre[c] onward -- one warp per chunk, lanes over its entries
+            // (coalesced stores, no per-entry search for the chunk)
+            for (uint32_t c = uint32_t(warp - kLbFirst); c < nch; c += kLbWarps) {
+                const uint32_t base = S.chunk_pre[c], cnt = S.chunk_pre[c + 1] - base;
+                const uint32_t off = S.chunk_off[buf][c];
+                for (uint32_t i = lane; i < cnt; i += 32) {
+                    const uint64_t pos = G + base + i;
+                    if (pos < k.capacity) {
+                        k.out_idx[pos] = ti.toff + S.stg[buf].el.idx[off + i];
+                        k.out_val[pos] = S.stg[buf].el.val[off + i];
+                    }
                 }
             }
         } else {
