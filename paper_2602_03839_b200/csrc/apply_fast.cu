@@ -367,7 +367,8 @@ f_pass(ApplyArgs A) {
             }
         }
         bool marker = false;
-        uint32_t e = upper_index<uint64_t>(A.es, 0, A.n_e, c_first);
+        // the range's entry from F0 (new pipeline) instead of a binary search over the entries
+        uint32_t e = kPass != kAgg && A.range_flag ? A.range_e[rg] : upper_index<uint64_t>(A.es, 0, A.n_e, c_first);
         if (kPass == kAgg && lane == 0) A.range_e[rg] = e;
         // chunks end at the next 1024-aligned entry, the range end or the patch entry's end:
         // a chunk never straddles two entries, so only tensors >= 2^32 take the walker

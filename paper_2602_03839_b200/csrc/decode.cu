@@ -597,30 +597,32 @@ void launch_decode(const PlanDev& p, uint32_t repr, const uint8_t* body,
         // common case: fixed-layout payloads (no escapes) -- apply_fast.cu
         launch_apply_fast(p, repr, body, n_entries, carry, weights_slot, out_indices, p.d_flags, s);
         // general path (escapes, malformed sizes): runs only if d_layout / F1 raised flags[0]
-        d_clear_status<<<g, kThreads, 0, s>>>(p.d_status, 4 * p.d_status_len, p.d_flags);
-        PULSE_LAUNCHED("d_clear_status", s);
-        if (repr == PULSE_COO_INT32) {
-            d_fixed<false><<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, body, nullptr, st0, p.d_totals, out, p.err, p.d_flags);
-            PULSE_LAUNCHED("d_fixed<false>", s);
-        } else if (repr == PULSE_FLAT_INT32) {
-            d_fixed<true><<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, body, carry, st0, p.d_totals, out, p.err, p.d_flags);
-            PULSE_LAUNCHED("d_fixed<true>", s);
-        } else {
-            d_rows<<<g, kThreads, 0, s>>>(p.elay, p.d_ck, n_entries, body, st2, p.d_totals, p.rowgap, p.err, p.d_flags);
-            PULSE_LAUNCHED("d_rows", s);
-            d_col_layout<<<1, kLT, 0, s>>>(p.elay, n_entries, p.d_cu, p.d_totals, p.err, p.d_flags);
-            PULSE_LAUNCHED("d_col_layout", s);
-            d_cols<<<g, kThreads, 0, s>>>(p.elay, p.d_cu, n_entries, body, st3, p.d_totals, p.colent, p.err, p.d_flags);
-            PULSE_LAUNCHED("d_cols", s);
-            d_assemble<<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, p.rowgap, p.colent, st0, st1, p.d_totals, out, p.err, p.d_flags);
-            PULSE_LAUNCHED("d_assemble", s);
-        }
-        if (weights_slot >= 0)
-            {
-            d_scatter<<<g, kThreads, 0, s>>>(p.elay, p.d_es, n_entries, body, nullptr, out, nullptr,
-                                             p.slot[weights_slot], p.d_totals, p.err, p.d_flags);
-            PULSE_LAUNCHED("d_scatter", s);
+        launch_gated(s, p.d_flags, [&](cudaStream_t gs) {
+            d_clear_status<<<g, kThreads, 0, gs>>>(p.d_status, 4 * p.d_status_len, p.d_flags);
+            PULSE_LAUNCHED("d_clear_status", gs);
+            if (repr == PULSE_COO_INT32) {
+                d_fixed<false><<<g, kThreads, 0, gs>>>(p.elay, p.d_es, n_entries, body, nullptr, st0, p.d_totals, out, p.err, p.d_flags);
+                PULSE_LAUNCHED("d_fixed<false>", gs);
+            } else if (repr == PULSE_FLAT_INT32) {
+                d_fixed<true><<<g, kThreads, 0, gs>>>(p.elay, p.d_es, n_entries, body, carry, st0, p.d_totals, out, p.err, p.d_flags);
+                PULSE_LAUNCHED("d_fixed<true>", gs);
+            } else {
+                d_rows<<<g, kThreads, 0, gs>>>(p.elay, p.d_ck, n_entries, body, st2, p.d_totals, p.rowgap, p.err, p.d_flags);
+                PULSE_LAUNCHED("d_rows", gs);
+                d_col_layout<<<1, kLT, 0, gs>>>(p.elay, n_entries, p.d_cu, p.d_totals, p.err, p.d_flags);
+                PULSE_LAUNCHED("d_col_layout", gs);
+                d_cols<<<g, kThreads, 0, gs>>>(p.elay, p.d_cu, n_entries, body, st3, p.d_totals, p.colent, p.err, p.d_flags);
+                PULSE_LAUNCHED("d_cols", gs);
+                d_assemble<<<g, kThreads, 0, gs>>>(p.elay, p.d_es, n_entries, p.rowgap, p.colent, st0, st1, p.d_totals, out, p.err, p.d_flags);
+                PULSE_LAUNCHED("d_assemble", gs);
             }
+            if (weights_slot >= 0)
+                {
+                d_scatter<<<g, kThreads, 0, gs>>>(p.elay, p.d_es, n_entries, body, nullptr, out, nullptr,
+                                                 p.slot[weights_slot], p.d_totals, p.err, p.d_flags);
+                PULSE_LAUNCHED("d_scatter", gs);
+                }
+        });
     }
     d_finalize<<<1, 32, 0, s>>>(p.d_totals, n_entries, p.err, result);
     PULSE_LAUNCHED("d_finalize", s);

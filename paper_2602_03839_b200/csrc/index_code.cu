@@ -1062,7 +1062,7 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
     a.run_if = nullptr;
     a.optimistic = false;
     const unsigned g_scan = unsigned(sm_count() * occ_scan), g_emit = unsigned(sm_count() * occ_emit);
-    auto exact = [&](const uint32_t* run_if) {  // K2a escape counts -> layout -> emit
+    auto exact = [&](const uint32_t* run_if, cudaStream_t s) {  // K2a escape counts -> layout -> emit
         if (repr == PULSE_COO_DOWNSCALED || validate_args) {
             k2_scan_escapes<<<g_scan, kThreads, kWarps * kScanWarpSmem, s>>>(em, repr, p.range_cnt, p.t_resc, p.t_cesc,
                                                                             p.err, run_if);
@@ -1090,9 +1090,9 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
         k2_emit<<<g_emit, kThreads, kWarps * kEmitWarpSmem, s>>>(em, repr, p.tlay, p.range_pre, vals, result, body,
                                                                  nullptr, esc);
         PULSE_LAUNCHED("k2_emit (optimistic)", s);
-        exact(esc);
+        launch_gated(s, esc, [&](cudaStream_t gs) { exact(esc, gs); });
     } else {
-        exact(nullptr);
+        exact(nullptr, s);
     }
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -173,6 +174,9 @@ struct PerDeviceInt {
 // PULSE_DEBUG_SYNC=1: synchronise after every launch and report the first
 // failing kernel by name on stderr (debugging aid; off by default).
 void debug_sync(const char* kernel, cudaStream_t s);
+// gate.cu: `body` (launches on the stream it is given) runs only if *flag != 0
+// when the stream gets there -- a conditional graph node under stream capture.
+void launch_gated(cudaStream_t s, const uint32_t* flag, const std::function<void(cudaStream_t)>& body);
 #define PULSE_LAUNCHED(name, stream) ::pulse::dev::debug_sync(name, stream)
 // helpers.cu (host-buffer API support)
 void launch_export_indices(const PlanDev& p, int64_t* out, cudaStream_t s);

@@ -462,3 +462,46 @@ def test_clean_patch_checks_pass_on_plain_ranges():
         assert int(res["status"]) == 0, (repr_, res)
         for b, t in zip(currs, w):
             assert np.array_equal(t.cpu().numpy().view(np.uint16), b)
+
+
+@pytest.mark.parametrize("case", ["esc_cols", "esc_rows", "handcrafted", "roundtrip_s0"])
+@pytest.mark.parametrize("repr_", [COO_DOWNSCALED, FLAT_INT32])
+def test_graph_replay_runs_gated_paths(golden, case, repr_):
+    """encode + apply captured as a CUDA graph (the benchmark's launch mode): K2's
+    exact re-run and the escape-aware decoder sit behind conditional graph nodes.
+    Replays in both directions land exactly on the targets and produce the
+    reference's body, for patches that need those paths (escapes) and ones that do not."""
+    D = _dev()
+    prev, curr, m = golden.case(case)
+    ts, prev_d = upload(prev)
+    _, curr_d = upload(curr)
+    plan = make_plan(ts)
+    plan.bind(0, prev_d)
+    plan.bind(1, curr_d)
+    w = [t.clone() for t in prev_d]
+    plan.bind(2, w)
+    patches = [plan.new_patch(repr_), plan.new_patch(repr_)]
+    res = [torch.zeros(72, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    stream = torch.cuda.Stream()
+    graphs = []
+    with torch.cuda.stream(stream):
+        for k, (cs, ps) in enumerate(((1, 0), (0, 1))):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                plan.scan(cs, ps, stream=stream)
+                plan.emit(patches[k], stream=stream)
+                plan.apply_patch(2, patches[k], result=res[k], stream=stream)
+            graphs.append(g)
+    want = golden.pulp(case, repr_, IDENTITY)
+    for rep in range(2):
+        for k, target in ((0, curr_d), (1, prev_d)):
+            graphs[k].replay()
+            torch.cuda.synchronize()
+            r = D.parse_result(res[k])
+            assert int(r["status"]) == 0, (case, repr_, r)
+            for a, b in zip(w, target):
+                assert torch.equal(a, b), (case, repr_, rep, k)
+            if k == 0 and want is not None:
+                patches[0].fetch()
+                _, body = split_pulp(want)
+                assert patches[0].body[: patches[0].body_bytes].cpu().numpy().tobytes() == body
