@@ -221,7 +221,12 @@ struct ApplyArgs {
     uint32_t* range_e;                   // [ranges] F0 out: patch entry holding each range's first entry
     uint32_t* range_flag;                // [ranges] F1s out: list of the non-plain ranges (exact checks in F3)
     unsigned long long* n_flagged;       // its length (zeroed by decode_prologue)
-    ulonglong2* chunk_pre;               // [ranges x 4] F1s out (non-plain ranges): in-range prefix at each 1024-chunk
+    struct Piece {                       // F1s out: one chunk of a non-plain range, for F3
+        uint64_t c0, rg, ar, ac;         // first entry, range, in-range aggregate at c0
+        uint32_t len, e;                 // entries, patch entry
+    }* pieces;
+    unsigned long long* n_pieces;        // pieces appended (zeroed by decode_prologue)
+    uint64_t piece_cap;                  // beyond it F1s falls back to checking every range exactly
     uint64_t* slack;                     // [ranges] F1s out: cols - 1 - first row segment's local end column
     int vmode;                           // F3 validate: 0 = non-plain ranges (all if suspect), 1 = all if any failure
 };
@@ -337,23 +342,26 @@ f_pass(ApplyArgs A) {
 
     // F3 validate after F1s: exact checks where F1s could not decide (see f_stream).
     // Filtered: the non-plain ranges F1s listed, one 1024-entry chunk per warp, each
-    // starting from its range's carry combined with F1s's in-range chunk prefix.
+    // the pieces F1s listed (one entry-aligned chunk of a non-plain range each, with its
+    // in-range carry), one per warp.
     bool filter = false;
     uint64_t n_items = n_ranges;
     if (kPass == kValidate && A.range_flag) {
         const bool suspect = *(volatile const uint32_t*)(A.flags + 1) != 0;
         if (A.vmode == 0) {
             filter = !suspect;
-            if (filter) n_items = *(volatile const unsigned long long*)A.n_flagged * kChunksPerRange;
+            if (filter) n_items = min(uint64_t(*(volatile const unsigned long long*)A.n_pieces), A.piece_cap);
         } else {  // second launch: re-check everything only if the filtered pass found a failure
             if (suspect || *(volatile const uint64_t*)A.err == kNoError) return;
         }
     }
     for (uint64_t it = uint64_t(blockIdx.x) * kWarps + warp; it < n_items; it += stride) {
-        const uint64_t rg = filter ? A.range_flag[it / kChunksPerRange] : it;
-        const uint64_t r0 = rg * kRange, r_end = min(r0 + kRange, n);
-        const uint64_t c_first = filter ? r0 + (it % kChunksPerRange) * kChunk : r0;
-        const uint64_t r1 = filter ? min(c_first + kChunk, r_end) : r_end;
+        ApplyArgs::Piece pc{};
+        if (filter) pc = A.pieces[it];
+        const uint64_t rg = filter ? pc.rg : it;
+        const uint64_t r0 = rg * kRange;
+        const uint64_t c_first = filter ? pc.c0 : r0;
+        const uint64_t r1 = filter ? pc.c0 + pc.len : min(r0 + kRange, n);
         if (c_first >= r1) continue;
         uint64_t ar = 0, ac = 0;  // kAgg: aggregates; else running (row, col) / sums
         if (kPass != kAgg) {
@@ -361,14 +369,14 @@ f_pass(ApplyArgs A) {
             ar = p.x;
             ac = p.y;
             if (filter) {
-                const ulonglong2 q = A.chunk_pre[rg * kChunksPerRange + it % kChunksPerRange];
-                ar = SegSumOp::op(ar, q.x) & (H - 1);
-                ac = SegSumOp::op(ac, q.y) & (H - 1);
+                ar = SegSumOp::op(ar, pc.ar) & (H - 1);
+                ac = SegSumOp::op(ac, pc.ac) & (H - 1);
             }
         }
         bool marker = false;
-        // the range's entry from F0 (new pipeline) instead of a binary search over the entries
-        uint32_t e = kPass != kAgg && A.range_flag ? A.range_e[rg] : upper_index<uint64_t>(A.es, 0, A.n_e, c_first);
+        // the chunk's entry from F1s / F0 (new pipeline) instead of a binary search over the entries
+        uint32_t e = filter ? pc.e
+                   : kPass != kAgg && A.range_flag ? A.range_e[rg] : upper_index<uint64_t>(A.es, 0, A.n_e, c_first);
         if (kPass == kAgg && lane == 0) A.range_e[rg] = e;
         // chunks end at the next 1024-aligned entry, the range end or the patch entry's end:
         // a chunk never straddles two entries, so only tensors >= 2^32 take the walker
@@ -602,8 +610,6 @@ struct SLay {
     static constexpr uint32_t warp = 2 * buf + (kAgg_ ? 0 : 4 * ch);          // 2 buffers (+ decoded indices)
 };
 
-static_assert(SLay<kCoo, true>::ch == kChunk && SLay<kI32, true>::ch == kChunk,
-              "F1s chunks are F3's validate chunks (chunk_pre)");
 
 // Queues the 16-byte blocks covering [g, g+len) into dst (swizzle V); returns g & 15.
 template <int V>
@@ -926,8 +932,16 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
             }
             len_nx = chunk_len(rg_nx, c_nx, nx);
         }
-        if (agg && !plain && lane == 0 && c0 % kChunk == 0)
-            A.chunk_pre[rg * kChunksPerRange + (c0 - rg * kRange) / kChunk] = make_ulonglong2(ar, ac);
+        if (agg && !plain) {  // this chunk gets F3's exact checks: list it with its in-range carry
+            unsigned long long slot = 0;
+            if (lane == 0) slot = atomicAdd(A.n_pieces, 1ull);
+            slot = __shfl_sync(0xffffffffu, slot, 0);
+            if (slot < A.piece_cap) {
+                if (lane == 0) A.pieces[slot] = ApplyArgs::Piece{c0, rg, ar, ac, len, cur.e};
+            } else {
+                suspect = true;  // list full: every range gets the exact checks
+            }
+        }
         if (!is_fast(cur, c0, len)) {
             // straddles patch entries or a tensor >= 2^32 elements: per-round walker (never plain)
             slow_span<kRepr, agg ? kAgg : kScatter>(A, c0, c0 + len, ar, ac, marker, has_prev, gap_base);
@@ -1169,7 +1183,10 @@ void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uin
     a.range_e = p.colent;
     a.range_flag = p.colent + n_rg;
     a.n_flagged = reinterpret_cast<unsigned long long*>(p.d_totals + 14);  // zeroed by decode_prologue
-    a.chunk_pre = a.agg + n_rg;  // flat scratch [cap] u64 >= 10 x ranges u64
+    // flat scratch [cap] u64: range aggregates, then the piece list
+    a.pieces = reinterpret_cast<ApplyArgs::Piece*>(a.agg + n_rg);
+    a.piece_cap = (8 * p.cap - 16 * n_rg) / sizeof(ApplyArgs::Piece);
+    a.n_pieces = reinterpret_cast<unsigned long long*>(p.d_totals + 13);  // zeroed by decode_prologue
     a.slack = reinterpret_cast<uint64_t*>(p.rowgap);
     a.vmode = 0;
     if (out_indices) a.weights = nullptr;
