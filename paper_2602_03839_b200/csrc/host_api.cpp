@@ -1923,6 +1923,16 @@ namespace {
 
 constexpr size_t kHashChunk = 64u << 20;
 
+// Runs a resident's calls on the device it lives on, restoring the caller's device.
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
 // SHA-256 of device tensors in the given order (sha256.hpp:93-116 over HBM):
 // chunk k+1 is copied to pinned memory while chunk k is hashed.
 void hash_device(pulse_resident* r, const std::vector<std::pair<const uint8_t*, uint64_t>>& parts, uint8_t out[32]) {
@@ -2152,6 +2162,7 @@ pulse_status pulse_resident_create_device(const pulse_checkpoint* c, uint64_t ma
 
 void pulse_resident_destroy(pulse_resident* r) {
     if (!r) return;
+    DeviceGuard dg(r->device);
     cudaDeviceSynchronize();
     delete r;
 }
@@ -2173,6 +2184,7 @@ pulse_status pulse_resident_tensor(const pulse_resident* r, uint32_t i, void** d
 pulse_status pulse_resident_download(const pulse_resident* r, uint16_t* const* out) {
     return guarded([&] {
         if (!r || (!out && !r->names.empty())) raise(PULSE_E_ARGUMENT, "null argument");
+        DeviceGuard dg(r->device);
         Engine& E = engine();
         std::lock_guard<std::mutex> lk(E.mu);
         for (uint32_t i = 0; i < r->names.size(); ++i) E.stager.d2h(out[i], r->tensor(i), r->numel[i] * 2, E.stream);
@@ -2184,6 +2196,7 @@ pulse_status pulse_resident_apply(pulse_resident* r, const uint8_t* pulp, uint64
                                   const uint8_t* expected_hash32, int verify_hash) {
     return guarded([&] {
         if (!r || (n && !pulp)) raise(PULSE_E_ARGUMENT, "null argument");
+        DeviceGuard dg(r->device);
         ParsedPulp pp = parse_pulp(pulp, n);
         Engine& E = engine();
         std::lock_guard<std::mutex> lk(E.mu);
@@ -2197,6 +2210,7 @@ pulse_status pulse_resident_walk(pulse_resident* r, const uint8_t* const* pulps,
     return guarded([&] {
         if (!r || (k && (!pulps || !sizes))) raise(PULSE_E_ARGUMENT, "null argument");
         if (k == 0) return;
+        DeviceGuard dg(r->device);
         // the next patch is parsed (JSON header, codec) on a host thread while this one applies
         std::future<ParsedPulp> next = std::async(std::launch::async, [&] { return parse_pulp(pulps[0], sizes[0]); });
         for (uint32_t j = 0; j < k; ++j) {
@@ -2222,6 +2236,7 @@ pulse_status pulse_resident_publish(pulse_resident* r, const void* const* dev_cu
     return guarded([&] {
         if (!r || !out_pulp || (!dev_current && !r->names.empty())) raise(PULSE_E_ARGUMENT, "null argument");
         if (step != r->step + 1) raise(PULSE_E_ARGUMENT, "publish requires consecutive steps");
+        DeviceGuard dg(r->device);
         repr_name(repr);
         if (codec > PULSE_GZIP6) raise(PULSE_E_ARGUMENT, "unknown codec");
         const uint32_t T = uint32_t(r->names.size());
