@@ -439,9 +439,14 @@ def run_pulse(args):
         # f_range_scan, f_pass validate x2, f_stream scatter, d_clear_status, general-path kernels that exit
         # at once on the fast path [COO: d_rows, d_col_layout, d_cols, d_assemble; int32: d_fixed],
         # d_scatter, d_finalize)
-        n_emit = 5 if args.repr == 0 else 2
+        # (replayed graphs: the idle paths sit in conditional nodes -- one k_set_cond each instead)
+        if used_graph:
+            n_emit = 3 if args.repr == 0 else 2
+            n_apply = 9
+        else:
+            n_emit = 5 if args.repr == 0 else 2
+            n_apply = 14 if args.repr == 0 else 11
         n_carry = 1 if (world > 1 and args.repr == 2) else 0
-        n_apply = 14 if args.repr == 0 else 11
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True,
