@@ -226,6 +226,9 @@ namespace tma {
 #ifndef PULSE_K1_BUFS
 #define PULSE_K1_BUFS 3
 #endif
+#ifndef PULSE_K1_COOP_STAGE
+#define PULSE_K1_COOP_STAGE 1  // element mode: warp-cooperative staging (0: per-lane loop over mask bits)
+#endif
 #ifndef PULSE_K1_RECCAP
 #define PULSE_K1_RECCAP 1344
 #endif
@@ -627,6 +630,51 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                     if (off + total > kStageCap) S.overflow[buf] = 1;
                 }
                 if (total && k.experiment != 3) {
+#if PULSE_K1_COOP_STAGE
+                    // warp-cooperative: slot s of vector group j (element order: lane, then
+                    // bit) is filled by lane s % 32 in round s / 32.  Its owner is the first
+                    // lane whose inclusive count exceeds s (binary lifting over shuffles), its
+                    // element the (s - owner's exclusive count)-th set bit of the owner's mask
+                    // -- no per-lane loop over mask bits, so no divergence on dense vectors.
+                    const uint32_t tj[4] = {t0, t1, t2, t3};
+                    uint32_t pbase = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (tj[j]) {
+                            const uint32_t incl = pj[j] - pbase + __popc(m[j]);
+                            for (uint32_t s0 = 0; s0 < tj[j]; s0 += 32) {
+                                const uint32_t s = s0 + uint32_t(lane);
+                                uint32_t own = 0;
+#pragma unroll
+                                for (uint32_t step = 16; step; step >>= 1)
+                                    if (__shfl_sync(0xffffffffu, incl, int(own + step - 1)) <= s) own += step;
+                                const int src = int(own & 31);
+                                const uint32_t om = __shfl_sync(0xffffffffu, m[j], src);
+                                const uint32_t oin = __shfl_sync(0xffffffffu, incl, src);
+                                const uint32_t w0 = __shfl_sync(0xffffffffu, cv[j].x, src);
+                                const uint32_t w1 = __shfl_sync(0xffffffffu, cv[j].y, src);
+                                const uint32_t w2 = __shfl_sync(0xffffffffu, cv[j].z, src);
+                                const uint32_t w3 = __shfl_sync(0xffffffffu, cv[j].w, src);
+                                if (s < tj[j]) {
+                                    uint32_t r = s - (oin - __popc(om)), q = 0;  // r-th set bit of om
+                                    uint32_t c = __popc(om & 0xFu);
+                                    if (r >= c) { q = 4; r -= c; }
+                                    c = __popc((om >> q) & 3u);
+                                    if (r >= c) { q += 2; r -= c; }
+                                    if (r >= ((om >> q) & 1u)) q += 1;
+                                    const uint32_t w = q < 4 ? (q < 2 ? w0 : w1) : (q < 6 ? w2 : w3);
+                                    const uint32_t pos = off + pbase + s;
+                                    if (pos < kStageCap) {
+                                        S.stg[buf].el.idx[pos] =
+                                            uint16_t(d.sub * kSubElems + (warp * kVecPerWarp + uint32_t(src) + 32 * j) * 8 + q);
+                                        S.stg[buf].el.val[pos] = uint16_t(w >> ((q & 1) * 16));
+                                    }
+                                }
+                            }
+                        }
+                        pbase += tj[j];
+                    }
+#else
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         uint32_t mm = m[j];
@@ -642,6 +690,7 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                             ++pos;
                         }
                     }
+#endif
                 }
                 wcount += total;
             }
