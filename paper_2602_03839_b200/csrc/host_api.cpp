@@ -79,8 +79,8 @@ struct pulse_bytes {
 struct PatchTensor {
     std::string name;
     std::vector<int64_t> shape;
-    std::vector<int64_t> indices;
-    std::vector<uint16_t> values;
+    RawVec<int64_t> indices;  // no zero fill on resize: always overwritten (hundreds of MB at 7B)
+    RawVec<uint16_t> values;
 };
 
 // The identity-coded payloads of a patch, as K2 lays them out: one body with
@@ -488,7 +488,7 @@ pulse_result fetch_result(Engine& E, const void* dev_result) {
 }
 
 // Exception text for a device-detected failure, in the reference's words.
-std::string device_message(const pulse_result& r, const std::string& name, const std::vector<int64_t>* idx) {
+std::string device_message(const pulse_result& r, const std::string& name, const RawVec<int64_t>* idx) {
     switch (r.err_check) {
         case PULSE_CHECK_TRUNCATED: return "unexpected end of data";
         case PULSE_CHECK_ZERO_GAP: return "zero index gap in tensor '" + name + "'";
@@ -740,7 +740,7 @@ void validate_for_write(const pulse_patch* p) {  // patch_file.hpp:31-42
     }
 }
 
-std::vector<uint8_t> value_payload(const std::vector<uint16_t>& v) {  // patch.hpp:78-83 (LE u16)
+std::vector<uint8_t> value_payload(const RawVec<uint16_t>& v) {  // patch.hpp:78-83 (LE u16)
     std::vector<uint8_t> out(v.size() * 2);
     for (size_t i = 0; i < v.size(); ++i) {
         out[2 * i] = uint8_t(v[i]);
@@ -1092,8 +1092,8 @@ pulse_status pulse_encode(const pulse_checkpoint* current, const pulse_checkpoin
             cuda_check(counted_copy(seg_start.data(), d.seg_start, seg_start.size() * 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
             int64_t* didx = E.out64.as<int64_t>(n);
             launch_export_indices(d, didx, E.stream);
-            std::vector<int64_t> idx(n);
-            std::vector<uint16_t> val(n);
+            RawVec<int64_t> idx(n);
+            RawVec<uint16_t> val(n);
             E.stager.d2h(idx.data(), didx, n * 8, E.stream);
             E.stager.d2h(val.data(), d.val16, n * 2, E.stream);
             E.sync();
@@ -1215,25 +1215,23 @@ pulse_status pulse_decode(const pulse_checkpoint* previous, const pulse_patch* p
             pulse_patch_entry* dent = nullptr;
             std::vector<uint64_t> at(stop + 1, 0);
             if (stop > 0 && n > 0) {
-                // gathered on host threads while the base snapshot's DMA (queued above) runs
-                RawVec<int64_t> idx(n);
-                RawVec<uint16_t> val(n);
                 std::vector<pulse_patch_entry> ents(stop);
                 for (uint32_t k = 0; k < stop; ++k) {
                     const auto& tp = patch->tensors[k];
                     ents[k] = pulse_patch_entry{target[k], 0, tp.indices.size(), 0, 0, 0};
                     at[k + 1] = at[k] + tp.indices.size();
                 }
-                pool().parallel_for(stop, [&](size_t k) {
-                    const auto& tp = patch->tensors[k];
-                    const size_t m = tp.indices.size();
-                    if (m) std::memcpy(idx.data() + at[k], tp.indices.data(), m * 8);
-                    if (m) std::memcpy(val.data() + at[k], tp.values.data(), m * 2);
-                });
+                // each tensor's indices / values straight into their place on the device
+                // (one pass through the pinned staging, no host-side gather copy)
                 didx = E.idx64.as<int64_t>(n);
                 dval = E.vals.as<uint16_t>(n);
-                E.stager.h2d(didx, idx.data(), n * 8, E.stream);
-                E.stager.h2d(dval, val.data(), n * 2, E.stream);
+                for (uint32_t k = 0; k < stop; ++k) {
+                    const auto& tp = patch->tensors[k];
+                    const size_t m = tp.indices.size();
+                    if (!m) continue;
+                    E.stager.h2d(didx + at[k], tp.indices.data(), m * 8, E.stream);
+                    E.stager.h2d(dval + at[k], tp.values.data(), m * 2, E.stream);
+                }
                 dent = E.entries.as<pulse_patch_entry>(stop);
                 cuda_check(counted_copy(dent, ents.data(), stop * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice,
                                            E.stream), "H2D");
