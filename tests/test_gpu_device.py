@@ -505,3 +505,48 @@ def test_graph_replay_runs_gated_paths(golden, case, repr_):
                 patches[0].fetch()
                 _, body = split_pulp(want)
                 assert patches[0].body[: patches[0].body_bytes].cpu().numpy().tobytes() == body
+
+
+@pytest.mark.parametrize("repr_", [COO_DOWNSCALED, COO_INT32, FLAT_INT32])
+def test_many_tiny_tensors_small_plan(repr_):
+    """Hundreds of tiny tensors under a plan sized for few changes: the list of
+    pieces F3 checks overflows, apply falls back to exact checks of every range,
+    and both a clean and a corrupted patch behave exactly as the reference's."""
+    D = _dev()
+    rng = np.random.default_rng(17)
+    sizes = [(int(rng.integers(1, 50)) * 64, 64) for _ in range(700)]  # row gaps < 255: no escapes
+    prevs = [rng.integers(0, 65536, n, dtype=np.uint16) for n, _ in sizes]
+    currs = []
+    for a in prevs:
+        b = a.copy()
+        b[rng.integers(0, a.size, 2)] ^= 1
+        currs.append(b)
+    total_changes = sum(int((a != b).sum()) for a, b in zip(prevs, currs))
+    plan = D.DevicePlan(sizes, max(1024, total_changes))
+    plan.bind(0, [torch.from_numpy(a.view(np.int16)).cuda() for a in prevs])
+    plan.bind(1, [torch.from_numpy(b.view(np.int16)).cuda() for b in currs])
+    w = [torch.from_numpy(a.view(np.int16)).cuda() for a in prevs]
+    plan.bind(2, w)
+    p = plan.encode(1, 0, repr_)
+    assert p.status == 0 and p.n_changes == total_changes
+    body = p.body[: p.body_bytes].cpu().numpy().copy()
+    res = D.parse_result(plan.apply(2, p))
+    assert int(res["status"]) == 0, res
+    for b, t in zip(currs, w):
+        assert np.array_equal(t.cpu().numpy().view(np.uint16), b)
+    # corrupt one entry in the middle tensor: the reference's first failure, nothing written
+    for a, t in zip(prevs, w):
+        t.copy_(torch.from_numpy(a.view(np.int16)))
+    e = p.host_entries[p.n_entries // 2]
+    off, cnt = int(e["idx_off"]), int(e["count"])
+    if repr_ == COO_DOWNSCALED:
+        body[off + cnt:off + cnt + 2] = [0xFE, 0xFF]   # first column entry past any row
+    else:
+        body[off:off + 4] = [0xF0, 0xFF, 0xFF, 0x7F]
+    want = _first_failure(repr_, p.host_entries[: p.n_entries], body.tobytes(), sizes)
+    p.body[: p.body_bytes] = torch.from_numpy(body).cuda()
+    res = D.parse_result(plan.apply(2, p))
+    assert int(res["status"]) == 7
+    assert (int(res["err_tensor"]), int(res["err_check"]), int(res["err_elem"])) == want
+    for a, t in zip(prevs, w):
+        assert np.array_equal(t.cpu().numpy().view(np.uint16), a)
