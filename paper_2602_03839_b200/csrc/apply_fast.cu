@@ -219,8 +219,7 @@ struct ApplyArgs {
     unsigned long long* scan_ticket;     // F2 block ticket (zeroed per call)
     uint32_t scan_blocks;                // F2 grid: blocks for the plan's capacity
     uint32_t* range_e;                   // [ranges] F0 out: patch entry holding each range's first entry
-    uint32_t* range_flag;                // [ranges] F1s out: list of the non-plain ranges (exact checks in F3)
-    unsigned long long* n_flagged;       // its length (zeroed by decode_prologue)
+    bool checked;                        // the F0-F5 pipeline (F1s checks, F3 on listed pieces)
     struct Piece {                       // F1s out: one chunk of a non-plain range, for F3
         uint64_t c0, rg, ar, ac;         // first entry, range, in-range aggregate at c0
         uint32_t len, e;                 // entries, patch entry
@@ -346,7 +345,7 @@ f_pass(ApplyArgs A) {
     // in-range carry), one per warp.
     bool filter = false;
     uint64_t n_items = n_ranges;
-    if (kPass == kValidate && A.range_flag) {
+    if (kPass == kValidate && A.checked) {
         const bool suspect = *(volatile const uint32_t*)(A.flags + 1) != 0;
         if (A.vmode == 0) {
             filter = !suspect;
@@ -376,7 +375,7 @@ f_pass(ApplyArgs A) {
         bool marker = false;
         // the chunk's entry from F1s / F0 (new pipeline) instead of a binary search over the entries
         uint32_t e = filter ? pc.e
-                   : kPass != kAgg && A.range_flag ? A.range_e[rg] : upper_index<uint64_t>(A.es, 0, A.n_e, c_first);
+                   : kPass != kAgg && A.checked ? A.range_e[rg] : upper_index<uint64_t>(A.es, 0, A.n_e, c_first);
         if (kPass == kAgg && lane == 0) A.range_e[rg] = e;
         // chunks end at the next 1024-aligned entry, the range end or the patch entry's end:
         // a chunk never straddles two entries, so only tensors >= 2^32 take the walker
@@ -963,7 +962,6 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
         if (agg && range_done) {
             if (lane == 0) {
                 A.agg[rg] = make_ulonglong2(ar, ac);
-                if (!plain) A.range_flag[atomicAdd(A.n_flagged, 1ull)] = uint32_t(rg);
                 A.slack[rg] = plain ? slack : kNoSlack;
             }
             if (marker && lane == 0) atomicExch(A.flags, 1u);
@@ -1129,7 +1127,7 @@ void launch_all(const ApplyArgs& a, bool scatter, cudaStream_t s) {
     static const int mode = getenv("PULSE_APPLY_MODE") ? atoi(getenv("PULSE_APPLY_MODE")) : 0;
     if (mode == 1 || mode == 2) {
         ApplyArgs b = a;
-        b.range_flag = nullptr;
+        b.checked = false;
         launch_pass<kRepr, kAgg>(b, s);
         launch_range_scan(b, nullptr, s);
         if (b.weights && mode == 1) {
@@ -1181,8 +1179,7 @@ void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uin
     // [cap] u32 >= 2 x ranges u64 (the legacy backup of PULSE_APPLY_MODE=1 uses rowgap instead)
     const uint64_t n_rg = p.cap / kRange + 2;
     a.range_e = p.colent;
-    a.range_flag = p.colent + n_rg;
-    a.n_flagged = reinterpret_cast<unsigned long long*>(p.d_totals + 14);  // zeroed by decode_prologue
+    a.checked = true;
     // flat scratch [cap] u64: range aggregates, then the piece list
     a.pieces = reinterpret_cast<ApplyArgs::Piece*>(a.agg + n_rg);
     a.piece_cap = (8 * p.cap - 16 * n_rg) / sizeof(ApplyArgs::Piece);
