@@ -218,8 +218,8 @@ struct ApplyArgs {
     uint64_t* scan_status;               // F2 look-back words (2 per block, zeroed per call)
     unsigned long long* scan_ticket;     // F2 block ticket (zeroed per call)
     uint32_t scan_blocks;                // F2 grid: blocks for the plan's capacity
-    uint32_t* range_e;                   // [ranges] F0 out: patch entry holding each range's first entry
-    bool checked;                        // the F0-F5 pipeline (F1s checks, F3 on listed pieces)
+    uint32_t* range_e;                   // [ranges] F1s out: patch entry holding each range's first entry
+    bool checked;                        // the F1s-F5 pipeline (F1s checks, F3 on listed pieces)
     struct Piece {                       // F1s out: one chunk of a non-plain range, for F3
         uint64_t c0, rg, ar, ac;         // first entry, range, in-range aggregate at c0
         uint32_t len, e;                 // entries, patch entry
@@ -373,7 +373,7 @@ f_pass(ApplyArgs A) {
             }
         }
         bool marker = false;
-        // the chunk's entry from F1s / F0 (new pipeline) instead of a binary search over the entries
+        // the chunk's entry from F1s (new pipeline) instead of a binary search over the entries
         uint32_t e = filter ? pc.e
                    : kPass != kAgg && A.checked ? A.range_e[rg] : upper_index<uint64_t>(A.es, 0, A.n_e, c_first);
         if (kPass == kAgg && lane == 0) A.range_e[rg] = e;
@@ -573,8 +573,8 @@ f_pass(ApplyArgs A) {
 //    current one decodes; the payload's byte alignment is removed on the
 //    shared-memory read (funnel shifts), not through registers;
 //  * per-lane running values in 32 bits where they fit (COO rows / columns);
-//  * each range's patch entry comes from F0 f_range_entries (two dependent
-//    loads per range instead of a binary search).
+//  * each range's patch entry: a warp search in F1s (two dependent loads for a
+//    few hundred entries), recorded for F3 / F5 (one load per range).
 //
 // Checks without the carry.  Inside a range that holds no patch-entry start or
 // end ("plain" range) every reference check but one is local or monotone:
@@ -652,15 +652,6 @@ __device__ __forceinline__ void load_sctx(SCtx& c, const ApplyArgs& A, uint32_t 
     c.flat_base = L.flat_base;
 }
 
-// F0: the patch entry holding each range's first entry.
-__global__ void f_range_entries(ApplyArgs A) {
-    if (fast_blocked(A.flags)) return;
-    const uint64_t n = A.totals[0];
-    const uint64_t n_ranges = (n + kRange - 1) / kRange;
-    for (uint64_t rg = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; rg < n_ranges;
-         rg += uint64_t(gridDim.x) * blockDim.x)
-        A.range_e[rg] = upper_index<uint64_t>(A.es, 0, A.n_e, rg * kRange);
-}
 
 // One staged fast chunk of f_stream: lane aggregates + warp scan, then either
 // the carry-free checks (F1s) or the decode + scatter (F5).  Branch-free per
@@ -857,11 +848,23 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
     const uint64_t gap_base = has_prev ? A.carry->gap_base : 0;
     const uint64_t stride = uint64_t(gridDim.x) * kWarps;
 
+    if (agg) {  // F2's look-back words start cleared (no memset node ahead of F2)
+        for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < 2ull * A.scan_blocks;
+             i += uint64_t(gridDim.x) * blockDim.x)
+            A.scan_status[i] = 0;
+    }
+    // F1s finds each range's patch entry (a warp search) and records it for F3 / F5
+    auto range_entry = [&](uint64_t r) -> uint32_t {
+        if (!agg) return A.range_e[r];
+        const uint32_t e = warp_upper_index(A.es, A.n_e, r * kRange);
+        if ((threadIdx.x & 31) == 0) A.range_e[r] = e;
+        return e;
+    };
     uint64_t rg = uint64_t(blockIdx.x) * kWarps + warp;
     if (rg >= n_ranges) return;
     uint64_t c0 = rg * kRange;
     SCtx cur;
-    load_sctx(cur, A, A.range_e[rg]);
+    load_sctx(cur, A, range_entry(rg));
     auto range_end = [&](uint64_t r) { return min(r * kRange + kRange, n); };
     // chunks end at the next kSChunk-aligned entry, the range end or the patch entry's
     // end: a chunk never straddles two entries, so only tensors >= 2^32 take the walker
@@ -923,7 +926,7 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
         if (has_nx) {
             if (rg_nx != rg) {
                 if (!agg) carry_nx = A.agg[rg_nx];
-                load_sctx(nx, A, A.range_e[rg_nx]);
+                load_sctx(nx, A, range_entry(rg_nx));
             } else if (c_nx >= cur.hi) {
                 uint32_t e = cur.e + 1;
                 while (A.es[e + 1] <= c_nx) ++e;
@@ -1139,13 +1142,13 @@ void launch_all(const ApplyArgs& a, bool scatter, cudaStream_t s) {
         }
         return;
     }
-    // F0 range entries -> F1s aggregates + carry-free checks -> F2 scan (+ deferred column
+    // F1s aggregates + carry-free checks + range entries -> F2 scan (+ deferred column
     // check) -> F3 exact checks where F1s could not decide (twice: the second only re-checks
     // everything if the first found a failure, to report the reference's first one) -> F5 scatter
-    f_range_entries<<<unsigned(sm_count() * 2), kThreads, 0, s>>>(a);
-    PULSE_LAUNCHED("f_range_entries", s);
-    launch_stream<kRepr, true>(a, s);
-    launch_range_scan(a, a.slack, s);
+    launch_stream<kRepr, true>(a, s);  // F1s (F0 folded in; it also clears F2's look-back words)
+    f_range_scan<<<a.scan_blocks, kScanThreads, 0, s>>>(a.totals, a.agg, a.flags, a.scan_status, a.scan_ticket,
+                                                        a.slack);
+    PULSE_LAUNCHED("f_range_scan", s);
     ApplyArgs v = a;
     v.vmode = 0;
     launch_pass<kRepr, kValidate>(v, s);

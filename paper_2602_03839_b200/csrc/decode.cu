@@ -97,6 +97,12 @@ d_layout(const pulse_patch_entry* __restrict__ entries, uint32_t n_e, const uint
          uint64_t* __restrict__ err, uint32_t* __restrict__ flags, uint64_t cap,
          const pulse_result* __restrict__ patch_result) {
     __shared__ uint64_t s_tmp[32];
+    // per-call state (totals and tickets, flags, first-error key), zeroed here rather
+    // than by three memset nodes ahead of this 1-CTA kernel
+    if (threadIdx.x < 16) totals[threadIdx.x] = 0;
+    if (threadIdx.x < 4) flags[threadIdx.x] = 0;
+    if (threadIdx.x == 0) *err = kNoError;
+    __syncthreads();
     // With `patch_result` (the encode's device result) the entry count comes from
     // the device and a failed encode applies nothing: entries past the count are
     // empty, and the encode's own first error becomes this call's error.
@@ -567,9 +573,6 @@ static unsigned persistent_grid() { return unsigned(sm_count() * 8); }
 
 static void decode_prologue(const PlanDev& p, const pulse_patch_entry* entries, uint32_t n_entries,
                             uint32_t repr, cudaStream_t s, const pulse_result* patch_result = nullptr) {
-    cudaMemsetAsync(p.d_totals, 0, 16 * sizeof(uint64_t), s);
-    cudaMemsetAsync(p.d_flags, 0, 4 * sizeof(uint32_t), s);
-    cudaMemsetAsync(p.err, 0xFF, sizeof(uint64_t), s);
     d_layout<<<1, kLT, 0, s>>>(entries, n_entries, p.numel, p.cols, repr, p.elay, p.d_es, p.d_ck,
                               p.d_totals, p.err, p.d_flags, p.cap, patch_result);
     PULSE_LAUNCHED("d_layout", s);

@@ -143,6 +143,21 @@ __device__ __forceinline__ uint32_t upper_index(const T* a, uint32_t lo, uint32_
     return lo;
 }
 
+// Largest i in [0, n) with a[i] <= x (a[0] <= x), by the whole warp: 32 probes
+// per round, so a few hundred segments take two dependent loads, not nine.
+__device__ __forceinline__ uint32_t warp_upper_index(const uint64_t* a, uint32_t n, uint64_t x) {
+    const int lane = threadIdx.x & 31;
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t p = lo + uint32_t(lane) * step;
+        const uint32_t m = __ballot_sync(0xffffffffu, p < hi && a[p] <= x);
+        lo += uint32_t(31 - __clz(m)) * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
+
 // ------------------------------------------------------------------------------------------
 // Scan operators over 62-bit payloads (status words keep 2 flag bits).
 // ------------------------------------------------------------------------------------------
