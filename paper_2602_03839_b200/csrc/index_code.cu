@@ -571,7 +571,9 @@ struct LayoutArgs {
     uint64_t* err;
     uint64_t cap;  // K1 capacity (mode A); ~0 for mode B
     const uint32_t* run_if;  // run only if *run_if != 0 (exact re-run after an optimistic pass)
-    bool optimistic;         // COO: lay out assuming no escapes (range_pre pre-zeroed)
+    bool optimistic;         // COO: lay out assuming no escapes (zeroes range_pre itself)
+    uint32_t* zero_u32[3];   // optimistic: per-call state this kernel clears first (t_resc, t_cesc, esc flag)
+    uint64_t n_range_pre;    //   and range_pre entries to clear
 };
 
 __device__ __forceinline__ int64_t entry_local(const EntryMap& em, uint64_t i) {
@@ -588,6 +590,18 @@ __global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
     const uint64_t n = em.seg_start[em.n_segs];
     const bool coo = a.repr == PULSE_COO_DOWNSCALED;
     const bool overflow = n > a.cap;
+    if (a.optimistic) {  // per-call state, cleared here instead of by memset nodes ahead of K2
+        for (uint32_t i = tid; i < a.n_tensors; i += kLayoutThreads) {
+            a.zero_u32[0][i] = 0;
+            a.zero_u32[1][i] = 0;
+        }
+        if (tid == 0) {
+            *a.zero_u32[2] = 0;
+            *a.err = kNoError;
+        }
+        for (uint64_t i = tid; i < a.n_range_pre; i += kLayoutThreads) a.range_pre[i] = make_ulonglong2(0, 0);
+        __syncthreads();
+    }
 
     // (1) COO_DOWNSCALED: exclusive scan of the per-range escape counts (each
     // thread sums a contiguous block, one CTA scan, then writes its block)
@@ -1011,9 +1025,12 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
                         const pulse_scan_summary* gathered, uint32_t n_ranks, uint32_t rank,
                         const uint16_t* vals, uint8_t* body, uint64_t body_cap, pulse_patch_entry* entries,
                         pulse_result* result, uint64_t cap, cudaStream_t s) {
-    cudaMemsetAsync(p.t_resc, 0, p.n_tensors * sizeof(uint32_t), s);
-    cudaMemsetAsync(p.t_cesc, 0, p.n_tensors * sizeof(uint32_t), s);
-    cudaMemsetAsync(p.err, 0xFF, sizeof(uint64_t), s);
+    const bool optimistic = repr == PULSE_COO_DOWNSCALED && !validate_args && !em.idx64;
+    if (!optimistic) {  // (the optimistic k2_layout clears these itself)
+        cudaMemsetAsync(p.t_resc, 0, p.n_tensors * sizeof(uint32_t), s);
+        cudaMemsetAsync(p.t_cesc, 0, p.n_tensors * sizeof(uint32_t), s);
+        cudaMemsetAsync(p.err, 0xFF, sizeof(uint64_t), s);
+    }
     static PerDeviceInt occ_scan_d, occ_emit_d;
     int& occ_scan = occ_scan_d.here();
     int& occ_emit = occ_emit_d.here();
@@ -1061,14 +1078,16 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
                                                                  run_if, nullptr);
         PULSE_LAUNCHED("k2_emit", s);
     };
-    if (repr == PULSE_COO_DOWNSCALED && !validate_args && !em.idx64) {
+    a.zero_u32[0] = p.t_resc;
+    a.zero_u32[1] = p.t_cesc;
+    a.zero_u32[2] = p.d_flags + 2;
+    a.n_range_pre = p.cap / kRangeEntries + 2;
+    if (optimistic) {
         // Optimistic COO_DOWNSCALED: lay out and emit assuming no entry needs an
         // escape (none does on these shapes at <= 99.9% sparsity); the emit flags
         // any escape it meets, and only then the exact pipeline re-runs (its three
         // kernels return at once otherwise).
         uint32_t* esc = p.d_flags + 2;
-        cudaMemsetAsync(esc, 0, sizeof(uint32_t), s);
-        cudaMemsetAsync(p.range_pre, 0, (p.cap / kRangeEntries + 2) * sizeof(ulonglong2), s);
         a.optimistic = true;
         k2_layout<<<1, kLayoutThreads, 0, s>>>(a);
         PULSE_LAUNCHED("k2_layout (optimistic)", s);
