@@ -966,8 +966,10 @@ static int k1_variant() {
 
 void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot, pulse_scan_summary* copy_out,
                         cudaStream_t s) {
-    // status words + ticket must start at zero each launch
-    cudaMemsetAsync(p.k1_status, 0, p.n_tiles * sizeof(uint64_t), s);
+    // status words + ticket must start at zero each launch (the TMA kernel's status words are
+    // per 65536-element ticket: 8x fewer than the 8192-element tiles of the other variants)
+    const bool tma_path = k1_variant() == 0 && p.tma_tiles > 0;
+    cudaMemsetAsync(p.k1_status, 0, (tma_path ? p.tma_tiles : p.n_tiles) * sizeof(uint64_t), s);
     cudaMemsetAsync(p.counters, 0, 8 * sizeof(uint64_t), s);
     static const int experiment = getenv("PULSE_K1_EXPERIMENT") ? atoi(getenv("PULSE_K1_EXPERIMENT")) : 0;
     K1Args k{p.trace, experiment, p.segs, p.tile_seg, p.n_segs, p.n_tiles, p.slot[prev_slot], p.slot[curr_slot], p.idx32, p.val16,
