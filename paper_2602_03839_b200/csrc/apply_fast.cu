@@ -1153,7 +1153,7 @@ void launch_all(const ApplyArgs& a, bool scatter, cudaStream_t s) {
     v.vmode = 0;
     launch_pass<kRepr, kValidate>(v, s);
     v.vmode = 1;
-    launch_pass<kRepr, kValidate>(v, s);
+    launch_gated_on_error(s, a.err, [&](cudaStream_t gs) { launch_pass<kRepr, kValidate>(v, gs); });
     if (scatter && a.weights) launch_stream<kRepr, false>(a, s);
     else if (scatter) launch_pass<kRepr, kScatter>(a, s);
 }

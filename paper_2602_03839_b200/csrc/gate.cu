@@ -13,8 +13,10 @@
 namespace pulse {
 namespace dev {
 
-__global__ void k_set_cond(cudaGraphConditionalHandle h, const uint32_t* __restrict__ flag) {
-    cudaGraphSetConditional(h, *(volatile const uint32_t*)flag != 0 ? 1u : 0u);
+__global__ void k_set_cond(cudaGraphConditionalHandle h, const uint32_t* __restrict__ flag,
+                           const uint64_t* __restrict__ key) {
+    const bool on = flag ? *(volatile const uint32_t*)flag != 0 : *(volatile const uint64_t*)key != kNoError;
+    cudaGraphSetConditional(h, on ? 1u : 0u);
 }
 
 namespace {
@@ -37,7 +39,8 @@ bool gating_enabled() {
 }
 }  // namespace
 
-void launch_gated(cudaStream_t s, const uint32_t* flag, const std::function<void(cudaStream_t)>& body) {
+static void gate(cudaStream_t s, const uint32_t* flag, const uint64_t* key,
+                 const std::function<void(cudaStream_t)>& body) {
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
     cudaGraph_t g = nullptr;
     const cudaGraphNode_t* deps = nullptr;
@@ -54,7 +57,7 @@ void launch_gated(cudaStream_t s, const uint32_t* flag, const std::function<void
         body(s);
         return;
     }
-    k_set_cond<<<1, 1, 0, s>>>(h, flag);
+    k_set_cond<<<1, 1, 0, s>>>(h, flag, key);
     PULSE_LAUNCHED("k_set_cond", s);
     cudaStreamGetCaptureInfo(s, &st, nullptr, &g, &deps, &nd);  // now: after k_set_cond
     cudaGraphNodeParams np{};
@@ -74,6 +77,14 @@ void launch_gated(cudaStream_t s, const uint32_t* flag, const std::function<void
     body(aux);
     cudaStreamEndCapture(aux, &inner);
     cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
+}
+
+void launch_gated(cudaStream_t s, const uint32_t* flag, const std::function<void(cudaStream_t)>& body) {
+    gate(s, flag, nullptr, body);
+}
+
+void launch_gated_on_error(cudaStream_t s, const uint64_t* err_key, const std::function<void(cudaStream_t)>& body) {
+    gate(s, nullptr, err_key, body);
 }
 
 }  // namespace dev

@@ -177,6 +177,8 @@ void debug_sync(const char* kernel, cudaStream_t s);
 // gate.cu: `body` (launches on the stream it is given) runs only if *flag != 0
 // when the stream gets there -- a conditional graph node under stream capture.
 void launch_gated(cudaStream_t s, const uint32_t* flag, const std::function<void(cudaStream_t)>& body);
+// ... only if a first-error key has been recorded (*err_key != kNoError).
+void launch_gated_on_error(cudaStream_t s, const uint64_t* err_key, const std::function<void(cudaStream_t)>& body);
 #define PULSE_LAUNCHED(name, stream) ::pulse::dev::debug_sync(name, stream)
 // helpers.cu (host-buffer API support)
 void launch_export_indices(const PlanDev& p, int64_t* out, cudaStream_t s);
