@@ -699,12 +699,10 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
         n += tp.values.size();
     }
     pulse_plan* plan = E.get_plan(geom, std::max<uint64_t>({n, body_len / 3 + 1, 1}));
-    RawVec<uint8_t> body(body_len);
-    pool().parallel_for(T, [&](size_t t) {
-        if (lens[t]) std::memcpy(body.data() + ents[t].idx_off, pl[t], lens[t]);
-    });
+    // each payload straight into its place in the device body (one pass through the staging)
     uint8_t* dbody = E.body.as<uint8_t>(body_len + 64);
-    E.stager.h2d(dbody, body.data(), body_len, E.stream);
+    for (uint32_t t = 0; t < T; ++t)
+        if (lens[t]) E.stager.h2d(dbody + ents[t].idx_off, pl[t], lens[t], E.stream);
     auto* dent = E.entries.as<pulse_patch_entry>(T);
     cuda_check(counted_copy(dent, ents.data(), T * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice, E.stream), "H2D");
     int64_t* dout = E.out64.as<int64_t>(n);
@@ -715,15 +713,15 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
         const std::string nm = r.err_tensor < T ? p->tensors[r.err_tensor].name : "?";
         raise(pulse_status(r.status), device_message(r, nm, nullptr));
     }
-    RawVec<int64_t> flat(n);
-    E.stager.d2h(flat.data(), dout, n * 8, E.stream);
-    std::vector<uint64_t> at(T + 1, 0);
-    for (uint32_t t = 0; t < T; ++t) at[t + 1] = at[t] + p->tensors[t].values.size();
-    pool().parallel_for(T, [&](size_t t) {
+    // each tensor's indices straight into its vector (no intermediate host copy)
+    uint64_t at = 0;
+    for (uint32_t t = 0; t < T; ++t) {
         auto& tp = p->tensors[t];
         tp.indices.resize(tp.values.size());
-        if (!tp.indices.empty()) std::memcpy(tp.indices.data(), flat.data() + at[t], tp.indices.size() * 8);
-    });
+        if (!tp.indices.empty()) E.stager.d2h(tp.indices.data(), dout + at, tp.indices.size() * 8, E.stream);
+        at += tp.values.size();
+    }
+    E.sync();
 }
 
 void validate_for_write(const pulse_patch* p) {  // patch_file.hpp:31-42
