@@ -435,17 +435,17 @@ def run_pulse(args):
         k1_gbs = k1_bytes / (scan_ms / 1e3) / 1e9
         # our launches per step: K1 (k1_tma, k1_finalize); K2 (COO: optimistic k2_layout + k2_emit, then
         # k2_scan_escapes / k2_layout / k2_emit that return at once unless an escape was seen; int32:
-        # k2_layout, k2_emit); FLAT carry [sharded FLAT only]; apply (d_layout, f_range_entries, f_stream agg,
-        # f_range_scan, f_pass validate x2, f_stream scatter, d_clear_status, general-path kernels that exit
-        # at once on the fast path [COO: d_rows, d_col_layout, d_cols, d_assemble; int32: d_fixed],
-        # d_scatter, d_finalize)
-        # (replayed graphs: the idle paths sit in conditional nodes -- one k_set_cond each instead)
+        # k2_layout, k2_emit); FLAT carry [sharded FLAT only]; apply (d_layout, f_stream agg, f_range_scan,
+        # f_pass validate, its full re-check (exits at once unless a check failed), f_stream scatter,
+        # d_clear_status, general-path kernels that exit at once on the fast path [COO: d_rows,
+        # d_col_layout, d_cols, d_assemble; int32: d_fixed], d_scatter, d_finalize).
+        # Replayed graphs: every idle path sits in a conditional node, one k_set_cond each instead.
         if used_graph:
             n_emit = 3 if args.repr == 0 else 2
-            n_apply = 9
+            n_apply = 8
         else:
             n_emit = 5 if args.repr == 0 else 2
-            n_apply = 14 if args.repr == 0 else 11
+            n_apply = 13 if args.repr == 0 else 10
         n_carry = 1 if (world > 1 and args.repr == 2) else 0
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
