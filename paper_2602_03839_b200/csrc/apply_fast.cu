@@ -6,36 +6,40 @@
 // tensor has its row gap at byte o, its column entry at byte count + 2o (or its
 // u32 gap at byte 4o) of the index payload (index_coding.hpp:104-127,
 // patch.hpp:120-156).  Decoding is then a pair of segmented prefix sums over
-// the entries, read straight from the body:
+// the entries, read straight from the body.  The pipeline (launch_all):
 //
-//   F1 f_agg<0>      per warp range of 4096 entries: segmented-sum aggregates
-//                    (rows: restart at each tensor; columns: restart at each new
-//                    row, index_coding.hpp:141-153); flags escape markers.
-//   F2 f_range_scan  one CTA: exclusive scan of the range aggregates.
-//   F3 f_pass<apply> recompute every (row, col) / index, apply the reference
-//                    checks (zero gap, column range, index range) and, for each
-//                    entry that passes, save W[flat] to a backup and write the
-//                    value -- an entry that fails is never written.
-//   F4 f_pass<restore> only if some check failed anywhere: recompute and put the
-//                    backed-up values back, so a bad patch never half-applies
-//                    (the reference validates on a copy, patch.hpp:311).
-//   (decode-only callers -- int64 indices out -- run validate, then scatter.)
+//   F1s f_stream<agg>  per warp range of 4096 entries: segmented-sum aggregates
+//                      (rows restart at each tensor; columns at each new row,
+//                      index_coding.hpp:141-153), escape markers, the range's
+//                      patch entry, and every reference check that needs no
+//                      carry (see "Checks without the carry" below); lists the
+//                      chunks of non-plain ranges for F3.
+//   F2 f_range_scan    exclusive scan of the range aggregates (decoupled
+//                      look-back over blocks) + F1s's deferred column check.
+//   F3 f_pass<validate> the exact reference checks on F1s's listed chunks (on
+//                      every range if anything looked wrong); a second pass,
+//                      behind a conditional graph node, re-checks everything
+//                      only if a check failed, so the reported error is the
+//                      reference's first failing entry.
+//   F5 f_stream<scatter> decode + write, only if nothing failed: a bad patch
+//                      never half-applies (the reference validates on a copy,
+//                      patch.hpp:311), and no backup of the old values is needed.
+//   (decode-only callers -- int64 indices out -- use f_pass<scatter> last.)
+//   PULSE_APPLY_MODE=1|2 selects the earlier pipelines (F1 f_pass<agg>, then a
+//   checked scatter with backup + restore, or exact validation of every range)
+//   for A/B measurements.
 //
-// Data movement.  A warp works on 1024-entry chunks.  It stages a chunk's row
-// bytes / column units / u32 gaps (and, for F4, its values) from the body into
-// its own shared memory with coalesced 16-byte loads, funnel-shifting the
-// arbitrary byte alignment of the payload away; each lane then decodes 32
-// CONSECUTIVE entries serially from shared memory (one warp segmented scan per
-// chunk, not per 32 entries).  Shared-memory vectors are XOR-swizzled so both
-// the staging stores and the per-lane 16-byte reads are bank-conflict free.
-// F4 transposes the decoded indices back to entry order through shared memory
-// so each warp store instruction covers 32 consecutive changes (a few sectors
-// for clustered updates) rather than 32 scattered ones.
+// Data movement.  f_stream stages the next chunk (rows / columns / u32 gaps /
+// values) with cp.async while the current one decodes, and removes the
+// payload's byte misalignment on the shared-memory read (funnel shifts); each
+// lane decodes 16 or 32 CONSECUTIVE entries serially (one warp segmented scan
+// per chunk).  F5 transposes the decoded indices back to entry order through
+// shared memory so each warp store instruction covers 32 consecutive changes
+// (a few sectors for clustered updates) rather than 32 scattered ones.  Chunks
+// never straddle two patch entries; only tensors with >= 2^32 elements take the
+// per-round walker path.
 //
-// A chunk that straddles two patch entries (at most one per changed tensor) or
-// a tensor with >= 2^32 elements takes the per-round walker path instead.
-//
-// If d_layout or F1 finds anything the fixed layout cannot express (escapes,
+// If d_layout or F1s finds anything the fixed layout cannot express (escapes,
 // short/long payloads, marker bytes), `flags[0]` routes the patch to the
 // general parser in decode.cu instead; every kernel checks it on entry.
 #include <cstdlib>
