@@ -723,21 +723,22 @@ __device__ __forceinline__ void chunk_body(const ApplyArgs& A, const SCtx& cur, 
 #pragma unroll
             for (int w = 0; w < kBW; ++w) mk |= ((~bw[w] - 0x00010001u) & bw[w] & 0x80008000u) != 0;  // 0xFFFF
         }
-        uint32_t c = 0;
-        const uint32_t cols = uint32_t(cur.cols);
+        uint32_t c = 0, cmax = 0;
+        bool zero = false;
 #pragma unroll
         for (int j = 0; j < kPer; ++j) {
             const uint32_t a = PULSE_SA(j), bv = PULSE_SB(j);
             const bool nr = a != 0 || (j == 0 && lane_first);
             if (j == 0) head0 = nr;
             if (kAgg_) {
-                bad |= !nr && bv == 0 && (kFull || j < nv);  // zero column gap within a row
-                P += (hc || nr) ? 0u : bv;
+                zero |= !nr && bv == 0 && (kFull || j < nv);  // zero column gap within a row
+                if (nr && !hc) P = c;  // the lane's first row start: P = the column sum before it
             }
             c = nr ? bv : c + bv;
             hc |= nr;
-            if (kAgg_) bad |= hc && c >= cols;  // rows that start in this lane: columns known
+            if (kAgg_ && hc) cmax = max(cmax, c);  // rows that start in this lane: columns known
         }
+        if (kAgg_) bad |= zero || cmax >= uint32_t(cur.cols);
         lr = uint64_t(rs) | (lane_first ? H : 0);
         lc = uint64_t(c) | (hc ? H : 0);
     } else {
