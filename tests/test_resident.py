@@ -140,3 +140,23 @@ def test_publish_requires_consecutive_steps(golden):
         pub.publish(cur_d, 3)
     assert ei.value.kind == "ArgumentError"
     assert pub.step == 0 and same(pub.download(), mirror(prev))
+
+
+@pytest.mark.skipif(not have_reference(), reason="oracle/_ref not built")
+def test_walk_stops_on_hash_mismatch_and_keeps_the_last_good_step():
+    """A walk with verification over a chain whose third delta carries a tampered
+    value (identity codec): steps 1-2 apply, step 3 fails with HashMismatchError,
+    and the held weights, step and hash are exactly those of step 2."""
+    R = reference()
+    base, _ = R.generate_synthetic([(48, 32), (700,)], 0.96, 8, 5)
+    chain = [base]
+    for k in range(4):
+        chain.append(R.mutate(chain[-1], 0.97, 8, 300 + k, k + 1))
+    wires = [bytearray(R.write_patch_bytes(R.encode(chain[k + 1], chain[k], 0, IDENTITY))) for k in range(4)]
+    wires[2][-1] ^= 0x01  # last value byte of the third delta
+    r = H.Resident(mirror(chain[0]))
+    with pytest.raises(PulseError) as ei:
+        r.walk([bytes(w) for w in wires], verify=True)
+    assert ei.value.kind == "HashMismatchError"
+    assert r.last_walk_applied == 2 and r.step == 2
+    assert r.weights_hash == R.hash_weights(chain[2]) and same(r.download(), mirror(chain[2]))
