@@ -101,6 +101,20 @@ struct pulse_patch {
     Coded coded;
     bool coded_valid = false;
     uint32_t coded_repr = 0;
+    // read_patch_bytes decodes the indices on the device; they stay there (tensor order, flat)
+    // so decode() need not upload them again.  Any change to the tensors drops them.
+    int64_t* dev_idx = nullptr;
+    int dev_idx_device = -1;
+    uint64_t dev_idx_n = 0;
+    bool dev_idx_valid = false;
+    ~pulse_patch() {
+        if (!dev_idx) return;
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev_idx_device);
+        cudaFree(dev_idx);
+        cudaSetDevice(prev);
+    }
 };
 
 struct pulse_sha256_ctx {
@@ -705,7 +719,22 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
         if (lens[t]) E.stager.h2d(dbody + ents[t].idx_off, pl[t], lens[t], E.stream);
     auto* dent = E.entries.as<pulse_patch_entry>(T);
     cuda_check(counted_copy(dent, ents.data(), T * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice, E.stream), "H2D");
-    int64_t* dout = E.out64.as<int64_t>(n);
+    p->dev_idx_valid = false;
+    if (p->dev_idx && (p->dev_idx_n < n || p->dev_idx_device != E.device)) {
+        E.sync();
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(p->dev_idx_device);
+        cudaFree(p->dev_idx);
+        cudaSetDevice(prev);
+        p->dev_idx = nullptr;
+    }
+    if (!p->dev_idx) {
+        cuda_check(cudaMalloc(&p->dev_idx, std::max<uint64_t>(n, 1) * 8), "patch indices");
+        p->dev_idx_n = std::max<uint64_t>(n, 1);
+        p->dev_idx_device = E.device;
+    }
+    int64_t* dout = p->dev_idx;
     auto* dres = E.result.as<pulse_result>(1);
     launch_decode(plan->dev, p->representation, dbody, dent, T, nullptr, -1, dout, dres, E.stream);
     const pulse_result r = fetch_result(E, dres);
@@ -722,6 +751,7 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
         at += tp.values.size();
     }
     E.sync();
+    p->dev_idx_valid = true;
 }
 
 void validate_for_write(const pulse_patch* p) {  // patch_file.hpp:31-42
@@ -1010,6 +1040,7 @@ pulse_status pulse_patch_add_tensor(pulse_patch* p, const pulse_tensor_patch* v)
     t.values.assign(v->values, v->values + v->n_values);
     p->tensors.push_back(std::move(t));
     p->coded_valid = false;
+    p->dev_idx_valid = false;
     return PULSE_OK;
 }
 
@@ -1221,13 +1252,17 @@ pulse_status pulse_decode(const pulse_checkpoint* previous, const pulse_patch* p
                 }
                 // each tensor's indices / values straight into their place on the device
                 // (one pass through the pinned staging, no host-side gather copy)
-                didx = E.idx64.as<int64_t>(n);
+                // indices a read_patch_bytes left on this device (same tensors, same order) are
+                // used in place; otherwise uploaded
+                const bool resident = patch->dev_idx_valid && patch->dev_idx_device == E.device &&
+                                      patch->dev_idx_n >= n;
+                didx = resident ? patch->dev_idx : E.idx64.as<int64_t>(n);
                 dval = E.vals.as<uint16_t>(n);
                 for (uint32_t k = 0; k < stop; ++k) {
                     const auto& tp = patch->tensors[k];
                     const size_t m = tp.indices.size();
                     if (!m) continue;
-                    E.stager.h2d(didx + at[k], tp.indices.data(), m * 8, E.stream);
+                    if (!resident) E.stager.h2d(didx + at[k], tp.indices.data(), m * 8, E.stream);
                     E.stager.h2d(dval + at[k], tp.values.data(), m * 2, E.stream);
                 }
                 dent = E.entries.as<pulse_patch_entry>(stop);
