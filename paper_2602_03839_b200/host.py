@@ -8,6 +8,7 @@ Checkpoints are lists of (name, shape, uint16 ndarray of bf16 bit patterns).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -182,18 +183,19 @@ def write_patch_bytes(patch) -> bytes:
 
 
 def write_patch_array(patch) -> np.ndarray:
-    """write_patch_bytes into a uint8 ndarray (the reference's Bytes is a byte
-    vector): one memcpy into a fresh array, which NumPy backs with huge pages --
-    cheaper than building a 100s-of-MB bytes object."""
+    """write_patch_bytes as a uint8 ndarray (the reference's Bytes is a byte
+    vector) viewing the library's buffer directly -- no copy of the 100s of MB;
+    the buffer is freed when the array (and any view of it) is."""
     h = patch if isinstance(patch, PatchHandle) else PatchHandle.from_patch(patch)
     b = C.c_void_p()
     N.check(N.lib.pulse_write_patch_bytes(h.ptr, C.byref(b)))
     n = N.lib.pulse_bytes_size(b)
-    out = np.empty(n, np.uint8)
-    if n:
-        C.memmove(out.ctypes.data, N.lib.pulse_bytes_data(b), n)
-    N.lib.pulse_bytes_free(b)
-    return out
+    if not n:
+        N.lib.pulse_bytes_free(b)
+        return np.empty(0, np.uint8)
+    raw = (C.c_uint8 * n).from_address(N.lib.pulse_bytes_data(b))
+    weakref.finalize(raw, N.lib.pulse_bytes_free, b)
+    return np.frombuffer(raw, np.uint8)
 
 
 def read_patch_handle(data) -> PatchHandle:
