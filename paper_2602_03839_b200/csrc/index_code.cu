@@ -750,10 +750,14 @@ __global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
 // K2b: emit
 // =============================================================================================
 // Per-round walker path of K2b over entries [first, last); (R, Cc): global row /
-// column escapes before `first` (COO_DOWNSCALED), advanced in place.
-__device__ __noinline__ void k2b_span(const EntryMap& em, uint32_t repr, uint64_t n, uint64_t first, uint64_t last,
-                                      const TensorLayout* __restrict__ tlay, const uint16_t* __restrict__ vals,
-                                      uint8_t* __restrict__ body, uint64_t& R, uint64_t& Cc) {
+// column escapes before `first` (COO_DOWNSCALED), returned advanced.  Everything
+// by value, not by reference: an address-taken R/Cc/EntryMap lived in local
+// memory across K2b's whole chunk loop (its reloads were the top long-scoreboard
+// stalls in the r1f ncu capture; k2_emit's LDL/STL count 294 -> 53).
+__device__ __noinline__ ulonglong2 k2b_span(const EntryMap em, uint32_t repr, uint64_t n, uint64_t first,
+                                            uint64_t last, const TensorLayout* __restrict__ tlay,
+                                            const uint16_t* __restrict__ vals, uint8_t* __restrict__ body, uint64_t R,
+                                            uint64_t Cc) {
     const int lane = threadIdx.x & 31;
     const bool coo = repr == PULSE_COO_DOWNSCALED;
     Walker w(em, n, first, last);
@@ -857,6 +861,7 @@ __device__ __noinline__ void k2b_span(const EntryMap& em, uint32_t repr, uint64_
       }
       w.rotate();
     }
+    return make_ulonglong2(R, Cc);
 }
 
 // One staged fast chunk of K2b: COO_DOWNSCALED row/column entries or int32 gaps,
@@ -1008,7 +1013,9 @@ k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
         }
         if (!done) {  // segment boundary, caller int64 indices, or escapes: per-round walker
             cp_async_wait<1>();  // this chunk's staging lands before its buffer is reused
-            k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
+            const ulonglong2 rc = k2b_span(em, repr, n, c0, c0 + len, tlay, vals, body, R, Cc);
+            R = rc.x;
+            Cc = rc.y;
             __syncwarp();
         }
         if (esc_flag && (R | Cc) && lane == 0) atomicExch(esc_flag, 1u);  // optimistic pass: escapes seen
