@@ -235,10 +235,18 @@ struct ApplyArgs {
 };
 
 // Walker path over entries [first, last) for one pass.  (ar, ac): aggregates
-// (kAgg) or running values (validate / scatter); updated in place.
+// (kAgg) or running values (validate / scatter); returned advanced with the
+// marker flag.  Everything by value, not by reference: an address-taken
+// ApplyArgs / ar / ac / marker would live in local memory across the caller's
+// whole streaming loop (the same fix took K2 emit's LDL/STL count 294 -> 53).
+struct SpanState {
+    uint64_t ar, ac;
+    bool marker;
+};
+
 template <int kRepr, int kPass>
-__device__ __noinline__ void slow_span(const ApplyArgs& A, uint64_t first, uint64_t last, uint64_t& ar, uint64_t& ac,
-                                       bool& marker, bool has_prev, uint64_t gap_base) {
+__device__ __noinline__ SpanState slow_span(const ApplyArgs A, uint64_t first, uint64_t last, uint64_t ar,
+                                            uint64_t ac, bool marker, bool has_prev, uint64_t gap_base) {
     constexpr bool coo = kRepr == kCoo;
     EWalker w(A.el, A.es, A.n_e, first, last);
     while (w.base < w.end) {
@@ -315,6 +323,7 @@ __device__ __noinline__ void slow_span(const ApplyArgs& A, uint64_t first, uint6
             A.weights[f.tensor][flat] = A.backup[i];
         }
     }
+    return SpanState{ar, ac, marker};
 }
 
 }  // namespace
@@ -390,7 +399,10 @@ f_pass(ApplyArgs A) {
             const uint32_t len = uint32_t(c_end - c0);
             const EntryLayout L = A.el[e];
             if (L.numel >= (1ull << 32)) {
-                slow_span<kRepr, kPass>(A, c0, c0 + len, ar, ac, marker, has_prev, gap_base);
+                const SpanState st = slow_span<kRepr, kPass>(A, c0, c0 + len, ar, ac, marker, has_prev, gap_base);
+                ar = st.ar;
+                ac = st.ac;
+                marker = st.marker;
                 continue;
             }
             const uint64_t o0 = c0 - lo;
@@ -951,7 +963,11 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
         }
         if (!is_fast(cur, c0, len)) {
             // straddles patch entries or a tensor >= 2^32 elements: per-round walker (never plain)
-            slow_span<kRepr, agg ? kAgg : kScatter>(A, c0, c0 + len, ar, ac, marker, has_prev, gap_base);
+            const SpanState st =
+                slow_span<kRepr, agg ? kAgg : kScatter>(A, c0, c0 + len, ar, ac, marker, has_prev, gap_base);
+            ar = st.ar;
+            ac = st.ac;
+            marker = st.marker;
             prefetch(has_nx, nx, c_nx, len_nx, b ^ 1, sh_nx);
         } else {
             prefetch(has_nx, nx, c_nx, len_nx, b ^ 1, sh_nx);
