@@ -338,10 +338,11 @@ __device__ __forceinline__ void st_u32_any(uint8_t* p, uint32_t v) {
     }
 }
 
-// Per-round walker path of K2a over entries [first, last).
-__device__ __noinline__ void k2a_span(const EntryMap& em, uint32_t repr, uint64_t n, uint64_t first, uint64_t last,
-                                      uint32_t* __restrict__ t_resc, uint32_t* __restrict__ t_cesc,
-                                      uint64_t* __restrict__ err, uint32_t& re, uint32_t& ce) {
+// Per-round walker path of K2a over entries [first, last); (re, ce) returned
+// advanced (by value, like k2b_span: no address-taken state in the caller's loop).
+__device__ __noinline__ uint2 k2a_span(const EntryMap em, uint32_t repr, uint64_t n, uint64_t first, uint64_t last,
+                                       uint32_t* __restrict__ t_resc, uint32_t* __restrict__ t_cesc,
+                                       uint64_t* __restrict__ err, uint32_t re, uint32_t ce) {
     const bool coo = repr == PULSE_COO_DOWNSCALED;
     const int lane = threadIdx.x & 31;
     Walker w(em, n, first, last);
@@ -420,6 +421,7 @@ __device__ __noinline__ void k2a_span(const EntryMap& em, uint32_t repr, uint64_
       }
       w.rotate();
     }
+    return make_uint2(re, ce);
 }
 
 // =============================================================================================
@@ -454,7 +456,9 @@ k2_scan_escapes(EntryMap em, uint32_t repr, uint64_t* __restrict__ range_cnt, ui
         const uint32_t len = cur.len;
         const FastCtx c = fast_ctx(em, c0, len, sg);
         if (!staged || !c.fast) {
-            k2a_span(em, repr, n, c0, c0 + len, t_resc, t_cesc, err, re, ce);
+            const uint2 rc = k2a_span(em, repr, n, c0, c0 + len, t_resc, t_cesc, err, re, ce);
+            re = rc.x;
+            ce = rc.y;
         } else {
             const uint4* sidx = bufs + b * (kSIdx / 16);
             cp_async_wait<1>();
