@@ -406,7 +406,9 @@ typedef struct pulse_resident pulse_resident;
 pulse_status pulse_resident_create(const pulse_checkpoint* checkpoint, uint64_t max_changes, pulse_resident** out);
 /* The same from a checkpoint already in HBM: `checkpoint` gives names, shapes
  * and step, its `data` pointers are device pointers of the current device
- * (copied device to device; the hash is taken from HBM). */
+ * (copied device to device; the hash is taken from HBM).  The call first waits
+ * for all work already queued on the device (cudaDeviceSynchronize), so writes
+ * to those buffers pending on any caller stream complete before they are read. */
 pulse_status pulse_resident_create_device(const pulse_checkpoint* checkpoint, uint64_t max_changes,
                                           pulse_resident** out);
 void pulse_resident_destroy(pulse_resident* r);
@@ -440,7 +442,10 @@ pulse_status pulse_resident_walk(pulse_resident* r, const uint8_t* const* pulps,
  * come straight from the device body (codec on host threads) with
  * anchor_step as given; the target hash (sha256 of dev_current, computed
  * once) goes to out_hash32.  advance != 0 then applies the patch to the held
- * weights, so the resident becomes the new last-published snapshot. */
+ * weights, so the resident becomes the new last-published snapshot.  Like
+ * create_device, it waits for all queued device work before reading
+ * `dev_current`, so a snapshot still being written on another stream is
+ * never encoded or hashed half-updated. */
 pulse_status pulse_resident_publish(pulse_resident* r, const void* const* dev_current, uint64_t step,
                                     uint32_t representation, uint32_t codec, uint64_t anchor_step, int advance,
                                     pulse_bytes** out_pulp, uint8_t* out_hash32);

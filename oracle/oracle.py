@@ -151,7 +151,7 @@ class Reference:
     # -- plumbing -----------------------------------------------------------------------
     def _check(self, rc: int):
         if rc != 0:
-            raise OracleError(rc, self.L.ref_last_error().decode())
+            raise OracleError(rc, self.L.ref_last_error().decode(errors="replace"))
 
     def _take_buf(self, h) -> bytes:
         n = self.L.ref_buf_size(h)
@@ -260,6 +260,35 @@ class Reference:
             self.L.ref_ckpt_free(hc)
             self.L.ref_ckpt_free(hp)
         return self.patch_from_handle(out.value)
+
+    def encode_pulps(self, cur: Checkpoint, prev: Checkpoint, reprs=(COO_DOWNSCALED, COO_INT32, FLAT_INT32),
+                     codec=IDENTITY):
+        """{representation: write_patch_bytes(encode(cur, prev, repr, codec))}: one
+        reference encode (the patch's indices and values do not depend on the
+        representation, patch.hpp:296-301), then the representation field is
+        switched on the same patch object before each write."""
+        hc, hp = self.ckpt_handle(cur), self.ckpt_handle(prev)
+        out = C.c_void_p()
+        try:
+            self._check(self.L.ref_encode(hc, hp, reprs[0], codec, C.byref(out)))
+        finally:
+            self.L.ref_ckpt_free(hc)
+            self.L.ref_ckpt_free(hp)
+        h = out.value
+        try:
+            steps = (C.c_int64 * 3)()
+            r_, c_ = C.c_uint32(), C.c_uint32()
+            hb = C.create_string_buffer(32)
+            self.L.ref_patch_header(h, steps, C.byref(r_), C.byref(c_), hb)
+            wires = {}
+            for r in reprs:
+                self.L.ref_patch_set_header(h, steps, r, codec, hb.raw)
+                buf = C.c_void_p()
+                self._check(self.L.ref_write_patch_bytes(h, C.byref(buf)))
+                wires[r] = self._take_buf(buf.value)
+            return wires
+        finally:
+            self.L.ref_patch_free(h)
 
     def decode(self, prev: Checkpoint, patch: Patch, verify=True) -> Checkpoint:
         hp, hq = self.ckpt_handle(prev), self.patch_handle(patch)

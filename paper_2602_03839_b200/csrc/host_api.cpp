@@ -30,6 +30,7 @@
 #include <string>
 #include <thread>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "errors.hpp"
@@ -501,6 +502,23 @@ pulse_result fetch_result(Engine& E, const void* dev_result) {
     return r;
 }
 
+// Boundaries [0 = b0 < b1 < ... = n] of the runs of consecutive patch entries in which
+// no target tensor repeats (greedy, in patch order).  One run (two boundaries) when
+// the patch names every tensor at most once.
+std::vector<uint32_t> distinct_target_runs(const uint32_t* target, uint32_t n) {
+    std::vector<uint32_t> b{0};
+    std::unordered_set<uint32_t> seen;
+    for (uint32_t k = 0; k < n; ++k) {
+        if (!seen.insert(target[k]).second) {
+            b.push_back(k);
+            seen.clear();
+            seen.insert(target[k]);
+        }
+    }
+    b.push_back(n);
+    return b;
+}
+
 // Exception text for a device-detected failure, in the reference's words.
 std::string device_message(const pulse_result& r, const std::string& name, const RawVec<int64_t>* idx) {
     switch (r.err_check) {
@@ -663,7 +681,8 @@ Coded device_index_code(Engine& E, const pulse_patch* p, bool with_values) {
     E.stager.h2d(dval, flat_val.data(), n * 2, E.stream);
     cuda_check(counted_copy(d.id_start, start.data(), (T + 1) * 8, cudaMemcpyHostToDevice, E.stream), "H2D");
     tm.lap("h2d");
-    const uint64_t cap = 10 * n + 64;
+    // worst case per entry: COO_DOWNSCALED with both escapes, 5 + 6 index bytes + 2 value bytes
+    const uint64_t cap = 13 * n + 64;
     uint8_t* dbody = E.body.as<uint8_t>(cap);
     auto* dent = E.entries.as<pulse_patch_entry>(T);
     auto* dres = E.result.as<pulse_result>(1);
@@ -876,6 +895,7 @@ ParsedPulp parse_pulp(const uint8_t* bytes, uint64_t n) {
     // error must still win, as in the reference's one-tensor-at-a-time read.
     struct Blob {
         uint64_t count, ipos, inb, vpos, vnb;
+        bool vtrunc;  // value blob runs past the end: raised after this tensor's index blob decompresses
     };
     std::vector<Blob> blobs;
     pulse_status stop_st = PULSE_OK;
@@ -924,7 +944,14 @@ ParsedPulp parse_pulp(const uint8_t* bytes, uint64_t n) {
             if (b.inb > n - pos) raise(PULSE_E_TRUNCATION, "index blob truncated");
             b.ipos = pos;
             pos += b.inb;
-            if (b.vnb > n - pos) raise(PULSE_E_TRUNCATION, "value blob truncated");
+            if (b.vnb > n - pos) {
+                // patch_file.hpp:129-131: the reference decompresses this tensor's index
+                // blob before it finds the value blob short, so a codec error there wins
+                b.vtrunc = true;
+                blobs.push_back(b);
+                p->tensors.push_back(std::move(tp));
+                raise(PULSE_E_TRUNCATION, "value blob truncated");
+            }
             b.vpos = pos;
             pos += b.vnb;
             blobs.push_back(b);
@@ -956,6 +983,7 @@ ParsedPulp parse_pulp(const uint8_t* bytes, uint64_t n) {
             if (p->codec == PULSE_IDENTITY) {
                 pl[t] = bytes + b.ipos;
                 lens[t] = b.inb;
+                if (b.vtrunc) raise(PULSE_E_TRUNCATION, "value blob truncated");
                 if (b.vnb != b.count * 2)
                     raise(PULSE_E_FORMAT, "value payload length does not match change count for tensor " + tp.name);
                 tp.values.resize(b.count);
@@ -964,6 +992,7 @@ ParsedPulp parse_pulp(const uint8_t* bytes, uint64_t n) {
                 payloads[t] = codec_decompress(bytes + b.ipos, b.inb, p->codec);
                 pl[t] = payloads[t].data();
                 lens[t] = payloads[t].size();
+                if (b.vtrunc) raise(PULSE_E_TRUNCATION, "value blob truncated");
                 const auto vp = codec_decompress(bytes + b.vpos, b.vnb, p->codec);
                 if (vp.size() != b.count * 2)
                     raise(PULSE_E_FORMAT, "value payload length does not match change count for tensor " + tp.name);
@@ -1230,7 +1259,12 @@ pulse_status pulse_decode(const pulse_checkpoint* previous, const pulse_patch* p
             // Page-locked base and output buffers and no host-side error: validate the
             // whole patch first, then run upload | scatter | download as a pipeline
             // over groups of tensors, so both copy engines work at once.
-            bool pipelined = stop == P && host_err.st == PULSE_OK;
+            // Duplicate tensor names (read_patch_bytes accepts them, patch_file.hpp:114-139):
+            // the reference applies tensors one after another, so the last entry for a
+            // tensor wins (patch.hpp:313-339).  Such patches validate as a whole, then
+            // scatter in runs with no tensor twice, in patch order.
+            const auto runs = distinct_target_runs(target.data(), stop);
+            bool pipelined = stop == P && host_err.st == PULSE_OK && runs.size() <= 2;
             for (uint32_t i = 0; i < T && pipelined; ++i)
                 if (numel[i] && !(is_pinned(previous->tensors[i].data) && is_pinned(out_data[i]))) pipelined = false;
             if (!pipelined)
@@ -1269,13 +1303,20 @@ pulse_status pulse_decode(const pulse_checkpoint* previous, const pulse_patch* p
                 cuda_check(counted_copy(dent, ents.data(), stop * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice,
                                            E.stream), "H2D");
                 auto* dres = E.result.as<pulse_result>(1);
-                // sequential: validate + scatter in one go; pipelined: validate only here
-                launch_apply_idx64(plan->dev, didx, dval, dent, stop, pipelined ? -1 : 2, dres, E.stream);
+                // sequential: validate + scatter in one go; pipelined or in runs: validate only here
+                const bool whole = !pipelined && runs.size() <= 2;
+                launch_apply_idx64(plan->dev, didx, dval, dent, stop, whole ? 2 : -1, dres, E.stream);
                 const pulse_result r = fetch_result(E, dres);
                 if (r.status != PULSE_OK) {
                     const auto& tp = patch->tensors[r.err_tensor];
                     raise(pulse_status(r.status), device_message(r, tp.name, &tp.indices));
                 }
+                if (!pipelined && !whole)
+                    for (size_t q = 0; q + 1 < runs.size(); ++q) {
+                        const uint32_t k0 = runs[q], k1 = runs[q + 1];
+                        launch_apply_idx64(plan->dev, didx + at[k0], dval + at[k0], dent + k0, k1 - k0, 2, dres,
+                                           E.stream);
+                    }
             }
             tm.lap(pipelined ? "gather+upload+validate" : "upload+gather+apply");
             if (host_err.st != PULSE_OK) raise(host_err.st, host_err.msg);
@@ -1668,7 +1709,8 @@ pulse_status pulse_downscale_coo(const int64_t* rows, uint64_t n_rows, const int
             Engine& E = engine();
             std::lock_guard<std::mutex> lk(E.mu);
             int64_t* d = E.idx64.as<int64_t>(2 * n_rows);
-            uint8_t* dout = E.body.as<uint8_t>(10 * n_rows + 16);
+            // up to 11 bytes per entry: 0xFF + u32 row escape and 0xFFFF + u32 column escape
+            uint8_t* dout = E.body.as<uint8_t>(11 * n_rows + 16);
             uint64_t* misc = E.misc.as<uint64_t>(2);
             cuda_check(cudaMemsetAsync(misc, 0xFF, 8, E.stream), "memset");
             E.stager.h2d(d, rows, n_rows * 8, E.stream);
@@ -1932,7 +1974,7 @@ struct pulse_resident {
     std::unordered_map<std::string, uint32_t> by_name;
     void* arena = nullptr;                    // resident weights; tensor i at element off[i]
     std::vector<uint64_t> off;
-    DevBuf body, entries, result, idx64, backup, start;
+    DevBuf body, entries, result, idx64, backup, start, vals;
     void* pinned[2] = {nullptr, nullptr};     // hash pipeline (D2H | SHA-256)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaStream_t hstream = nullptr;
@@ -1944,7 +1986,7 @@ struct pulse_resident {
             if (ev[i]) cudaEventDestroy(ev[i]);
         }
         if (hstream) cudaStreamDestroy(hstream);
-        for (DevBuf* b : {&body, &entries, &result, &idx64, &backup, &start})
+        for (DevBuf* b : {&body, &entries, &result, &idx64, &backup, &start, &vals})
             if (b->p) cudaFree(b->p);
     }
     uint16_t* tensor(uint32_t i) const { return static_cast<uint16_t*>(arena) + off[i]; }
@@ -2034,25 +2076,42 @@ void resident_plan(pulse_resident* r, Engine& E, uint64_t cap) {
 void resident_apply_parsed(pulse_resident* r, Engine& E, ParsedPulp& pp, uint64_t step, const uint8_t* expected,
                            bool verify) {
     const pulse_patch* p = pp.p.get();
+    // apply_delta's order: read_patch_bytes (which decodes every index payload against
+    // the patch's own shapes) -> the step / hash protocol checks -> decode's tensor
+    // checks (patch.hpp:314-324).  The payloads are decoded on the device during the
+    // apply below, so when a host-side check is about to fail, the payloads are
+    // decoded first and their error, if any, wins.
+    Failure host_err{PULSE_OK, ""};
     if (p->base_step != int64_t(r->step))
-        raise(PULSE_E_PROTOCOL, "delta at step " + std::to_string(step) + " does not base on the held step");
-    if (p->target_step != int64_t(step)) raise(PULSE_E_PROTOCOL, "patch steps disagree with the manifest");
-    if (expected && std::memcmp(p->target_hash, expected, 32) != 0)
-        raise(PULSE_E_PROTOCOL, "patch target hash disagrees with the manifest");
+        host_err = {PULSE_E_PROTOCOL, "delta at step " + std::to_string(step) + " does not base on the held step"};
+    else if (p->target_step != int64_t(step))
+        host_err = {PULSE_E_PROTOCOL, "patch steps disagree with the manifest"};
+    else if (expected && std::memcmp(p->target_hash, expected, 32) != 0)
+        host_err = {PULSE_E_PROTOCOL, "patch target hash disagrees with the manifest"};
     const uint32_t P = uint32_t(p->tensors.size());
-    // decode's tensor checks (patch.hpp:314-324), in patch order
     std::vector<pulse_patch_entry> ents(P);
+    std::vector<uint32_t> target(P);
     uint64_t body_len = 0, n = 0;
-    for (uint32_t k = 0; k < P; ++k) {
+    for (uint32_t k = 0; k < P && host_err.st == PULSE_OK; ++k) {
         const auto& tp = p->tensors[k];
         const auto it = r->by_name.find(tp.name);
-        if (it == r->by_name.end()) raise(PULSE_E_TENSOR_SET, "patch references unknown tensor '" + tp.name + "'");
-        if (tp.shape != r->shapes[it->second])
-            raise(PULSE_E_SHAPE_MISMATCH, "tensor '" + tp.name + "' shape differs between patch and checkpoint");
+        if (it == r->by_name.end()) {
+            host_err = {PULSE_E_TENSOR_SET, "patch references unknown tensor '" + tp.name + "'"};
+            break;
+        }
+        if (tp.shape != r->shapes[it->second]) {
+            host_err = {PULSE_E_SHAPE_MISMATCH, "tensor '" + tp.name + "' shape differs between patch and checkpoint"};
+            break;
+        }
         const uint64_t cnt = tp.values.size();
-        ents[k] = pulse_patch_entry{r->plan_of[it->second], 0, cnt, body_len, pp.lens[k], body_len + pp.lens[k]};
+        target[k] = r->plan_of[it->second];
+        ents[k] = pulse_patch_entry{target[k], 0, cnt, body_len, pp.lens[k], body_len + pp.lens[k]};
         body_len += pp.lens[k] + 2 * cnt;
         n += cnt;
+    }
+    if (host_err.st != PULSE_OK) {
+        device_decode_payloads(E, pp.p.get(), pp.pl, pp.lens);  // raises a payload error first
+        raise(host_err.st, host_err.msg);
     }
     if (P == 0) {
         r->step = step;
@@ -2081,21 +2140,42 @@ void resident_apply_parsed(pulse_resident* r, Engine& E, ParsedPulp& pp, uint64_
     int64_t* didx = nullptr;
     uint16_t* dbak = nullptr;
     uint64_t* dstart = nullptr;
-    if (verify) {  // keep what the scatter overwrites: indices, then the old values
+    // duplicate tensor names: decode (validates everything), then scatter the decoded
+    // indices run by run in patch order so the last entry for a tensor wins (patch.hpp:313-339)
+    const auto runs = distinct_target_runs(target.data(), P);
+    const bool in_runs = runs.size() > 2;
+    std::vector<uint64_t> at(P + 1, 0);
+    for (uint32_t k = 0; k < P; ++k) at[k + 1] = at[k] + ents[k].count;
+    uint16_t* dvals = nullptr;
+    if (verify || in_runs) {  // indices (and, for verify, the values the scatter overwrites)
         didx = r->idx64.as<int64_t>(n);
         if (pulse_decode_indices(r->plan, p->representation, dbody, dent, P, nullptr, didx, dres, E.stream) != PULSE_OK)
             raise(PULSE_E_CUDA, pulse_last_error());
         fail_on(fetch_result(E, dres));
-        std::vector<uint64_t> st(P + 1, 0);
-        for (uint32_t k = 0; k < P; ++k) st[k + 1] = st[k] + ents[k].count;
-        dstart = r->start.as<uint64_t>(P + 1);
-        cuda_check(counted_copy(dstart, st.data(), (P + 1) * 8, cudaMemcpyHostToDevice, E.stream), "H2D");
-        dbak = r->backup.as<uint16_t>(n);
-        launch_gather_values(r->plan->dev, 0, dent, dstart, P, didx, dbak, E.stream);
+        if (verify) {
+            dstart = r->start.as<uint64_t>(P + 1);
+            cuda_check(counted_copy(dstart, at.data(), (P + 1) * 8, cudaMemcpyHostToDevice, E.stream), "H2D");
+            dbak = r->backup.as<uint16_t>(n);
+            launch_gather_values(r->plan->dev, 0, dent, dstart, P, didx, dbak, E.stream);
+        }
     }
-    if (pulse_apply(r->plan, 0, p->representation, dbody, dent, P, nullptr, dres, E.stream) != PULSE_OK)
-        raise(PULSE_E_CUDA, pulse_last_error());
-    fail_on(fetch_result(E, dres));  // validate-then-scatter: a failure wrote nothing
+    if (!in_runs) {
+        if (pulse_apply(r->plan, 0, p->representation, dbody, dent, P, nullptr, dres, E.stream) != PULSE_OK)
+            raise(PULSE_E_CUDA, pulse_last_error());
+        fail_on(fetch_result(E, dres));  // validate-then-scatter: a failure wrote nothing
+    } else {
+        // values contiguous in patch order, next to the decoded indices
+        RawVec<uint16_t> hv(std::max<uint64_t>(n, 1));
+        for (uint32_t k = 0; k < P; ++k)
+            if (ents[k].count) std::memcpy(hv.data() + at[k], p->tensors[k].values.data(), ents[k].count * 2);
+        dvals = r->vals.as<uint16_t>(n);
+        E.stager.h2d(dvals, hv.data(), n * 2, E.stream);
+        for (size_t q = 0; q + 1 < runs.size(); ++q) {
+            const uint32_t k0 = runs[q], k1 = runs[q + 1];
+            launch_apply_idx64(r->plan->dev, didx + at[k0], dvals + at[k0], dent + k0, k1 - k0, 0, dres, E.stream);
+            fail_on(fetch_result(E, dres));
+        }
+    }
     if (verify) {  // patch.hpp:341-346 on the resident weights
         std::vector<const void*> ptrs(r->names.size());
         for (uint32_t i = 0; i < ptrs.size(); ++i) ptrs[i] = r->tensor(i);
@@ -2137,6 +2217,9 @@ pulse_status pulse_resident_create(const pulse_checkpoint* c, uint64_t max_chang
         r->off = arena_offsets(r->numel, total);
         // the hash of the held checkpoint (checkpoint_to_state), overlapping the upload
         auto hash = std::async(std::launch::async, [&] { hash_checkpoint(c, r->hash); });
+        // the caller's pending writes to these buffers (any stream, e.g. an async
+        // optimizer step) land before the copy reads them
+        cuda_check(cudaDeviceSynchronize(), "wait for pending device work");
         Engine& E = engine();
         std::lock_guard<std::mutex> lk(E.mu);
         cudaGetDevice(&r->device);
@@ -2175,6 +2258,9 @@ pulse_status pulse_resident_create_device(const pulse_checkpoint* c, uint64_t ma
         }
         uint64_t total = 0;
         r->off = arena_offsets(r->numel, total);
+        // the caller's pending writes to these buffers (any stream, e.g. an async
+        // optimizer step) land before the copy reads them
+        cuda_check(cudaDeviceSynchronize(), "wait for pending device work");
         Engine& E = engine();
         std::lock_guard<std::mutex> lk(E.mu);
         cudaGetDevice(&r->device);
@@ -2279,6 +2365,9 @@ pulse_status pulse_resident_publish(pulse_resident* r, const void* const* dev_cu
                 raise(PULSE_E_ARGUMENT, "tensor " + r->names[i] + ": current data is not a device pointer");
             }
         }
+        // order the encode and the hash after the caller's pending writes to `dev_current`
+        // on any stream: nothing below may read a half-written snapshot
+        cuda_check(cudaDeviceSynchronize(), "wait for pending device work");
         Engine& E = engine();
         std::lock_guard<std::mutex> lk(E.mu);
         uint8_t target_hash[32] = {};

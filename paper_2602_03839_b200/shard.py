@@ -123,7 +123,6 @@ class ShardedPulse:
         self.send = torch.zeros(SUMMARY_BYTES, dtype=torch.uint8, device=self.device)
         self.gathered = torch.zeros(SUMMARY_BYTES * self.world, dtype=torch.uint8, device=self.device)
         self.carry_dev = torch.zeros(16, dtype=torch.uint8, device=self.device)
-        self._carry_host = torch.zeros(16, dtype=torch.uint8).pin_memory()
         # device-side size exchange: bytes 8..24 of every rank's pulse_result
         # (body_bytes u64, n_entries u32, status i32)
         self.size_send = torch.zeros(16, dtype=torch.uint8, device=self.device)
@@ -165,9 +164,9 @@ class ShardedPulse:
         """Validate-then-scatter this rank's section into its resident shard."""
         carry = None
         if sec.patch.representation == 2 and sec.carry[0]:
-            self._carry_host.numpy().view(np.uint64)[:] = sec.carry
-            self.carry_dev.copy_(self._carry_host, non_blocking=True)
-            carry = self.carry_dev
+            # a fresh device buffer per call (synchronous copy from pageable memory):
+            # a later apply cannot overwrite the carry an earlier queued apply reads
+            carry = torch.from_numpy(np.array(sec.carry, np.uint64).view(np.uint8)).to(self.device)
         return self.plan.apply(weights_slot, sec.patch, carry=carry)
 
     # ---- fully device-side step (no host round trip) ---------------------------------------------

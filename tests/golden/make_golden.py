@@ -62,15 +62,70 @@ def handcrafted(Checkpoint, Tensor):
     return prev, curr
 
 
+def h5_unchanged(Checkpoint, Tensor):
+    """FLAT_INT32 gap bases when unchanged tensors sit before and between
+    changed ones (patch.hpp:131-156: the base advances only over tensors the
+    patch carries, and encode omits unchanged tensors, patch.hpp:302-304).
+    Name order: a.lead (unchanged), b.changed, c.mid (unchanged), d.changed,
+    e.tail (unchanged)."""
+    rng = np.random.default_rng(55)
+    shapes = {"a.lead": (300, 7), "b.changed": (64, 33), "c.mid": (5000,), "d.changed": (17, 19, 3),
+              "e.tail": (129,)}
+    prev, curr = [], []
+    for name, shp in shapes.items():
+        n = int(np.prod(shp))
+        a = rng.integers(0, 65536, n, dtype=np.uint16)
+        b = a.copy()
+        if "changed" in name:
+            b[rng.random(n) < 0.05] ^= 1
+            b[0 if name.startswith("d") else n - 1] ^= 0x8000   # first element of d, last of b
+        prev.append(Tensor(name, shp, a))
+        curr.append(Tensor(name, shp, b))
+    return Checkpoint(0, prev), Checkpoint(1, curr)
+
+
+def h5_sparse_lead(Checkpoint, Tensor):
+    """A large unchanged leading tensor, then changed tensors separated by
+    unchanged ones (counting their numel into the base would shift every later gap)."""
+    rng = np.random.default_rng(56)
+    shapes = [("m.a", (70000,)), ("m.b", (40, 40)), ("m.c", (200000,)), ("m.d", (3, 5)), ("m.e", (8, 8)),
+              ("m.f", (2000,))]
+    changed = {"m.b", "m.d", "m.f"}
+    prev, curr = [], []
+    for name, shp in shapes:
+        n = int(np.prod(shp))
+        a = rng.integers(0, 65536, n, dtype=np.uint16)
+        b = a.copy()
+        if name in changed:
+            b[rng.choice(n, max(1, n // 20), replace=False)] ^= 1
+        prev.append(Tensor(name, shp, a))
+        curr.append(Tensor(name, shp, b))
+    return Checkpoint(0, prev), Checkpoint(1, curr)
+
+
+HANDCRAFTED = {"handcrafted": handcrafted, "h5_unchanged": h5_unchanged, "h5_sparse_lead": h5_sparse_lead}
+
+# Spec-only cases at real Qwen2.5-7B tensor shapes: the inputs are too large to
+# store, so the tests regenerate them with the reference generator
+# (oracle/_ref, draw for draw) and check the stored target hash first.  Only
+# the identity-codec PULP bytes are kept (large.npz).
+LARGE = [
+    # 99.99% on mlp.gate_proj [18944, 3584]: sparse enough that row gaps reach
+    # 255 and COO_DOWNSCALED emits 0xFF + u32 row escapes
+    ("s7b_9999", [(18944, 3584), (3584,), (512,)], 0.9999, 64, 77),
+    # 99% on the same tensors: the headline sparsity, no escapes
+    ("s7b_99", [(18944, 3584), (3584,), (512,)], 0.99, 64, 78),
+]
+
 CODECS = [IDENTITY, LZ4, ZSTD1, ZSTD3, GZIP6]
 
 
 def main():
     R = reference()
     snaps, patches, manifest = {}, {}, {"cases": {}}
-    for name, shapes, sp, cw, seed in CASES + [("handcrafted", None, None, None, None)]:
+    for name, shapes, sp, cw, seed in CASES + [(h, None, None, None, None) for h in HANDCRAFTED]:
         if shapes is None:
-            prev, curr = handcrafted(Checkpoint, Tensor)
+            prev, curr = HANDCRAFTED[name](Checkpoint, Tensor)
             shapes = [t.shape for t in prev.tensors]
         else:
             prev, curr = R.generate_synthetic(shapes, sp, cw, seed)
@@ -103,6 +158,25 @@ def main():
             c1["pulp_nbytes"][f"{r}/{c}"] = len(R.write_patch_bytes(p))
     manifest["config1"] = c1
     print("config1", c1)
+
+    large, large_bytes = {}, {}
+    for name, shapes, sp, cw, seed in LARGE:
+        prev, curr = R.generate_synthetic(shapes, sp, cw, seed)
+        p = R.encode(curr, prev, 0, IDENTITY)
+        entry = {"shapes": [list(s) for s in shapes], "sparsity": sp, "cluster_width": cw, "seed": seed,
+                 "names": [t.name for t in prev.tensors], "prev_hash": R.hash_weights(prev).hex(),
+                 "target_hash": R.hash_weights(curr).hex(), "changes": p.total_changes(), "pulp_nbytes": {}}
+        for r in (0, 1, 2):
+            p.representation = r
+            wire = R.write_patch_bytes(p)
+            if len(wire) <= (256 << 10):  # small enough to keep; larger ones by digest
+                large_bytes[f"{name}/{r}"] = np.frombuffer(wire, np.uint8)
+            entry["pulp_nbytes"][str(r)] = len(wire)
+            entry.setdefault("pulp_sha256", {})[str(r)] = R.sha256(wire).hex()
+        large[name] = entry
+        print(name, entry["changes"], entry["pulp_nbytes"])
+    manifest["large"] = large
+    np.savez_compressed(os.path.join(HERE, "large.npz"), **large_bytes)
 
     np.savez_compressed(os.path.join(HERE, "synth_cases.npz"), **snaps)
     np.savez_compressed(os.path.join(HERE, "patches.npz"), **patches)
