@@ -49,7 +49,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-elems", type=int, default=96_000_000)
+    ap.add_argument("--cpu-sample-elems", type=int, default=480_000_000)
     return ap.parse_args()
 
 
@@ -208,14 +208,12 @@ def cpu_sample(tensors, target_elems):
     order starting after the embeddings, up to ~target_elems elements."""
     picked, total = [], 0
     start = 2 if len(tensors) > 3 else 0
-    for name, shp in tensors[start:]:
+    for name, shp in tensors[start:]:  # consecutive in name order (FLAT gaps continue across them)
         n = numel(shp)
         if total and total + n > target_elems:
-            continue
+            break
         picked.append((name, shp))
         total += n
-        if total >= target_elems * 0.9:
-            break
     return picked, total
 
 

@@ -908,10 +908,11 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
 // Scan summary: totals, capacity status, and the FLAT gap base of the last
 // changed tensor (needed by the next shard's first entry).
 __global__ void k1_finalize(const SegDesc* __restrict__ segs, uint32_t n_segs,
-                            const uint64_t* __restrict__ numel, const uint64_t* __restrict__ seg_start,
+                            const uint64_t* __restrict__ numel, uint64_t* __restrict__ seg_start,
                             const uint32_t* __restrict__ idx32, uint64_t capacity,
                             pulse_scan_summary* out, pulse_scan_summary* copy_out) {
     if (threadIdx.x != 0) return;
+    if (n_segs == 0) seg_start[0] = 0;  // a plan with no tensors (a shard with none): K1 did not run
     const uint64_t n = seg_start[n_segs];
     pulse_scan_summary s;
     s.n_changes = n;

@@ -41,6 +41,7 @@ extern "C" {
 size_t ZSTD_compress(void* dst, size_t dst_capacity, const void* src, size_t src_size, int level);
 size_t ZSTD_decompress(void* dst, size_t dst_capacity, const void* src, size_t src_size);
 size_t ZSTD_compressBound(size_t src_size);
+unsigned long long ZSTD_decompressBound(const void* src, size_t src_size);
 unsigned ZSTD_isError(size_t code);
 int LZ4_compress_default(const char* src, char* dst, int src_size, int dst_capacity);
 int LZ4_decompress_safe(const char* src, char* dst, int compressed_size, int dst_capacity);
@@ -520,7 +521,8 @@ std::vector<uint32_t> distinct_target_runs(const uint32_t* target, uint32_t n) {
 }
 
 // Exception text for a device-detected failure, in the reference's words.
-std::string device_message(const pulse_result& r, const std::string& name, const RawVec<int64_t>* idx) {
+std::string device_message(const pulse_result& r, const std::string& name, const RawVec<int64_t>* idx,
+                           uint32_t repr = PULSE_COO_INT32) {
     switch (r.err_check) {
         case PULSE_CHECK_TRUNCATED: return "unexpected end of data";
         case PULSE_CHECK_ZERO_GAP: return "zero index gap in tensor '" + name + "'";
@@ -528,7 +530,9 @@ std::string device_message(const pulse_result& r, const std::string& name, const
         case PULSE_CHECK_COL_RANGE: return "column index out of range in tensor '" + name + "'";
         case PULSE_CHECK_INDEX_RANGE: return "index out of range in tensor '" + name + "'";
         case PULSE_CHECK_TRAILING:
-            return r.err_stage == 3 ? "index payload has trailing bytes" : "downscaled payload has trailing bytes";
+            // patch.hpp:211-213 / 238-240 (int32 payloads) vs upscale_coo, index_coding.hpp:154-156
+            return repr == PULSE_COO_DOWNSCALED ? "downscaled payload has trailing bytes"
+                                                : "index payload has trailing bytes";
         case PULSE_CHECK_NEGATIVE: return "indices must be non-negative";
         case PULSE_CHECK_ORDER: return "indices must be strictly increasing";
         case PULSE_CHECK_FLAT_GAP: return "index gap exceeds 32 bits";
@@ -593,6 +597,27 @@ std::vector<uint8_t> codec_decompress(const uint8_t* env, size_t n, uint32_t cod
     if (raw == 0) {
         if (bn) raise(PULSE_E_CORRUPT_STREAM, "codec envelope has trailing bytes");
         return {};
+    }
+    // A declared size the stream cannot possibly produce fails exactly as the
+    // reference's decompression would (produced != raw_size), but without first
+    // zero-filling up to 1 TiB of host memory for it: lz4 expands at most ~255x,
+    // deflate ~1032x, and zstd reports a bound over all frames of the stream.
+    {
+        const char* what = nullptr;
+        unsigned long long bound = 0;
+        switch (codec) {
+            case PULSE_LZ4: bound = 255ull * bn + 64; what = "lz4 stream is corrupt"; break;
+            case PULSE_GZIP6: bound = 1032ull * bn + 64; what = "deflate stream is corrupt"; break;
+            case PULSE_ZSTD1:
+            case PULSE_ZSTD3: {
+                const unsigned long long b = ZSTD_decompressBound(body, bn);
+                bound = b >= (0ULL - 2) ? 0 : b;  // ZSTD_CONTENTSIZE_ERROR: no valid frame, nothing decodes
+                what = "zstd stream is corrupt";
+                break;
+            }
+            default: break;
+        }
+        if (what && raw > bound) raise(PULSE_E_CORRUPT_STREAM, what);
     }
     std::vector<uint8_t> out(raw);
     switch (codec) {
@@ -759,7 +784,7 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
     const pulse_result r = fetch_result(E, dres);
     if (r.status != PULSE_OK) {
         const std::string nm = r.err_tensor < T ? p->tensors[r.err_tensor].name : "?";
-        raise(pulse_status(r.status), device_message(r, nm, nullptr));
+        raise(pulse_status(r.status), device_message(r, nm, nullptr, p->representation));
     }
     // each tensor's indices straight into its vector (no intermediate host copy)
     uint64_t at = 0;
@@ -1303,13 +1328,20 @@ pulse_status pulse_decode(const pulse_checkpoint* previous, const pulse_patch* p
                 cuda_check(counted_copy(dent, ents.data(), stop * sizeof(pulse_patch_entry), cudaMemcpyHostToDevice,
                                            E.stream), "H2D");
                 auto* dres = E.result.as<pulse_result>(1);
-                // sequential: validate + scatter in one go; pipelined or in runs: validate only here
+                // sequential: validate + scatter in one go; pipelined: validate only here.
+                // Runs (duplicate names; a launch covers at most one entry per tensor): validate
+                // every run in patch order first -- the first failing run holds the reference's
+                // first failure -- then scatter them in order.
                 const bool whole = !pipelined && runs.size() <= 2;
-                launch_apply_idx64(plan->dev, didx, dval, dent, stop, whole ? 2 : -1, dres, E.stream);
-                const pulse_result r = fetch_result(E, dres);
-                if (r.status != PULSE_OK) {
-                    const auto& tp = patch->tensors[r.err_tensor];
-                    raise(pulse_status(r.status), device_message(r, tp.name, &tp.indices));
+                for (size_t q = 0; q + 1 < runs.size(); ++q) {
+                    const uint32_t k0 = runs[q], k1 = runs[q + 1];
+                    launch_apply_idx64(plan->dev, didx + at[k0], dval + at[k0], dent + k0, k1 - k0, whole ? 2 : -1,
+                                       dres, E.stream);
+                    const pulse_result r = fetch_result(E, dres);
+                    if (r.status != PULSE_OK) {
+                        const auto& tp = patch->tensors[k0 + r.err_tensor];
+                        raise(pulse_status(r.status), device_message(r, tp.name, &tp.indices));
+                    }
                 }
                 if (!pipelined && !whole)
                     for (size_t q = 0; q + 1 < runs.size(); ++q) {
@@ -1974,7 +2006,7 @@ struct pulse_resident {
     std::unordered_map<std::string, uint32_t> by_name;
     void* arena = nullptr;                    // resident weights; tensor i at element off[i]
     std::vector<uint64_t> off;
-    DevBuf body, entries, result, idx64, backup, start, vals;
+    DevBuf body, entries, result, idx64, backup, start, vals, carry;
     void* pinned[2] = {nullptr, nullptr};     // hash pipeline (D2H | SHA-256)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaStream_t hstream = nullptr;
@@ -1986,7 +2018,7 @@ struct pulse_resident {
             if (ev[i]) cudaEventDestroy(ev[i]);
         }
         if (hstream) cudaStreamDestroy(hstream);
-        for (DevBuf* b : {&body, &entries, &result, &idx64, &backup, &start, &vals})
+        for (DevBuf* b : {&body, &entries, &result, &idx64, &backup, &start, &vals, &carry})
             if (b->p) cudaFree(b->p);
     }
     uint16_t* tensor(uint32_t i) const { return static_cast<uint16_t*>(arena) + off[i]; }
@@ -2135,7 +2167,7 @@ void resident_apply_parsed(pulse_resident* r, Engine& E, ParsedPulp& pp, uint64_
     auto fail_on = [&](const pulse_result& res) {
         if (res.status == PULSE_OK) return;
         const std::string nm = res.err_tensor < P ? p->tensors[res.err_tensor].name : "?";
-        raise(pulse_status(res.status), device_message(res, nm, nullptr));
+        raise(pulse_status(res.status), device_message(res, nm, nullptr, p->representation));
     };
     int64_t* didx = nullptr;
     uint16_t* dbak = nullptr;
@@ -2149,9 +2181,40 @@ void resident_apply_parsed(pulse_resident* r, Engine& E, ParsedPulp& pp, uint64_
     uint16_t* dvals = nullptr;
     if (verify || in_runs) {  // indices (and, for verify, the values the scatter overwrites)
         didx = r->idx64.as<int64_t>(n);
-        if (pulse_decode_indices(r->plan, p->representation, dbody, dent, P, nullptr, didx, dres, E.stream) != PULSE_OK)
-            raise(PULSE_E_CUDA, pulse_last_error());
-        fail_on(fetch_result(E, dres));
+        // one decode per run (a launch takes at most one entry per tensor); FLAT_INT32's gap
+        // stream continues into the next run through the carry: the global position of the
+        // last decoded index, rebased past the numel of every entry since (patch.hpp:185-259)
+        auto* dcarry = r->carry.as<pulse_flat_carry>(1);
+        bool have_last = false;
+        uint64_t since_last = 0;  // numel of entries from the last decoded index's entry onward
+        int64_t last_idx = 0;
+        for (size_t q = 0; q + 1 < runs.size(); ++q) {
+            const uint32_t k0 = runs[q], k1 = runs[q + 1];
+            const pulse_flat_carry* cp = nullptr;
+            if (p->representation == PULSE_FLAT_INT32 && have_last) {
+                const pulse_flat_carry c{1, since_last - uint64_t(last_idx)};
+                cuda_check(counted_copy(dcarry, &c, sizeof(c), cudaMemcpyHostToDevice, E.stream), "H2D");
+                cp = dcarry;
+            }
+            if (pulse_decode_indices(r->plan, p->representation, dbody, dent + k0, k1 - k0, cp, didx + at[k0], dres,
+                                     E.stream) != PULSE_OK)
+                raise(PULSE_E_CUDA, pulse_last_error());
+            pulse_result res = fetch_result(E, dres);
+            if (res.status != PULSE_OK) res.err_tensor += k0;
+            fail_on(res);
+            if (p->representation == PULSE_FLAT_INT32 && in_runs)
+                for (uint32_t k = k0; k < k1; ++k) {
+                    const uint64_t numel_k = r->numel[r->order[ents[k].tensor]];
+                    if (ents[k].count) {
+                        cuda_check(counted_copy(&last_idx, didx + at[k + 1] - 1, 8, cudaMemcpyDeviceToHost, E.stream),
+                                   "D2H");
+                        E.sync();
+                        have_last = true;
+                        since_last = 0;
+                    }
+                    since_last += numel_k;
+                }
+        }
         if (verify) {
             dstart = r->start.as<uint64_t>(P + 1);
             cuda_check(counted_copy(dstart, at.data(), (P + 1) * 8, cudaMemcpyHostToDevice, E.stream), "H2D");
@@ -2182,8 +2245,11 @@ void resident_apply_parsed(pulse_resident* r, Engine& E, ParsedPulp& pp, uint64_
         uint8_t h[32];
         hash_device(r, name_order_parts(r, ptrs), h);
         if (std::memcmp(h, p->target_hash, 32) != 0) {
-            launch_apply_idx64(r->plan->dev, didx, dbak, dent, P, 0, dres, E.stream);  // put the old values back
-            fail_on(fetch_result(E, dres));
+            for (size_t q = 0; q + 1 < runs.size(); ++q) {  // put the old values back
+                const uint32_t k0 = runs[q], k1 = runs[q + 1];
+                launch_apply_idx64(r->plan->dev, didx + at[k0], dbak + at[k0], dent + k0, k1 - k0, 0, dres, E.stream);
+                fail_on(fetch_result(E, dres));
+            }
             raise(PULSE_E_HASH_MISMATCH, "hash mismatch: expected " + hex(p->target_hash) + ", actual " + hex(h));
         }
     }

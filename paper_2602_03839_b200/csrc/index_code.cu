@@ -745,6 +745,9 @@ __global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
             r.status = PULSE_E_CAPACITY;
             r.err_check = kCapacity;
             r.required = body_base;
+            // the optimistic layout assumed no escapes: have the exact pipeline (gated on the
+            // escape flag) re-run so `required` is the exact body size
+            if (a.optimistic) *a.zero_u32[2] = 1;
         }
         *a.result = r;
     }

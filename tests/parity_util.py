@@ -1,12 +1,12 @@
 """Test helpers for parity at BASELINE sizes (test infrastructure only).
 
-* `device_state`: a name-sorted state dict generated on the device (K5, the
-  benchmark's own inputs) in one arena, with per-tensor views.
+* `device_pair`: a name-sorted state dict generated on the device (K5, the
+  benchmark's own inputs) in one arena, with per-tensor views (`DeviceState`).
 * `host_checkpoint`: the D2H copy of such a state as an oracle Checkpoint, so
   the reference (oracle/_ref) encodes exactly the bytes the GPU encoded
   ("D2H copies of the *same* device inputs fed to the
   reference `pulse::encode`").
-* `sharded_encode` / `sharded_apply`: N ranks of `shard.ShardedPulse` simulated
+* `ShardedSim`: N ranks of `shard.ShardedPulse` simulated
   on ONE device without NCCL.  Each rank gets a DevicePlan over its contiguous
   name-ordered range (`shapes.shard`), its K1 summary lands in its slot of a
   shared `gathered` buffer (what the all-gather would produce), K2 runs with

@@ -65,9 +65,18 @@ def assemble(hdr, blobs):
     return b"PULP" + struct.pack("<IQ", 1, len(h)) + h + b"".join(i + v for i, v in blobs)
 
 
+def _guard(pos, codec):
+    """Non-identity blobs start with a u64 declared raw size (compression.hpp:
+    157-167): bytes 3..7 are left alone so a mutation never declares more than
+    16 MiB -- the reference would zero-fill the declared size (up to 1 TiB)
+    before decompressing."""
+    return pos if codec == 0 or pos < 3 or pos >= 8 else 8
+
+
 def mutate(rng, wire):
     """One seeded mutation of a PULP file; returns (kind, bytes)."""
     hdr, blobs = parse_layout(wire)
+    codec = hdr["codec"]
     T = len(blobs)
     body0 = len(wire) - sum(len(i) + len(v) for i, v in blobs)
     k = int(rng.integers(0, 14))
@@ -79,21 +88,22 @@ def mutate(rng, wire):
     if k in (1, 2) and ib:  # bit flips in an index blob
         b = bytearray(ib)
         for _ in range(int(rng.integers(1, 4))):
-            p = int(rng.integers(0, len(b)))
-            b[p] ^= 1 << int(rng.integers(0, 8))
+            p = _guard(int(rng.integers(0, len(b))), codec)
+            if p < len(b):
+                b[p] ^= 1 << int(rng.integers(0, 8))
         blobs[t][0] = bytes(b)
         return "index_flip", assemble(hdr, blobs)
     if k == 3 and ib:  # 0xFF / 0xFFFF marker runs
         b = bytearray(ib)
-        p = int(rng.integers(0, len(b)))
-        run = int(rng.choice([1, 2, 3, 4, 5, 6, 8]))
+        p = _guard(int(rng.integers(0, len(b))), codec)
+        run = int(rng.choice([1, 2, 3, 4, 5, 6, 8])) if codec == 0 else 1
         b[p:p + run] = b"\xff" * len(b[p:p + run])
         blobs[t][0] = bytes(b)
         return "marker_run", assemble(hdr, blobs)
     if k == 4 and ib:  # zeroed gap bytes
         b = bytearray(ib)
-        p = int(rng.integers(0, len(b)))
-        n = int(rng.integers(1, 5))
+        p = _guard(int(rng.integers(0, len(b))), codec)
+        n = int(rng.integers(1, 5)) if codec == 0 else 1
         b[p:p + n] = b"\0" * len(b[p:p + n])
         blobs[t][0] = bytes(b)
         return "zero_run", assemble(hdr, blobs)
@@ -120,7 +130,9 @@ def mutate(rng, wire):
         e = dict(hdr["tensors"][t])
         if rng.random() < 0.5 and vb:  # the duplicate carries different values
             vb2 = bytearray(vb)
-            vb2[int(rng.integers(0, len(vb2)))] ^= 0x40
+            p = _guard(int(rng.integers(0, len(vb2))), codec)
+            if p < len(vb2):
+                vb2[p] ^= 0x40
             vb = bytes(vb2)
         hdr["tensors"].insert(t + 1, e)
         blobs.insert(t + 1, [ib, vb])
@@ -145,7 +157,9 @@ def mutate(rng, wire):
         return "shape_edit", assemble(hdr, blobs)
     if k == 11 and vb:  # value bit flips (read succeeds; decode's hash check fails)
         b = bytearray(vb)
-        b[int(rng.integers(0, len(b)))] ^= 1 << int(rng.integers(0, 8))
+        p = _guard(int(rng.integers(0, len(b))), codec)
+        if p < len(b):
+            b[p] ^= 1 << int(rng.integers(0, 8))
         blobs[t][1] = bytes(b)
         return "value_flip", assemble(hdr, blobs)
     if k == 12:  # unknown tensor name / header field edits
@@ -162,7 +176,7 @@ def mutate(rng, wire):
             hdr["tensors"][t].pop(str(rng.choice(["count", "index_nbytes", "value_nbytes", "shape", "name"])))
         return "header_field", assemble(hdr, blobs)
     # header byte noise (JSON syntax / schema errors) and whole-file bit flips
-    p = int(rng.integers(0, body0 if rng.random() < 0.7 else len(w)))
+    p = int(rng.integers(0, body0 if (rng.random() < 0.7 or codec != 0) else len(w)))
     w[p] = int(rng.integers(0, 256))
     return "byte_noise", bytes(w)
 

@@ -550,3 +550,63 @@ def test_many_tiny_tensors_small_plan(repr_):
     assert (int(res["err_tensor"]), int(res["err_check"]), int(res["err_elem"])) == want
     for a, t in zip(prevs, w):
         assert np.array_equal(t.cpu().numpy().view(np.uint16), a)
+
+
+# ---- out-of-bounds writes: canaries around every caller buffer -----------------------------------
+# (compute-sanitizer is not available on the GPU pool; these guard bytes catch a kernel that writes
+# past a weight tensor, the patch body, the entry table or the result record)
+_CANARY = 0x5A
+
+
+def _guarded(n, dtype, pad):
+    """A view of n elements inside a buffer of canary bytes (pad elements each side, 16-byte aligned)."""
+    base = torch.full((n + 2 * pad,), 0, dtype=dtype, device="cuda")
+    base.view(torch.uint8).fill_(_CANARY)
+    return base, base[pad:pad + n]
+
+
+def _intact(base, view, pad):
+    b = base.view(torch.uint8).cpu().numpy()
+    es = base.element_size()
+    return bool((b[: pad * es] == _CANARY).all() and (b[(pad + view.numel()) * es:] == _CANARY).all())
+
+
+@pytest.mark.parametrize("case", ["handcrafted", "esc_rows", "esc_cols", "esc_cols_wide", "dense_all",
+                                  "h5_unchanged", "h5_sparse_lead", "roundtrip_s3"])
+def test_no_writes_outside_caller_buffers(golden, case):
+    D = _dev()
+    prev, curr, _ = golden.case(case)
+    ts = prev.sorted()
+    cs = curr.sorted()
+    PAD = 4096
+    # weights: each tensor between canaries
+    wbufs = [_guarded(t.data.size, torch.int16, PAD) for t in ts]
+    pd = [torch.from_numpy(t.data.view(np.int16).copy()).cuda() for t in ts]
+    cd = [torch.from_numpy(t.data.view(np.int16).copy()).cuda() for t in cs]
+    plan = make_plan(ts)
+    plan.bind(0, pd)
+    plan.bind(1, cd)
+    plan.bind(2, [v for _, v in wbufs])
+    for r in (COO_DOWNSCALED, COO_INT32, FLAT_INT32):
+        want = golden.pulp(case, r, IDENTITY)
+        _, body = split_pulp(want)
+        for cap in (len(body), max(0, len(body) - 1), len(body) // 2, 16, plan.body_capacity(r)):
+            bb, bv = _guarded(max(cap, 1), torch.uint8, PAD)
+            eb, ev = _guarded(max(1, len(ts)) * 40, torch.uint8, PAD)
+            rb, rv = _guarded(72, torch.uint8, PAD)
+            p = D.DevicePatch(r, bv[:cap] if cap else bv[:0], ev, rv)
+            plan.scan(1, 0)
+            plan.emit(p)
+            p.fetch()
+            assert _intact(bb, bv, PAD) and _intact(eb, ev, PAD) and _intact(rb, rv, PAD), (case, r, cap)
+            if cap >= len(body):
+                assert p.status == 0 and p.body[: p.body_bytes].cpu().numpy().tobytes() == body
+                for (wb, wv), a in zip(wbufs, pd):
+                    wv.copy_(a)
+                res = D.parse_result(plan.apply(2, p))
+                assert int(res["status"]) == 0
+                assert all(torch.equal(wv, c) for (_, wv), c in zip(wbufs, cd))
+                assert all(_intact(wb, wv, PAD) for wb, wv in wbufs), (case, r)
+                idx, _ = plan.decode_indices(p)
+            else:
+                assert p.status == 15 and int(p.host_result["required"]) >= len(body), (case, r, cap, p.status)
