@@ -220,19 +220,39 @@ __global__ void __launch_bounds__(kThreads, 4) k1_ticket(K1Args k) {
 // a ticket held by a stalled CTA.
 // ---------------------------------------------------------------------------------------------
 namespace tma {
+// Two staging shapes, picked per plan (launch_encode_scan).  Sparse patches gain
+// from more ring stages and more tickets in flight between the consumers and
+// the look-back/flush group (measured at 7B / 99%: 4 stages x 3 buffers 4.83 ms,
+// 5 x 5 4.49 ms); dense ones need room for element entries per buffer (90%:
+// 3 x 4 with 8192 entries 13.7 ms; the sparse shape would overflow its staging
+// and re-stream nearly every ticket).  PULSE_K1_* macros override the sparse
+// shape for experiments; PULSE_K1_SHAPE=sparse|dense forces one per launch.
 #ifndef PULSE_K1_STAGES
-#define PULSE_K1_STAGES 4
+#define PULSE_K1_STAGES 5
 #endif
 #ifndef PULSE_K1_BUFS
-#define PULSE_K1_BUFS 3
+#define PULSE_K1_BUFS 5
 #endif
 #ifndef PULSE_K1_COOP_STAGE
 #define PULSE_K1_COOP_STAGE 1  // element mode: warp-cooperative staging (0: per-lane loop over mask bits)
 #endif
 #ifndef PULSE_K1_RECCAP
-#define PULSE_K1_RECCAP 1344
+#define PULSE_K1_RECCAP 448
 #endif
-constexpr int kStages = PULSE_K1_STAGES;
+#ifndef PULSE_K1_STAGECAP
+#define PULSE_K1_STAGECAP 2688
+#endif
+template <int S, int B, uint32_t RC, uint32_t SC>
+struct Cfg {
+    static constexpr int kStages = S;          // TMA ring stages (16 KiB prev + 16 KiB curr each)
+    static constexpr int kBufs = B;            // ticket staging buffers (consumers may run ahead)
+    static constexpr uint32_t kRecCap = RC;    // record mode: staged changed 16-byte vectors per buffer
+    static constexpr uint32_t kStageCap = SC;  // element mode: staged changed elements per buffer
+    // changes above which the next ticket stages element entries (below the element capacity)
+    static constexpr uint32_t kDenseTicket = SC * 3 / 4 < 3072 ? SC * 3 / 4 : 3072;
+};
+using SparseCfg = Cfg<PULSE_K1_STAGES, PULSE_K1_BUFS, PULSE_K1_RECCAP, PULSE_K1_STAGECAP>;
+using DenseCfg = Cfg<3, 4, 1344, 8192>;
 constexpr uint32_t kSubElems = 8192;                 // elements per stage (16 KiB + 16 KiB)
 constexpr uint32_t kSubs = kTicketElems / kSubElems; // 8 sub-tiles per ticket
 constexpr int kConsumerWarps = 8;
@@ -242,14 +262,7 @@ constexpr int kLbWarps = 4;                          // warps 9..12
 constexpr int kLbFirst = kConsumerWarps + 1;
 constexpr int kLbThreads = kLbWarps * 32;
 constexpr int kThreadsTotal = (kConsumerWarps + 1 + kLbWarps) * 32;  // 416
-constexpr uint32_t kRecCap = PULSE_K1_RECCAP;        // record mode: staged changed 16-byte vectors per buffer
-#ifndef PULSE_K1_STAGECAP
-#define PULSE_K1_STAGECAP 8192
-#endif
-constexpr uint32_t kStageCap = PULSE_K1_STAGECAP;    // element mode: staged changed elements per buffer
-constexpr uint32_t kDenseTicket = 3072;              // changes above which the next ticket uses element mode
 enum : uint32_t { kModeRecords = 0, kModeElements = 1 };
-constexpr int kBufs = PULSE_K1_BUFS;                 // ticket staging buffers (consumers may run ahead)
 constexpr uint32_t kChunks = kSubs * kConsumerWarps; // (sub-tile, warp) chunks per ticket
 constexpr uint32_t kBarLb = 2;                       // named barrier id of the look-back group
 static_assert(kVecPerWarp % 32 == 0, "whole vectors per lane");
@@ -269,7 +282,10 @@ struct TicketInfo {
     uint32_t si, toff, n_sub;
 };
 
+template <class C>
 struct Smem {
+    static constexpr int kStages = C::kStages, kBufs = C::kBufs;
+    static constexpr uint32_t kRecCap = C::kRecCap, kStageCap = C::kStageCap;
     uint4 prev[kStages][kSubElems / 8];
     uint4 curr[kStages][kSubElems / 8];
     // Staging, one buffer per ticket in flight, in one of two layouts chosen per
@@ -305,7 +321,8 @@ struct Smem {
     uint32_t lb_run, lb_count;
     uint64_t lb_G;
 };
-static_assert(sizeof(Smem) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
+static_assert(sizeof(Smem<SparseCfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
+static_assert(sizeof(Smem<DenseCfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
 }  // namespace tma
 
 // Look-back with 4 status words per lane per round (128 predecessors).
@@ -358,10 +375,13 @@ __device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t til
     return excl;
 }
 
+template <class C>
 __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
     using namespace tma;
+    constexpr int kStages = C::kStages, kBufs = C::kBufs;
+    constexpr uint32_t kRecCap = C::kRecCap, kStageCap = C::kStageCap, kDenseTicket = C::kDenseTicket;
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+    tma::Smem<C>& S = *reinterpret_cast<tma::Smem<C>*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
@@ -990,14 +1010,27 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
         if (k1_variant() == 0 && p.tma_tiles > 0) {
             int& attr = tma_attr.here();
             if (!attr) {
-                cudaFuncSetAttribute(k1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(tma::Smem)));
+                cudaFuncSetAttribute(k1_tma<tma::SparseCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(tma::Smem<tma::SparseCfg>)));
+                cudaFuncSetAttribute(k1_tma<tma::DenseCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(tma::Smem<tma::DenseCfg>)));
                 attr = 1;
             }
             K1Args kt = k;
             kt.n_tiles = p.tma_tiles;
             kt.tile_seg = p.tma_tile_seg;
             const uint64_t grid = std::min<uint64_t>(uint64_t(sm_count()), p.tma_tiles);
-            k1_tma<<<unsigned(grid), tma::kThreadsTotal, sizeof(tma::Smem), s>>>(kt);
+            // the plan's change capacity says which regime the caller sized it for: >= 3% of its
+            // elements -> dense staging (element entries need room), else more tickets in flight
+            const int shape_override = [] {  // PULSE_K1_SHAPE=sparse|dense (tests, A/B runs; read per launch)
+                const char* e = getenv("PULSE_K1_SHAPE");
+                return !e ? -1 : std::string(e) == "dense" ? 1 : std::string(e) == "sparse" ? 0 : -1;
+            }();
+            if (shape_override >= 0 ? shape_override == 1 : p.k1_dense != 0) {
+                k1_tma<tma::DenseCfg><<<unsigned(grid), tma::kThreadsTotal, sizeof(tma::Smem<tma::DenseCfg>), s>>>(kt);
+            } else {
+                k1_tma<tma::SparseCfg><<<unsigned(grid), tma::kThreadsTotal, sizeof(tma::Smem<tma::SparseCfg>), s>>>(kt);
+            }
             PULSE_LAUNCHED("k1_tma", s);
             launched = true;
         }

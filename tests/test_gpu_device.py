@@ -37,8 +37,17 @@ def make_plan(ts, max_changes=None):
     return D.DevicePlan(geoms, cap)
 
 
+@pytest.fixture(params=["auto", "sparse", "dense"])
+def k1_shape(request, monkeypatch):
+    """K1's staging shape (encode.cu tma::SparseCfg / DenseCfg): chosen from the plan's
+    capacity, or forced through PULSE_K1_SHAPE so both run on every golden case."""
+    if request.param != "auto":
+        monkeypatch.setenv("PULSE_K1_SHAPE", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("repr_", [COO_DOWNSCALED, COO_INT32, FLAT_INT32])
-def test_encode_body_matches_reference_pulp(golden, repr_):
+def test_encode_body_matches_reference_pulp(golden, repr_, k1_shape):
     for name in golden.names:
         prev, curr, m = golden.case(name)
         want = golden.pulp(name, repr_, IDENTITY)
@@ -150,7 +159,13 @@ def test_config1_16m_matches_reference_bytes(golden):
         assert len(want) == golden.manifest["config1"]["pulp_nbytes"][f"{r}/0"]
 
 
-def test_dense_ticket_slow_path():
+@pytest.mark.parametrize("shape", ["sparse", "dense"])
+def test_dense_ticket_slow_path(shape, monkeypatch):
+    monkeypatch.setenv("PULSE_K1_SHAPE", shape)
+    _dense_ticket_slow_path()
+
+
+def _dense_ticket_slow_path():
     """A fully changed ticket overflows the shared-memory staging of K1 and is
     re-streamed from global memory; results must not change."""
     D = _dev()
