@@ -56,7 +56,6 @@ namespace {
 constexpr uint32_t kRange = 4096;  // entries per warp range (aggregate granularity)
 constexpr uint32_t kChunk = 1024;  // entries staged per warp step
 constexpr uint32_t kPer = kChunk / 32;  // consecutive entries per lane
-constexpr uint32_t kChunksPerRange = kRange / kChunk;
 constexpr uint64_t H = SegSumOp::kHead;
 
 enum Repr : int { kCoo = 0, kI32 = 1, kFlat = 2 };
@@ -620,9 +619,9 @@ struct SLay {
     static constexpr uint32_t vb = per / 8;                                   // columns
     static constexpr uint32_t a_slots = 32 * va + 1;
     static constexpr uint32_t b_slots = coo ? 32 * vb + 1 : 0;
-    static constexpr uint32_t v_slots = kAgg_ ? 0 : 2 * ch / 16 + 1;          // values (V=1)
+    static constexpr uint32_t v_slots = kAgg_ ? 0 : 2 * ch / 16 + 1;          // values (V=2)
     static constexpr uint32_t buf = 16 * (a_slots + b_slots + v_slots);
-    static constexpr uint32_t warp = 2 * buf + (kAgg_ ? 0 : 4 * ch);          // 2 buffers (+ decoded indices)
+    static constexpr uint32_t warp = 2 * buf + (kAgg_ ? 0 : 8 * ch);          // 2 buffers (+ (index, value) pairs)
 };
 
 
@@ -804,45 +803,45 @@ __device__ __forceinline__ void chunk_body(const ApplyArgs& A, const SCtx& cur, 
     const uint32_t cols32 = uint32_t(cur.cols);
     uint32_t r32 = uint32_t(row), c32 = uint32_t(col);
     const uint64_t flat_off = gap_base + cur.flat_base;
+    // this lane's 16 values: two funnel-aligned 16-byte reads of the staged value blob
+    const uint4* svb = reinterpret_cast<const uint4*>(bb + 16 * (Y::a_slots + Y::b_slots));
+    const uint4 v0 = staged16<2>(svb, uint32_t(2 * lane), sh[2]);
+    const uint4 v1 = staged16<2>(svb, uint32_t(2 * lane + 1), sh[2]);
+    const uint32_t vw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint32_t xv[kPer];
 #pragma unroll
-    for (int i = 0; i < kPer / 4; ++i) {
-        uint32_t xv[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int j = 4 * i + k;
-            const uint32_t a = PULSE_SA(j), bv = PULSE_SB(j);
-            const bool first = j == 0 && lane_first;
-            if (coo) {
-                r32 = first ? a : r32 + a;
-                c32 = (first || a != 0) ? bv : c32 + bv;
-                xv[k] = r32 * cols32 + c32;
-            } else if (kRepr == kI32) {
-                r32 = first ? a : r32 + a;
-                xv[k] = r32;
-            } else {
-                row += a;
-                xv[k] = uint32_t(row - flat_off);
-            }
+    for (int j = 0; j < kPer; ++j) {
+        const uint32_t a = PULSE_SA(j), bv = PULSE_SB(j);
+        const bool first = j == 0 && lane_first;
+        if (coo) {
+            r32 = first ? a : r32 + a;
+            c32 = (first || a != 0) ? bv : c32 + bv;
+            xv[j] = r32 * cols32 + c32;
+        } else if (kRepr == kI32) {
+            r32 = first ? a : r32 + a;
+            xv[j] = r32;
+        } else {
+            row += a;
+            xv[j] = uint32_t(row - flat_off);
         }
-        reinterpret_cast<uint4*>(sx)[swz<4>(uint32_t(lane * 4 + i))] = make_uint4(xv[0], xv[1], xv[2], xv[3]);
     }
+    // (index, value) pairs, lane-consecutive, two per 16-byte slot (swizzled: conflict-free both ways)
+    uint4* sp = reinterpret_cast<uint4*>(sx);
+#pragma unroll
+    for (int i = 0; i < kPer / 2; ++i)
+        sp[swz<8>(uint32_t(lane * (kPer / 2) + i))] =
+            make_uint4(xv[2 * i], vw[i] & 0xFFFFu, xv[2 * i + 1], vw[i] >> 16);
 #undef PULSE_SA
 #undef PULSE_SB
     __syncwarp();
-    // 32 consecutive changes per store instruction
+    // scatter: each store instruction covers 32 of 64 consecutive changes (a few sectors)
     uint16_t* W = A.weights[cur.tensor];
-    const uint8_t* sv = bb + 16 * (Y::a_slots + Y::b_slots);
-    const uint32_t sv_s = sh[2];
-    if ((sv_s & 1) == 0) {
-        const uint16_t* sv16 = reinterpret_cast<const uint16_t*>(sv + sv_s);
+    const uint32_t npairs = (len + 1) / 2;
 #pragma unroll 4
-        for (uint32_t k = lane; k < len; k += 32) W[smem_word<4>(reinterpret_cast<const uint4*>(sx), k)] = sv16[k];
-    } else {
-#pragma unroll 4
-        for (uint32_t k = lane; k < len; k += 32) {
-            const uint32_t vb = sv_s + 2 * k;
-            W[smem_word<4>(reinterpret_cast<const uint4*>(sx), k)] = uint16_t(sv[vb] | uint32_t(sv[vb + 1]) << 8);
-        }
+    for (uint32_t k2 = lane; k2 < npairs; k2 += 32) {
+        const uint4 q = lds128(sp + swz<8>(k2));
+        W[q.x] = uint16_t(q.y);
+        if (2 * k2 + 1 < len) W[q.z] = uint16_t(q.w);
     }
 }
 
@@ -852,7 +851,7 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
     using Y = SLay<kRepr, kAgg_>;
     constexpr bool coo = kRepr == kCoo;
     constexpr bool agg = kAgg_;
-    constexpr uint32_t kSChunk = Y::ch, kSPer = Y::per;
+    constexpr uint32_t kSChunk = Y::ch;
     if (fast_blocked(A.flags)) return;
     if (!agg && *(volatile const uint64_t*)A.err != kNoError) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -905,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
                 sh[0] = stage_cover<Y::va>(reinterpret_cast<uint4*>(bb), A.body + c.idx_off + 4 * o0, 4 * len);
             }
             if (!agg)
-                sh[2] = stage_cover<1>(reinterpret_cast<uint4*>(bb + 16 * (Y::a_slots + Y::b_slots)),
+                sh[2] = stage_cover<2>(reinterpret_cast<uint4*>(bb + 16 * (Y::a_slots + Y::b_slots)),
                                        A.body + c.val_off + 2 * o0, 2 * len);
         }
         cp_async_commit();

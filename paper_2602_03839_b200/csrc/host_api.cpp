@@ -1458,7 +1458,7 @@ pulse_status pulse_write_patch_bytes(const pulse_patch* p, pulse_bytes** out) {
     return guarded([&] {
         if (!p || !out) raise(PULSE_E_ARGUMENT, "null argument");
         validate_for_write(p);
-        const char* rname = repr_name(p->representation);
+        repr_name(p->representation);  // validates the representation
         if (p->codec > PULSE_GZIP6) raise(PULSE_E_ARGUMENT, "unknown codec");
         StageTimer tm{"write_patch_bytes"};
         Coded computed;

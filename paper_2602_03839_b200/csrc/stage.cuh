@@ -153,15 +153,14 @@ __device__ __forceinline__ void unstage(uint8_t* dst, const uint4* src, uint32_t
     const uint32_t tail_k = nblk - 1;
     const bool head_partial = s != 0 || len < 16;
     const bool tail_partial = ((s + len) & 15) != 0;
-    uint4 carry = make_uint4(0, 0, 0, 0);  // slot (round start - 1)
     uint4 head = make_uint4(0, 0, 0, 0), tail = head;  // partial blocks, held by their lanes
     for (uint32_t k0 = 0; k0 < nblk; k0 += 32) {
         const uint32_t k = k0 + lane;
-        const uint4 cur = k < nslots ? lds128(src + swz<V>(k)) : make_uint4(0, 0, 0, 0);
-        uint4 prv = shfl_up4(cur, 1);
-        if (lane == 0) prv = carry;
-        carry = shfl4(cur, 31);
         if (k >= nblk) continue;
+        const uint4 cur = k < nslots ? lds128(src + swz<V>(k)) : make_uint4(0, 0, 0, 0);
+        // the slot before: a second conflict-free load (consecutive lanes, consecutive slots)
+        // instead of eight shuffles and a carry across rounds
+        const uint4 prv = (s != 0 && k > 0) ? lds128(src + swz<V>(k - 1)) : make_uint4(0, 0, 0, 0);
         const uint4 out = s == 0 ? cur : funnel16(prv, cur, sw, sh);
         const bool partial = (k == 0 && head_partial) || (k == tail_k && tail_partial);
         if (!partial) *reinterpret_cast<uint4*>(base + 16 * k) = out;
