@@ -442,7 +442,8 @@ def run_pulse(args):
         k1_bytes = 4 * D_el
         k1_gbs = k1_bytes / (scan_ms / 1e3) / 1e9
         k1_moved = 4 * D_el + 6 * state["changes"]
-        # our launches per step: K1 (k1_tma, k1_finalize); K2 (COO: optimistic k2_layout + k2_emit, then
+        # our launches per step: K1 (k1_tma, k1_deferred [graph: k_set_cond; K1b runs only if a ticket
+        # was deferred], k1_finalize); K2 (COO: optimistic k2_layout + k2_emit, then
         # k2_scan_escapes / k2_layout / k2_emit that return at once unless an escape was seen; int32:
         # k2_layout, k2_emit); FLAT carry [sharded FLAT only]; apply (d_layout, f_stream agg, f_range_scan,
         # f_pass validate, its full re-check (exits at once unless a check failed), f_stream scatter,
@@ -490,7 +491,7 @@ def run_pulse(args):
                        for k, t, b in (("k1_scan", scan_max, 4 * d_total + 6 * changes_total),
                                        ("k2_emit", emit_max, 6 * changes_total + body_total),
                                        ("apply", apply_max, body_total + 2 * changes_total))},
-            "gpu_launches": (2 + n_emit + n_carry + n_apply) * args.steps,
+            "gpu_launches": (3 + n_emit + n_carry + n_apply) * args.steps,
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -89,6 +89,20 @@ __device__ __forceinline__ void warp_segscan2(uint64_t& r, uint64_t& c) {
     }
 }
 
+// The same on 32-bit words, segment head in bit 31 (values below 2^31).
+__device__ __forceinline__ void warp_segscan2_32(uint32_t& r, uint32_t& c) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t pr = __shfl_up_sync(0xffffffffu, r, off);
+        const uint32_t pc = __shfl_up_sync(0xffffffffu, c, off);
+        if (lane >= off) {
+            r = (r & 0x80000000u) ? r : ((pr + r) | (pr & 0x80000000u));
+            c = (c & 0x80000000u) ? c : ((pc + c) | (pc & 0x80000000u));
+        }
+    }
+}
+
 // ---- per-round walker (fallback for chunks that straddle patch entries) -------------------
 struct ECtx {
     uint32_t e;
@@ -633,7 +647,8 @@ __device__ __forceinline__ uint32_t stage_cover(uint4* dst, const uint8_t* g, ui
     const uint32_t s = uint32_t(ga & 15);
     const uint8_t* base = reinterpret_cast<const uint8_t*>(ga - s);
     const uint32_t nslots = len ? (s + len + 15) >> 4 : 0;
-    for (uint32_t q = lane; q < nslots; q += 32) cp_async16(dst + swz<V>(q), base + 16 * q);
+    const uint32_t sdst = smem_u32(dst);
+    for (uint32_t q = lane; q < nslots; q += 32) cp_async16_s(sdst + 16 * swz<V>(q), base + 16 * q);
     return s;
 }
 
@@ -765,11 +780,29 @@ __device__ __forceinline__ void chunk_body(const ApplyArgs& A, const SCtx& cur, 
         }
         lr = r | (kRepr == kI32 && lane_first ? H : 0);
     }
-    uint64_t ir = lr, ic = lc;
-    warp_segscan2(ir, ic);
-    const uint64_t tr = __shfl_sync(0xffffffffu, ir, 31), tc = __shfl_sync(0xffffffffu, ic, 31);
-    uint64_t er = __shfl_up_sync(0xffffffffu, ir, 1), ec = __shfl_up_sync(0xffffffffu, ic, 1);
-    if (lane == 0) er = ec = 0;
+    uint64_t tr, tc, er, ec;
+    if (coo) {
+        // COO lane aggregates fit 31 bits (<= 32 row bytes, <= 32 u16 columns per lane; <= 32 lanes):
+        // the warp scan runs on 32-bit words with the segment head in bit 31
+        uint32_t r = uint32_t(lr) | (lr & H ? 0x80000000u : 0u), cc = uint32_t(lc) | (lc & H ? 0x80000000u : 0u);
+        warp_segscan2_32(r, cc);
+        const uint32_t t_r = __shfl_sync(0xffffffffu, r, 31), t_c = __shfl_sync(0xffffffffu, cc, 31);
+        uint32_t e_r = __shfl_up_sync(0xffffffffu, r, 1), e_c = __shfl_up_sync(0xffffffffu, cc, 1);
+        if (lane == 0) e_r = e_c = 0;
+        auto widen = [](uint32_t x) { return uint64_t(x & 0x7FFFFFFFu) | (x >> 31 ? H : 0); };
+        tr = widen(t_r);
+        tc = widen(t_c);
+        er = widen(e_r);
+        ec = widen(e_c);
+    } else {
+        uint64_t ir = lr, ic = lc;
+        warp_segscan2(ir, ic);
+        tr = __shfl_sync(0xffffffffu, ir, 31);
+        tc = __shfl_sync(0xffffffffu, ic, 31);
+        er = __shfl_up_sync(0xffffffffu, ir, 1);
+        ec = __shfl_up_sync(0xffffffffu, ic, 1);
+        if (lane == 0) er = ec = 0;
+    }
     if (kAgg_) {
         uint64_t pend = kNoSlack;
         if (coo && hc && !lane_first) {

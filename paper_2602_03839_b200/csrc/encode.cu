@@ -99,6 +99,8 @@ struct K1Args {
     uint64_t* seg_start;
     uint64_t* status;
     unsigned long long* ticket;
+    ulonglong2* defer;              // (ticket, output offset) of the tickets K1b writes
+    unsigned long long* n_defer;
 };
 
 // Count / order / look-back / write for one loaded tile.  `prefetch` is called
@@ -242,17 +244,37 @@ namespace tma {
 #ifndef PULSE_K1_STAGECAP
 #define PULSE_K1_STAGECAP 2688
 #endif
-template <int S, int B, uint32_t RC, uint32_t SC>
+#ifndef PULSE_K1_DSTAGES
+#define PULSE_K1_DSTAGES 3
+#endif
+#ifndef PULSE_K1_DBUFS
+#define PULSE_K1_DBUFS 4
+#endif
+#ifndef PULSE_K1_DRECCAP
+#define PULSE_K1_DRECCAP 1344
+#endif
+#ifndef PULSE_K1_DSTAGECAP
+#define PULSE_K1_DSTAGECAP 8192
+#endif
+#ifndef PULSE_K1_DDENSE
+#define PULSE_K1_DDENSE 3072
+#endif
+template <int S, int B, uint32_t RC, uint32_t SC, uint32_t DT, uint32_t DF>
 struct Cfg {
     static constexpr int kStages = S;          // TMA ring stages (16 KiB prev + 16 KiB curr each)
     static constexpr int kBufs = B;            // ticket staging buffers (consumers may run ahead)
     static constexpr uint32_t kRecCap = RC;    // record mode: staged changed 16-byte vectors per buffer
     static constexpr uint32_t kStageCap = SC;  // element mode: staged changed elements per buffer
-    // changes above which the next ticket stages element entries (below the element capacity)
-    static constexpr uint32_t kDenseTicket = SC * 3 / 4 < 3072 ? SC * 3 / 4 : 3072;
+    static constexpr uint32_t kDenseTicket = DT;  // changes above which the next ticket stages element entries
+    static constexpr uint32_t kDeferTicket = DF;  // ... above which it is only counted and deferred to K1b
 };
-using SparseCfg = Cfg<PULSE_K1_STAGES, PULSE_K1_BUFS, PULSE_K1_RECCAP, PULSE_K1_STAGECAP>;
-using DenseCfg = Cfg<3, 4, 1344, 8192>;
+using SparseCfg = Cfg<PULSE_K1_STAGES, PULSE_K1_BUFS, PULSE_K1_RECCAP, PULSE_K1_STAGECAP,
+                      (PULSE_K1_STAGECAP * 3 / 4 < 3072 ? PULSE_K1_STAGECAP * 3 / 4 : 3072), PULSE_K1_STAGECAP>;
+using DenseCfg = Cfg<PULSE_K1_DSTAGES, PULSE_K1_DBUFS, PULSE_K1_DRECCAP, PULSE_K1_DSTAGECAP, PULSE_K1_DDENSE,
+                     PULSE_K1_DSTAGECAP>;
+// patches denser than ~4.5%: records only (no element staging), larger record buffers, fewer
+// stages; tickets too dense even for those are counted in K1 and written by K1b
+using Dense2Cfg = Cfg<2, 3, 2200, 0, 0xFFFFFFFFu, 8000>;
 constexpr uint32_t kSubElems = 8192;                 // elements per stage (16 KiB + 16 KiB)
 constexpr uint32_t kSubs = kTicketElems / kSubElems; // 8 sub-tiles per ticket
 constexpr int kConsumerWarps = 8;
@@ -262,7 +284,7 @@ constexpr int kLbWarps = 4;                          // warps 9..12
 constexpr int kLbFirst = kConsumerWarps + 1;
 constexpr int kLbThreads = kLbWarps * 32;
 constexpr int kThreadsTotal = (kConsumerWarps + 1 + kLbWarps) * 32;  // 416
-enum : uint32_t { kModeRecords = 0, kModeElements = 1 };
+enum : uint32_t { kModeRecords = 0, kModeElements = 1, kModeCount = 2 };
 constexpr uint32_t kChunks = kSubs * kConsumerWarps; // (sub-tile, warp) chunks per ticket
 constexpr uint32_t kBarLb = 2;                       // named barrier id of the look-back group
 static_assert(kVecPerWarp % 32 == 0, "whole vectors per lane");
@@ -300,8 +322,8 @@ struct Smem {
             uint2 meta[kRecCap];
         } rec;
         struct {
-            uint16_t idx[kStageCap];
-            uint16_t val[kStageCap];
+            uint16_t idx[kStageCap > 0 ? kStageCap : 1];
+            uint16_t val[kStageCap > 0 ? kStageCap : 1];
         } el;
     } stg[kBufs];
     uint32_t chunk_off[kBufs][kChunks];  // where each (sub, warp) chunk was staged (first record / element)
@@ -323,6 +345,7 @@ struct Smem {
 };
 static_assert(sizeof(Smem<SparseCfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
 static_assert(sizeof(Smem<DenseCfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
+static_assert(sizeof(Smem<Dense2Cfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
 }  // namespace tma
 
 // Look-back with 4 status words per lane per round (128 predecessors).
@@ -380,6 +403,7 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
     using namespace tma;
     constexpr int kStages = C::kStages, kBufs = C::kBufs;
     constexpr uint32_t kRecCap = C::kRecCap, kStageCap = C::kStageCap, kDenseTicket = C::kDenseTicket;
+    constexpr uint32_t kDeferTicket = C::kDeferTicket;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     tma::Smem<C>& S = *reinterpret_cast<tma::Smem<C>*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -583,7 +607,16 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
             }
 
             const uint32_t chunk = d.sub * kConsumerWarps + warp;
-            if (tmode == kModeRecords) {
+            if (tmode == kModeCount) {
+                // deferred ticket: counted here, written by K1b (k1_deferred) after K1
+                const uint32_t total = __reduce_add_sync(0xffffffffu, __popc(m[0]) + __popc(m[1]) + __popc(m[2]) +
+                                                                          __popc(m[3]));
+                if (lane == 0) {
+                    S.chunk_cnt[buf][chunk] = total;
+                    if (total) S.overflow[buf] = 1;
+                }
+                wcount += total;
+            } else if (tmode == kModeRecords) {
                 // one record per changed vector, records in (j, lane) order = element
                 // order; the flush group derives each record's element offset, so the
                 // consumers only need the chunk total (one warp reduction)
@@ -838,73 +871,12 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
                     }
                 }
             }
-        } else {
-            // dense ticket (more changes than the staging buffer holds): the look-back
-            // group re-streams it from global memory (L2-resident, TMA just read it):
-            // 16 elements per thread per round as two 16-byte loads of each snapshot,
-            // the next round prefetched in registers, one group scan per round.
-            const SegDesc sd = k.segs[ti.si];
-            const uint16_t* pp = k.prev_ptrs[sd.tensor] + sd.elem_off + ti.toff;
-            const uint16_t* cp = k.curr_ptrs[sd.tensor] + sd.elem_off + ti.toff;
-            const uint32_t nin = min(kTicketElems, sd.numel - ti.toff);
-            constexpr uint32_t kPer = 16, kRound = kLbThreads * kPer;  // 2048 elements per round
-            auto load16 = [&](uint32_t e, uint4 (&a)[2], uint4 (&c)[2]) {
-                if (e + kPer <= nin) {  // ticket bases are 16-byte aligned (tensor base, 2^31 and 2^16 offsets)
-                    a[0] = ld_stream(pp + e);
-                    a[1] = ld_stream(pp + e + 8);
-                    c[0] = ld_stream(cp + e);
-                    c[1] = ld_stream(cp + e + 8);
-                } else {
-                    uint32_t ta[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                    for (uint32_t q = 0; q < kPer && e + q < nin; ++q) {
-                        ta[q >> 1] |= uint32_t(pp[e + q]) << ((q & 1) * 16);
-                        tc[q >> 1] |= uint32_t(cp[e + q]) << ((q & 1) * 16);
-                    }
-                    a[0] = make_uint4(ta[0], ta[1], ta[2], ta[3]);
-                    a[1] = make_uint4(ta[4], ta[5], ta[6], ta[7]);
-                    c[0] = make_uint4(tc[0], tc[1], tc[2], tc[3]);
-                    c[1] = make_uint4(tc[4], tc[5], tc[6], tc[7]);
-                }
-            };
-            uint4 na[2], nc[2];
-            if (uint32_t(lt) * kPer < nin) load16(uint32_t(lt) * kPer, na, nc);
-            uint64_t run = 0;
-            for (uint32_t e0 = 0; e0 < nin; e0 += kRound) {
-                const uint32_t e = e0 + uint32_t(lt) * kPer;
-                uint4 av[2] = {na[0], na[1]}, cv2[2] = {nc[0], nc[1]};
-                const bool mine = e < nin;
-                if (e0 + kRound < nin && e + kRound < nin) load16(e + kRound, na, nc);
-                const uint32_t mm = mine ? (change_mask(av[0], cv2[0]) | (change_mask(av[1], cv2[1]) << 8)) : 0u;
-                const uint32_t cnt = __popc(mm);
-                uint32_t inc = cnt;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += x;
-                }
-                if (lane == 31) S.lb_warp_tot[warp - kLbFirst] = inc;
-                named_sync(kBarLb, kLbThreads);
-                uint32_t before = 0, all = 0;
-#pragma unroll
-                for (int w = 0; w < kLbWarps; ++w) {
-                    const uint32_t t = S.lb_warp_tot[w];
-                    if (w < warp - kLbFirst) before += t;
-                    all += t;
-                }
-                uint64_t pos = G + run + before + inc - cnt;
-                uint32_t m2 = mm;
-                while (m2) {
-                    const int q = __ffs(m2) - 1;
-                    m2 &= m2 - 1;
-                    if (pos < k.capacity) {
-                        k.out_idx[pos] = ti.toff + e + q;
-                        k.out_val[pos] = lane_value(q < 8 ? cv2[0] : cv2[1], q & 7);
-                    }
-                    ++pos;
-                }
-                run += all;
-                named_sync(kBarLb, kLbThreads);  // lb_warp_tot is rewritten next round
-            }
+        } else if (lt == 0 && count > 0) {
+            // staging overflowed (or the ticket was only counted): K1b writes this ticket after
+            // K1 from a list of (ticket, output offset), with the whole GPU's memory parallelism
+            // -- re-streaming it here would stall the ring behind four warps
+            const unsigned long long slot = atomicAdd(k.n_defer, 1ull);
+            k.defer[slot] = make_ulonglong2(ti.tile, G);
         }
         named_sync(kBarLb, kLbThreads);  // flush done before the buffer is reused
         if (lt == 0) {
@@ -913,7 +885,7 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
             S.overflow[buf] = 0;
             // layout for the next ticket staged in this buffer: neighbouring tickets
             // have similar density (same tensor), so follow this one's
-            S.mode[buf] = count > kDenseTicket ? kModeElements : kModeRecords;
+            S.mode[buf] = count > kDeferTicket ? kModeCount : count > kDenseTicket ? kModeElements : kModeRecords;
             S.tk_cnt[buf] = 0;
             S.tk_arrived[buf] = 0;
             mbar_arrive(&S.tk_empty[buf]);
@@ -921,6 +893,114 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
         if (++buf == kBufs) {
             buf = 0;
             bphase ^= 1;
+        }
+    }
+}
+
+// K1b: the deferred tickets -- dense beyond what K1's staging holds.  K1 counted them
+// and its look-back placed them (output offset G); here a CTA re-streams one ticket at
+// a time (8 loads of 16 bytes in flight per thread, several CTAs per SM) and writes
+// every change at G + its ordered position.  Nothing to do (one atomic per CTA) when
+// no ticket was deferred -- the common case for sparse patches.
+constexpr int kDeferThreads = 256;
+__global__ void __launch_bounds__(kDeferThreads, 3) k1_deferred(K1Args k, const uint64_t* __restrict__ n_defer,
+                                                             unsigned long long* __restrict__ cursor) {
+    __shared__ uint32_t s_warp[kDeferThreads / 32];
+    __shared__ uint64_t s_t;
+    __shared__ uint32_t s_out[32 * kDeferThreads];  // a round's changes: (offset in round << 16) | value
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t n = *n_defer;
+    while (true) {
+        if (tid == 0) s_t = atomicAdd(cursor, 1ull);
+        __syncthreads();
+        const uint64_t t = s_t;
+        __syncthreads();
+        if (t >= n) return;
+        const ulonglong2 dt = k.defer[t];
+        const uint64_t tile = dt.x;
+        const uint32_t si = k.tile_seg[tile];
+        const SegDesc sd = k.segs[si];
+        const uint32_t toff = uint32_t((tile - sd.ticket_start) * kTicketElems);
+        const uint32_t nin = min(kTicketElems, sd.numel - toff);
+        const uint16_t* pp = k.prev_ptrs[sd.tensor] + sd.elem_off + toff;
+        const uint16_t* cp = k.curr_ptrs[sd.tensor] + sd.elem_off + toff;
+        uint64_t pos0 = dt.y;
+        // rounds of 8192 elements: thread `tid` compares elements [32 tid, 32 tid + 32) of the
+        // round; the next round's 8 loads are issued before this round is compacted and written
+        auto load_round = [&](uint32_t r0, uint4 (&a)[4], uint4 (&c)[4]) {
+            const uint32_t e = r0 + 32 * uint32_t(tid);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t ej = e + 8 * j;
+                if (ej + 8 <= nin) {
+                    a[j] = ld_stream(pp + ej);
+                    c[j] = ld_stream(cp + ej);
+                } else {
+                    uint32_t ta[4] = {0, 0, 0, 0}, tb[4] = {0, 0, 0, 0};
+                    for (uint32_t q = 0; q < 8 && ej + q < nin; ++q) {
+                        ta[q >> 1] |= uint32_t(pp[ej + q]) << ((q & 1) * 16);
+                        tb[q >> 1] |= uint32_t(cp[ej + q]) << ((q & 1) * 16);
+                    }
+                    a[j] = make_uint4(ta[0], ta[1], ta[2], ta[3]);
+                    c[j] = make_uint4(tb[0], tb[1], tb[2], tb[3]);
+                }
+            }
+        };
+        uint4 na[4], nc[4];
+        load_round(0, na, nc);
+        for (uint32_t r0 = 0; r0 < nin; r0 += 32 * kDeferThreads) {
+            uint4 a[4], c[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                a[j] = na[j];
+                c[j] = nc[j];
+            }
+            if (r0 + 32 * kDeferThreads < nin) load_round(r0 + 32 * kDeferThreads, na, nc);
+            uint32_t m[4], cnt = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                m[j] = change_mask(a[j], c[j]);
+                cnt += __popc(m[j]);
+            }
+            uint32_t inc = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += x;
+            }
+            if (lane == 31) s_warp[warp] = inc;
+            __syncthreads();
+            uint32_t before = 0, all = 0;
+#pragma unroll
+            for (int w = 0; w < kDeferThreads / 32; ++w) {
+                const uint32_t x = s_warp[w];
+                before += w < warp ? x : 0u;
+                all += x;
+            }
+            // compact the round into shared memory (element order), then write it out with
+            // consecutive threads on consecutive outputs (coalesced; per-thread runs would
+            // scatter every store instruction over 32 sectors)
+            uint32_t o = before + inc - cnt;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t mm = m[j];
+                while (mm) {
+                    const int q = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    s_out[o++] = (uint32_t(32 * tid + 8 * j + q) << 16) | lane_value(c[j], q);
+                }
+            }
+            __syncthreads();
+            for (uint32_t i = tid; i < all; i += kDeferThreads) {
+                const uint64_t pos = pos0 + i;
+                if (pos < k.capacity) {
+                    const uint32_t w = s_out[i];
+                    k.out_idx[pos] = toff + r0 + (w >> 16);
+                    k.out_val[pos] = uint16_t(w);
+                }
+            }
+            __syncthreads();  // s_warp / s_out are rewritten next round
+            pos0 += all;
         }
     }
 }
@@ -994,7 +1074,8 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
     cudaMemsetAsync(p.counters, 0, 8 * sizeof(uint64_t), s);
     static const int experiment = getenv("PULSE_K1_EXPERIMENT") ? atoi(getenv("PULSE_K1_EXPERIMENT")) : 0;
     K1Args k{p.trace, experiment, p.segs, p.tile_seg, p.n_segs, p.n_tiles, p.slot[prev_slot], p.slot[curr_slot], p.idx32, p.val16,
-             p.cap, p.seg_start, p.k1_status, reinterpret_cast<unsigned long long*>(p.counters)};
+             p.cap, p.seg_start, p.k1_status, reinterpret_cast<unsigned long long*>(p.counters),
+             p.k1_defer, reinterpret_cast<unsigned long long*>(p.counters + 1)};
     if (p.n_tiles > 0) {
         static PerDeviceInt occ_static, occ_ticket, tma_attr;
         int& per_sm_static = occ_static.here();
@@ -1014,6 +1095,8 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
                                      int(sizeof(tma::Smem<tma::SparseCfg>)));
                 cudaFuncSetAttribute(k1_tma<tma::DenseCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(sizeof(tma::Smem<tma::DenseCfg>)));
+                cudaFuncSetAttribute(k1_tma<tma::Dense2Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(tma::Smem<tma::Dense2Cfg>)));
                 attr = 1;
             }
             K1Args kt = k;
@@ -1022,16 +1105,27 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
             const uint64_t grid = std::min<uint64_t>(uint64_t(sm_count()), p.tma_tiles);
             // the plan's change capacity says which regime the caller sized it for: >= 3% of its
             // elements -> dense staging (element entries need room), else more tickets in flight
-            const int shape_override = [] {  // PULSE_K1_SHAPE=sparse|dense (tests, A/B runs; read per launch)
+            const int shape_override = [] {  // PULSE_K1_SHAPE=sparse|dense|dense2 (tests, A/B runs; per launch)
                 const char* e = getenv("PULSE_K1_SHAPE");
-                return !e ? -1 : std::string(e) == "dense" ? 1 : std::string(e) == "sparse" ? 0 : -1;
+                return !e ? -1 : std::string(e) == "dense2" ? 2 : std::string(e) == "dense" ? 1
+                               : std::string(e) == "sparse" ? 0 : -1;
             }();
-            if (shape_override >= 0 ? shape_override == 1 : p.k1_dense != 0) {
+            const int shape = shape_override >= 0 ? shape_override : int(p.k1_dense);
+            if (shape == 2) {
+                k1_tma<tma::Dense2Cfg><<<unsigned(grid), tma::kThreadsTotal, sizeof(tma::Smem<tma::Dense2Cfg>), s>>>(kt);
+            } else if (shape == 1) {
                 k1_tma<tma::DenseCfg><<<unsigned(grid), tma::kThreadsTotal, sizeof(tma::Smem<tma::DenseCfg>), s>>>(kt);
             } else {
                 k1_tma<tma::SparseCfg><<<unsigned(grid), tma::kThreadsTotal, sizeof(tma::Smem<tma::SparseCfg>), s>>>(kt);
             }
             PULSE_LAUNCHED("k1_tma", s);
+            // K1b only if some ticket was deferred (a conditional graph node under capture;
+            // eagerly it launches and returns at once on an empty list)
+            launch_gated(s, reinterpret_cast<const uint32_t*>(p.counters + 1), [&](cudaStream_t gs) {
+                k1_deferred<<<unsigned(sm_count() * 6), kDeferThreads, 0, gs>>>(
+                    kt, p.counters + 1, reinterpret_cast<unsigned long long*>(p.counters + 2));
+                PULSE_LAUNCHED("k1_deferred", gs);
+            });
             launched = true;
         }
         if (!launched && k1_variant() == 2 && per_sm_static > 0) {

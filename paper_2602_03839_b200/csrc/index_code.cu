@@ -575,9 +575,8 @@ struct LayoutArgs {
     uint64_t* err;
     uint64_t cap;  // K1 capacity (mode A); ~0 for mode B
     const uint32_t* run_if;  // run only if *run_if != 0 (exact re-run after an optimistic pass)
-    bool optimistic;         // COO: lay out assuming no escapes (zeroes range_pre itself)
+    bool optimistic;         // COO: lay out assuming no escapes (the optimistic emit reads no range_pre)
     uint32_t* zero_u32[3];   // optimistic: per-call state this kernel clears first (t_resc, t_cesc, esc flag)
-    uint64_t n_range_pre;    //   and range_pre entries to clear
 };
 
 __device__ __forceinline__ int64_t entry_local(const EntryMap& em, uint64_t i) {
@@ -603,7 +602,6 @@ __global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
             *a.zero_u32[2] = 0;
             *a.err = kNoError;
         }
-        for (uint64_t i = tid; i < a.n_range_pre; i += kLayoutThreads) a.range_pre[i] = make_ulonglong2(0, 0);
         __syncthreads();
     }
 
@@ -991,7 +989,7 @@ k2_emit(EntryMap em, uint32_t repr, const TensorLayout* __restrict__ tlay,
         prefetch(nx, b ^ 1);
         if (cur.range_start()) {
             R = Cc = 0;
-            if (coo) {
+            if (coo && !esc_flag) {  // exact pass: escapes before the range (the optimistic pass assumes none)
                 const ulonglong2 p = range_pre[cur.rg];
                 R = p.x;
                 Cc = p.y;
@@ -1095,7 +1093,6 @@ static void emit_common(const PlanDev& p, const EntryMap& em, uint32_t repr, boo
     a.zero_u32[0] = p.t_resc;
     a.zero_u32[1] = p.t_cesc;
     a.zero_u32[2] = p.d_flags + 2;
-    a.n_range_pre = p.cap / kRangeEntries + 2;
     if (optimistic) {
         // Optimistic COO_DOWNSCALED: lay out and emit assuming no entry needs an
         // escape (none does on these shapes at <= 99.9% sparsity); the emit flags

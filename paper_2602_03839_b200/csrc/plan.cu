@@ -159,7 +159,7 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
     p.cap = std::max<uint64_t>(max_changes, 1);
     uint64_t elems = 0;
     for (uint32_t t = 0; t < n_tensors; ++t) elems += tensors[t].numel;
-    p.k1_dense = p.cap * 100 >= elems * 3 ? 1u : 0u;
+    p.k1_dense = p.cap * 1000 >= elems * 45 ? 2u : p.cap * 100 >= elems * 3 ? 1u : 0u;
     const uint64_t T = n_tensors, S = segs.size(), cap = p.cap;
     const uint64_t n_chunks = cap / kChunkEntries + 2;
     p.dec_bytes_cap = 10 * cap + kParseBytes * (T + 1);
@@ -174,7 +174,7 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
     for (int s = 0; s < PULSE_MAX_SLOTS; ++s) { uint16_t** sp = nullptr; A(sp, T); p.slot[s] = sp; }
     // idx32 / val16: +8 entries so 16-byte async copies of a partial last chunk stay in bounds
     A(p.idx32, cap + 8); A(p.val16, cap + 8); A(p.seg_start, S + 1); A(p.k1_status, tiles + 1);
-    A(p.counters, 8); A(p.scan, 1);
+    A(p.counters, 8); A(p.scan, 1); A(p.k1_defer, tickets + 1);
     ColDiv* coldiv_d = nullptr; A(coldiv_d, T);
     A(p.range_cnt, cap / 4096 + 2); A(p.range_pre, cap / 4096 + 2);
     A(p.t_resc, T); A(p.t_cesc, T); A(p.tlay, T); A(p.err, 1); A(p.result, 1);

@@ -108,6 +108,10 @@ __device__ __forceinline__ void stage(uint4* dst, const uint8_t* g, uint32_t len
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
+// The same with the shared-memory address already in the .shared window (no per-copy cvta).
+__device__ __forceinline__ void cp_async16_s(uint32_t sdst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -118,7 +122,8 @@ template <int V>
 __device__ __forceinline__ void stage_async(uint4* dst, const uint8_t* g, uint32_t len) {
     const int lane = threadIdx.x & 31;
     const uint32_t nslots = (len + 15) >> 4;
-    for (uint32_t q = lane; q < nslots; q += 32) cp_async16(dst + swz<V>(q), g + 16 * q);
+    const uint32_t sdst = smem_u32(dst);
+    for (uint32_t q = lane; q < nslots; q += 32) cp_async16_s(sdst + 16 * swz<V>(q), g + 16 * q);
 }
 
 // 32-bit word `w` of a swizzled buffer (single scalar accesses only).
