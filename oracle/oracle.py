@@ -155,7 +155,8 @@ class Reference:
 
     def _take_buf(self, h) -> bytes:
         n = self.L.ref_buf_size(h)
-        out = C.string_at(self.L.ref_buf_data(h), n) if n else b""
+        # (ctypes.string_at takes a C int size: buffers of 2 GiB and more go through an array view)
+        out = bytes((C.c_char * n).from_address(self.L.ref_buf_data(h))) if n else b""
         self.L.ref_buf_free(h)
         return out
 

@@ -85,7 +85,7 @@ __device__ __forceinline__ uint16_t lane_value(const uint4& v, int k) {
 
 struct K1Args {
     uint32_t* trace;  // optional per-ticket progress trace (debug)
-    int experiment;   // 1: consumers only release stages (TMA streaming rate); 2: no global
+    int experiment;   // 1: consumers only release stages (TMA streaming rate); 4: coalesced dummy write-back; 2: no global
                       // write-back of staged entries; 3: consumers count but do not stage
     const SegDesc* segs;
     const uint32_t* tile_seg;
@@ -798,6 +798,15 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
         const uint32_t count = S.lb_count;
         if (k.experiment == 2 || k.experiment == 3) {
             // attribution experiments: no write-back
+        } else if (k.experiment == 4) {
+            // attribution: the same bytes written coalesced (consecutive threads, consecutive outputs)
+            for (uint32_t i = lt; i < count; i += kLbThreads) {
+                const uint64_t pos = G + i;
+                if (pos < k.capacity) {
+                    k.out_idx[pos] = i;
+                    k.out_val[pos] = 0;
+                }
+            }
         } else if (!S.overflow[buf] && S.mode[buf] == kModeRecords) {
             // expand the staged records: record -> its changed elements at G + its
             // chunk's element prefix + its offset in the chunk.  Records sit in the

@@ -34,6 +34,7 @@ struct SegDesc {
     uint32_t numel;        // elements in the segment (<= 2^31)
 };
 constexpr uint32_t kTicketElems = 65536;
+constexpr uint32_t kK2RangeEntries = 1024;  // K2 warp range (index_code.cu kRangeEntries)
 
 // Division by a tensor's column extent (COO_DOWNSCALED view, patch.hpp:105-109):
 // q = (umulhi(n, magic) + n) >> shift for 32-bit n when cols < 2^32.
@@ -105,8 +106,8 @@ struct PlanDev {
     uint64_t* counters;         // [8] tickets
     pulse_scan_summary* scan;   // device
     const ColDiv* coldiv;       // [T]
-    uint64_t* range_cnt;        // [cap/4096 + 2] packed (row | col << 32) escapes per 4096-entry warp range
-    ulonglong2* range_pre;      // [cap/4096 + 2] global (row, col) escapes before each range
+    uint64_t* range_cnt;        // [cap/kK2RangeEntries + 2] packed (row | col << 32) escapes per K2 warp range
+    ulonglong2* range_pre;      // [cap/kK2RangeEntries + 2] global (row, col) escapes before each range
     uint32_t* t_resc;           // [T]
     uint32_t* t_cesc;           // [T]
     TensorLayout* tlay;         // [T]

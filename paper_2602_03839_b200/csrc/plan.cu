@@ -176,7 +176,7 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
     A(p.idx32, cap + 8); A(p.val16, cap + 8); A(p.seg_start, S + 1); A(p.k1_status, tiles + 1);
     A(p.counters, 8); A(p.scan, 1); A(p.k1_defer, tickets + 1);
     ColDiv* coldiv_d = nullptr; A(coldiv_d, T);
-    A(p.range_cnt, cap / 4096 + 2); A(p.range_pre, cap / 4096 + 2);
+    A(p.range_cnt, cap / kK2RangeEntries + 2); A(p.range_pre, cap / kK2RangeEntries + 2);
     A(p.t_resc, T); A(p.t_cesc, T); A(p.tlay, T); A(p.err, 1); A(p.result, 1);
     A(id_segs_d, T); A(id_first_d, T + 1); A(p.id_start, T + 1);
     A(p.elay, T); A(p.d_es, T + 1); A(p.d_ck, T + 1); A(p.d_cu, T + 1);

@@ -247,3 +247,48 @@ def test_host_api_on_two_devices_in_one_process(golden):
             for a, b in zip(sorted(out.tensors, key=lambda t: t.name), curr.sorted()):
                 assert np.array_equal(a.data, b.data), (dev, repr_)
     torch.cuda.set_device(0)
+
+
+@pytest.mark.gpu
+def test_index_helpers_large_and_errors_match_reference():
+    """delta_decode_indices / downscale_coo at sizes spanning many scan blocks, the first
+    failure deep inside, and downscale_coo entries that all take both escapes (11 bytes
+    each) right after a small call sized the library's scratch (the advisor's overrun case)."""
+    if not have_reference():
+        pytest.skip("oracle/_ref not built")
+    from oracle.oracle import OracleError
+    R = reference()
+    rng = np.random.default_rng(11)
+    gaps = rng.integers(1, 1000, 3_000_000).astype(np.int64)
+    idx = np.cumsum(gaps)
+    assert np.array_equal(H.delta_decode_indices(gaps), idx)
+    bad = gaps.copy()
+    bad[2_345_678] = 0
+    bad[2_900_000] = -5
+    with pytest.raises(H.PulseError) as ei:
+        H.delta_decode_indices(bad)
+    with pytest.raises(OracleError) as er:
+        R.delta_decode(bad)
+    assert ei.value.kind == er.value.kind
+    rows = np.sort(rng.integers(0, 1 << 30, 2_000_000)).astype(np.int64)
+    cols = rng.integers(0, 1 << 17, 2_000_000).astype(np.int64)
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    keep = np.concatenate([[True], (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])])
+    rows, cols = rows[keep], cols[keep]
+    assert H.downscale_coo(rows, cols) == R.downscale_coo(rows, cols)
+    # small call first, then entries that all need the row and the column escape
+    H.downscale_coo(np.array([0, 1], np.int64), np.array([0, 0], np.int64))
+    m = 200_000
+    r2 = (np.arange(m, dtype=np.int64) + 1) * 300    # row gaps (and the first row) 300 >= 255
+    c2 = np.full(m, 70_000, dtype=np.int64)          # every entry a new row, column 70000 >= 65535
+    want = R.downscale_coo(r2, c2)
+    assert len(want) == 11 * m
+    assert H.downscale_coo(r2, c2) == want
+    r3, c3 = r2.copy(), c2.copy()
+    r3[150_000] = r3[149_999]                        # same row, column not increasing
+    with pytest.raises(H.PulseError) as ei:
+        H.downscale_coo(r3, c3)
+    with pytest.raises(OracleError) as er:
+        R.downscale_coo(r3, c3)
+    assert ei.value.kind == er.value.kind and str(ei.value).endswith(er.value.msg)
