@@ -456,7 +456,8 @@ __global__ void __launch_bounds__(kThreads)
 d_assemble(const EntryLayout* __restrict__ el, const uint64_t* __restrict__ es, uint32_t n_e,
            const uint32_t* __restrict__ rowgap, const uint32_t* __restrict__ colent,
            uint64_t* __restrict__ st_rows, uint64_t* __restrict__ st_cols, uint64_t* __restrict__ totals,
-           uint64_t* __restrict__ out, uint64_t* __restrict__ err, const uint32_t* __restrict__ flags) {
+           uint64_t* __restrict__ out, uint64_t* __restrict__ err, const uint32_t* __restrict__ flags,
+           int64_t* __restrict__ raw_rows = nullptr, int64_t* __restrict__ raw_cols = nullptr) {
     if (*(volatile const uint32_t*)flags == 0) return;  // fixed-layout fast path handled it
     constexpr uint64_t H = SegSumOp::kHead;
     __shared__ uint64_t s_warp[kWarps];
@@ -501,6 +502,11 @@ d_assemble(const EntryLayout* __restrict__ el, const uint64_t* __restrict__ es, 
             const EntryLayout& L = el[e];
             if (!new_row && entry == 0) { report(err, error_key(e, kStageCols, o, kZeroColGap)); return; }
             const uint64_t r = row & (H - 1), cc = col & (H - 1);
+            if (raw_rows) {  // upscale_coo: the coordinates themselves, no tensor range checks
+                raw_rows[i] = int64_t(r);
+                raw_cols[i] = int64_t(cc);
+                return;
+            }
             if (cc >= L.cols) { report(err, error_key(e, kStageRange, o, kColRange)); return; }
             const uint64_t flat = r * L.cols + cc;
             if (flat >= L.numel) { report(err, error_key(e, kStageRange, o, kIdxRange)); return; }
@@ -647,6 +653,37 @@ void launch_apply_idx64(const PlanDev& p, const int64_t* idx64, const uint16_t* 
             }
     }
     d_finalize<<<1, 32, 0, s>>>(p.d_totals, n_entries, p.err, result);
+    PULSE_LAUNCHED("d_finalize", s);
+}
+
+// upscale_coo (index_coding.hpp:130-158) of one payload, in parallel: the general decoder's
+// row and column stream parses (sync-point rule) for a one-entry table, then the segmented
+// sums written as (row, column) pairs.  The caller's plan has one tensor; its geometry is
+// not checked (no range checks in raw mode).
+__global__ void d_force_general(uint32_t* __restrict__ flags) { flags[0] = 1u; }
+
+void launch_coo_unpack_par(const PlanDev& p, const uint8_t* body, const pulse_patch_entry* entry,
+                           int64_t* rows, int64_t* cols, pulse_result* result, cudaStream_t s) {
+    decode_prologue(p, entry, 1, PULSE_COO_DOWNSCALED, s);
+    d_force_general<<<1, 1, 0, s>>>(p.d_flags);
+    PULSE_LAUNCHED("d_force_general", s);
+    const unsigned g = persistent_grid();
+    uint64_t* st0 = p.d_status;
+    uint64_t* st1 = p.d_status + p.d_status_len;
+    uint64_t* st2 = p.d_status + 2 * p.d_status_len;
+    uint64_t* st3 = p.d_status + 3 * p.d_status_len;
+    d_clear_status<<<g, kThreads, 0, s>>>(p.d_status, 4 * p.d_status_len, p.d_flags);
+    PULSE_LAUNCHED("d_clear_status", s);
+    d_rows<<<g, kThreads, 0, s>>>(p.elay, p.d_ck, 1, body, st2, p.d_totals, p.rowgap, p.err, p.d_flags);
+    PULSE_LAUNCHED("d_rows", s);
+    d_col_layout<<<1, kLT, 0, s>>>(p.elay, 1, p.d_cu, p.d_totals, p.err, p.d_flags);
+    PULSE_LAUNCHED("d_col_layout", s);
+    d_cols<<<g, kThreads, 0, s>>>(p.elay, p.d_cu, 1, body, st3, p.d_totals, p.colent, p.err, p.d_flags);
+    PULSE_LAUNCHED("d_cols", s);
+    d_assemble<<<g, kThreads, 0, s>>>(p.elay, p.d_es, 1, p.rowgap, p.colent, st0, st1, p.d_totals, nullptr, p.err,
+                                      p.d_flags, rows, cols);
+    PULSE_LAUNCHED("d_assemble", s);
+    d_finalize<<<1, 32, 0, s>>>(p.d_totals, 1, p.err, result);
     PULSE_LAUNCHED("d_finalize", s);
 }
 

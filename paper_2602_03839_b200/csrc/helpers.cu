@@ -2,9 +2,9 @@
 // conversions (include/pulse_cuda.h, "host-buffer API").  Sizes here are
 // whatever a caller hands the reference's helper functions: grid-stride maps,
 // and reduce-then-scan over up to 1024 block segments for the prefix sums of
-// delta_decode_indices and downscale_coo.  upscale_coo's stream parse stays
-// sequential here (the apply path parses in parallel, decode.cu).  The hot
-// path does not use these.
+// delta_decode_indices and downscale_coo.  upscale_coo runs on the general
+// decoder's parallel parse (decode.cu launch_coo_unpack_par).  The hot path
+// does not use these.
 #include <mutex>
 
 #include "device.cuh"
@@ -200,44 +200,6 @@ __global__ void __launch_bounds__(kHT) k_coo_write(const int64_t* __restrict__ r
     }
 }
 
-// upscale_coo (index_coding.hpp:130-158): one sequential parse, as the format
-// carries no entry offsets (a helper; the apply path parses in parallel).
-__global__ void k_coo_unpack(const uint8_t* __restrict__ p, uint64_t len, uint64_t count, int64_t* __restrict__ rows,
-                             int64_t* __restrict__ cols, uint64_t* __restrict__ err) {
-    if (threadIdx.x || blockIdx.x) return;
-    uint64_t pos = 0;
-    int64_t row = 0, col = 0;
-    for (uint64_t i = 0; i < count; ++i) {
-        if (pos + 1 > len) { report(err, error_key(0, kStageRows, i, kTrunc)); return; }
-        int64_t e = p[pos++];
-        if (e == 0xFF) {
-            if (pos + 4 > len) { report(err, error_key(0, kStageRows, i, kTrunc)); return; }
-            e = rd_u32(p + pos);
-            pos += 4;
-        }
-        row = i == 0 ? e : row + e;
-        rows[i] = row;
-    }
-    for (uint64_t i = 0; i < count; ++i) {
-        const bool nr = i == 0 || rows[i] != rows[i - 1];
-        if (pos + 2 > len) { report(err, error_key(0, kStageCols, i, kTrunc)); return; }
-        int64_t e = rd_u16(p + pos);
-        pos += 2;
-        if (e == 0xFFFF) {
-            if (pos + 4 > len) { report(err, error_key(0, kStageCols, i, kTrunc)); return; }
-            e = rd_u32(p + pos);
-            pos += 4;
-        }
-        if (nr) col = e;
-        else {
-            if (e <= 0) { report(err, error_key(0, kStageCols, i, kZeroColGap)); return; }
-            col += e;
-        }
-        cols[i] = col;
-    }
-    if (pos != len) report(err, error_key(0, kStageTrailing, 0, kTrailing));
-}
-
 // Values at decoded indices: out[i] = W_t[idx[i]] for entry e's tensor t,
 // entries [start[e], start[e+1]) (the resident apply's undo copy).
 __global__ void k_gather_values(uint16_t* const* __restrict__ w, const pulse_patch_entry* __restrict__ ents,
@@ -304,12 +266,6 @@ void launch_coo_pack(const int64_t* rows, const int64_t* cols, uint64_t n, uint8
     k_coo_write<<<nb, kHT, 0, s>>>(rows, cols, n, seg, nb, part_r, part_c, out, nbytes, err);
     PULSE_LAUNCHED("k_coo_write", s);
 }
-void launch_coo_unpack(const uint8_t* p, uint64_t len, uint64_t count, int64_t* rows, int64_t* cols, uint64_t* err,
-                       cudaStream_t s) {
-    k_coo_unpack<<<1, 32, 0, s>>>(p, len, count, rows, cols, err);
-    PULSE_LAUNCHED("k_coo_unpack", s);
-}
-
 PULSE_DEFINE_WATCHDOG_SETTER(set_watchdog_helpers)
 
 }  // namespace dev

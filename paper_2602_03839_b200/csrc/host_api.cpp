@@ -1766,27 +1766,31 @@ pulse_status pulse_downscale_coo(const int64_t* rows, uint64_t n_rows, const int
 
 pulse_status pulse_upscale_coo(const uint8_t* data, uint64_t n, uint64_t count, int64_t* rows, int64_t* cols) {
     return guarded([&] {
+        if (count == 0) {  // index_coding.hpp:154-156: nothing to read, anything left is trailing
+            if (n) raise(PULSE_E_CORRUPT_STREAM, "downscaled payload has trailing bytes");
+            return;
+        }
+        if (!data && n) raise(PULSE_E_ARGUMENT, "null argument");
         Engine& E = engine();
         std::lock_guard<std::mutex> lk(E.mu);
-        uint8_t* dp = E.body.as<uint8_t>(n + 16);
+        // the general decoder's parallel parse of a one-entry table (decode.cu launch_coo_unpack_par)
+        std::vector<pulse_tensor_geom> geom(1);
+        geom[0].numel = count;
+        geom[0].cols = 1;
+        pulse_plan* plan = E.get_plan(geom, std::max<uint64_t>({count, n / 3 + 1, 1}));
+        uint8_t* dp = E.body.as<uint8_t>(n + 64);
         int64_t* d = E.out64.as<int64_t>(2 * count + 2);
-        uint64_t* err = E.misc.as<uint64_t>(1);
-        cuda_check(cudaMemsetAsync(err, 0xFF, 8, E.stream), "memset");
         if (n) E.stager.h2d(dp, data, n, E.stream);
-        launch_coo_unpack(dp, n, count, d, d + count, err, E.stream);
-        uint64_t k = 0;
-        cuda_check(counted_copy(&k, err, 8, cudaMemcpyDeviceToHost, E.stream), "D2H");
+        const pulse_patch_entry ent{0, 0, count, 0, n, n};
+        auto* dent = E.entries.as<pulse_patch_entry>(1);
+        cuda_check(counted_copy(dent, &ent, sizeof(ent), cudaMemcpyHostToDevice, E.stream), "H2D");
+        auto* dres = E.result.as<pulse_result>(1);
+        launch_coo_unpack_par(plan->dev, dp, dent, d, d + count, dres, E.stream);
+        const pulse_result r = fetch_result(E, dres);
+        if (r.status != PULSE_OK) raise(pulse_status(r.status), device_message(r, "", nullptr, PULSE_COO_DOWNSCALED));
+        E.stager.d2h(rows, d, count * 8, E.stream);
+        E.stager.d2h(cols, d + count, count * 8, E.stream);
         E.sync();
-        if (k != kNoError) {
-            const uint32_t c = key_check(k);
-            if (c == kTrunc) raise(PULSE_E_TRUNCATION, "unexpected end of data");
-            if (c == kZeroColGap) raise(PULSE_E_CORRUPT_STREAM, "non-positive column gap within a row");
-            raise(PULSE_E_CORRUPT_STREAM, "downscaled payload has trailing bytes");
-        }
-        if (count) {
-            E.stager.d2h(rows, d, count * 8, E.stream);
-            E.stager.d2h(cols, d + count, count * 8, E.stream);
-        }
     });
 }
 

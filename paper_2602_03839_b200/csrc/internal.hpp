@@ -191,8 +191,8 @@ void launch_delta_encode(const int64_t* in, uint64_t n, int64_t* out, uint64_t* 
 void launch_delta_decode(const int64_t* in, uint64_t n, int64_t* out, uint64_t* err, cudaStream_t s);
 void launch_coo_pack(const int64_t* rows, const int64_t* cols, uint64_t n, uint8_t* out, uint64_t* nbytes,
                      uint64_t* err, cudaStream_t s);
-void launch_coo_unpack(const uint8_t* p, uint64_t len, uint64_t count, int64_t* rows, int64_t* cols, uint64_t* err,
-                       cudaStream_t s);
+void launch_coo_unpack_par(const PlanDev& p, const uint8_t* body, const pulse_patch_entry* entry, int64_t* rows,
+                           int64_t* cols, pulse_result* result, cudaStream_t s);
 void set_watchdog_helpers(unsigned long long* slot);
 void set_watchdog_encode(unsigned long long* slot);
 void set_watchdog_decode(unsigned long long* slot);

@@ -292,3 +292,47 @@ def test_index_helpers_large_and_errors_match_reference():
     with pytest.raises(OracleError) as er:
         R.downscale_coo(r3, c3)
     assert ei.value.kind == er.value.kind and str(ei.value).endswith(er.value.msg)
+
+
+@pytest.mark.gpu
+def test_upscale_coo_parallel_matches_reference():
+    """upscale_coo (index_coding.hpp:130-158) on the general decoder's parallel parse:
+    large payloads with and without escapes, and damaged ones (truncated row / column
+    streams, trailing bytes, zero column gaps, injected 0xFF / 0xFFFF markers) give the
+    reference's coordinates or its exception class and message."""
+    if not have_reference():
+        pytest.skip("oracle/_ref not built")
+    from oracle.oracle import OracleError
+    R = reference()
+    rng = np.random.default_rng(12)
+    for n, rmax, cmax in ((1_000_000, 1 << 22, 4000), (300_000, 1 << 31, 1 << 20), (50, 300, 70_000)):
+        rows = np.sort(rng.integers(0, rmax, n)).astype(np.int64)
+        cols = rng.integers(0, cmax, n).astype(np.int64)
+        order = np.lexsort((cols, rows))
+        rows, cols = rows[order], cols[order]
+        keep = np.concatenate([[True], (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])])
+        rows, cols = rows[keep], cols[keep]
+        blob = R.downscale_coo(rows, cols)
+        r2, c2 = H.upscale_coo(blob, rows.size)
+        assert np.array_equal(r2, rows) and np.array_equal(c2, cols)
+        variants = [blob[:-1], blob[: len(blob) // 2], blob + b"\x00", blob[:3]]
+        for _ in range(30):
+            b = bytearray(blob)
+            p = int(rng.integers(0, len(b)))
+            b[p:p + 2] = rng.choice([b"\xff\xff", b"\x00\x00", b"\xff", b"\x00"])
+            variants.append(bytes(b))
+        for v in variants:
+            try:
+                want = ("ok", R.upscale_coo(v, rows.size))
+            except OracleError as e:
+                want = (e.kind, e.msg)
+            try:
+                got = ("ok", H.upscale_coo(v, rows.size))
+            except H.PulseError as e:
+                got = (e.kind, str(e).split(": ", 1)[1])
+            assert got[0] == want[0], (got[0], want[0])
+            if want[0] == "ok":
+                assert np.array_equal(got[1][0], want[1][0]) and np.array_equal(got[1][1], want[1][1])
+            else:
+                assert got[1] == want[1]
+    assert H.upscale_coo(b"", 0)[0].size == 0
