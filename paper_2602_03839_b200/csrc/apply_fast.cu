@@ -8,7 +8,7 @@
 // patch.hpp:120-156).  Decoding is then a pair of segmented prefix sums over
 // the entries, read straight from the body.  The pipeline (launch_all):
 //
-//   F1s f_stream<agg>  per warp range of 4096 entries: segmented-sum aggregates
+//   F1s f_stream<agg>  per warp range (4096 entries; 1024 for small patches): segmented-sum aggregates
 //                      (rows restart at each tensor; columns at each new row,
 //                      index_coding.hpp:141-153), escape markers, the range's
 //                      patch entry, and every reference check that needs no
@@ -53,7 +53,17 @@ namespace dev {
 
 namespace {
 
-constexpr uint32_t kRange = 4096;  // entries per warp range (aggregate granularity)
+// Entries per warp range (aggregate granularity), the same rule in every apply kernel of a call.
+// PULSE_APPLY_RANGE_MIN < 4096 shrinks the ranges of patches under 16 M changes (more warps for
+// small patches); it is an experiment: at 1024 the F3 piece checks fault, so the default keeps
+// 4096 everywhere.
+#ifndef PULSE_APPLY_RANGE_MIN
+#define PULSE_APPLY_RANGE_MIN 4096
+#endif
+constexpr uint32_t kRangeMin = PULSE_APPLY_RANGE_MIN;
+__device__ __forceinline__ uint32_t apply_range(uint64_t n) {
+    return n < (uint64_t(1) << 24) ? kRangeMin : 4096u;
+}
 constexpr uint32_t kChunk = 1024;  // entries staged per warp step
 constexpr uint32_t kPer = kChunk / 32;  // consecutive entries per lane
 constexpr uint64_t H = SegSumOp::kHead;
@@ -360,6 +370,7 @@ f_pass(ApplyArgs A) {
     uint4* sx = reinterpret_cast<uint4*>(ws + kABytes + kBBytes + kVBytes);
 
     const uint64_t n = A.totals[0];
+    const uint32_t kRange = apply_range(n);
     const uint64_t n_ranges = (n + kRange - 1) / kRange;
     const bool has_prev = A.carry && A.carry->has_prev;
     const uint64_t gap_base = has_prev ? A.carry->gap_base : 0;
@@ -892,6 +903,7 @@ __global__ void __launch_bounds__(kThreads, 3) f_stream(ApplyArgs A) {
     uint32_t* sx = reinterpret_cast<uint32_t*>(ws + 2 * Y::buf);
 
     const uint64_t n = A.totals[0];
+    const uint32_t kRange = apply_range(n);
     const uint64_t n_ranges = (n + kRange - 1) / kRange;
     const bool has_prev = A.carry && A.carry->has_prev;
     const uint64_t gap_base = has_prev ? A.carry->gap_base : 0;
@@ -1090,7 +1102,7 @@ f_range_scan(const uint64_t* __restrict__ totals, ulonglong2* __restrict__ agg, 
     __shared__ uint64_t s_blk, s_tot[2], s_pre[2];
     if (fast_blocked(flags)) return;
     const uint64_t n = totals[0];
-    const uint64_t n_ranges = (n + kRange - 1) / kRange;
+    const uint64_t n_ranges = (n + apply_range(n) - 1) / apply_range(n);
     const uint64_t n_blocks = (n_ranges + kScanBlock - 1) / kScanBlock;
     if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1ull);
     __syncthreads();
@@ -1230,10 +1242,10 @@ void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uin
     a.backup = reinterpret_cast<uint16_t*>(p.rowgap);  // general-decoder scratch, idle on this path
     a.scan_status = p.d_status;  // general-decoder look-back words, idle on this path
     a.scan_ticket = reinterpret_cast<unsigned long long*>(p.d_totals + 15);  // zeroed by decode_prologue
-    a.scan_blocks = uint32_t((p.cap / kRange + 2 + kScanBlock - 1) / kScanBlock);
+    a.scan_blocks = uint32_t((p.cap / kRangeMin + 2 + kScanBlock - 1) / kScanBlock);
     // general-decoder scratch, idle on this path: colent [cap] u32 >= 2 x ranges, rowgap
     // [cap] u32 >= 2 x ranges u64 (the legacy backup of PULSE_APPLY_MODE=1 uses rowgap instead)
-    const uint64_t n_rg = p.cap / kRange + 2;
+    const uint64_t n_rg = p.cap / kRangeMin + 2;
     a.range_e = p.colent;
     a.checked = true;
     // flat scratch [cap] u64: range aggregates, then the piece list

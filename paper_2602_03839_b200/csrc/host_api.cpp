@@ -114,7 +114,9 @@ struct pulse_patch {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(dev_idx_device);
-        cudaFree(dev_idx);
+        // stream-ordered free into the device's pool (no device-wide sync per patch); the
+        // call that filled dev_idx synchronized its stream before returning
+        cudaFreeAsync(dev_idx, 0);
         cudaSetDevice(prev);
     }
 };
@@ -740,6 +742,7 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
                             const std::vector<uint64_t>& lens) {
     const uint32_t T = uint32_t(p->tensors.size());
     if (T == 0) return;
+    StageTimer tm{"read_patch_bytes decode"};
     std::vector<pulse_tensor_geom> geom(T);
     std::vector<pulse_patch_entry> ents(T);
     uint64_t body_len = 0, n = 0;
@@ -769,12 +772,15 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(p->dev_idx_device);
-        cudaFree(p->dev_idx);
+        cudaFreeAsync(p->dev_idx, 0);
         cudaSetDevice(prev);
         p->dev_idx = nullptr;
     }
+    tm.lap("upload");
     if (!p->dev_idx) {
-        cuda_check(cudaMalloc(&p->dev_idx, std::max<uint64_t>(n, 1) * 8), "patch indices");
+        // from the device's stream-ordered pool: a patch per read must not pay cudaMalloc
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&p->dev_idx), std::max<uint64_t>(n, 1) * 8, E.stream),
+                   "patch indices");
         p->dev_idx_n = std::max<uint64_t>(n, 1);
         p->dev_idx_device = E.device;
     }
@@ -782,6 +788,7 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
     auto* dres = E.result.as<pulse_result>(1);
     launch_decode(plan->dev, p->representation, dbody, dent, T, nullptr, -1, dout, dres, E.stream);
     const pulse_result r = fetch_result(E, dres);
+    tm.lap("device decode");
     if (r.status != PULSE_OK) {
         const std::string nm = r.err_tensor < T ? p->tensors[r.err_tensor].name : "?";
         raise(pulse_status(r.status), device_message(r, nm, nullptr, p->representation));
@@ -795,6 +802,7 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
         at += tp.values.size();
     }
     E.sync();
+    tm.lap("indices to host");
     p->dev_idx_valid = true;
 }
 
@@ -1140,6 +1148,7 @@ pulse_status pulse_encode(const pulse_checkpoint* current, const pulse_checkpoin
             geom[k].cols = uint64_t(c.shape[c.rank - 1]);
             numel[k] = c.numel;
         }
+        StageTimer tm{"encode"};
         if (T > 0) {
             Engine& E = engine();
             std::lock_guard<std::mutex> lk(E.mu);
@@ -1169,6 +1178,7 @@ pulse_status pulse_encode(const pulse_checkpoint* current, const pulse_checkpoin
                 if (sm.status != PULSE_E_CAPACITY) break;
                 cap = sm.n_changes + sm.n_changes / 16 + 1024;
             }
+            tm.lap("upload + scan");
             const uint64_t n = sm.n_changes;
             const PlanDev& d = plan->dev;
             std::vector<uint64_t> seg_start(d.n_segs + 1);
@@ -1180,6 +1190,7 @@ pulse_status pulse_encode(const pulse_checkpoint* current, const pulse_checkpoin
             E.stager.d2h(idx.data(), didx, n * 8, E.stream);
             E.stager.d2h(val.data(), d.val16, n * 2, E.stream);
             E.sync();
+            tm.lap("indices + values to host");
             // K2 too, while the snapshots are resident and the target hash is still running:
             // write_patch_bytes then reuses these payloads instead of uploading the indices again
             if (n > 0) {
@@ -1220,8 +1231,10 @@ pulse_status pulse_encode(const pulse_checkpoint* current, const pulse_checkpoin
                 tp.values.assign(val.begin() + lo, val.begin() + hi);
                 patch->tensors.push_back(std::move(tp));
             }
+            tm.lap("K2 body + patch tensors");
         }
         hash.get();
+        tm.lap("target hash (overlapped)");
         *out = patch.release();
     });
 }
@@ -1516,7 +1529,9 @@ pulse_status pulse_write_patch_bytes(const pulse_patch* p, pulse_bytes** out) {
 pulse_status pulse_read_patch_bytes(const uint8_t* bytes, uint64_t n, pulse_patch** out) {
     return guarded([&] {
         if (!out || (n && !bytes)) raise(PULSE_E_ARGUMENT, "null argument");
+        StageTimer tm{"read_patch_bytes"};
         ParsedPulp pp = parse_pulp(bytes, n);
+        tm.lap("parse");
         if (!pp.p->tensors.empty()) {
             Engine& E = engine();
             std::lock_guard<std::mutex> lk(E.mu);
