@@ -53,6 +53,9 @@ def parse_args():
     return ap.parse_args()
 
 
+READ_STREAM_GBS = 7400.0  # profiles/r2a_bw_probe.txt: best read-only streaming kernel on B200
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -483,7 +486,12 @@ def run_pulse(args):
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": k1_bytes,
                          "bytes_moved_per_launch": k1_moved,
-                         "frac_incl_intermediate": round(k1_moved / (scan_ms / 1e3) / 1e9 / peak, 4)},
+                         "frac_incl_intermediate": round(k1_moved / (scan_ms / 1e3) / 1e9 / peak, 4),
+                         # the measured peak is a copy (half read, half write); K1 only reads (+0.2% writes),
+                         # and a read-only stream runs faster on B200: best of the read probe in
+                         # profiles/r2a_bw_probe.txt (tools/bw_probe.cu, 30.5 GB read, 7.40 TB/s)
+                         "read_stream_peak": READ_STREAM_GBS,
+                         "frac_of_read_stream": round(k1_gbs / READ_STREAM_GBS, 4)},
             # every phase against the peak of the GPUs doing it (eager pass, CUDA events on the launching
             # stream, max over ranks); whole-job bytes per SURVEY 8(d): K2 reads the K1 intermediate
             # (6 B/change) and writes the body; apply reads the body and writes 2 B per change (scattered)

@@ -48,6 +48,9 @@ for repr_ in (0, 1, 2):
     patch = sp.new_patch(repr_)
     sec = sp.encode(1, 0, patch)
     torch.cuda.synchronize(); dist.barrier()
+    if repr_ == 0:  # untimed first gather: NCCL sets up its point-to-point connections lazily
+        sp.gather(sec)
+        torch.cuda.synchronize(); dist.barrier()
     g0 = torch.cuda.Event(enable_timing=True); g1 = torch.cuda.Event(enable_timing=True)
     g0.record()
     body, ents = sp.gather(sec)
