@@ -8,7 +8,7 @@
 // patch.hpp:120-156).  Decoding is then a pair of segmented prefix sums over
 // the entries, read straight from the body.  The pipeline (launch_all):
 //
-//   F1s f_stream<agg>  per warp range (4096 entries; 1024 for small patches): segmented-sum aggregates
+//   F1s f_stream<agg>  per warp range (4096 entries; 1024 under 16 M changes): segmented-sum aggregates
 //                      (rows restart at each tensor; columns at each new row,
 //                      index_coding.hpp:141-153), escape markers, the range's
 //                      patch entry, and every reference check that needs no
@@ -53,16 +53,18 @@ namespace dev {
 
 namespace {
 
-// Entries per warp range (aggregate granularity), the same rule in every apply kernel of a call.
-// PULSE_APPLY_RANGE_MIN < 4096 shrinks the ranges of patches under 16 M changes (more warps for
-// small patches); it is an experiment: at 1024 the F3 piece checks fault, so the default keeps
-// 4096 everywhere.
+// Entries per warp range (aggregate granularity), the same rule in every apply kernel of a call:
+// 4096 for large patches, 1024 under PULSE_APPLY_RANGE_SPLIT (16 M) changes so small patches keep
+// enough warps busy (C1, 168 K changes: 41 ranges of 4096 left most of the GPU idle in F1s / F5).
 #ifndef PULSE_APPLY_RANGE_MIN
-#define PULSE_APPLY_RANGE_MIN 4096
+#define PULSE_APPLY_RANGE_MIN 1024
+#endif
+#ifndef PULSE_APPLY_RANGE_SPLIT
+#define PULSE_APPLY_RANGE_SPLIT (uint64_t(1) << 24)
 #endif
 constexpr uint32_t kRangeMin = PULSE_APPLY_RANGE_MIN;
 __device__ __forceinline__ uint32_t apply_range(uint64_t n) {
-    return n < (uint64_t(1) << 24) ? kRangeMin : 4096u;
+    return n < uint64_t(PULSE_APPLY_RANGE_SPLIT) ? kRangeMin : 4096u;
 }
 constexpr uint32_t kChunk = 1024;  // entries staged per warp step
 constexpr uint32_t kPer = kChunk / 32;  // consecutive entries per lane
@@ -397,7 +399,11 @@ f_pass(ApplyArgs A) {
         const uint64_t rg = filter ? pc.rg : it;
         const uint64_t r0 = rg * kRange;
         const uint64_t c_first = filter ? pc.c0 : r0;
-        const uint64_t r1 = filter ? pc.c0 + pc.len : min(r0 + kRange, n);
+        // r1 as c_first + a 32-bit span: the form `filter ? pc.c0 + pc.len : min(r0 + kRange, n)`
+        // with a run-time kRange made ptxas 12.9 guard the spill of r1 with the carry-out of its
+        // own predicated add (tools/sass_pred_check.py), leaving a stale r1 in local memory
+        const uint32_t span = filter ? pc.len : uint32_t(min(uint64_t(kRange), n > r0 ? n - r0 : 0));
+        const uint64_t r1 = c_first + span;
         if (c_first >= r1) continue;
         uint64_t ar = 0, ac = 0;  // kAgg: aggregates; else running (row, col) / sums
         if (kPass != kAgg) {

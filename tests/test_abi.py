@@ -56,3 +56,12 @@ def test_plain_c_consumer_round_trip():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "C ABI round trip OK" in r.stdout
+
+
+@pytest.mark.skipif(not os.path.exists("/usr/local/cuda/bin/cuobjdump"), reason="needs cuobjdump")
+def test_sass_has_no_guarded_predicate_clobber():
+    """The shipped SASS is free of the ptxas 12.9 pattern that once left F3's range end stale
+    (an add guarded by Pk that writes its carry into Pk, then a store still guarded by Pk)."""
+    r = subprocess.run(["python", os.path.join(ROOT, "tools", "sass_pred_check.py"), LIB], capture_output=True,
+                       text=True, env={**os.environ, "PATH": os.environ.get("PATH", "") + ":/usr/local/cuda/bin"})
+    assert r.returncode == 0, r.stdout[-2000:]

@@ -17,9 +17,9 @@ for r in rows[start + 1:]:
     metric = r[idx['Metric Name']]
     unit = r[idx['Metric Unit']]
     v = float(r[idx['Metric Value']].replace(',', ''))
-    if unit == 'msecond':
+    if unit in ('msecond', 'ms'):
         v *= 1e3
-    elif unit == 'nsecond':
+    elif unit in ('nsecond', 'ns'):
         v *= 1e-3
     elif unit == 'byte':
         v /= 1e6
