@@ -1074,30 +1074,6 @@ __global__ void __launch_bounds__(kThreads, kAgg_ ? 3 : PULSE_F5_MINB) f_stream(
 constexpr int kScanThreads = 1024;
 constexpr int kScanPer = 4;  // items per thread
 
-__device__ __forceinline__ void cta_seg_exclusive(uint64_t& vr, uint64_t& vc, uint64_t* s_r, uint64_t* s_c) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t ir = vr, ic = vc;
-    warp_segscan2(ir, ic);
-    if (lane == 31) {
-        s_r[warp] = ir;
-        s_c[warp] = ic;
-    }
-    __syncthreads();
-    uint64_t br = 0, bc = 0;
-    for (int w = 0; w < warp; ++w) {
-        br = SegSumOp::op(br, s_r[w]);
-        bc = SegSumOp::op(bc, s_c[w]);
-    }
-    uint64_t er = __shfl_up_sync(0xffffffffu, ir, 1), ec = __shfl_up_sync(0xffffffffu, ic, 1);
-    if (lane == 0) {
-        er = 0;
-        ec = 0;
-    }
-    vr = SegSumOp::op(br, er);
-    vc = SegSumOp::op(bc, ec);
-    __syncthreads();
-}
-
 // One 1024-thread CTA per block of 4096 range aggregates, blocks taken in ticket
 // order and chained by a decoupled look-back (one status word per block and
 // stream) -- the scan is spread over several SMs instead of serialising ~18K
@@ -1108,8 +1084,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
 f_range_scan(const uint64_t* __restrict__ totals, ulonglong2* __restrict__ agg, uint32_t* __restrict__ flags,
              uint64_t* __restrict__ status, unsigned long long* __restrict__ ticket,
              const uint64_t* __restrict__ slack) {
-    __shared__ uint64_t s_r[32], s_c[32];
-    __shared__ uint64_t s_blk, s_tot[2], s_pre[2];
+    __shared__ uint64_t s_scan[33 * 2];
+    __shared__ uint64_t s_blk, s_pre[2];
     if (fast_blocked(flags)) return;
     const uint64_t n = totals[0];
     const uint64_t n_ranges = (n + apply_range(n) - 1) / apply_range(n);
@@ -1128,16 +1104,12 @@ f_range_scan(const uint64_t* __restrict__ totals, ulonglong2* __restrict__ agg, 
         ar = SegSumOp::op(ar, v[j].x);
         ac = SegSumOp::op(ac, v[j].y);
     }
-    uint64_t er = ar, ec = ac;
-    cta_seg_exclusive(er, ec, s_r, s_c);  // -> exclusive within the block
-    if (threadIdx.x == kScanThreads - 1) {
-        s_tot[0] = SegSumOp::op(er, ar);
-        s_tot[1] = SegSumOp::op(ec, ac);
-    }
-    __syncthreads();
+    uint64_t ex[2] = {ar, ac}, tot[2];
+    cta_exclusive_scan<2, kScanThreads, AllSegSum>(ex, tot, s_scan);  // -> exclusive within the block
+    const uint64_t er = ex[0], ec = ex[1];
     if (threadIdx.x < 32) {  // warp 0: the block's exclusive prefix for both streams
-        const uint64_t pr = lookback<SegSumOp>(status, blk, s_tot[0]);
-        const uint64_t pc = lookback<SegSumOp>(status + n_blocks, blk, s_tot[1]);
+        const uint64_t pr = lookback<SegSumOp>(status, blk, tot[0]);
+        const uint64_t pc = lookback<SegSumOp>(status + n_blocks, blk, tot[1]);
         if (threadIdx.x == 0) {
             s_pre[0] = pr;
             s_pre[1] = pc;

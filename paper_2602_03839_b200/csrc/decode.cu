@@ -69,34 +69,13 @@ __device__ __forceinline__ void walk(const uint64_t* es, uint32_t n_e, uint64_t 
 // =============================================================================================
 constexpr int kLT = 1024;
 
-__device__ __forceinline__ uint64_t cta_excl_sum(uint64_t v, uint64_t* s_tmp, uint64_t& total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t inc = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint64_t o = __shfl_up_sync(0xffffffffu, inc, off);
-        if (lane >= off) inc += o;
-    }
-    if (lane == 31) s_tmp[warp] = inc;
-    __syncthreads();
-    uint64_t before = 0, all = 0;
-    for (int w = 0; w < kLT / 32; ++w) {
-        const uint64_t x = s_tmp[w];
-        if (w < warp) before += x;
-        all += x;
-    }
-    total = all;
-    __syncthreads();
-    return before + inc - v;
-}
-
 __global__ void __launch_bounds__(kLT, 1)
 d_layout(const pulse_patch_entry* __restrict__ entries, uint32_t n_e, const uint64_t* __restrict__ numel,
          const uint64_t* __restrict__ cols, uint32_t repr, EntryLayout* __restrict__ el,
          uint64_t* __restrict__ es, uint64_t* __restrict__ ck, uint64_t* __restrict__ totals,
          uint64_t* __restrict__ err, uint32_t* __restrict__ flags, uint64_t cap,
          const pulse_result* __restrict__ patch_result) {
-    __shared__ uint64_t s_tmp[32];
+    __shared__ uint64_t s_tmp[33 * 3];
     // per-call state (totals and tickets, flags, first-error key), zeroed here rather
     // than by three memset nodes ahead of this 1-CTA kernel
     if (threadIdx.x < 16) totals[threadIdx.x] = 0;
@@ -122,10 +101,10 @@ d_layout(const pulse_patch_entry* __restrict__ entries, uint32_t n_e, const uint
         if (v) pe = entries[e];
         const uint64_t ne = v ? numel[pe.tensor] : 0;
         const uint64_t nchunks = v ? (pe.idx_nbytes + kParseBytes - 1) / kParseBytes : 0;
-        uint64_t te, tc, tf;
-        const uint64_t xe = cta_excl_sum(v ? pe.count : 0, s_tmp, te);
-        const uint64_t xc = cta_excl_sum(nchunks, s_tmp, tc);
-        const uint64_t xf = cta_excl_sum(ne, s_tmp, tf);
+        uint64_t sc[3] = {v ? pe.count : 0, nchunks, ne}, tot[3];
+        cta_exclusive_scan<3, kLT, AllSum>(sc, tot, s_tmp);
+        const uint64_t xe = sc[0], xc = sc[1], xf = sc[2];
+        const uint64_t te = tot[0], tc = tot[1], tf = tot[2];
         if (!v && e < n_e) {  // empty entry (past the device-side count)
             EntryLayout L{};
             L.es = base_e + xe;
@@ -342,7 +321,7 @@ d_col_layout(EntryLayout* __restrict__ el, uint32_t n_e, uint64_t* __restrict__ 
              uint64_t* __restrict__ totals, uint64_t* __restrict__ err,
              const uint32_t* __restrict__ flags) {
     if (*(volatile const uint32_t*)flags == 0) return;
-    __shared__ uint64_t s_tmp[32];
+    __shared__ uint64_t s_tmp[33];
     uint64_t base = 0;
     for (uint32_t e0 = 0; e0 < n_e; e0 += kLT) {
         const uint32_t e = e0 + threadIdx.x;
@@ -353,8 +332,9 @@ d_col_layout(EntryLayout* __restrict__ el, uint32_t n_e, uint64_t* __restrict__ 
             chunks = (len + kParseBytes - 1) / kParseBytes;
             if (len == 0 && L.count > 0) report(err, error_key(e, kStageCols, 0, kTrunc));
         }
-        uint64_t t;
-        const uint64_t x = cta_excl_sum(chunks, s_tmp, t);
+        uint64_t xs[1] = {chunks}, ts[1];
+        cta_exclusive_scan<1, kLT, AllSum>(xs, ts, s_tmp);
+        const uint64_t x = xs[0], t = ts[0];
         if (e < n_e) {
             el[e].cu = base + x;
             cu[e] = base + x;

@@ -173,6 +173,74 @@ struct SegSumOp {
     }
 };
 
+// Max with 0 as identity (callers store x + 1 so "none" is 0).
+struct MaxOp {
+    static __device__ __forceinline__ uint64_t op(uint64_t earlier, uint64_t later) {
+        return earlier > later ? earlier : later;
+    }
+};
+
+// CTA-wide exclusive scan of K independent 64-bit lanes of values (lane k uses Ops<k>::op,
+// identity 0) over the kT threads of the block: one warp-shuffle pass for all K, the kT/32
+// warp aggregates scanned by warp 0 -- two barriers for all K values (a serial per-thread walk
+// over the warp totals with two barriers per value made the one-CTA layout kernels
+// barrier-bound).  x[k] becomes the exclusive prefix, total[k] the block aggregate.
+// s_tmp: 33 * K words of shared memory.  Ends with a barrier (s_tmp reusable).
+template <int K, int kT, class Ops>
+__device__ __forceinline__ void cta_exclusive_scan(uint64_t (&x)[K], uint64_t (&total)[K], uint64_t* s_tmp) {
+    static_assert(kT % 32 == 0 && kT <= 1024, "block of whole warps");
+    constexpr int kW = kT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t inc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) inc[k] = x[k];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint64_t o = __shfl_up_sync(0xffffffffu, inc[k], off);
+            if (lane >= off) inc[k] = Ops::op(k, o, inc[k]);
+        }
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) s_tmp[32 * k + warp] = inc[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint64_t w = lane < kW ? s_tmp[32 * k + lane] : 0;
+            uint64_t wi = w;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint64_t o = __shfl_up_sync(0xffffffffu, wi, off);
+                if (lane >= off) wi = Ops::op(k, o, wi);
+            }
+            uint64_t we = __shfl_up_sync(0xffffffffu, wi, 1);
+            if (lane == 0) we = 0;
+            s_tmp[32 * k + lane] = we;  // exclusive prefix of warp `lane`
+            if (lane == 31) s_tmp[32 * K + k] = wi;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        // exclusive within the warp: the inclusive value of the lane before
+        uint64_t ex = __shfl_up_sync(0xffffffffu, inc[k], 1);
+        if (lane == 0) ex = 0;
+        x[k] = lane == 0 ? s_tmp[32 * k + warp] : Ops::op(k, s_tmp[32 * k + warp], ex);
+        total[k] = s_tmp[32 * K + k];
+    }
+    __syncthreads();
+}
+struct AllSum {
+    static __device__ __forceinline__ uint64_t op(int, uint64_t a, uint64_t b) { return a + b; }
+};
+struct AllSegSum {
+    static __device__ __forceinline__ uint64_t op(int, uint64_t a, uint64_t b) { return SegSumOp::op(a, b); }
+};
+
 enum : uint64_t { kStatInvalid = 0, kStatAggregate = 1, kStatPrefix = 2 };
 
 // Decoupled look-back (single-pass scan).  Called by all 32 lanes of ONE warp

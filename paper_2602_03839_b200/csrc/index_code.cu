@@ -523,49 +523,12 @@ k2_scan_escapes(EntryMap em, uint32_t repr, uint64_t* __restrict__ range_cnt, ui
 // =============================================================================================
 constexpr int kLayoutThreads = 1024;
 
-__device__ __forceinline__ uint64_t cta_exclusive(uint64_t v, uint64_t* s_tmp, uint64_t& total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t inc = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint64_t o = __shfl_up_sync(0xffffffffu, inc, off);
-        if (lane >= off) inc += o;
+// k2_layout's fused scan: four sums and one max (slot 4).
+struct LayoutOps {
+    static __device__ __forceinline__ uint64_t op(int k, uint64_t a, uint64_t b) {
+        return k == 4 ? (a > b ? a : b) : a + b;
     }
-    if (lane == 31) s_tmp[warp] = inc;
-    __syncthreads();
-    uint64_t before = 0, all = 0;
-    for (int w = 0; w < kLayoutThreads / 32; ++w) {
-        const uint64_t x = s_tmp[w];
-        if (w < warp) before += x;
-        all += x;
-    }
-    total = all;
-    __syncthreads();
-    return before + inc - v;
-}
-
-__device__ __forceinline__ int64_t cta_exclusive_max(int64_t v, int64_t* s_tmp, int64_t& total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int64_t inc = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const int64_t o = __shfl_up_sync(0xffffffffu, inc, off);
-        if (lane >= off) inc = max(inc, o);
-    }
-    if (lane == 31) s_tmp[warp] = inc;
-    __syncthreads();
-    int64_t before = -1, all = -1;
-    for (int w = 0; w < kLayoutThreads / 32; ++w) {
-        const int64_t x = s_tmp[w];
-        if (w < warp) before = max(before, x);
-        all = max(all, x);
-    }
-    total = all;
-    int64_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
-    if (lane == 0) ex = -1;
-    __syncthreads();
-    return max(before, ex);
-}
+};
 
 struct LayoutArgs {
     const uint64_t* range_cnt;   // COO: packed (row | col << 32) escapes per warp range (k2_range_entries)
@@ -596,8 +559,7 @@ __device__ __forceinline__ int64_t entry_local(const EntryMap& em, uint64_t i) {
 
 __global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
     if (a.run_if && *(volatile const uint32_t*)a.run_if == 0) return;
-    __shared__ uint64_t s_tmp[32];
-    __shared__ int64_t s_max[32];
+    __shared__ uint64_t s_tmp[33 * 5];
     const int tid = threadIdx.x;
     const EntryMap& em = a.em;
     const uint64_t n = em.seg_start[em.n_segs];
@@ -627,9 +589,9 @@ __global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
             sr += v & 0xFFFFFFFFull;
             sc += v >> 32;
         }
-        uint64_t tr, tc;
-        uint64_t er = cta_exclusive(sr, s_tmp, tr);
-        uint64_t ec = cta_exclusive(sc, s_tmp, tc);
+        uint64_t x2[2] = {sr, sc}, t2[2];
+        cta_exclusive_scan<2, kLayoutThreads, AllSum>(x2, t2, s_tmp);
+        uint64_t er = x2[0], ec = x2[1];
         for (uint64_t q = q0; q < q1; ++q) {
             const uint64_t v = a.range_cnt[q];
             a.range_pre[q] = make_ulonglong2(er, ec);
@@ -667,14 +629,16 @@ __global__ void __launch_bounds__(kLayoutThreads, 1) k2_layout(LayoutArgs a) {
             }
         }
         const bool changed = count > 0 && !overflow;
-        uint64_t tb, tr, tc, te;
-        const uint64_t eb = cta_exclusive(changed ? idx_nb + 2 * count : 0, s_tmp, tb);
-        const uint64_t er = cta_exclusive(resc, s_tmp, tr);
-        const uint64_t ec = cta_exclusive(cesc, s_tmp, tc);
-        const uint64_t ee = cta_exclusive(changed ? 1 : 0, s_tmp, te);
-        int64_t mx;
-        const int64_t pc_round = cta_exclusive_max(changed ? int64_t(t) : -1, s_max, mx);
-        const int64_t pc = max(prev_changed, pc_round);  // previous changed tensor before t
+        // one fused scan: body bytes, row / column escapes, entries (sums) and the last changed
+        // tensor before t (max of t + 1; 0 = none)
+        uint64_t x5[5] = {changed ? idx_nb + 2 * count : 0, resc, cesc, changed ? 1ull : 0ull,
+                          changed ? uint64_t(t) + 1 : 0ull},
+                 t5[5];
+        cta_exclusive_scan<5, kLayoutThreads, LayoutOps>(x5, t5, s_tmp);
+        const uint64_t eb = x5[0], er = x5[1], ec = x5[2], ee = x5[3];
+        const uint64_t tb = t5[0], tr = t5[1], tc = t5[2], te = t5[3];
+        const int64_t mx = int64_t(t5[4]) - 1;
+        const int64_t pc = max(prev_changed, int64_t(x5[4]) - 1);  // previous changed tensor before t
         if (valid) {
             TensorLayout L;
             L.idx_off = body_base + eb;
