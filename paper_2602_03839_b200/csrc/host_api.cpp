@@ -367,6 +367,46 @@ public:
         }
     }
 
+    // One pipelined D2H of a contiguous device range into several host buffers (the
+    // per-tensor index vectors of a patch): `segs` lists (destination, bytes) in device order.
+    // One copy instead of one synchronised copy per tensor (339 at 7B).
+    void d2h_scatter(const std::vector<std::pair<void*, size_t>>& segs, const void* src, cudaStream_t s) {
+        size_t n = 0;
+        for (const auto& g : segs) n += g.second;
+        if (n == 0) return;
+        const size_t chunks = (n + kChunk - 1) / kChunk;
+        auto issue = [&](size_t k) {
+            const int b = int(k & 1);
+            const size_t off = k * kChunk, len = std::min(kChunk, n - off);
+            cuda_check(counted_copy(buf_[b], static_cast<const uint8_t*>(src) + off, len, cudaMemcpyDeviceToHost, s), "D2H");
+            cuda_check(cudaEventRecord(ev_[b], s), "event");
+        };
+        size_t seg = 0, seg_off = 0;  // segment holding byte `off` of the range, its start
+        struct Piece {
+            uint8_t* dst;
+            const uint8_t* src;
+            size_t len;
+        };
+        std::vector<Piece> pieces;
+        issue(0);
+        for (size_t k = 0; k < chunks; ++k) {
+            if (k + 1 < chunks) issue(k + 1);
+            const int b = int(k & 1);
+            cuda_check(cudaEventSynchronize(ev_[b]), "D2H wait");
+            const size_t off = k * kChunk, len = std::min(kChunk, n - off);
+            pieces.clear();
+            for (size_t at = off; at < off + len;) {
+                while (seg_off + segs[seg].second <= at) seg_off += segs[seg++].second;
+                const size_t in_seg = at - seg_off;
+                const size_t take = std::min({off + len - at, segs[seg].second - in_seg, size_t(4) << 20});
+                pieces.push_back({static_cast<uint8_t*>(segs[seg].first) + in_seg,
+                                  static_cast<const uint8_t*>(buf_[b]) + (at - off), take});
+                at += take;
+            }
+            pool().parallel_for(pieces.size(), [&](size_t i) { std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].len); });
+        }
+    }
+
 private:
     void* buf_[2] = {nullptr, nullptr};
     cudaEvent_t ev_[2];
@@ -812,14 +852,15 @@ void device_decode_payloads(Engine& E, pulse_patch* p, const std::vector<const u
         const std::string nm = r.err_tensor < T ? p->tensors[r.err_tensor].name : "?";
         raise(pulse_status(r.status), device_message(r, nm, nullptr, p->representation));
     }
-    // each tensor's indices straight into its vector (no intermediate host copy)
-    uint64_t at = 0;
+    // each tensor's indices straight into its vector (no intermediate host copy), one pipelined D2H
+    std::vector<std::pair<void*, size_t>> segs;
+    segs.reserve(T);
     for (uint32_t t = 0; t < T; ++t) {
         auto& tp = p->tensors[t];
         tp.indices.resize(tp.values.size());
-        if (!tp.indices.empty()) E.stager.d2h(tp.indices.data(), dout + at, tp.indices.size() * 8, E.stream);
-        at += tp.values.size();
+        if (!tp.indices.empty()) segs.emplace_back(tp.indices.data(), tp.indices.size() * 8);
     }
+    E.stager.d2h_scatter(segs, dout, E.stream);
     E.sync();
     tm.lap("indices to host");
     p->dev_idx_valid = true;
