@@ -682,7 +682,10 @@ struct SCtx {
     uint32_t e;
     uint32_t tensor;
     uint64_t lo, hi;  // entries [lo, hi) belong to patch entry e
-    uint64_t idx_off, count, val_off, numel, cols, flat_base;
+    const uint8_t* rows;  // body + idx_off: COO row bytes / u32 gaps
+    const uint8_t* colp;  // COO column units (body + idx_off + count)
+    const uint8_t* vals;  // body + val_off
+    uint64_t numel, cols, flat_base;
 };
 
 __device__ __forceinline__ void load_sctx(SCtx& c, const ApplyArgs& A, uint32_t e) {
@@ -691,9 +694,9 @@ __device__ __forceinline__ void load_sctx(SCtx& c, const ApplyArgs& A, uint32_t 
     c.hi = A.es[e + 1];
     const EntryLayout& L = A.el[e];
     c.tensor = uint32_t(L.tensor);
-    c.idx_off = L.idx_off;
-    c.count = L.count;
-    c.val_off = L.val_off;
+    c.rows = A.body + L.idx_off;
+    c.colp = A.body + L.idx_off + L.count;
+    c.vals = A.body + L.val_off;
     c.numel = L.numel;
     c.cols = L.cols;
     c.flat_base = L.flat_base;
@@ -952,15 +955,14 @@ __global__ void __launch_bounds__(kThreads, kAgg_ ? 3 : PULSE_F5_MINB) f_stream(
             uint8_t* bb = ws + b * Y::buf;
             const uint64_t o0 = cc - c.lo;
             if (coo) {
-                sh[0] = stage_cover<Y::va>(reinterpret_cast<uint4*>(bb), A.body + c.idx_off + o0, len);
-                sh[1] = stage_cover<Y::vb>(reinterpret_cast<uint4*>(bb + 16 * Y::a_slots),
-                                           A.body + c.idx_off + c.count + 2 * o0, 2 * len);
+                sh[0] = stage_cover<Y::va>(reinterpret_cast<uint4*>(bb), c.rows + o0, len);
+                sh[1] = stage_cover<Y::vb>(reinterpret_cast<uint4*>(bb + 16 * Y::a_slots), c.colp + 2 * o0, 2 * len);
             } else {
-                sh[0] = stage_cover<Y::va>(reinterpret_cast<uint4*>(bb), A.body + c.idx_off + 4 * o0, 4 * len);
+                sh[0] = stage_cover<Y::va>(reinterpret_cast<uint4*>(bb), c.rows + 4 * o0, 4 * len);
             }
             if (!agg)
-                sh[2] = stage_cover<2>(reinterpret_cast<uint4*>(bb + 16 * (Y::a_slots + Y::b_slots)),
-                                       A.body + c.val_off + 2 * o0, 2 * len);
+                sh[2] = stage_cover<2>(reinterpret_cast<uint4*>(bb + 16 * (Y::a_slots + Y::b_slots)), c.vals + 2 * o0,
+                                       2 * len);
         }
         cp_async_commit();
     };

@@ -114,8 +114,11 @@ struct Ent {
 // large patches (fewer per-range look-ups), one for patches under 16 M changes, so small
 // patches with escapes (walker path) still keep thousands of warps busy (7B / 99.99%: K2
 // 0.33 -> 0.14 ms; 99%: 0.333 ms with 1024, 0.310 ms with 4096).
+#ifndef PULSE_K2_RANGE_SPLIT
+#define PULSE_K2_RANGE_SPLIT (uint64_t(1) << 24)
+#endif
 __device__ __forceinline__ uint32_t k2_range_entries(uint64_t n) {
-    return n < (uint64_t(1) << 24) ? kK2RangeEntries : 4 * kK2RangeEntries;
+    return n < uint64_t(PULSE_K2_RANGE_SPLIT) ? kK2RangeEntries : 4 * kK2RangeEntries;
 }
 
 struct Walker {
