@@ -188,3 +188,46 @@ def test_sharded_sections_edge_cases(n_ranks, layout):
         w.copy_(prev.buf)
         assert all(int(x["status"]) == 0 for x in sim.apply(2, patches))
         assert torch.equal(w, curr.buf), (layout, n_ranks, r)
+
+
+@needs_ref
+@pytest.mark.parametrize("n_ranks", [1, 3])
+def test_more_tensors_than_one_layout_round(n_ranks):
+    """2,600 tensors: k2_layout and d_layout scan 1,024 tensors per CTA round, so the body
+    offsets, entry numbering and the FLAT 'previous changed tensor' carry cross two round
+    boundaries -- with unchanged runs placed right across them -- and must still equal the
+    reference's PULP body byte for byte; apply rebuilds the target."""
+    PU = _pu()
+    R = reference()
+    rng = np.random.default_rng(2600)
+    n_t = 2600
+    unchanged = set(range(1020, 1030)) | set(range(2040, 2056)) | {0, 1, n_t - 1}
+    tensors, a, b = [], [], []
+    for i in range(n_t):
+        shp = (int(rng.integers(1, 6)) * 8, int(rng.choice([1, 8, 24])))
+        n = shp[0] * shp[1]
+        x = rng.integers(0, 65536, n, dtype=np.uint16)
+        y = x.copy()
+        if i not in unchanged:
+            y[rng.random(n) < 0.05] ^= 1
+            y[int(rng.integers(0, n))] ^= 0x8000
+        tensors.append((f"m.{i:05d}", shp))
+        a.append(x)
+        b.append(y)
+    prev, curr = _upload_state(tensors, a), _upload_state(tensors, b)
+    hp = Checkpoint(0, [Tensor(n, s, x) for (n, s), x in zip(tensors, a)])
+    hc = Checkpoint(1, [Tensor(n, s, x) for (n, s), x in zip(tensors, b)])
+    want = R.encode_pulps(hc, hp)
+    w = prev.buf.clone()
+    sim = PU.ShardedSim(tensors, n_ranks, max_changes_frac=0.5)
+    sim.bind(0, prev)
+    sim.bind(1, curr)
+    sim.bind(2, PU.DeviceState(tensors, w, prev.offs))
+    for r in REPRS:
+        header, body = PU.split_pulp(want[r])
+        got, ents, patches = sim.encode(r)
+        assert got == body, (n_ranks, r)
+        PU.assert_entries_match_header(ents, header, tensors)
+        w.copy_(prev.buf)
+        assert all(int(x["status"]) == 0 for x in sim.apply(2, patches))
+        assert torch.equal(w, curr.buf), (n_ranks, r)
