@@ -259,8 +259,9 @@ namespace tma {
 #ifndef PULSE_K1_DDENSE
 #define PULSE_K1_DDENSE 3072
 #endif
-template <int S, int B, uint32_t RC, uint32_t SC, uint32_t DT, uint32_t DF>
+template <int S, int B, uint32_t RC, uint32_t SC, uint32_t DT, uint32_t DF, int LB = 4>
 struct Cfg {
+    static constexpr int kLbWarps = LB;        // look-back / flush warps (the flush expands every change)
     static constexpr int kStages = S;          // TMA ring stages (16 KiB prev + 16 KiB curr each)
     static constexpr int kBufs = B;            // ticket staging buffers (consumers may run ahead)
     static constexpr uint32_t kRecCap = RC;    // record mode: staged changed 16-byte vectors per buffer
@@ -268,22 +269,36 @@ struct Cfg {
     static constexpr uint32_t kDenseTicket = DT;  // changes above which the next ticket stages element entries
     static constexpr uint32_t kDeferTicket = DF;  // ... above which it is only counted and deferred to K1b
 };
+#ifndef PULSE_K1_LB
+#define PULSE_K1_LB 4
+#endif
+#ifndef PULSE_K1_DLB
+#define PULSE_K1_DLB 4
+#endif
+#ifndef PULSE_K1_D2LB
+#define PULSE_K1_D2LB 4
+#endif
 using SparseCfg = Cfg<PULSE_K1_STAGES, PULSE_K1_BUFS, PULSE_K1_RECCAP, PULSE_K1_STAGECAP,
-                      (PULSE_K1_STAGECAP * 3 / 4 < 3072 ? PULSE_K1_STAGECAP * 3 / 4 : 3072), PULSE_K1_STAGECAP>;
+                      (PULSE_K1_STAGECAP * 3 / 4 < 3072 ? PULSE_K1_STAGECAP * 3 / 4 : 3072), PULSE_K1_STAGECAP,
+                      PULSE_K1_LB>;
 using DenseCfg = Cfg<PULSE_K1_DSTAGES, PULSE_K1_DBUFS, PULSE_K1_DRECCAP, PULSE_K1_DSTAGECAP, PULSE_K1_DDENSE,
-                     PULSE_K1_DSTAGECAP>;
+                     PULSE_K1_DSTAGECAP, PULSE_K1_DLB>;
 // patches denser than ~4.5%: records only (no element staging), larger record buffers, fewer
 // stages; tickets too dense even for those are counted in K1 and written by K1b
-using Dense2Cfg = Cfg<2, 3, 2200, 0, 0xFFFFFFFFu, 8000>;
+using Dense2Cfg = Cfg<2, 3, 2200, 0, 0xFFFFFFFFu, 8000, PULSE_K1_D2LB>;
+// patches denser than ~8%: the same staging and six flush warps -- at 90% the four-warp flush
+// (expanding ~6,500 changes per ticket) was the bottleneck: K1 10.3 -> 9.0 ms; at 95% the extra
+// warps cost more issue slots than they save (6.87 -> 7.00 ms), hence a separate shape
+using Dense3Cfg = Cfg<2, 3, 2200, 0, 0xFFFFFFFFu, 8000, 6>;
 constexpr uint32_t kSubElems = 8192;                 // elements per stage (16 KiB + 16 KiB)
 constexpr uint32_t kSubs = kTicketElems / kSubElems; // 8 sub-tiles per ticket
 constexpr int kConsumerWarps = 8;
 constexpr uint32_t kVecPerWarp = kSubElems / 8 / kConsumerWarps;  // 128 vectors = 4 per lane
 constexpr int kProducerWarp = kConsumerWarps;        // warp 8
-constexpr int kLbWarps = 4;                          // warps 9..12
-constexpr int kLbFirst = kConsumerWarps + 1;
-constexpr int kLbThreads = kLbWarps * 32;
-constexpr int kThreadsTotal = (kConsumerWarps + 1 + kLbWarps) * 32;  // 416
+constexpr int kLbFirst = kConsumerWarps + 1;         // flush warps: 9 .. 9 + Cfg::kLbWarps - 1
+constexpr int kLbWarpsMax = 8;
+template <class C>
+constexpr int threads_total() { return (kConsumerWarps + 1 + C::kLbWarps) * 32; }  // 416 with 4 flush warps
 enum : uint32_t { kModeRecords = 0, kModeElements = 1, kModeCount = 2 };
 constexpr uint32_t kChunks = kSubs * kConsumerWarps; // (sub-tile, warp) chunks per ticket
 constexpr uint32_t kBarLb = 2;                       // named barrier id of the look-back group
@@ -339,13 +354,14 @@ struct Smem {
     TicketInfo info[kBufs];
     uint64_t full[kStages], empty[kStages];
     uint64_t tk_full[kBufs], tk_empty[kBufs];
-    uint32_t lb_warp_tot[kLbWarps];
+    uint32_t lb_warp_tot[kLbWarpsMax];
     uint32_t lb_run, lb_count;
     uint64_t lb_G;
 };
 static_assert(sizeof(Smem<SparseCfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
 static_assert(sizeof(Smem<DenseCfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
 static_assert(sizeof(Smem<Dense2Cfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
+static_assert(sizeof(Smem<Dense3Cfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
 }  // namespace tma
 
 // Look-back with 4 status words per lane per round (128 predecessors).
@@ -399,9 +415,11 @@ __device__ __forceinline__ uint64_t lookback_wide(uint64_t* status, uint64_t til
 }
 
 template <class C>
-__global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
+__global__ void __launch_bounds__((tma::kConsumerWarps + 1 + C::kLbWarps) * 32, 1) k1_tma(K1Args k) {
     using namespace tma;
     constexpr int kStages = C::kStages, kBufs = C::kBufs;
+    constexpr int kLbWarps = C::kLbWarps, kLbThreads = kLbWarps * 32;
+    static_assert(kLbWarps >= 1 && kLbWarps <= kLbWarpsMax, "flush warps");
     constexpr uint32_t kRecCap = C::kRecCap, kStageCap = C::kStageCap, kDenseTicket = C::kDenseTicket;
     constexpr uint32_t kDeferTicket = C::kDeferTicket;
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -757,7 +775,7 @@ __global__ void __launch_bounds__(tma::kThreadsTotal, 1) k1_tma(K1Args k) {
     }
 
     // ---------------------------------------------------------------- look-back group
-    const int lt = tid - kLbFirst * 32;  // 0..127
+    const int lt = tid - kLbFirst * 32;  // 0 .. kLbThreads - 1
     int buf = 0;
     uint32_t bphase = 0;
     while (true) {
@@ -1106,6 +1124,8 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
                                      int(sizeof(tma::Smem<tma::DenseCfg>)));
                 cudaFuncSetAttribute(k1_tma<tma::Dense2Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(sizeof(tma::Smem<tma::Dense2Cfg>)));
+                cudaFuncSetAttribute(k1_tma<tma::Dense3Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(tma::Smem<tma::Dense3Cfg>)));
                 attr = 1;
             }
             K1Args kt = k;
@@ -1114,18 +1134,20 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
             const uint64_t grid = std::min<uint64_t>(uint64_t(sm_count()), p.tma_tiles);
             // the plan's change capacity says which regime the caller sized it for: >= 3% of its
             // elements -> dense staging (element entries need room), else more tickets in flight
-            const int shape_override = [] {  // PULSE_K1_SHAPE=sparse|dense|dense2 (tests, A/B runs; per launch)
+            const int shape_override = [] {  // PULSE_K1_SHAPE=sparse|dense|dense2|dense3 (tests, A/B runs; per launch)
                 const char* e = getenv("PULSE_K1_SHAPE");
-                return !e ? -1 : std::string(e) == "dense2" ? 2 : std::string(e) == "dense" ? 1
-                               : std::string(e) == "sparse" ? 0 : -1;
+                return !e ? -1 : std::string(e) == "dense3" ? 3 : std::string(e) == "dense2" ? 2
+                               : std::string(e) == "dense" ? 1 : std::string(e) == "sparse" ? 0 : -1;
             }();
             const int shape = shape_override >= 0 ? shape_override : int(p.k1_dense);
-            if (shape == 2) {
-                k1_tma<tma::Dense2Cfg><<<unsigned(grid), tma::kThreadsTotal, sizeof(tma::Smem<tma::Dense2Cfg>), s>>>(kt);
+            if (shape == 3) {
+                k1_tma<tma::Dense3Cfg><<<unsigned(grid), tma::threads_total<tma::Dense3Cfg>(), sizeof(tma::Smem<tma::Dense3Cfg>), s>>>(kt);
+            } else if (shape == 2) {
+                k1_tma<tma::Dense2Cfg><<<unsigned(grid), tma::threads_total<tma::Dense2Cfg>(), sizeof(tma::Smem<tma::Dense2Cfg>), s>>>(kt);
             } else if (shape == 1) {
-                k1_tma<tma::DenseCfg><<<unsigned(grid), tma::kThreadsTotal, sizeof(tma::Smem<tma::DenseCfg>), s>>>(kt);
+                k1_tma<tma::DenseCfg><<<unsigned(grid), tma::threads_total<tma::DenseCfg>(), sizeof(tma::Smem<tma::DenseCfg>), s>>>(kt);
             } else {
-                k1_tma<tma::SparseCfg><<<unsigned(grid), tma::kThreadsTotal, sizeof(tma::Smem<tma::SparseCfg>), s>>>(kt);
+                k1_tma<tma::SparseCfg><<<unsigned(grid), tma::threads_total<tma::SparseCfg>(), sizeof(tma::Smem<tma::SparseCfg>), s>>>(kt);
             }
             PULSE_LAUNCHED("k1_tma", s);
             // K1b only if some ticket was deferred (a conditional graph node under capture;
