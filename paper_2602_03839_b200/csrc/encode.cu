@@ -289,7 +289,19 @@ using Dense2Cfg = Cfg<2, 3, 2200, 0, 0xFFFFFFFFu, 8000, PULSE_K1_D2LB>;
 // patches denser than ~8%: the same staging and six flush warps -- at 90% the four-warp flush
 // (expanding ~6,500 changes per ticket) was the bottleneck: K1 10.3 -> 9.0 ms; at 95% the extra
 // warps cost more issue slots than they save (6.87 -> 7.00 ms), hence a separate shape
-using Dense3Cfg = Cfg<2, 3, 2200, 0, 0xFFFFFFFFu, 8000, 6>;
+#ifndef PULSE_K1_D3S
+#define PULSE_K1_D3S 2
+#endif
+#ifndef PULSE_K1_D3B
+#define PULSE_K1_D3B 3
+#endif
+#ifndef PULSE_K1_D3RC
+#define PULSE_K1_D3RC 2200
+#endif
+#ifndef PULSE_K1_D3LB
+#define PULSE_K1_D3LB 6
+#endif
+using Dense3Cfg = Cfg<PULSE_K1_D3S, PULSE_K1_D3B, PULSE_K1_D3RC, 0, 0xFFFFFFFFu, 8000, PULSE_K1_D3LB>;
 constexpr uint32_t kSubElems = 8192;                 // elements per stage (16 KiB + 16 KiB)
 constexpr uint32_t kSubs = kTicketElems / kSubElems; // 8 sub-tiles per ticket
 constexpr int kConsumerWarps = 8;
