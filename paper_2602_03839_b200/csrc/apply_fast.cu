@@ -62,9 +62,12 @@ namespace {
 #ifndef PULSE_APPLY_RANGE_SPLIT
 #define PULSE_APPLY_RANGE_SPLIT (uint64_t(1) << 24)
 #endif
+#ifndef PULSE_APPLY_RANGE_MAX
+#define PULSE_APPLY_RANGE_MAX 4096
+#endif
 constexpr uint32_t kRangeMin = PULSE_APPLY_RANGE_MIN;
 __device__ __forceinline__ uint32_t apply_range(uint64_t n) {
-    return n < uint64_t(PULSE_APPLY_RANGE_SPLIT) ? kRangeMin : 4096u;
+    return n < uint64_t(PULSE_APPLY_RANGE_SPLIT) ? kRangeMin : uint32_t(PULSE_APPLY_RANGE_MAX);
 }
 constexpr uint32_t kChunk = 1024;  // entries staged per warp step
 constexpr uint32_t kPer = kChunk / 32;  // consecutive entries per lane

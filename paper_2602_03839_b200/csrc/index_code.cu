@@ -110,15 +110,19 @@ struct Ent {
     int64_t L, Lp;      // local index; previous local index (-1 when j == 0)
 };
 
-// Entries per K2 warp range, the same rule in every K2 kernel of a call: four staged chunks for
+// Entries per K2 warp range, the same rule in every K2 kernel of a call: eight staged chunks for
 // large patches (fewer per-range look-ups), one for patches under 16 M changes, so small
 // patches with escapes (walker path) still keep thousands of warps busy (7B / 99.99%: K2
-// 0.33 -> 0.14 ms; 99%: 0.333 ms with 1024, 0.310 ms with 4096).
+// 0.33 -> 0.14 ms; 99%: 0.333 ms with 1024, 0.310 with 4096, 0.290 with 8192 and 0.296 with
+// 16384 entries; 90%: 2.34 -> 2.24 ms from 4096 to 8192, profiles/r2d_ab_variants.txt).
 #ifndef PULSE_K2_RANGE_SPLIT
 #define PULSE_K2_RANGE_SPLIT (uint64_t(1) << 24)
 #endif
+#ifndef PULSE_K2_RANGE_MUL
+#define PULSE_K2_RANGE_MUL 8
+#endif
 __device__ __forceinline__ uint32_t k2_range_entries(uint64_t n) {
-    return n < uint64_t(PULSE_K2_RANGE_SPLIT) ? kK2RangeEntries : 4 * kK2RangeEntries;
+    return n < uint64_t(PULSE_K2_RANGE_SPLIT) ? kK2RangeEntries : PULSE_K2_RANGE_MUL * kK2RangeEntries;
 }
 
 struct Walker {
