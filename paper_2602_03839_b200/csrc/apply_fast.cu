@@ -905,8 +905,11 @@ __device__ __forceinline__ void chunk_body(const ApplyArgs& A, const SCtx& cur, 
 #ifndef PULSE_F5_MINB
 #define PULSE_F5_MINB 3
 #endif
+#ifndef PULSE_F1_MINB
+#define PULSE_F1_MINB 3
+#endif
 template <int kRepr, bool kAgg_>
-__global__ void __launch_bounds__(kThreads, kAgg_ ? 3 : PULSE_F5_MINB) f_stream(ApplyArgs A) {
+__global__ void __launch_bounds__(kThreads, kAgg_ ? PULSE_F1_MINB : PULSE_F5_MINB) f_stream(ApplyArgs A) {
     extern __shared__ __align__(16) uint8_t smem[];
     using Y = SLay<kRepr, kAgg_>;
     constexpr bool coo = kRepr == kCoo;
