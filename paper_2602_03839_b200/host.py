@@ -379,21 +379,6 @@ def write_checkpoint_bytes_from_device(step: int, names, shapes, device_tensors)
 
 
 # ---- resident checkpoints: the sync path on the device (sync.hpp) -----------------------------
-def _after_pending_writes(device_tensors):
-    """The library reads caller device buffers on its own non-blocking streams
-    (include/pulse_cuda.h, pulse_resident_create_device / publish): wait for the
-    work queued on the tensors' current torch streams (an optimizer step still
-    writing them) before handing their pointers over."""
-    seen = set()
-    for t in device_tensors:
-        dev = getattr(t, "device", None)
-        if dev is None or getattr(dev, "type", None) != "cuda" or dev in seen:
-            continue
-        seen.add(dev)
-        import torch
-        torch.cuda.current_stream(dev).synchronize()
-
-
 class Resident:
     """A checkpoint held in HBM with its step and weights hash (the consumer's
     SyncState, sync.hpp:78-92, and the publisher's last published snapshot).
@@ -421,7 +406,6 @@ class Resident:
         ck = N.CheckpointC(step, arr, len(names))
         self = cls.__new__(cls)
         h = C.c_void_p()
-        _after_pending_writes(device_tensors)
         N.check(N.lib.pulse_resident_create_device(C.byref(ck), max_changes, C.byref(h)))
         self.h = h
         self.names = list(names)
@@ -482,7 +466,6 @@ class Resident:
         out = C.c_void_p()
         hsh = C.create_string_buffer(32)
         anchor = self.step if anchor_step is None else anchor_step
-        _after_pending_writes(device_tensors)
         N.check(N.lib.pulse_resident_publish(self.h, arr, step, representation, codec, anchor, int(advance),
                                              C.byref(out), hsh))
         return _take(out), hsh.raw

@@ -4,7 +4,7 @@
 # captures of k1_tma / k2_emit / the apply streaming passes.
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
-t=r2f
+t=${TAG:-r2f}
 timeout 300 python __graft_entry__.py smoke 2>&1 | tail -1
 timeout 1200 python bench.py > gpurun_out/${t}_bench.json 2> gpurun_out/${t}_bench.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference > gpurun_out/${t}_bench_ref.json 2> gpurun_out/${t}_bench_ref.err; echo "ref rc=$?"
