@@ -281,6 +281,10 @@ struct Cfg {
 using SparseCfg = Cfg<PULSE_K1_STAGES, PULSE_K1_BUFS, PULSE_K1_RECCAP, PULSE_K1_STAGECAP,
                       (PULSE_K1_STAGECAP * 3 / 4 < 3072 ? PULSE_K1_STAGECAP * 3 / 4 : 3072), PULSE_K1_STAGECAP,
                       PULSE_K1_LB>;
+// plans sized for < 1.5% changes: one more ticket in flight between the consumers and the
+// flush group, smaller staging per ticket (99%: K1 4.50 -> 4.44 ms; at 98% it would overflow
+// the staging: 5.1 -> 6.7 ms, so plans sized for more changes keep SparseCfg)
+using SparseLowCfg = Cfg<5, 6, 384, 2304, 1728, 2304, PULSE_K1_LB>;
 using DenseCfg = Cfg<PULSE_K1_DSTAGES, PULSE_K1_DBUFS, PULSE_K1_DRECCAP, PULSE_K1_DSTAGECAP, PULSE_K1_DDENSE,
                      PULSE_K1_DSTAGECAP, PULSE_K1_DLB>;
 // patches denser than ~4.5%: records only (no element staging), larger record buffers, fewer
@@ -371,6 +375,7 @@ struct Smem {
     uint64_t lb_G;
 };
 static_assert(sizeof(Smem<SparseCfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
+static_assert(sizeof(Smem<SparseLowCfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
 static_assert(sizeof(Smem<DenseCfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
 static_assert(sizeof(Smem<Dense2Cfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
 static_assert(sizeof(Smem<Dense3Cfg>) <= 232448, "K1 shared memory exceeds the 227 KiB per-block limit");
@@ -920,11 +925,16 @@ __global__ void __launch_bounds__((tma::kConsumerWarps + 1 + C::kLbWarps) * 32, 
         named_sync(kBarLb, kLbThreads);  // flush done before the buffer is reused
         if (lt == 0) {
             if (k.trace) atomicOr(k.trace + ti.tile, 16u);
+            // changed vectors staged (or asked for) in record mode: scattered changes (one per
+            // 16-byte vector) overflow the records long before the element count is "dense"
+            const bool rec_overflow = S.mode[buf] == kModeRecords && S.fill[buf] > kRecCap;
             S.fill[buf] = 0;
             S.overflow[buf] = 0;
             // layout for the next ticket staged in this buffer: neighbouring tickets
             // have similar density (same tensor), so follow this one's
-            S.mode[buf] = count > kDeferTicket ? kModeCount : count > kDenseTicket ? kModeElements : kModeRecords;
+            S.mode[buf] = count > kDeferTicket                                  ? kModeCount
+                          : (count > kDenseTicket || (kStageCap > 0 && rec_overflow)) ? kModeElements
+                                                                                  : kModeRecords;
             S.tk_cnt[buf] = 0;
             S.tk_arrived[buf] = 0;
             mbar_arrive(&S.tk_empty[buf]);
@@ -1132,6 +1142,8 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
             if (!attr) {
                 cudaFuncSetAttribute(k1_tma<tma::SparseCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(sizeof(tma::Smem<tma::SparseCfg>)));
+                cudaFuncSetAttribute(k1_tma<tma::SparseLowCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(tma::Smem<tma::SparseLowCfg>)));
                 cudaFuncSetAttribute(k1_tma<tma::DenseCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(sizeof(tma::Smem<tma::DenseCfg>)));
                 cudaFuncSetAttribute(k1_tma<tma::Dense2Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1146,13 +1158,16 @@ void launch_encode_scan(const PlanDev& p, uint32_t curr_slot, uint32_t prev_slot
             const uint64_t grid = std::min<uint64_t>(uint64_t(sm_count()), p.tma_tiles);
             // the plan's change capacity says which regime the caller sized it for: >= 3% of its
             // elements -> dense staging (element entries need room), else more tickets in flight
-            const int shape_override = [] {  // PULSE_K1_SHAPE=sparse|dense|dense2|dense3 (tests, A/B runs; per launch)
+            const int shape_override = [] {  // PULSE_K1_SHAPE=sparse|sparse_low|dense|dense2|dense3 (tests, A/B runs; per launch)
                 const char* e = getenv("PULSE_K1_SHAPE");
                 return !e ? -1 : std::string(e) == "dense3" ? 3 : std::string(e) == "dense2" ? 2
-                               : std::string(e) == "dense" ? 1 : std::string(e) == "sparse" ? 0 : -1;
+                               : std::string(e) == "dense" ? 1 : std::string(e) == "sparse" ? 0
+                               : std::string(e) == "sparse_low" ? 4 : -1;
             }();
             const int shape = shape_override >= 0 ? shape_override : int(p.k1_dense);
-            if (shape == 3) {
+            if (shape == 4) {
+                k1_tma<tma::SparseLowCfg><<<unsigned(grid), tma::threads_total<tma::SparseLowCfg>(), sizeof(tma::Smem<tma::SparseLowCfg>), s>>>(kt);
+            } else if (shape == 3) {
                 k1_tma<tma::Dense3Cfg><<<unsigned(grid), tma::threads_total<tma::Dense3Cfg>(), sizeof(tma::Smem<tma::Dense3Cfg>), s>>>(kt);
             } else if (shape == 2) {
                 k1_tma<tma::Dense2Cfg><<<unsigned(grid), tma::threads_total<tma::Dense2Cfg>(), sizeof(tma::Smem<tma::Dense2Cfg>), s>>>(kt);

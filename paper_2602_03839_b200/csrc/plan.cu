@@ -159,7 +159,8 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
     p.cap = std::max<uint64_t>(max_changes, 1);
     uint64_t elems = 0;
     for (uint32_t t = 0; t < n_tensors; ++t) elems += tensors[t].numel;
-    p.k1_dense = p.cap * 100 >= elems * 8 ? 3u : p.cap * 1000 >= elems * 45 ? 2u : p.cap * 100 >= elems * 3 ? 1u : 0u;
+    p.k1_dense = p.cap * 100 >= elems * 8 ? 3u : p.cap * 1000 >= elems * 45 ? 2u : p.cap * 100 >= elems * 3 ? 1u
+               : p.cap * 1000 < elems * 15 ? 4u : 0u;
     const uint64_t T = n_tensors, S = segs.size(), cap = p.cap;
     const uint64_t n_chunks = cap / kChunkEntries + 2;
     p.dec_bytes_cap = 10 * cap + kParseBytes * (T + 1);

@@ -37,7 +37,7 @@ def make_plan(ts, max_changes=None):
     return D.DevicePlan(geoms, cap)
 
 
-@pytest.fixture(params=["auto", "sparse", "dense", "dense2", "dense3"])
+@pytest.fixture(params=["auto", "sparse", "sparse_low", "dense", "dense2", "dense3"])
 def k1_shape(request, monkeypatch):
     """K1's staging shape (encode.cu tma::SparseCfg / DenseCfg / Dense2Cfg / Dense3Cfg): chosen from the
     plan's capacity, or forced through PULSE_K1_SHAPE so each runs on every golden case."""
@@ -159,7 +159,7 @@ def test_config1_16m_matches_reference_bytes(golden):
         assert len(want) == golden.manifest["config1"]["pulp_nbytes"][f"{r}/0"]
 
 
-@pytest.mark.parametrize("shape", ["sparse", "dense", "dense2", "dense3"])
+@pytest.mark.parametrize("shape", ["sparse", "sparse_low", "dense", "dense2", "dense3"])
 def test_dense_ticket_slow_path(shape, monkeypatch):
     monkeypatch.setenv("PULSE_K1_SHAPE", shape)
     _dense_ticket_slow_path()

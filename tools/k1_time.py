@@ -19,7 +19,7 @@ n = sum(sizes)
 prev = torch.empty(n, dtype=torch.int16, device="cuda")
 curr = torch.empty_like(prev)
 D.synth_base(prev, seed=1002)
-D.synth_mutate(prev, curr, sp, 64, seed=1002)
+D.synth_mutate(prev, curr, sp, int(os.environ.get("CW", "64")), seed=1002)
 offs = np.concatenate([[0], np.cumsum(sizes)])
 views = lambda b: [b[int(offs[i]):int(offs[i + 1])] for i in range(len(sizes))]
 plan = D.DevicePlan([(m, s[-1]) for m, (_, s) in zip(sizes, tensors)], int(n * (1 - sp) * 1.02) + 65536)
