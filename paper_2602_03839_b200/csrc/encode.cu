@@ -928,12 +928,15 @@ __global__ void __launch_bounds__((tma::kConsumerWarps + 1 + C::kLbWarps) * 32, 
             // changed vectors staged (or asked for) in record mode: scattered changes (one per
             // 16-byte vector) overflow the records long before the element count is "dense"
             const bool rec_overflow = S.mode[buf] == kModeRecords && S.fill[buf] > kRecCap;
+            // ... and stays there while its changes could not fit the records either (no
+            // records / elements ping-pong that defers every other ticket)
+            const bool el_keep = S.mode[buf] == kModeElements && count > kRecCap;
             S.fill[buf] = 0;
             S.overflow[buf] = 0;
             // layout for the next ticket staged in this buffer: neighbouring tickets
             // have similar density (same tensor), so follow this one's
             S.mode[buf] = count > kDeferTicket                                  ? kModeCount
-                          : (count > kDenseTicket || (kStageCap > 0 && rec_overflow)) ? kModeElements
+                          : (count > kDenseTicket || (kStageCap > 0 && (rec_overflow || el_keep))) ? kModeElements
                                                                                   : kModeRecords;
             S.tk_cnt[buf] = 0;
             S.tk_arrived[buf] = 0;
