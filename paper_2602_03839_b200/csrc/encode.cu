@@ -238,6 +238,9 @@ namespace tma {
 #ifndef PULSE_K1_COOP_STAGE
 #define PULSE_K1_COOP_STAGE 1  // element mode: warp-cooperative staging (0: per-lane loop over mask bits)
 #endif
+#ifndef PULSE_K1_COOP_MIN_BITS
+#define PULSE_K1_COOP_MIN_BITS 2  // ... only for warp chunks with a vector of more changes than this
+#endif
 #ifndef PULSE_K1_RECCAP
 #define PULSE_K1_RECCAP 448
 #endif
@@ -718,7 +721,13 @@ __global__ void __launch_bounds__((tma::kConsumerWarps + 1 + C::kLbWarps) * 32, 
                     if (off + total > kStageCap) S.overflow[buf] = 1;
                 }
                 if (total && k.experiment != 3) {
-#if PULSE_K1_COOP_STAGE
+                    // warp-cooperative staging pays off when some vector holds several
+                    // changes (the per-lane loop over mask bits would diverge); with at most
+                    // PULSE_K1_COOP_MIN_BITS changes per vector (scattered changes) the plain
+                    // per-lane loop is cheaper (99% with cluster width 1: K1 12.3 -> 9.0 ms)
+                    const uint32_t vmax = __reduce_max_sync(
+                        0xffffffffu, max(max(__popc(m[0]), __popc(m[1])), max(__popc(m[2]), __popc(m[3]))));
+                    if (PULSE_K1_COOP_STAGE && vmax > PULSE_K1_COOP_MIN_BITS) {
                     // warp-cooperative: slot s of vector group j (element order: lane, then
                     // bit) is filled by lane s % 32 in round s / 32.  Its owner is the first
                     // lane whose inclusive count exceeds s (binary lifting over shuffles), its
@@ -762,7 +771,7 @@ __global__ void __launch_bounds__((tma::kConsumerWarps + 1 + C::kLbWarps) * 32, 
                         }
                         pbase += tj[j];
                     }
-#else
+                    } else {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         uint32_t mm = m[j];
@@ -778,7 +787,7 @@ __global__ void __launch_bounds__((tma::kConsumerWarps + 1 + C::kLbWarps) * 32, 
                             ++pos;
                         }
                     }
-#endif
+                    }
                 }
                 wcount += total;
             }

@@ -62,6 +62,40 @@ using namespace pulse::dev;
 // advised as transparent huge pages: first-touch page faults were most of
 // read_patch_bytes' host time (150 K 4 KB faults for the indices alone).
 constexpr size_t kHugeBytes = size_t(64) << 20, kHugeAlign = size_t(2) << 20;
+// Freed large blocks are kept (up to 4 GiB, 16 blocks) and reused by the next allocation of a
+// similar size: a patch per call (7B: 608 MB of indices, 152 MB of values, 381 MB of bytes)
+// then neither unmaps nor first-touches its pages again -- those costs made the host legs of
+// the end-to-end step vary 0.07-0.55 s between boxes.
+struct BigBlocks {
+    static constexpr size_t kMaxBytes = size_t(4) << 30, kMaxBlocks = 16;
+    std::mutex mu;
+    std::vector<std::pair<void*, size_t>> free_blocks;
+    size_t held = 0;
+    void* take(size_t len) {
+        std::lock_guard<std::mutex> lk(mu);
+        size_t best = free_blocks.size();
+        for (size_t i = 0; i < free_blocks.size(); ++i) {
+            const size_t l = free_blocks[i].second;
+            if (l >= len && l <= 2 * len && (best == free_blocks.size() || l < free_blocks[best].second)) best = i;
+        }
+        if (best == free_blocks.size()) return nullptr;
+        void* p = free_blocks[best].first;
+        held -= free_blocks[best].second;
+        free_blocks.erase(free_blocks.begin() + long(best));
+        return p;
+    }
+    bool keep(void* p, size_t len) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (held + len > kMaxBytes || free_blocks.size() >= kMaxBlocks) return false;
+        free_blocks.emplace_back(p, len);
+        held += len;
+        return true;
+    }
+};
+inline BigBlocks& big_blocks() {
+    static BigBlocks* b = new BigBlocks();  // never destroyed: vectors may be freed during exit
+    return *b;
+}
 template <class T>
 struct NoInit : std::allocator<T> {
     template <class U>
@@ -75,14 +109,20 @@ struct NoInit : std::allocator<T> {
         const size_t bytes = n * sizeof(T);
         if (bytes < kHugeBytes) return std::allocator<T>::allocate(n);
         const size_t len = (bytes + kHugeAlign - 1) / kHugeAlign * kHugeAlign;
+        if (void* q = big_blocks().take(len)) return static_cast<T*>(q);
         void* p = std::aligned_alloc(kHugeAlign, len);
         if (!p) throw std::bad_alloc();
         madvise(p, len, MADV_HUGEPAGE);  // advisory: ignored where THP is off
         return static_cast<T*>(p);
     }
     void deallocate(T* p, size_t n) {
-        if (n * sizeof(T) < kHugeBytes) std::allocator<T>::deallocate(p, n);
-        else std::free(p);
+        const size_t bytes = n * sizeof(T);
+        if (bytes < kHugeBytes) {
+            std::allocator<T>::deallocate(p, n);
+            return;
+        }
+        const size_t len = (bytes + kHugeAlign - 1) / kHugeAlign * kHugeAlign;
+        if (!big_blocks().keep(p, len)) std::free(p);
     }
     template <class U, class... A>
     void construct(U* p, A&&... a) {
@@ -418,9 +458,16 @@ struct Engine {
     pulse_context* ctx = nullptr;
     cudaStream_t stream = nullptr;
     Stager stager;
-    pulse_plan* plan = nullptr;
-    std::vector<pulse_tensor_geom> plan_geom;
-    uint64_t plan_cap = 0;
+    // plans by geometry, least recently used last: encode (the whole checkpoint), read
+    // (the patch's tensors) and decode alternate in one end-to-end step, and rebuilding a
+    // plan (device scratch for its change capacity) on every switch cost 0.1-0.4 s
+    struct CachedPlan {
+        pulse_plan* plan;
+        std::vector<pulse_tensor_geom> geom;
+        uint64_t cap;
+    };
+    static constexpr size_t kMaxPlans = 3;
+    std::vector<CachedPlan> plans;
     DevBuf arena_a, arena_b, idx64, vals, body, entries, result, misc, out64;
     std::mutex mu;
     // decode pipeline: upload and download streams + per-group events (lazy)
@@ -448,22 +495,34 @@ struct Engine {
     }
 
     pulse_plan* get_plan(const std::vector<pulse_tensor_geom>& geom, uint64_t cap) {
-        const bool same = plan && geom.size() == plan_geom.size() &&
-                          std::equal(geom.begin(), geom.end(), plan_geom.begin(), [](auto& a, auto& b) {
-                              return a.numel == b.numel && a.cols == b.cols;
-                          });
-        if (same && cap <= plan_cap) return plan;
-        if (plan) {
+        auto same_geom = [&](const CachedPlan& c) {
+            return geom.size() == c.geom.size() &&
+                   std::equal(geom.begin(), geom.end(), c.geom.begin(),
+                              [](auto& a, auto& b) { return a.numel == b.numel && a.cols == b.cols; });
+        };
+        for (size_t i = 0; i < plans.size(); ++i) {
+            if (!same_geom(plans[i])) continue;
+            CachedPlan c = plans[i];
+            plans.erase(plans.begin() + long(i));
+            if (cap <= c.cap) {
+                plans.insert(plans.begin(), c);
+                return c.plan;
+            }
+            cudaStreamSynchronize(stream);  // too small: replaced below
+            pulse_plan_destroy(c.plan);
+            break;
+        }
+        if (plans.size() >= kMaxPlans) {
             cudaStreamSynchronize(stream);
-            pulse_plan_destroy(plan);
-            plan = nullptr;
+            pulse_plan_destroy(plans.back().plan);
+            plans.pop_back();
         }
         const uint64_t c = std::max<uint64_t>(cap, 1024);
-        if (pulse_plan_create(ctx, geom.data(), uint32_t(geom.size()), c, &plan) != PULSE_OK)
+        pulse_plan* np = nullptr;
+        if (pulse_plan_create(ctx, geom.data(), uint32_t(geom.size()), c, &np) != PULSE_OK)
             raise(PULSE_E_CUDA, std::string("plan: ") + pulse_last_error());
-        plan_geom = geom;
-        plan_cap = c;
-        return plan;
+        plans.insert(plans.begin(), CachedPlan{np, geom, c});
+        return np;
     }
 
     void sync() { cuda_check(cudaStreamSynchronize(stream), "stream sync"); }
