@@ -333,7 +333,9 @@ def run_pulse(args):
             raise RuntimeError(f"apply failed: {res}")
         state["body"] = patch.body_bytes
         state["changes"] = patch.n_changes
-        if world > 1:  # the device-side size exchange saw this rank's section and no failures
+        if world > 1 and not os.environ.get("PULSE_SKIP_SIZE_EXCHANGE"):  # the size exchange saw this rank's section
+            torch.cuda.synchronize()
+            dist.barrier()  # every rank's peer stores of its sizes have landed
             bb, _, st = sp.exchanged_sizes()
             if int(bb[rank]) != patch.body_bytes or any(int(x) != 0 for x in st):
                 raise RuntimeError(f"size exchange mismatch: {bb} {st}")

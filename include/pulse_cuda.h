@@ -207,6 +207,22 @@ pulse_status pulse_apply_patch(pulse_plan* plan, uint32_t weights_slot, uint32_t
 pulse_status pulse_flat_carry_from_summaries(const pulse_scan_summary* dev_gathered, uint32_t rank,
                                              pulse_flat_carry* dev_out, void* stream);
 
+/* Stores `nbytes` (<= 256) device bytes from `dev_src` at each of the `n_dst` (<= 64)
+ * device addresses in the host array `dsts`, from one kernel on `stream` (on the
+ * stream's device, which gets peer access to every destination's device on first use):
+ * with peer-mapped destinations (CUDA IPC, NVLink) this is a one-sided exchange of small
+ * per-step tables between ranks -- the sharded driver's (body bytes, entries, status)
+ * table -- without a collective. Ordering for the readers is the caller's (e.g. device
+ * synchronize + barrier before reading). */
+pulse_status pulse_store_to_peers(const void* dev_src, void* const* dsts, uint32_t n_dst, uint32_t nbytes,
+                                  void* stream);
+
+/* Maps another process's device allocation (a 64-byte cudaIpcMemHandle_t, e.g. from torch's
+ * storage sharing) into the context of `device` in this process, with peer access enabled,
+ * so kernels on `device` can load / store it over NVLink; pulse_ipc_close unmaps it. */
+pulse_status pulse_ipc_open(const void* ipc_handle, int device, void** dev_ptr);
+pulse_status pulse_ipc_close(void* dev_ptr, int device);
+
 /* Analyses (absorption.hpp:38-78) on bound snapshots, one HBM pass each:
  * elements whose bit patterns differ between two slots (the count behind
  * sparsity(), :55-78), and elements whose bf16 magnitude pattern (bits &

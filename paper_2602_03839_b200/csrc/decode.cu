@@ -667,6 +667,18 @@ void launch_coo_unpack_par(const PlanDev& p, const uint8_t* body, const pulse_pa
     PULSE_LAUNCHED("d_finalize", s);
 }
 
+// Small device-to-peers store (pulse_store_to_peers): thread t copies byte t % nbytes to
+// destination t / nbytes (NVLink stores when the destinations are peer-mapped).
+__global__ void k_store_to_peers(const uint8_t* __restrict__ src, PeerPtrs dst, uint32_t n_dst, uint32_t nbytes) {
+    for (uint32_t t = threadIdx.x; t < n_dst * nbytes; t += blockDim.x)
+        static_cast<uint8_t*>(dst.p[t / nbytes])[t % nbytes] = src[t % nbytes];
+}
+
+void launch_store_to_peers(const void* src, const PeerPtrs& dst, uint32_t n_dst, uint32_t nbytes, cudaStream_t s) {
+    k_store_to_peers<<<1, 256, 0, s>>>(static_cast<const uint8_t*>(src), dst, n_dst, nbytes);
+    PULSE_LAUNCHED("k_store_to_peers", s);
+}
+
 // FLAT_INT32 carry of shard `rank` from all ranks' scan summaries (device side
 // of shard.flat_carry): the nearest earlier rank that emitted an index.
 __global__ void k_flat_carry(const pulse_scan_summary* __restrict__ gathered, uint32_t rank,

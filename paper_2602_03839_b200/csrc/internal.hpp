@@ -145,6 +145,10 @@ void launch_decode(const PlanDev& p, uint32_t repr, const uint8_t* body,
                    const pulse_flat_carry* carry, int weights_slot, int64_t* out_indices,
                    pulse_result* result, cudaStream_t s, const pulse_result* patch_result = nullptr);
 void launch_flat_carry(const pulse_scan_summary* gathered, uint32_t rank, pulse_flat_carry* out, cudaStream_t s);
+struct PeerPtrs {
+    void* p[64];
+};
+void launch_store_to_peers(const void* src, const PeerPtrs& dst, uint32_t n_dst, uint32_t nbytes, cudaStream_t s);
 // Validate caller-provided int64 indices (decode over an in-memory SparsePatch,
 // patch.hpp:325-336) and scatter values into `weights_slot`.
 void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uint32_t n_entries,

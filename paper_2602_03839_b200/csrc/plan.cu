@@ -3,6 +3,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -340,6 +341,61 @@ pulse_status pulse_flat_carry_from_summaries(const pulse_scan_summary* dev_gathe
     launch_flat_carry(dev_gathered, rank, dev_out, static_cast<cudaStream_t>(stream));
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "flat_carry launch");
+}
+
+pulse_status pulse_store_to_peers(const void* dev_src, void* const* dsts, uint32_t n_dst, uint32_t nbytes,
+                                  void* stream) {
+    if (!dev_src || (n_dst && !dsts) || nbytes == 0 || nbytes > 256 || n_dst > 64)
+        return fail(PULSE_E_ARGUMENT, "store_to_peers: bad argument");
+    if (n_dst == 0) return PULSE_OK;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int dev = 0;
+    cudaError_t e = s ? cudaStreamGetDevice(s, &dev) : cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "store_to_peers: stream device");
+    cudaSetDevice(dev);
+    PeerPtrs pp{};
+    for (uint32_t i = 0; i < n_dst; ++i) pp.p[i] = dsts[i];
+    // peer access from this device to every device it can reach, once per device (the
+    // destinations are usually IPC mappings another runtime opened on their own device)
+    static std::mutex mu;
+    static std::set<int> enabled;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (enabled.insert(dev).second) {
+            int n = 0;
+            cudaGetDeviceCount(&n);
+            for (int q = 0; q < n; ++q) {
+                int can = 0;
+                if (q == dev || cudaDeviceCanAccessPeer(&can, dev, q) != cudaSuccess || !can) continue;
+                const cudaError_t pe = cudaDeviceEnablePeerAccess(q, 0);
+                if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) {
+                    enabled.erase(dev);
+                    return cuda_fail(pe, "store_to_peers: peer access");
+                }
+            }
+            cudaGetLastError();
+        }
+    }
+    launch_store_to_peers(dev_src, pp, n_dst, nbytes, s);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "store_to_peers launch");
+}
+
+pulse_status pulse_ipc_open(const void* ipc_handle, int device, void** dev_ptr) {
+    if (!ipc_handle || !dev_ptr) return fail(PULSE_E_ARGUMENT, "ipc_open: null argument");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "ipc_open: device");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, sizeof(h));
+    e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "ipc_open");
+}
+
+pulse_status pulse_ipc_close(void* dev_ptr, int device) {
+    if (!dev_ptr) return PULSE_OK;
+    cudaSetDevice(device);
+    const cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "ipc_close");
 }
 
 pulse_status pulse_decode_indices(pulse_plan* plan, uint32_t repr, const uint8_t* dev_body,

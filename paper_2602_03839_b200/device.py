@@ -198,6 +198,26 @@ def flat_carry_from_summaries(gathered: torch.Tensor, rank: int, out: torch.Tens
     return out
 
 
+def store_to_peers(src: torch.Tensor, dst_ptrs, nbytes: int, stream=None):
+    """`nbytes` of device `src` stored at every device address in `dst_ptrs` (ints, e.g.
+    peer-mapped over NVLink), one kernel on `stream` (peer access enabled on first use)."""
+    arr = (C.c_void_p * max(1, len(dst_ptrs)))(*[C.c_void_p(int(p)) for p in dst_ptrs])
+    N.check(N.lib.pulse_store_to_peers(_ptr(src), arr, len(dst_ptrs), nbytes, _stream_ptr(stream)))
+
+
+def ipc_open(handle: bytes, device: int) -> int:
+    """Device address of another process's allocation (its 64-byte CUDA IPC handle), mapped
+    for kernels on `device` (peer access over NVLink)."""
+    ptr = C.c_void_p()
+    buf = C.create_string_buffer(bytes(handle), 64)
+    N.check(N.lib.pulse_ipc_open(buf, int(device), C.byref(ptr)))
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int, device: int):
+    N.check(N.lib.pulse_ipc_close(C.c_void_p(ptr), int(device)))
+
+
 def parse_result(res: torch.Tensor):
     return res.to("cpu").numpy().view(N.RESULT_DTYPE)[0]
 
