@@ -22,3 +22,18 @@ def test_sharded_gather_two_ranks():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "CHECK_SHARD PASS" in r.stdout, r.stdout[-2000:]
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_sharded_bench_step_two_ranks():
+    """The device-side sharded step (K1 -> K2 -> size table over NVLink peer stores -> apply),
+    captured as CUDA graphs: the weights land on the target and every rank's size row arrives."""
+    import json
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29614", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--workload", "qwen2.5-1.5b", "--steps", "4", "--warmup", "3", "--no-e2e",
+           "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["verified"] and line["config"]["launch"] == "cuda-graph replay", line
