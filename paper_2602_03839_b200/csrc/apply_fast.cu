@@ -56,6 +56,9 @@ namespace {
 // Entries per warp range (aggregate granularity), the same rule in every apply kernel of a call:
 // 4096 for large patches, 1024 under PULSE_APPLY_RANGE_SPLIT (16 M) changes so small patches keep
 // enough warps busy (C1, 168 K changes: 41 ranges of 4096 left most of the GPU idle in F1s / F5).
+#ifndef PULSE_F5_NATURAL
+#define PULSE_F5_NATURAL 0  // F5 scatter in entry order (1) or as interleaved pairs (0)
+#endif
 #ifndef PULSE_APPLY_RANGE_MIN
 #define PULSE_APPLY_RANGE_MIN 1024
 #endif
@@ -890,8 +893,17 @@ __device__ __forceinline__ void chunk_body(const ApplyArgs& A, const SCtx& cur, 
 #undef PULSE_SA
 #undef PULSE_SB
     __syncwarp();
-    // scatter: each store instruction covers 32 of 64 consecutive changes (a few sectors)
     uint16_t* W = A.weights[cur.tensor];
+#if PULSE_F5_NATURAL
+    // scatter in entry order: each store instruction covers 32 consecutive changes
+    const uint2* sp2 = reinterpret_cast<const uint2*>(sp);
+#pragma unroll 4
+    for (uint32_t k = lane; k < len; k += 32) {
+        const uint2 q = sp2[2 * swz<8>(k >> 1) + (k & 1)];
+        W[q.x] = uint16_t(q.y);
+    }
+#else
+    // scatter: each store instruction covers 32 of 64 consecutive changes (a few sectors)
     const uint32_t npairs = (len + 1) / 2;
 #pragma unroll 4
     for (uint32_t k2 = lane; k2 < npairs; k2 += 32) {
@@ -899,12 +911,14 @@ __device__ __forceinline__ void chunk_body(const ApplyArgs& A, const SCtx& cur, 
         W[q.x] = uint16_t(q.y);
         if (2 * k2 + 1 < len) W[q.z] = uint16_t(q.w);
     }
+#endif
 }
 
 // F5 resident CTAs per SM (the COO scatter spills ~170 B at 3; 2 measured ~0.5% faster at 7B)
 #ifndef PULSE_F5_MINB
 #define PULSE_F5_MINB 3
 #endif
+
 #ifndef PULSE_F1_MINB
 #define PULSE_F1_MINB 3
 #endif
