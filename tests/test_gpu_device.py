@@ -588,7 +588,7 @@ def _intact(base, view, pad):
 
 @pytest.mark.parametrize("case", ["handcrafted", "esc_rows", "esc_cols", "esc_cols_wide", "dense_all",
                                   "h5_unchanged", "h5_sparse_lead", "roundtrip_s3"])
-def test_no_writes_outside_caller_buffers(golden, case):
+def test_no_writes_outside_caller_buffers(golden, case, k1_shape):
     D = _dev()
     prev, curr, _ = golden.case(case)
     ts = prev.sorted()
