@@ -2,21 +2,24 @@
 // encode_index_payloads (patch.hpp:116-174) and the value payloads, written
 // straight into the identity-codec PULP body (patch_file.hpp:76-82).
 //
-//   K2a k2_scan_escapes  COO_DOWNSCALED: per warp of 256 entries and per chunk
-//                        of 2048, the number of row / column entries that need
-//                        the 0xFF / 0xFFFF escape (index_coding.hpp:68-90), plus
-//                        the argument checks the reference applies to
-//                        caller-provided indices.
-//   K2L k2_layout        one CTA: exclusive scan of the chunk escape counts,
-//                        per-tensor payload sizes and body offsets, FLAT_INT32
-//                        cross-tensor gap bases (patch.hpp:131-156).
-//   K2b k2_emit          single pass: every row/column entry (or u32 gap) and
-//                        every value, at its final byte offset.
+//   K2a k2_scan_escapes  COO_DOWNSCALED: per warp range (k2_range_entries: 1,024 entries under
+//                        16 M changes, 8,192 above), the number of row / column entries that
+//                        need the 0xFF / 0xFFFF escape (index_coding.hpp:68-90), plus the
+//                        argument checks the reference applies to caller-provided indices.
+//   K2L k2_layout        one CTA: exclusive scan of the range escape counts, per-tensor payload
+//                        sizes and body offsets, FLAT_INT32 cross-tensor gap bases
+//                        (patch.hpp:131-156), the entry table and the result record.
+//   K2b k2_emit          single pass: every row/column entry (or u32 gap) and every value, at
+//                        its final byte offset.
+// COO_DOWNSCALED first runs optimistically (layout + emit assuming no escapes); K2a and the
+// exact layout + emit run only if the emit saw an escape (a conditional graph node).
 //
-// Entries are walked warp-contiguously: warp w of a 2048-entry chunk owns 256
-// consecutive entries, 8 rounds of 32 (lane l -> entry round*32 + l).  Loads are
-// coalesced, the previous entry (delta coding) comes from a shuffle, and the
-// segment/tensor context is warp-uniform and reloaded only at boundaries.
+// Fast path: a warp stages a 1,024-entry chunk of one segment in shared memory (cp.async, the
+// next chunk in flight) and each lane codes 32 consecutive entries serially, its predecessor
+// coming from the previous lane; the packed rows / columns / values leave through shared memory
+// as aligned 16-byte stores.  Segment boundaries, caller int64 indices and chunks with escapes
+// take the per-round walker: 32 entries per round, lane l -> entry round*32 + l, the previous
+// entry (delta coding) from a shuffle, the segment / tensor context warp-uniform.
 #include <algorithm>
 
 #include "device.cuh"
