@@ -1,12 +1,16 @@
 // PULSE encode on sm_100a.
 //
-//   K1  k1_diff_compact   bitwise diff of two resident bf16 snapshots and
-//                         order-preserving compaction of every changed element
-//                         (reference loop: patch.hpp:296-301).  One pass over
-//                         both snapshots with 128-bit streaming loads; per-tile
-//                         ballot/popc counts, a block scan, and a decoupled
-//                         look-back across tiles give each change its global
-//                         slot.  Output: u32 segment-relative index + u16 value.
+//   K1  k1_tma            bitwise diff of two resident bf16 snapshots and order-preserving
+//                         compaction of every changed element (reference loop:
+//                         patch.hpp:296-301).  One persistent CTA per SM, warp-specialised: a
+//                         producer warp streams 65,536-element tickets into a shared-memory ring
+//                         with TMA (cp.async.bulk), eight consumer warps diff and stage the
+//                         changes, a look-back / flush group orders the tickets (decoupled
+//                         look-back) and writes them out.  Output: u32 segment-relative index +
+//                         u16 value per change.  Five staging shapes (tma::Cfg, chosen from the
+//                         plan's change capacity) trade ring depth against staging room.
+//   K1b k1_deferred       tickets too dense for the staging, re-streamed after K1 (gated).
+//   k1_static / k1_ticket the earlier non-TMA K1 (8,192-element tiles), kept for A/B runs.
 // The index coders (K2) are in index_code.cu.
 #include <cstdio>
 #include <cstdlib>
@@ -228,7 +232,7 @@ namespace tma {
 // 5 x 5 4.49 ms); dense ones need room for element entries per buffer (90%:
 // 3 x 4 with 8192 entries 13.7 ms; the sparse shape would overflow its staging
 // and re-stream nearly every ticket).  PULSE_K1_* macros override the sparse
-// shape for experiments; PULSE_K1_SHAPE=sparse|dense forces one per launch.
+// shape for experiments; PULSE_K1_SHAPE=sparse|sparse_low|dense|dense2|dense3 forces one per launch.
 #ifndef PULSE_K1_STAGES
 #define PULSE_K1_STAGES 5
 #endif
