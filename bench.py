@@ -462,6 +462,13 @@ def run_pulse(args):
             n_emit = 5 if args.repr == 0 else 2
             n_apply = 13 if args.repr == 0 else 10
         n_carry = 1 if (world > 1 and args.repr == 2) else 0
+        # N > 1: the size table goes out by one peer-store kernel (k_store_to_peers) per step
+        # unless the NCCL fallback is in use (its kernels are not ours)
+        n_peer = 1 if (world > 1 and args.repr != 2 and getattr(sp, "_peer_ptrs", None) is not None
+                       and not os.environ.get("PULSE_SKIP_SIZE_EXCHANGE")) else 0
+        if world > 1:
+            print(f"[bench] size table: {'NVLink peer stores' if sp._peer_ptrs is not None else 'NCCL all-gather'}",
+                  file=sys.stderr)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True,
@@ -501,7 +508,7 @@ def run_pulse(args):
                        for k, t, b in (("k1_scan", scan_max, 4 * d_total + 6 * changes_total),
                                        ("k2_emit", emit_max, 6 * changes_total + body_total),
                                        ("apply", apply_max, body_total + 2 * changes_total))},
-            "gpu_launches": (3 + n_emit + n_carry + n_apply) * args.steps,
+            "gpu_launches": (3 + n_emit + n_carry + n_peer + n_apply) * args.steps,
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -208,14 +208,15 @@ pulse_status pulse_flat_carry_from_summaries(const pulse_scan_summary* dev_gathe
                                              pulse_flat_carry* dev_out, void* stream);
 
 /* Stores `nbytes` (<= 256) device bytes from `dev_src` at each of the `n_dst` (<= 64)
- * device addresses in the host array `dsts`, from one kernel on `stream` (on the
- * stream's device, which gets peer access to every destination's device on first use):
+ * device addresses in the host array `dsts`, from one kernel on `stream` (a stream of
+ * `device`, which gets peer access to every device it can reach on first use; call it
+ * once outside stream capture before capturing it):
  * with peer-mapped destinations (CUDA IPC, NVLink) this is a one-sided exchange of small
  * per-step tables between ranks -- the sharded driver's (body bytes, entries, status)
  * table -- without a collective. Ordering for the readers is the caller's (e.g. device
  * synchronize + barrier before reading). */
 pulse_status pulse_store_to_peers(const void* dev_src, void* const* dsts, uint32_t n_dst, uint32_t nbytes,
-                                  void* stream);
+                                  int device, void* stream);
 
 /* Maps another process's device allocation (a 64-byte cudaIpcMemHandle_t, e.g. from torch's
  * storage sharing) into the context of `device` in this process, with peer access enabled,

@@ -344,15 +344,14 @@ pulse_status pulse_flat_carry_from_summaries(const pulse_scan_summary* dev_gathe
 }
 
 pulse_status pulse_store_to_peers(const void* dev_src, void* const* dsts, uint32_t n_dst, uint32_t nbytes,
-                                  void* stream) {
+                                  int device, void* stream) {
     if (!dev_src || (n_dst && !dsts) || nbytes == 0 || nbytes > 256 || n_dst > 64)
         return fail(PULSE_E_ARGUMENT, "store_to_peers: bad argument");
     if (n_dst == 0) return PULSE_OK;
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    int dev = 0;
-    cudaError_t e = s ? cudaStreamGetDevice(s, &dev) : cudaGetDevice(&dev);
-    if (e != cudaSuccess) return cuda_fail(e, "store_to_peers: stream device");
-    cudaSetDevice(dev);
+    const int dev = device;
+    cudaError_t e = cudaSetDevice(dev);
+    if (e != cudaSuccess) return cuda_fail(e, "store_to_peers: device");
     PeerPtrs pp{};
     for (uint32_t i = 0; i < n_dst; ++i) pp.p[i] = dsts[i];
     // peer access from this device to every device it can reach, once per device (the

@@ -202,7 +202,8 @@ def store_to_peers(src: torch.Tensor, dst_ptrs, nbytes: int, stream=None):
     """`nbytes` of device `src` stored at every device address in `dst_ptrs` (ints, e.g.
     peer-mapped over NVLink), one kernel on `stream` (peer access enabled on first use)."""
     arr = (C.c_void_p * max(1, len(dst_ptrs)))(*[C.c_void_p(int(p)) for p in dst_ptrs])
-    N.check(N.lib.pulse_store_to_peers(_ptr(src), arr, len(dst_ptrs), nbytes, _stream_ptr(stream)))
+    N.check(N.lib.pulse_store_to_peers(_ptr(src), arr, len(dst_ptrs), nbytes, src.device.index,
+                                       _stream_ptr(stream)))
 
 
 def ipc_open(handle: bytes, device: int) -> int:

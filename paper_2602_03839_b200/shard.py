@@ -22,6 +22,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 import os
+import sys
 
 import numpy as np
 import torch
@@ -146,8 +147,16 @@ class ShardedPulse:
             return None
         try:
             share = self.sizes_all.untyped_storage()._share_cuda_()  # (device, handle, size, offset, ...)
+            handle = bytes(share[1])
+            # torch's caching allocator prefixes the 64-byte cudaIpcMemHandle_t with a format
+            # version byte and the segment kind, b"c" for a cudaMalloc segment (expandable
+            # segments would need the cuMem API: not supported here, NCCL is used instead)
+            if len(handle) == 66 and handle[1:2] == b"c":
+                handle = handle[2:]
+            if len(handle) != 64:
+                raise ValueError(f"unsupported CUDA IPC handle ({len(handle)} bytes)")
             shares = [None] * self.world
-            dist.all_gather_object(shares, (bytes(share[1]), int(share[3])))
+            dist.all_gather_object(shares, (handle, int(share[3])))
             ptrs = []
             for r in range(self.world):
                 if r == self.rank:
@@ -155,7 +164,9 @@ class ShardedPulse:
                 else:  # mapped for this device's kernels (NVLink peer access)
                     ptrs.append(self.D.ipc_open(shares[r][0], self.device.index) + shares[r][1])
             ok = torch.tensor([1], device=self.device)
-        except Exception:  # noqa: BLE001  (no IPC / peer access: every rank falls back together)
+        except Exception as exc:  # noqa: BLE001  (no IPC / peer access: every rank falls back together)
+            print(f"[shard] rank {self.rank}: NVLink size table unavailable ({type(exc).__name__}: {exc}); "
+                  "using NCCL", file=sys.stderr)
             ptrs, ok = None, torch.tensor([0], device=self.device)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         return ptrs if int(ok.item()) == 1 else None

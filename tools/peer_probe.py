@@ -15,7 +15,9 @@ for r in range(world):
     if r == rank:
         ptrs.append(buf.data_ptr()); continue
     dev, handle, size, off = hs[r][0], hs[r][1], hs[r][2], hs[r][3]
-    base = D.ipc_open(handle, local)
+    hb = bytes(handle)
+    hb = hb[2:] if len(hb) == 66 else hb
+    base = D.ipc_open(hb, local)
     ptrs.append(base + off)
     print(rank, "peer", r, "dev", dev, "base", hex(base), "off", off, "size", size, flush=True)
 src = torch.full((16,), rank + 1, dtype=torch.uint8, device="cuda")
