@@ -464,8 +464,10 @@ def run_pulse(args):
         n_carry = 1 if (world > 1 and args.repr == 2) else 0
         # N > 1: the size table goes out by one peer-store kernel (k_store_to_peers) per step
         # unless the NCCL fallback is in use (its kernels are not ours)
-        n_peer = 1 if (world > 1 and args.repr != 2 and getattr(sp, "_peer_ptrs", None) is not None
+        n_peer = 1 if (world > 1 and getattr(sp, "_peer_ptrs", None) is not None
                        and not os.environ.get("PULSE_SKIP_SIZE_EXCHANGE")) else 0
+        if world > 1 and args.repr == 2 and getattr(sp, "_sum_ptrs", None) is not None:
+            n_peer += 2  # k_peer_post + k_peer_wait (FLAT summaries over NVLink)
         if world > 1:
             print(f"[bench] size table: {'NVLink peer stores' if sp._peer_ptrs is not None else 'NCCL all-gather'}",
                   file=sys.stderr)

@@ -218,6 +218,17 @@ pulse_status pulse_flat_carry_from_summaries(const pulse_scan_summary* dev_gathe
 pulse_status pulse_store_to_peers(const void* dev_src, void* const* dsts, uint32_t n_dst, uint32_t nbytes,
                                   int device, void* stream);
 
+/* All-gather of one `nbytes` (<= 48) record per rank through peer-mapped tables, inside a
+ * stream / CUDA graph (no collective): `tables[r]` is rank r's table of 2 x world 64-byte
+ * slots (zeroed once; tables[rank] is this rank's own), `dev_epoch` a device u64 (zeroed
+ * once) that every rank advances once per call. The record goes to this rank's slot in
+ * every table tagged with the new epoch; the call then waits on the device until all
+ * ranks' slots carry it and copies the records to `dev_out` (world x nbytes, rank order).
+ * Slots alternate with the epoch's parity, so a rank one call ahead never overwrites a
+ * record its peers have not read. Every rank must make the same sequence of calls. */
+pulse_status pulse_peer_allgather(const void* dev_src, void* const* tables, uint32_t world, uint32_t rank,
+                                  uint32_t nbytes, uint64_t* dev_epoch, void* dev_out, int device, void* stream);
+
 /* Maps another process's device allocation (a 64-byte cudaIpcMemHandle_t, e.g. from torch's
  * storage sharing) into the context of `device` in this process, with peer access enabled,
  * so kernels on `device` can load / store it over NVLink; pulse_ipc_close unmaps it. */

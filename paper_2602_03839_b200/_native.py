@@ -140,6 +140,7 @@ _SIGS = {
     "pulse_apply_patch": (i32, [vp, u32, u32, vp, vp, vp, vp, vp, vp]),
     "pulse_flat_carry_from_summaries": (i32, [vp, u32, vp, vp]),
     "pulse_store_to_peers": (i32, [vp, vp, u32, u32, C.c_int, vp]),
+    "pulse_peer_allgather": (i32, [vp, vp, u32, u32, u32, vp, vp, C.c_int, vp]),
     "pulse_ipc_open": (i32, [vp, C.c_int, C.POINTER(vp)]),
     "pulse_ipc_close": (i32, [vp, C.c_int]),
     "pulse_decode_indices": (i32, [vp, u32, vp, vp, u32, vp, vp, vp, vp]),

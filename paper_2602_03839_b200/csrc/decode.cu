@@ -679,6 +679,60 @@ void launch_store_to_peers(const void* src, const PeerPtrs& dst, uint32_t n_dst,
     PULSE_LAUNCHED("k_store_to_peers", s);
 }
 
+// All-gather of small per-rank records over peer memory, inside a stream (or a graph):
+// every rank's table holds 2 x world slots of kSlotBytes (record, then a u64 epoch tag at
+// +kSlotTag), double-buffered by epoch parity so a rank one step ahead never overwrites a
+// slot its peers have not read.  Post: epoch += 1, the record to this rank's slot in every
+// table, a system fence, then the tag.  Wait: spin until every rank's slot carries the
+// epoch, fence, copy the records out contiguously.
+constexpr uint32_t kSlotBytes = 64, kSlotTag = 48;
+
+__global__ void k_peer_post(const uint8_t* __restrict__ src, PeerPtrs tables, uint32_t world, uint32_t rank,
+                            uint32_t nbytes, unsigned long long* __restrict__ epoch) {
+    __shared__ unsigned long long s_e;
+    if (threadIdx.x == 0) s_e = ++*epoch;
+    __syncthreads();
+    const unsigned long long e = s_e;
+    const uint32_t slot = uint32_t((e & 1) * world + rank) * kSlotBytes;
+    for (uint32_t t = threadIdx.x; t < world * nbytes; t += blockDim.x)
+        static_cast<uint8_t*>(tables.p[t / nbytes])[slot + t % nbytes] = src[t % nbytes];
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < world)
+        *reinterpret_cast<volatile unsigned long long*>(static_cast<uint8_t*>(tables.p[threadIdx.x]) + slot + kSlotTag) = e;
+}
+
+__global__ void k_peer_wait(const uint8_t* __restrict__ table, uint32_t world, uint32_t nbytes,
+                            const unsigned long long* __restrict__ epoch, uint8_t* __restrict__ out) {
+    const unsigned long long e = *epoch;
+    const uint8_t* base = table + (e & 1) * world * kSlotBytes;
+    if (threadIdx.x < world) {
+        const volatile unsigned long long* tag =
+            reinterpret_cast<const volatile unsigned long long*>(base + threadIdx.x * kSlotBytes + kSlotTag);
+        uint64_t spins = 0;
+        while (*tag != e) {
+            __nanosleep(64);
+            if (++spins > 64 * kSpinLimit) {  // seconds: a rank that never posts -- fail loudly
+                watchdog_fire(4, threadIdx.x, e, *tag);
+                __trap();
+            }
+        }
+    }
+    __threadfence_system();
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < world * nbytes; t += blockDim.x)
+        out[t] = reinterpret_cast<const volatile uint8_t*>(base)[(t / nbytes) * kSlotBytes + t % nbytes];
+}
+
+void launch_peer_allgather(const void* src, const PeerPtrs& tables, const void* my_table, uint32_t world,
+                           uint32_t rank, uint32_t nbytes, unsigned long long* epoch, void* out, cudaStream_t s) {
+    k_peer_post<<<1, 256, 0, s>>>(static_cast<const uint8_t*>(src), tables, world, rank, nbytes, epoch);
+    PULSE_LAUNCHED("k_peer_post", s);
+    k_peer_wait<<<1, 256, 0, s>>>(static_cast<const uint8_t*>(my_table), world, nbytes, epoch,
+                                  static_cast<uint8_t*>(out));
+    PULSE_LAUNCHED("k_peer_wait", s);
+}
+
 // FLAT_INT32 carry of shard `rank` from all ranks' scan summaries (device side
 // of shard.flat_carry): the nearest earlier rank that emitted an index.
 __global__ void k_flat_carry(const pulse_scan_summary* __restrict__ gathered, uint32_t rank,

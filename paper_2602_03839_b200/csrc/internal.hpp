@@ -149,6 +149,8 @@ struct PeerPtrs {
     void* p[64];
 };
 void launch_store_to_peers(const void* src, const PeerPtrs& dst, uint32_t n_dst, uint32_t nbytes, cudaStream_t s);
+void launch_peer_allgather(const void* src, const PeerPtrs& tables, const void* my_table, uint32_t world,
+                           uint32_t rank, uint32_t nbytes, unsigned long long* epoch, void* out, cudaStream_t s);
 // Validate caller-provided int64 indices (decode over an in-memory SparsePatch,
 // patch.hpp:325-336) and scatter values into `weights_slot`.
 void launch_apply_fast(const PlanDev& p, uint32_t repr, const uint8_t* body, uint32_t n_entries,

@@ -380,6 +380,21 @@ pulse_status pulse_store_to_peers(const void* dev_src, void* const* dsts, uint32
     return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "store_to_peers launch");
 }
 
+pulse_status pulse_peer_allgather(const void* dev_src, void* const* tables, uint32_t world, uint32_t rank,
+                                  uint32_t nbytes, uint64_t* dev_epoch, void* dev_out, int device, void* stream) {
+    if (!dev_src || !tables || !dev_epoch || !dev_out || world == 0 || world > 64 || rank >= world ||
+        nbytes == 0 || nbytes > 48)
+        return fail(PULSE_E_ARGUMENT, "peer_allgather: bad argument");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "peer_allgather: device");
+    PeerPtrs pp{};
+    for (uint32_t i = 0; i < world; ++i) pp.p[i] = tables[i];
+    launch_peer_allgather(dev_src, pp, tables[rank], world, rank, nbytes,
+                          reinterpret_cast<unsigned long long*>(dev_epoch), dev_out, static_cast<cudaStream_t>(stream));
+    e = cudaGetLastError();
+    return e == cudaSuccess ? PULSE_OK : cuda_fail(e, "peer_allgather launch");
+}
+
 pulse_status pulse_ipc_open(const void* ipc_handle, int device, void** dev_ptr) {
     if (!ipc_handle || !dev_ptr) return fail(PULSE_E_ARGUMENT, "ipc_open: null argument");
     cudaError_t e = cudaSetDevice(device);

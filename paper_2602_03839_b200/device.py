@@ -206,6 +206,15 @@ def store_to_peers(src: torch.Tensor, dst_ptrs, nbytes: int, stream=None):
                                        _stream_ptr(stream)))
 
 
+def peer_allgather(src: torch.Tensor, table_ptrs, rank: int, nbytes: int, epoch: torch.Tensor, out: torch.Tensor,
+                   stream=None):
+    """One `nbytes` record per rank gathered into `out` through peer-mapped slot tables
+    (pulse_peer_allgather): no collective, graph-capturable."""
+    arr = (C.c_void_p * max(1, len(table_ptrs)))(*[C.c_void_p(int(p)) for p in table_ptrs])
+    N.check(N.lib.pulse_peer_allgather(_ptr(src), arr, len(table_ptrs), rank, nbytes, _ptr(epoch), _ptr(out),
+                                       src.device.index, _stream_ptr(stream)))
+
+
 def ipc_open(handle: bytes, device: int) -> int:
     """Device address of another process's allocation (its 64-byte CUDA IPC handle), mapped
     for kernels on `device` (peer access over NVLink)."""

@@ -132,10 +132,45 @@ class ShardedPulse:
         self.sizes_all = torch.zeros(16 * self.world, dtype=torch.uint8, device=self.device)
         self.apply_res = torch.zeros(72, dtype=torch.uint8, device=self.device)
         self._side = None
+        # FLAT summaries over NVLink: 2 x world 64-byte slots per rank, an epoch per call
+        self.sum_table = torch.zeros(2 * self.world * 64, dtype=torch.uint8, device=self.device)
+        self.sum_epoch = torch.zeros(1, dtype=torch.int64, device=self.device)
         self._peer_sizes = self._open_peer_sizes() if self.world > 1 else None
         self._peer_ptrs = None
+        self._sum_ptrs = None
         if self._peer_sizes is not None:  # this rank's 16-byte slot in every rank's table
             self._peer_ptrs = [p + 16 * self.rank for p in self._peer_sizes]
+        # FLAT_INT32's summary all-gather over NVLink (pulse_peer_allgather) is opt-in: at 2 GPUs
+        # it matched NCCL (2.68 ms per step), at 4 its device-side wait made the step 2.04 ms
+        # against 1.46 with NCCL (profiles/r2l_peer_sizes.txt)
+        if self._peer_sizes is not None and os.environ.get("PULSE_PEER_SUMMARIES", "0") == "1":
+            try:
+                self._sum_ptrs = self._map_peers(self.sum_table)
+                ok = torch.tensor([1], device=self.device)
+            except Exception as exc:  # noqa: BLE001
+                print(f"[shard] rank {self.rank}: NVLink summary table unavailable ({exc}); using NCCL",
+                      file=sys.stderr)
+                ok = torch.tensor([0], device=self.device)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) != 1:
+                self._sum_ptrs = None
+
+    def _map_peers(self, t: torch.Tensor):
+        """Device addresses, valid for this device's kernels, of every rank's copy of `t`
+        (same shape on every rank): CUDA IPC handles exchanged once with all_gather_object."""
+        share = t.untyped_storage()._share_cuda_()  # (device, handle, size, offset, ...)
+        handle = bytes(share[1])
+        # torch's caching allocator prefixes the 64-byte cudaIpcMemHandle_t with a format
+        # version byte and the segment kind, b"c" for a cudaMalloc segment (expandable
+        # segments would need the cuMem API: not supported here, NCCL is used instead)
+        if len(handle) == 66 and handle[1:2] == b"c":
+            handle = handle[2:]
+        if len(handle) != 64:
+            raise ValueError(f"unsupported CUDA IPC handle ({len(handle)} bytes)")
+        shares = [None] * self.world
+        dist.all_gather_object(shares, (handle, int(share[3])))
+        return [t.data_ptr() if r == self.rank else self.D.ipc_open(shares[r][0], self.device.index) + shares[r][1]
+                for r in range(self.world)]
 
     def _open_peer_sizes(self):
         """Device addresses of every rank's `sizes_all`, mapped for this device over NVLink
@@ -146,23 +181,7 @@ class ShardedPulse:
         if os.environ.get("PULSE_PEER_SIZES", "1") == "0":
             return None
         try:
-            share = self.sizes_all.untyped_storage()._share_cuda_()  # (device, handle, size, offset, ...)
-            handle = bytes(share[1])
-            # torch's caching allocator prefixes the 64-byte cudaIpcMemHandle_t with a format
-            # version byte and the segment kind, b"c" for a cudaMalloc segment (expandable
-            # segments would need the cuMem API: not supported here, NCCL is used instead)
-            if len(handle) == 66 and handle[1:2] == b"c":
-                handle = handle[2:]
-            if len(handle) != 64:
-                raise ValueError(f"unsupported CUDA IPC handle ({len(handle)} bytes)")
-            shares = [None] * self.world
-            dist.all_gather_object(shares, (handle, int(share[3])))
-            ptrs = []
-            for r in range(self.world):
-                if r == self.rank:
-                    ptrs.append(self.sizes_all.data_ptr())
-                else:  # mapped for this device's kernels (NVLink peer access)
-                    ptrs.append(self.D.ipc_open(shares[r][0], self.device.index) + shares[r][1])
+            ptrs = self._map_peers(self.sizes_all)
             ok = torch.tensor([1], device=self.device)
         except Exception as exc:  # noqa: BLE001  (no IPC / peer access: every rank falls back together)
             print(f"[shard] rank {self.rank}: NVLink size table unavailable ({type(exc).__name__}: {exc}); "
@@ -223,7 +242,11 @@ class ShardedPulse:
             return
         main = torch.cuda.current_stream(self.device)
         if patch.representation == 2:
-            dist.all_gather_into_tensor(self.gathered, self.send)
+            if self._sum_ptrs is not None:  # device-side all-gather over NVLink (no collective)
+                self.D.peer_allgather(self.send, self._sum_ptrs, self.rank, SUMMARY_BYTES, self.sum_epoch,
+                                      self.gathered)
+            else:
+                dist.all_gather_into_tensor(self.gathered, self.send)
             self.plan.emit(patch, gathered=self.gathered, n_ranks=self.world, rank=self.rank)
             self.D.flat_carry_from_summaries(self.gathered, self.rank, self.carry_dev)
         else:
