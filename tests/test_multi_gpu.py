@@ -37,3 +37,21 @@ def test_sharded_bench_step_two_ranks():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["verified"] and line["config"]["launch"] == "cuda-graph replay", line
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_flat_summaries_over_nvlink_two_ranks():
+    """FLAT_INT32 sharded step with the scan summaries all-gathered over NVLink inside the
+    graph (pulse_peer_allgather, epoch-tagged slots): the FLAT carry it feeds must make every
+    rank's apply land on the target."""
+    import json
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29615", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--workload", "qwen2.5-1.5b", "--repr", "2", "--steps", "4", "--warmup", "3",
+           "--no-e2e", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env={**os.environ, "PULSE_PEER_SUMMARIES": "1"})
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["verified"] and line["config"]["launch"] == "cuda-graph replay", line
+    assert "NVLink summary table unavailable" not in r.stderr
