@@ -140,10 +140,10 @@ class ShardedPulse:
         self._sum_ptrs = None
         if self._peer_sizes is not None:  # this rank's 16-byte slot in every rank's table
             self._peer_ptrs = [p + 16 * self.rank for p in self._peer_sizes]
-        # FLAT_INT32's summary all-gather over NVLink (pulse_peer_allgather) is opt-in: correct and
-        # 2.68 ms per step at 2 GPUs, but at 4 its device-side wait made the step 2.04 ms against
-        # 1.46 with NCCL (profiles/r2l_peer_sizes.txt)
-        if self._peer_sizes is not None and os.environ.get("PULSE_PEER_SUMMARIES", "0") == "1":
+        # FLAT_INT32's summary all-gather over NVLink (pulse_peer_allgather, device-side wait):
+        # 2.67 vs 2.70-2.71 ms per step with NCCL at 2 GPUs, 1.43-1.52 vs 1.44-1.47 at 4 (one run
+        # on another box: 2.04; profiles/r2l_peer_sizes.txt); PULSE_PEER_SUMMARIES=0 uses NCCL
+        if self._peer_sizes is not None and os.environ.get("PULSE_PEER_SUMMARIES", "1") == "1":
             try:
                 self._sum_ptrs = self._map_peers(self.sum_table)
                 ok = torch.tensor([1], device=self.device)

@@ -50,7 +50,7 @@ def test_flat_summaries_over_nvlink_two_ranks():
            "--gpus", "2", "--workload", "qwen2.5-1.5b", "--repr", "2", "--steps", "4", "--warmup", "3",
            "--no-e2e", "--no-cpu-baseline"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
-                       env={**os.environ, "PULSE_PEER_SUMMARIES": "1"})
+                       env={k: v for k, v in os.environ.items() if k != "PULSE_PEER_SUMMARIES"})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["verified"] and line["config"]["launch"] == "cuda-graph replay", line
