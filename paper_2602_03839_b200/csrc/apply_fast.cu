@@ -56,6 +56,9 @@ namespace {
 // Entries per warp range (aggregate granularity), the same rule in every apply kernel of a call:
 // 4096 for large patches, 1024 under PULSE_APPLY_RANGE_SPLIT (16 M) changes so small patches keep
 // enough warps busy (C1, 168 K changes: 41 ranges of 4096 left most of the GPU idle in F1s / F5).
+#ifndef PULSE_F3_CTAS_PER_SM
+#define PULSE_F3_CTAS_PER_SM 64  // no cap
+#endif
 #ifndef PULSE_F5_NATURAL
 #define PULSE_F5_NATURAL 0  // F5 scatter in entry order (1) or as interleaved pairs (0)
 #endif
@@ -1166,7 +1169,10 @@ void launch_pass(const ApplyArgs& a, cudaStream_t s) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, f_pass<kRepr, kPass>, kThreads, smem);
         per_sm = v > 0 ? v : 1;
     }
-    f_pass<kRepr, kPass><<<unsigned(sm_count() * per_sm), kThreads, smem, s>>>(a);
+    // F3 (validate) walks a short list of pieces (or, rarely, every range): PULSE_F3_CTAS_PER_SM
+    // caps its grid below full occupancy (fewer idle CTAs to schedule for small patches)
+    const int cap = kPass == kValidate ? PULSE_F3_CTAS_PER_SM : per_sm;
+    f_pass<kRepr, kPass><<<unsigned(sm_count() * (per_sm < cap ? per_sm : cap)), kThreads, smem, s>>>(a);
     PULSE_LAUNCHED("f_pass", s);
 }
 
