@@ -373,6 +373,7 @@ struct Smem {
     uint32_t overflow[kBufs];
     uint32_t tk_cnt[kBufs];          // ticket count, summed by the consumer warps
     uint32_t tk_arrived[kBufs];      // consumer warps done with the ticket
+    uint32_t vcnt[kBufs];            // element mode: changed 16-byte vectors (what records would need)
     StageDesc desc[kStages];
     TicketInfo info[kBufs];
     uint64_t full[kStages], empty[kStages];
@@ -463,6 +464,7 @@ __global__ void __launch_bounds__((tma::kConsumerWarps + 1 + C::kLbWarps) * 32, 
             S.mode[i] = kModeRecords;
             S.tk_cnt[i] = 0;
             S.tk_arrived[i] = 0;
+            S.vcnt[i] = 0;
         }
         mbar_fence_init();
     }
@@ -717,7 +719,10 @@ __global__ void __launch_bounds__((tma::kConsumerWarps + 1 + C::kLbWarps) * 32, 
                 const uint32_t pj[4] = {exlo & 0xFFFF, t0 + (exlo >> 16), t0 + t1 + (exhi & 0xFFFF),
                                         t0 + t1 + t2 + (exhi >> 16)};
                 uint32_t off = 0;
-                if (lane == 0 && total) off = atomicAdd(&S.fill[buf], total);
+                if (lane == 0 && total) {
+                    off = atomicAdd(&S.fill[buf], total);
+                    atomicAdd(&S.vcnt[buf], __popc(rbj[0]) + __popc(rbj[1]) + __popc(rbj[2]) + __popc(rbj[3]));
+                }
                 off = __shfl_sync(0xffffffffu, off, 0);
                 if (lane == 0) {
                     S.chunk_off[buf][chunk] = off;
@@ -941,9 +946,11 @@ __global__ void __launch_bounds__((tma::kConsumerWarps + 1 + C::kLbWarps) * 32, 
             // changed vectors staged (or asked for) in record mode: scattered changes (one per
             // 16-byte vector) overflow the records long before the element count is "dense"
             const bool rec_overflow = S.mode[buf] == kModeRecords && S.fill[buf] > kRecCap;
-            // ... and stays there while its changes could not fit the records either (no
-            // records / elements ping-pong that defers every other ticket)
-            const bool el_keep = S.mode[buf] == kModeElements && count > kRecCap;
+            // ... and stays there while its changed vectors would not fit the records either
+            // (no records / elements ping-pong that defers every other ticket; clustered changes,
+            // several per vector, go back to records)
+            const bool el_keep = S.mode[buf] == kModeElements && S.vcnt[buf] > kRecCap;
+            S.vcnt[buf] = 0;
             S.fill[buf] = 0;
             S.overflow[buf] = 0;
             // layout for the next ticket staged in this buffer: neighbouring tickets
