@@ -297,7 +297,7 @@ using DenseCfg = Cfg<PULSE_K1_DSTAGES, PULSE_K1_DBUFS, PULSE_K1_DRECCAP, PULSE_K
 // patches denser than ~4.5%: records only (no element staging), larger record buffers, fewer
 // stages; tickets too dense even for those are counted in K1 and written by K1b
 using Dense2Cfg = Cfg<2, 3, 2200, 0, 0xFFFFFFFFu, 8000, PULSE_K1_D2LB>;
-// patches denser than ~8%: the same staging and six flush warps -- at 90% the four-warp flush
+// patches denser than ~5.6%: the same staging and six flush warps -- at 90% the four-warp flush
 // (expanding ~6,500 changes per ticket) was the bottleneck: K1 10.3 -> 9.0 ms; at 95% the extra
 // warps cost more issue slots than they save (6.87 -> 7.00 ms), hence a separate shape
 #ifndef PULSE_K1_D3S

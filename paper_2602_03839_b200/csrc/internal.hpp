@@ -89,7 +89,7 @@ struct PlanDev {
     const SegDesc* segs;
     const uint32_t* tile_seg;   // [n_tiles] segment of each K1 tile
     uint64_t tma_tiles;         // number of 65536-element tickets
-    uint32_t k1_dense;          // K1 staging shape from the capacity: 4 sparse (< 1.5%), 0 sparse (< 2.2%), 1 dense (>= 2.2%), 2 denser (>= 4.5%), 3 (>= 8%)
+    uint32_t k1_dense;          // K1 staging shape from the capacity: 4 sparse (< 1.5%), 0 sparse (< 2.2%), 1 dense (>= 2.2%), 2 denser (>= 4.5%), 3 (>= 5.6%)
     ulonglong2* k1_defer;       // [tma_tiles] (ticket, output offset) of the tickets K1b writes
     const uint32_t* tma_tile_seg;  // [tma_tiles] segment of each ticket
     uint32_t* trace;            // [tma_tiles] optional K1 progress trace (PULSE_TRACE=1)

@@ -162,7 +162,7 @@ pulse_status pulse_plan_create(pulse_context* ctx, const pulse_tensor_geom* tens
     for (uint32_t t = 0; t < n_tensors; ++t) elems += tensors[t].numel;
     // K1 staging shape from the change capacity (profiles/r2e_k1_sparse_shapes.txt: the sparse
     // shape's 448 records per ticket overflow from ~2.2% clustered changes on)
-    p.k1_dense = p.cap * 100 >= elems * 8 ? 3u : p.cap * 1000 >= elems * 45 ? 2u : p.cap * 1000 >= elems * 22 ? 1u
+    p.k1_dense = p.cap * 1000 >= elems * 56 ? 3u : p.cap * 1000 >= elems * 45 ? 2u : p.cap * 1000 >= elems * 22 ? 1u
                : p.cap * 1000 < elems * 15 ? 4u : 0u;
     const uint64_t T = n_tensors, S = segs.size(), cap = p.cap;
     const uint64_t n_chunks = cap / kChunkEntries + 2;
