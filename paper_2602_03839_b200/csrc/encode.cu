@@ -242,6 +242,9 @@ namespace tma {
 #ifndef PULSE_K1_COOP_STAGE
 #define PULSE_K1_COOP_STAGE 1  // element mode: warp-cooperative staging (0: per-lane loop over mask bits)
 #endif
+#ifndef PULSE_K1_FLAT_FLUSH
+#define PULSE_K1_FLAT_FLUSH 0  // element flush over the whole ticket when < this many entries per chunk
+#endif
 #ifndef PULSE_K1_COOP_MIN_BITS
 #define PULSE_K1_COOP_MIN_BITS 2  // ... only for warp chunks with a vector of more changes than this
 #endif
@@ -919,6 +922,25 @@ __global__ void __launch_bounds__((tma::kConsumerWarps + 1 + C::kLbWarps) * 32, 
                 }
             }
         } else if (!S.overflow[buf]) {
+            if (PULSE_K1_FLAT_FLUSH && count < PULSE_K1_FLAT_FLUSH * nch) {
+                // few entries per chunk (scattered changes): every flush thread takes entries of
+                // the whole ticket in order, finding each one's chunk by a binary search of the
+                // chunk prefix -- no per-chunk rounds that leave most lanes idle
+                for (uint32_t i = uint32_t(lt); i < count; i += kLbThreads) {
+                    uint32_t lo = 0, hi = nch;  // last chunk c with chunk_pre[c] <= i
+                    while (hi - lo > 1) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (S.chunk_pre[mid] <= i) lo = mid;
+                        else hi = mid;
+                    }
+                    const uint32_t off = S.chunk_off[buf][lo] + (i - S.chunk_pre[lo]);
+                    const uint64_t pos = G + i;
+                    if (pos < k.capacity) {
+                        k.out_idx[pos] = ti.toff + S.stg[buf].el.idx[off];
+                        k.out_val[pos] = S.stg[buf].el.val[off];
+                    }
+                }
+            } else {
             // element mode: each chunk's staged entries are contiguous and go to
             // G + chunk_pre[c] onward -- one warp per chunk, lanes over its entries
             // (coalesced stores, no per-entry search for the chunk)
@@ -932,6 +954,7 @@ __global__ void __launch_bounds__((tma::kConsumerWarps + 1 + C::kLbWarps) * 32, 
                         k.out_val[pos] = S.stg[buf].el.val[off + i];
                     }
                 }
+            }
             }
         } else if (lt == 0 && count > 0) {
             // staging overflowed (or the ticket was only counted): K1b writes this ticket after
